@@ -1,0 +1,133 @@
+/*
+ * stb200.h — C ABI of the B200-native tool-resident engine (libstb200.so).
+ *
+ * The reference (`/root/reference/pkg/src/spectool`) is a pure-Python
+ * discrete-event engine with no FFI: every phase is a virtual-time charge
+ * `sim.schedule(rate * tokens, continuation)`. Each entry point below is the
+ * device work that replaces one of those charges; the comment on each names
+ * the reference call site it stands in for. Plain pointers and sizes only:
+ * device pointers are raw CUDA addresses (torch tensors' data_ptr()),
+ * `stream` is a cudaStream_t passed as void*. All calls are stream-ordered,
+ * allocate nothing on the hot path, and return 0 or a negative STB_E* code;
+ * `stb_last_error()` holds the message for the calling thread.
+ *
+ * Layout: the KV pool owns, per layer, K and V pages
+ * `[num_blocks][n_kv][block_size=16][d_head]` bf16; the block table is
+ * `int32 [max_slots][max_blocks_per_slot]` on the device, mirrored on the host
+ * where the deterministic LIFO allocator runs.
+ */
+#ifndef STB200_H
+#define STB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STB_OK 0
+#define STB_EINVAL (-1)
+#define STB_ENOMEM (-2)
+#define STB_ECUDA (-3)
+#define STB_ECAPACITY (-4)
+
+typedef struct stb_kv_pool stb_kv_pool;
+
+/* ---- diagnostics ------------------------------------------------------- */
+const char* stb_last_error(void);
+int stb_version(void);
+/* number of kernel launches issued through this library since load */
+int64_t stb_launch_count(void);
+
+/* ---- K1: paged KV pool, block allocator, block table --------------------
+ * Replaces the reference's integer KV accounting: `seq.kv_tokens = ...`
+ * (engine.py:259,285,313,335,366), the evict/reset (engine.py:382-384) and
+ * the slot release (engine.py:385,397). The reference pool is unbounded
+ * (SPEC.md:521); this one is sized in blocks and reports STB_ECAPACITY.   */
+int stb_kv_pool_create(int device, int layers, int n_kv, int d_head, int block_size, int num_blocks,
+                       int max_slots, int max_blocks_per_slot, stb_kv_pool** out);
+int stb_kv_pool_destroy(stb_kv_pool* pool);
+/* grow slot's block list to ceil(new_len / block_size) blocks (LIFO pops) */
+int stb_kv_reserve(stb_kv_pool* pool, int slot, int new_len);
+/* free blocks beyond ceil(new_len / block_size) (rollback / evict-to-prefix) */
+int stb_kv_truncate(stb_kv_pool* pool, int slot, int new_len);
+/* free every block of the slot (request finished / vanilla evict) */
+int stb_kv_release(stb_kv_pool* pool, int slot);
+int stb_kv_free_blocks(const stb_kv_pool* pool);
+int stb_kv_slot_len(const stb_kv_pool* pool, int slot);
+/* host copy of a slot's block ids; returns the count (or error) */
+int stb_kv_slot_blocks(const stb_kv_pool* pool, int slot, int32_t* out, int cap);
+/* upload block-table rows changed since the last sync (async on stream) */
+int stb_kv_sync(stb_kv_pool* pool, void* stream);
+/* device addresses: K/V base of a layer, the device block table and its row stride */
+int stb_kv_layer_ptrs(const stb_kv_pool* pool, int layer, void** k_pages, void** v_pages);
+int stb_kv_block_table(const stb_kv_pool* pool, int32_t** dev_table, int* row_stride);
+/* K1 commit: scatter bf16 rows k,v [n][n_kv*d_head] (row stride ld elements)
+ * into the pages of (slot_of[i], pos_of[i]); 16-byte vector stores. */
+int stb_kv_commit(stb_kv_pool* pool, int layer, const void* k, const void* v, int64_t ld, const int32_t* slot_of,
+                  const int32_t* pos_of, int n, void* stream);
+/* K1 copy: duplicate whole blocks src[i] -> dst[i] in every layer (fork / COW) */
+int stb_kv_copy_blocks(stb_kv_pool* pool, const int32_t* src, const int32_t* dst, int n, void* stream);
+
+/* ---- fused QKV epilogue: RoPE on q/k + K1 commit of k/v -----------------
+ * qkv fp32 [n][(n_q + 2 n_kv) d_head] from the QKV GEMM; writes q bf16
+ * [n][n_q d_head] (rotated) and commits rotated k and v into the pool. */
+int stb_qkv_rope_commit(stb_kv_pool* pool, int layer, const float* qkv, void* q_out, const int32_t* slot_of,
+                        const int32_t* pos_of, int n, int n_q, float rope_theta, void* stream);
+
+/* ---- K3: paged decode attention (one query per sequence) ----------------
+ * Replaces the decode charges engine.py:270,276,302,317. q/out bf16
+ * [B][n_q][d_head]; slots/ctx_lens int32 [B]; split-K over the context with
+ * a merge pass. `work` is a caller-owned fp32 scratch of
+ * stb_attn_decode_workspace(B, n_q, d_head) bytes.                        */
+int64_t stb_attn_decode_workspace(int B, int n_q, int d_head);
+int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                    const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, void* work, void* stream);
+
+/* ---- K2: append-prefill attention (n new queries against resident pages)
+ * Replaces prefill engine.py:251, verify engine.py:296 and ingest
+ * engine.py:358. Sequence s owns query rows [q_start[s], q_start[s+1]) of
+ * q/out bf16 [T][n_q][d_head]; its keys are the first ctx_lens[s] pages
+ * rows (the new tokens already committed); query i sits at absolute
+ * position ctx_lens[s] - n_s + i and attends causally.                    */
+int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                     const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,
+                     int max_q, void* stream);
+
+/* ---- K4: speculation validation (greedy LCP, bit-exact int32) -----------
+ * Replaces validate_draft (engine.py:96-111) + the consume rule (engine.py:291).
+ * For sequence s: draft ids [d_off[s], d_off[s+1]), model ids (what the
+ * verify pass sampled at each draft position) [m_off[s], m_off[s+1]),
+ * span_len[s]. accepted = LCP(draft, model) clamped to span_len;
+ * consume = span_len if accepted == span_len else accepted + 1;
+ * new_len[s] = kv_len[s] + accepted + base_extra[s] (KV rows that survive
+ * rollback). */
+int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t* model, const int32_t* m_off,
+                      const int32_t* span_len, const int32_t* kv_len, const int32_t* base_extra, int S,
+                      int32_t* accepted, int32_t* consume, int32_t* new_len, void* stream);
+
+/* ---- K5: bf16 tensor-core GEMM (tcgen05 + TMA + TMEM) --------------------
+ * C[M][N] (fp32, row stride ldc) = A[M][K] (bf16, lda) * W[N][K]^T (bf16, ldw).
+ * split_k > 1 accumulates with fp32 reductions into a zeroed C.            */
+int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
+                  int split_k, void* stream);
+
+/* ---- small fused ops (HBM-bound elementwise / row ops) ------------------ */
+/* x fp32 [n][d] <- table bf16 [ids[i]][d] */
+int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, void* stream);
+/* x += delta (if delta != NULL); y bf16 = rmsnorm(x) * w */
+int stb_add_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps, void* stream);
+/* y bf16 [n][f] = silu(gu[:, :f]) * gu[:, f:]  (gu fp32 [n][2f]) */
+int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream);
+/* rows[i] = x[idx[i]] as bf16 after rmsnorm: final norm fused with row gather */
+int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,
+                       void* stream);
+/* script-forced greedy sampling: out[r] = argmax(logits[r] + bias * onehot(target[r]))
+ * (target < 0: plain argmax); raw_argmax[r] / raw_max[r] = unbiased argmax / max */
+int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
+                      int32_t* raw_argmax, float* raw_max, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STB200_H */

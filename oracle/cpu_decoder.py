@@ -1,0 +1,107 @@
+"""ORACLE (test infrastructure). fp32 CPU restatement of the decoder the B200
+engine runs (the reference has none: its phases are virtual-time charges,
+engine.py:251,270,296,358). Same random-init weights (the product's bf16 draw,
+upcast to fp32), standard Llama math: RMSNorm, rotate-half RoPE (theta,
+fp32 inverse frequencies from a float64 pow, fp32 angle pos*inv_freq), GQA
+causal attention, SwiGLU MLP, untied LM head. Each sequence keeps a
+contiguous fp32 K/V cache; `forward` appends rows at `start` and returns the
+logits of the requested rows.
+"""
+
+from __future__ import annotations
+
+import math
+import zlib
+
+import numpy as np
+import torch
+
+
+def draw(shape, seed: int, name: str, norm: bool) -> torch.Tensor:
+    """Same generator rule as the product's weights.draw (cpu), upcast to fp32."""
+    g = torch.Generator(device="cpu")
+    g.manual_seed((seed * 1000003 + zlib.crc32(name.encode())) & 0x7FFFFFFFFFFFFFFF)
+    t = torch.randn(shape, generator=g, dtype=torch.float32)
+    t = 1.0 + 0.1 * t if norm else 0.02 * t
+    return t.to(torch.bfloat16).to(torch.float32)
+
+
+class CpuDecoder:
+    def __init__(self, shape, seed: int = 0, layers: int | None = None, threads: int | None = None):
+        self.s = shape
+        self.L = shape.layers if layers is None else layers
+        if threads:
+            torch.set_num_threads(threads)
+        d, V = shape.d_model, shape.vocab
+        qd, kvd = shape.n_q * shape.d_head, shape.n_kv * shape.d_head
+        self.embed = draw((V, d), seed, "embed", False)
+        self.layers = []
+        for i in range(self.L):
+            self.layers.append({
+                "an": draw((d,), seed, f"l{i}.attn_norm", True),
+                "qkv": draw((qd + 2 * kvd, d), seed, f"l{i}.wqkv", False),
+                "o": draw((d, qd), seed, f"l{i}.wo", False),
+                "mn": draw((d,), seed, f"l{i}.mlp_norm", True),
+                "gu": draw((2 * shape.d_ff, d), seed, f"l{i}.w_gate_up", False),
+                "dn": draw((d, shape.d_ff), seed, f"l{i}.w_down", False),
+            })
+        self.fn = draw((d,), seed, "final_norm", True)
+        self.head = draw((V, d), seed, "lm_head", False)
+        half = shape.d_head // 2
+        inv = np.array([1.0 / math.pow(shape.rope_theta, 2.0 * i / shape.d_head) for i in range(half)])
+        self.inv_freq = torch.tensor(inv.astype(np.float32))
+        self.cache: dict[str, list] = {}
+
+    def _norm(self, x, w):
+        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps) * w
+
+    def _rope(self, x, pos):
+        # x [T, H, D]; pos [T]
+        ang = pos.to(torch.float32)[:, None] * self.inv_freq[None, :]  # fp32 angle, as on the GPU
+        a64 = ang.to(torch.float64)
+        c, s = torch.cos(a64).to(torch.float32)[:, None, :], torch.sin(a64).to(torch.float32)[:, None, :]
+        h = x.shape[-1] // 2
+        x1, x2 = x[..., :h], x[..., h:]
+        return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
+
+    def truncate(self, rid: str, n: int) -> None:
+        if rid in self.cache:
+            self.cache[rid] = [(k[:n], v[:n]) for k, v in self.cache[rid]]
+
+    def drop(self, rid: str) -> None:
+        self.cache.pop(rid, None)
+
+    def forward(self, rid: str, ids: list[int], start: int, rows: list[int]) -> torch.Tensor:
+        s = self.s
+        T = len(ids)
+        H, G, D = s.n_q, s.n_kv, s.d_head
+        cache = self.cache.setdefault(rid, [(torch.zeros(0, G, D), torch.zeros(0, G, D)) for _ in range(self.L)])
+        pos = torch.arange(start, start + T)
+        x = self.embed[torch.tensor(ids, dtype=torch.long)]
+        for i, w in enumerate(self.layers):
+            h = self._norm(x, w["an"])
+            qkv = h @ w["qkv"].T
+            q = qkv[:, : H * D].view(T, H, D)
+            k = qkv[:, H * D: (H + G) * D].view(T, G, D)
+            v = qkv[:, (H + G) * D:].view(T, G, D)
+            q, k = self._rope(q, pos), self._rope(k, pos)
+            kc, vc = cache[i]
+            kc = torch.cat([kc[:start], k])
+            vc = torch.cat([vc[:start], v])
+            cache[i] = (kc, vc)
+            n = kc.shape[0]
+            rep = H // G
+            kk = kc.repeat_interleave(rep, dim=1)  # [n, H, D]
+            vv = vc.repeat_interleave(rep, dim=1)
+            scores = torch.einsum("thd,nhd->htn", q, kk) / math.sqrt(D)
+            mask = torch.arange(n)[None, :] > pos[:, None]
+            scores = scores.masked_fill(mask[None], float("-inf"))
+            p = torch.softmax(scores, dim=-1)
+            attn = torch.einsum("htn,nhd->thd", p, vv).reshape(T, H * D)
+            x = x + attn @ w["o"].T
+            h = self._norm(x, w["mn"])
+            gu = h @ w["gu"].T
+            g, u = gu[:, : s.d_ff], gu[:, s.d_ff:]
+            x = x + (torch.nn.functional.silu(g) * u) @ w["dn"].T
+        sel = x[torch.tensor(rows, dtype=torch.long)]
+        return self._norm(sel, self.fn) @ self.head.T

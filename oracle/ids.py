@@ -1,0 +1,49 @@
+"""ORACLE (test infrastructure). Token-id rules, restated independently of
+paper_2512_15834_b200/tokens.py: ids 0/1/2 = TOOL_START/TOOL_END/EOS, other
+tokens numbered in first-interned order; uncounted content (prompt / tool
+output) ids = 3 + splitmix64(seed, fnv1a64(rid), salt, position) mod (V - 3).
+"""
+
+from __future__ import annotations
+
+MASK = (1 << 64) - 1
+SALT_PROMPT, SALT_OUTPUT = 1, 2
+
+
+class Interner:
+    def __init__(self, vocab: int):
+        self.vocab = vocab
+        self.ids = {}
+
+    def __call__(self, tok) -> int:
+        kind = tok.kind.value
+        fixed = {"tool_start": 0, "tool_end": 1, "eos": 2}
+        if kind in fixed and tok.text == "":
+            return fixed[kind]
+        key = (kind, tok.text)
+        if key not in self.ids:
+            self.ids[key] = 3 + len(self.ids)
+            assert self.ids[key] < self.vocab, "vocabulary exhausted"
+        return self.ids[key]
+
+    def many(self, toks) -> list[int]:
+        return [self(t) for t in toks]
+
+
+def _fnv(text: str) -> int:
+    h = 0xCBF29CE484222325
+    for b in text.encode("utf-8"):
+        h = ((h ^ b) * 0x100000001B3) & MASK
+    return h
+
+
+def _mix(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & MASK
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & MASK
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & MASK
+    return x ^ (x >> 31)
+
+
+def fill(seed: int, rid: str, salt: int, start: int, n: int, vocab: int) -> list[int]:
+    base = _fnv(rid) ^ ((seed & 0xFFFFFFFF) << 32) ^ salt
+    return [3 + _mix(base ^ ((p * 0x2545F4914F6CDD1D) & MASK)) % (vocab - 3) for p in range(start, start + n)]

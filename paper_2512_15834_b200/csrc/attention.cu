@@ -1,0 +1,520 @@
+// K3 — paged decode attention (one query per resident sequence), split-K over the
+// context with a log-sum-exp merge; and the warp-tile append-prefill attention used
+// for short query runs (verify passes, small ingests).
+//
+// Replaces the reference's decode charges (`engine.py:270,276,302,317`) and, for
+// short runs, the validate/ingest charges (`engine.py:296,358`).
+//
+// HBM layout (include/stb200.h): per layer K and V pages [num_blocks][n_kv][16][D].
+// One (block, kv-head) page is 16 x D bf16 = 4 KiB contiguous (D=128), so a page
+// is fetched with 16-byte cp.async by one warp into a 128B-swizzled smem tile and
+// consumed by ldmatrix + mma.sync (m16n8k16). GQA packing: the G = n_q / n_kv
+// query heads that share a kv head are rows of one 16-row MMA tile, so each K/V
+// page is read from HBM exactly once per step for the whole group. Softmax is
+// online (exp2 domain) with quad shuffles; rows of one warp live in one quad.
+#include "../../include/stb200.h"
+#include "common.cuh"
+#include "pool.cuh"
+
+using namespace stb;
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// byte offset of 16B chunk `c` of row `r` in a swizzled [16][D] page tile
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return (uint32_t)(r * D * 2 + (((c & ~7) | ((c ^ r) & 7)) << 4));
+}
+
+// one warp copies a [16][D] K page and the matching V page into smem (swizzled)
+template <int D>
+__device__ __forceinline__ void load_page(uint32_t ks, uint32_t vs, const __nv_bfloat16* kp,
+                                          const __nv_bfloat16* vp, int lane) {
+  constexpr int CH = D / 8;            // 16B chunks per row
+  constexpr int PER = 16 * CH / 32;    // chunks per lane per tile
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    int idx = i * 32 + lane;
+    int r = idx / CH, c = idx % CH;
+    cp_async16(ks + swz<D>(r, c), kp + r * D + c * 8);
+    cp_async16(vs + swz<D>(r, c), vp + r * D + c * 8);
+  }
+}
+
+// Running softmax state of the 16 packed rows held by one warp (C-fragment layout:
+// this lane owns rows lane/4 and lane/4+8).
+template <int D>
+struct RowState {
+  float o[D / 8][4];
+  float m[2];
+  float l[2];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    m[0] = m[1] = -INFINITY;
+    l[0] = l[1] = 0.f;
+  }
+};
+
+// S = Q K^T over one 16-key page, mask, online-softmax update, O += P V.
+// qf: A fragments of the 16 x D query tile (pre-scaled by scale*log2e).
+// lim0/lim1: number of valid keys of this page for rows lane/4 and lane/4+8
+// (key k of the page is valid iff k < lim).
+template <int D>
+__device__ __forceinline__ void page_step(const uint32_t (*qf)[4], uint32_t ks, uint32_t vs, int lim0, int lim1,
+                                          RowState<D>& st, int lane) {
+  float s[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+    for (int c0 = 0; c0 < D / 8; c0 += 4) {
+      int r = nt * 8 + (lane & 7);
+      int c = c0 + (lane >> 3);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(ks + swz<D>(r, c), b0, b1, b2, b3);
+      mma_bf16_16816(s[nt], qf[c0 / 2], b0, b1);
+      mma_bf16_16816(s[nt], qf[c0 / 2 + 1], b2, b3);
+    }
+  }
+  // mask + row max (rows lane/4 -> s[*][0..1], lane/4+8 -> s[*][2..3])
+  const int kc = (lane & 3) * 2;
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      int k = nt * 8 + kc + j;
+      if (k >= lim0) s[nt][j] = -INFINITY;
+      if (k >= lim1) s[nt][2 + j] = -INFINITY;
+      mx0 = fmaxf(mx0, s[nt][j]);
+      mx1 = fmaxf(mx1, s[nt][2 + j]);
+    }
+  }
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  float mn0 = fmaxf(st.m[0], mx0), mn1 = fmaxf(st.m[1], mx1);
+  // fully masked rows keep a finite reference so exp2 never sees (-inf) - (-inf)
+  float ref0 = mn0 == -INFINITY ? 0.f : mn0, ref1 = mn1 == -INFINITY ? 0.f : mn1;
+  float a0 = exp2f(st.m[0] - ref0), a1 = exp2f(st.m[1] - ref1);
+  st.m[0] = mn0;
+  st.m[1] = mn1;
+  float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      s[nt][j] = exp2f(s[nt][j] - ref0);
+      s[nt][2 + j] = exp2f(s[nt][2 + j] - ref1);
+      rs0 += s[nt][j];
+      rs1 += s[nt][2 + j];
+    }
+  }
+  st.l[0] = st.l[0] * a0 + rs0;
+  st.l[1] = st.l[1] * a1 + rs1;
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    st.o[n][0] *= a0;
+    st.o[n][1] *= a0;
+    st.o[n][2] *= a1;
+    st.o[n][3] *= a1;
+  }
+  uint32_t pf[4];
+  pf[0] = pack_bf16(s[0][0], s[0][1]);
+  pf[1] = pack_bf16(s[0][2], s[0][3]);
+  pf[2] = pack_bf16(s[1][0], s[1][1]);
+  pf[3] = pack_bf16(s[1][2], s[1][3]);
+#pragma unroll
+  for (int d0 = 0; d0 < D / 8; d0 += 2) {
+    int m = lane >> 3;
+    int r = (m & 1) * 8 + (lane & 7);
+    int c = d0 + (m >> 1);
+    uint32_t b0, b1, b2, b3;
+    ldsm_x4_t(vs + swz<D>(r, c), b0, b1, b2, b3);
+    mma_bf16_16816(st.o[d0], pf, b0, b1);
+    mma_bf16_16816(st.o[d0 + 1], pf, b2, b3);
+  }
+}
+
+// Load a 16 x D query tile into A fragments; row r -> (src row pointer or null)
+template <int D>
+__device__ __forceinline__ void load_q(uint32_t (*qf)[4], const __nv_bfloat16* row_lo, const __nv_bfloat16* row_hi,
+                                       float qscale, int lane) {
+  const int kc = (lane & 3) * 2;
+#pragma unroll
+  for (int ks = 0; ks < D / 16; ++ks) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int col = ks * 16 + h * 8 + kc;
+      float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
+      if (row_lo) lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(row_lo + col));
+      if (row_hi) hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(row_hi + col));
+      qf[ks][h * 2 + 0] = pack_bf16(lo.x * qscale, lo.y * qscale);
+      qf[ks][h * 2 + 1] = pack_bf16(hi.x * qscale, hi.y * qscale);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3 decode
+// grid: (splits, n_kv, B); 4 warps; warp w walks pages start+w, start+w+4, ...
+template <int D, int G, int STAGES>
+__global__ void __launch_bounds__(128) attn_decode_kernel(
+    const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
+    const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
+    const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int n_kv, float qscale,
+    int pages_per_split, float* __restrict__ o_part, float* __restrict__ lse_part) {
+  constexpr int PAGE = 16 * D * 2;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, kh = blockIdx.y, b = blockIdx.z;
+  const int splits = gridDim.x;
+  const int n_q = n_kv * G;
+  const int ctx = ctx_lens[b];
+  const int npages = (ctx + 15) >> 4;
+  const int p0 = split * pages_per_split;
+  const int p1 = min(npages, p0 + pages_per_split);
+  const int32_t* row = table + (int64_t)slots[b] * max_bps;
+
+  uint32_t qf[D / 16][4];
+  {
+    int r0 = lane >> 2, r1 = r0 + 8;
+    const __nv_bfloat16* base = q + ((int64_t)b * n_q + kh * G) * D;
+    load_q<D>(qf, r0 < G ? base + r0 * D : nullptr, r1 < G ? base + r1 * D : nullptr, qscale, lane);
+  }
+  RowState<D> st;
+  st.init();
+
+  const uint32_t wbase = smem_u32(smem) + warp * STAGES * 2 * PAGE;
+  auto page_ptr = [&](int p, const __nv_bfloat16* pages) {
+    return pages + (((int64_t)row[p] * n_kv + kh) * 16) * D;
+  };
+  // per-warp software pipeline over this warp's pages
+  int mine = p1 > p0 + warp ? (p1 - p0 - warp + 3) / 4 : 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < mine) {
+      int p = p0 + warp + 4 * s;
+      load_page<D>(wbase + s * 2 * PAGE, wbase + s * 2 * PAGE + PAGE, page_ptr(p, kpages), page_ptr(p, vpages), lane);
+    }
+    cp_async_commit();
+  }
+  for (int i = 0; i < mine; ++i) {
+    cp_async_wait<STAGES - 2>();
+    __syncwarp();
+    int stage = i % STAGES;
+    int p = p0 + warp + 4 * i;
+    int lim = ctx - p * 16;
+    page_step<D>(qf, wbase + stage * 2 * PAGE, wbase + stage * 2 * PAGE + PAGE, lim, lim, st, lane);
+    __syncwarp();
+    int nx = i + STAGES - 1;
+    if (nx < mine) {
+      int pn = p0 + warp + 4 * nx;
+      int sn = nx % STAGES;
+      load_page<D>(wbase + sn * 2 * PAGE, wbase + sn * 2 * PAGE + PAGE, page_ptr(pn, kpages), page_ptr(pn, vpages),
+                   lane);
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  // quad-reduce row sums (lanes of a quad hold disjoint keys)
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    st.l[j] += __shfl_xor_sync(0xffffffffu, st.l[j], 1);
+    st.l[j] += __shfl_xor_sync(0xffffffffu, st.l[j], 2);
+  }
+  __syncthreads();
+  // merge the 4 warps: smem[w] = {m[16], l[16], o[16][D]}
+  float* red = reinterpret_cast<float*>(smem);
+  constexpr int WSTRIDE = 32 + 16 * D;
+  float* mine_red = red + warp * WSTRIDE;
+  if ((lane & 3) == 0) {
+    mine_red[lane >> 2] = st.m[0];
+    mine_red[(lane >> 2) + 8] = st.m[1];
+    mine_red[16 + (lane >> 2)] = st.l[0];
+    mine_red[16 + (lane >> 2) + 8] = st.l[1];
+  }
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    int r = lane >> 2, c = n * 8 + (lane & 3) * 2;
+    mine_red[32 + r * D + c] = st.o[n][0];
+    mine_red[32 + r * D + c + 1] = st.o[n][1];
+    mine_red[32 + (r + 8) * D + c] = st.o[n][2];
+    mine_red[32 + (r + 8) * D + c + 1] = st.o[n][3];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+    int r = e / D, d = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[w * WSTRIDE + r]);
+    float L = 0.f, acc = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        float wt = exp2f(red[w * WSTRIDE + r] - M);
+        L += wt * red[w * WSTRIDE + 16 + r];
+        acc += wt * red[w * WSTRIDE + 32 + r * D + d];
+      }
+    }
+    int h = kh * G + r;
+    if (splits == 1) {
+      out[((int64_t)b * n_q + h) * D + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+    } else {
+      int64_t idx = ((int64_t)b * n_q + h) * splits + split;
+      o_part[idx * D + d] = L > 0.f ? acc / L : 0.f;
+      if (d == 0) lse_part[idx] = L > 0.f ? M + log2f(L) : -INFINITY;
+    }
+  }
+}
+
+// merge split partials: one warp per (b, head)
+template <int D>
+__global__ void attn_merge_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
+                                  __nv_bfloat16* __restrict__ out, int rows, int splits) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float* lse = lse_part + (int64_t)warp * splits;
+  float M = -INFINITY;
+  for (int s = lane; s < splits; s += 32) M = fmaxf(M, lse[s]);
+  M = warp_max(M);
+  float acc[D / 32];
+#pragma unroll
+  for (int j = 0; j < D / 32; ++j) acc[j] = 0.f;
+  float L = 0.f;
+  if (M != -INFINITY) {
+    for (int s = 0; s < splits; ++s) {
+      float w = exp2f(lse[s] - M);
+      L += w;
+      const float* o = o_part + ((int64_t)warp * splits + s) * D;
+#pragma unroll
+      for (int j = 0; j < D / 32; ++j) acc[j] += w * o[j * 32 + lane];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < D / 32; ++j)
+    out[(int64_t)warp * D + j * 32 + lane] = __float2bfloat16_rn(L > 0.f ? acc[j] / L : 0.f);
+}
+
+// ---------------------------------------------------------- short-run prefill
+// grid: (q tiles, n_kv, S); 4 warps share each K/V page (CTA-wide cp.async), each
+// warp owns 16 packed rows = 16/G queries x G heads. Rows are (query i, head g)
+// with r = i*G + g. Causal: row's query at position qpos attends keys <= qpos.
+template <int D, int G, int STAGES>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(
+    const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
+    const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
+    const int32_t* __restrict__ slots, const int32_t* __restrict__ q_start, const int32_t* __restrict__ ctx_lens,
+    int n_kv, float qscale) {
+  constexpr int PAGE = 16 * D * 2;
+  constexpr int QPW = 16 / G;  // queries per warp tile
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.z, kh = blockIdx.y;
+  const int n_q = n_kv * G;
+  const int t0 = q_start[s], n = q_start[s + 1] - t0;
+  const int qbase = blockIdx.x * 4 * QPW;  // first query of this CTA
+  if (qbase >= n) return;
+  const int ctx = ctx_lens[s];
+  const int pos0 = ctx - n;  // absolute position of query 0
+  const int32_t* row = table + (int64_t)slots[s] * max_bps;
+
+  const int wq0 = qbase + warp * QPW;  // first query of this warp
+  uint32_t qf[D / 16][4];
+  int qi_lo = wq0 + (lane >> 2) / G, qi_hi = wq0 + ((lane >> 2) + 8) / G;
+  int g_lo = (lane >> 2) % G, g_hi = ((lane >> 2) + 8) % G;
+  {
+    const __nv_bfloat16* lo = qi_lo < n ? q + ((int64_t)(t0 + qi_lo) * n_q + kh * G + g_lo) * D : nullptr;
+    const __nv_bfloat16* hi = qi_hi < n ? q + ((int64_t)(t0 + qi_hi) * n_q + kh * G + g_hi) * D : nullptr;
+    load_q<D>(qf, lo, hi, qscale, lane);
+  }
+  RowState<D> st;
+  st.init();
+  // the CTA needs keys up to the last query it owns
+  const int last_q = min(n, qbase + 4 * QPW) - 1;
+  const int npages = (pos0 + last_q) / 16 + 1;
+  const int lim_lo_abs = qi_lo < n ? pos0 + qi_lo + 1 : 0;  // keys < lim are visible
+  const int lim_hi_abs = qi_hi < n ? pos0 + qi_hi + 1 : 0;
+  const int warp_last = min(n - 1, wq0 + QPW - 1);
+  const int warp_pages = wq0 < n ? (pos0 + warp_last) / 16 + 1 : 0;
+
+  const uint32_t base = smem_u32(smem);
+  auto issue = [&](int p, int stage) {
+    // 128 threads copy one K page and one V page
+    constexpr int CH = D / 8;
+    const __nv_bfloat16* kp = kpages + (((int64_t)row[p] * n_kv + kh) * 16) * D;
+    const __nv_bfloat16* vp = vpages + (((int64_t)row[p] * n_kv + kh) * 16) * D;
+    uint32_t ks = base + stage * 2 * PAGE, vs = ks + PAGE;
+    for (int idx = threadIdx.x; idx < 16 * CH; idx += 128) {
+      int r = idx / CH, c = idx % CH;
+      cp_async16(ks + swz<D>(r, c), kp + r * D + c * 8);
+      cp_async16(vs + swz<D>(r, c), vp + r * D + c * 8);
+    }
+  };
+#pragma unroll
+  for (int st_i = 0; st_i < STAGES - 1; ++st_i) {
+    if (st_i < npages) issue(st_i, st_i);
+    cp_async_commit();
+  }
+  for (int p = 0; p < npages; ++p) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    int stage = p % STAGES;
+    if (p < warp_pages) {
+      int lo = lim_lo_abs - p * 16, hi = lim_hi_abs - p * 16;
+      page_step<D>(qf, base + stage * 2 * PAGE, base + stage * 2 * PAGE + PAGE, lo, hi, st, lane);
+    }
+    __syncthreads();
+    int nx = p + STAGES - 1;
+    if (nx < npages) issue(nx, nx % STAGES);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    st.l[j] += __shfl_xor_sync(0xffffffffu, st.l[j], 1);
+    st.l[j] += __shfl_xor_sync(0xffffffffu, st.l[j], 2);
+  }
+  float inv0 = st.l[0] > 0.f ? 1.f / st.l[0] : 0.f, inv1 = st.l[1] > 0.f ? 1.f / st.l[1] : 0.f;
+#pragma unroll
+  for (int nd = 0; nd < D / 8; ++nd) {
+    int c = nd * 8 + (lane & 3) * 2;
+    if (qi_lo < n) {
+      __nv_bfloat16* o = out + ((int64_t)(t0 + qi_lo) * n_q + kh * G + g_lo) * D + c;
+      *reinterpret_cast<uint32_t*>(o) = pack_bf16(st.o[nd][0] * inv0, st.o[nd][1] * inv0);
+    }
+    if (qi_hi < n) {
+      __nv_bfloat16* o = out + ((int64_t)(t0 + qi_hi) * n_q + kh * G + g_hi) * D + c;
+      *reinterpret_cast<uint32_t*>(o) = pack_bf16(st.o[nd][2] * inv1, st.o[nd][3] * inv1);
+    }
+  }
+}
+
+constexpr int kDecodeStages = 3;
+constexpr int kPrefillStages = 3;
+
+template <int D, int G>
+int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
+                  const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
+                  float qscale, int max_ctx, float* work, cudaStream_t st) {
+  int max_pages = (max_ctx + 15) / 16;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // aim for ~3 CTAs per SM in flight; at least 8 pages per split so the merge stays cheap
+  int pairs = B * n_kv;
+  int splits = (3 * sms + pairs - 1) / pairs;
+  int max_splits = (max_pages + 7) / 8;
+  if (splits > max_splits) splits = max_splits;
+  if (splits > 64) splits = 64;
+  if (splits < 1) splits = 1;
+  int pps = (max_pages + splits - 1) / splits;
+  splits = (max_pages + pps - 1) / pps;
+  if (splits < 1) splits = 1;
+  size_t smem = (size_t)4 * kDecodeStages * 2 * 16 * D * 2;
+  size_t red = (size_t)4 * (32 + 16 * D) * 4;
+  if (red > smem) smem = red;
+  auto kern = attn_decode_kernel<D, G, kDecodeStages>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  float* o_part = work;
+  float* lse_part = work + (size_t)B * n_kv * G * 64 * D;
+  kern<<<dim3(splits, n_kv, B), 128, smem, st>>>(q, out, kp, vp, table, max_bps, slots, ctx, n_kv, qscale, pps, o_part,
+                                                 lse_part);
+  count_launch();
+  if (splits > 1) {
+    int rows = B * n_kv * G;
+    attn_merge_kernel<D><<<(rows * 32 + 255) / 256, 256, 0, st>>>(o_part, lse_part, out, rows, splits);
+    count_launch();
+  }
+  STB_CHECK_LAUNCH("attn_decode");
+  return STB_OK;
+}
+
+template <int D, int G>
+int launch_prefill(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
+                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* q_start, const int32_t* ctx,
+                   int S, int n_kv, float qscale, int max_q, cudaStream_t st) {
+  constexpr int QPC = 4 * (16 / G);  // queries per CTA
+  size_t smem = (size_t)kPrefillStages * 2 * 16 * D * 2;
+  auto kern = attn_prefill_kernel<D, G, kPrefillStages>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((max_q + QPC - 1) / QPC, n_kv, S);
+  kern<<<grid, 128, smem, st>>>(q, out, kp, vp, table, max_bps, slots, q_start, ctx, n_kv, qscale);
+  count_launch();
+  STB_CHECK_LAUNCH("attn_prefill");
+  return STB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t stb_attn_decode_workspace(int B, int n_q, int d_head) {
+  // o_part [B][n_q][64 splits][D] + lse [B][n_q][64]
+  return (int64_t)B * n_q * 64 * (d_head + 1) * 4;
+}
+
+int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                    const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, void* work, void* stream) {
+  void *kp, *vp;
+  if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
+  int32_t* table;
+  int max_bps;
+  stb_kv_block_table(pool, &table, &max_bps);
+  if (B <= 0) return STB_OK;
+  if (max_ctx <= 0) return fail(STB_EINVAL, "attn_decode: max_ctx must be positive");
+  int n_kv, d_head;
+  stb_pool_geometry(pool, &n_kv, &d_head);
+  if (n_q % n_kv) return fail(STB_EINVAL, "attn_decode: n_q %% n_kv != 0");
+  int g = n_q / n_kv;
+  float qs = scale * kLog2e;
+  auto* qq = (const __nv_bfloat16*)q;
+  auto* oo = (__nv_bfloat16*)out;
+  auto* kk = (const __nv_bfloat16*)kp;
+  auto* vv = (const __nv_bfloat16*)vp;
+  cudaStream_t st = (cudaStream_t)stream;
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, max_ctx, (float*)work, st
+  if (d_head == 128 && g == 4) return launch_decode<128, 4>(ARGS);
+  if (d_head == 128 && g == 8) return launch_decode<128, 8>(ARGS);
+  if (d_head == 128 && g == 1) return launch_decode<128, 1>(ARGS);
+  if (d_head == 64 && g == 2) return launch_decode<64, 2>(ARGS);
+  if (d_head == 64 && g == 8) return launch_decode<64, 8>(ARGS);
+  if (d_head == 64 && g == 4) return launch_decode<64, 4>(ARGS);
+#undef ARGS
+  return fail(STB_EINVAL, "attn_decode: unsupported (d_head=%d, group=%d)", d_head, g);
+}
+
+int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                     const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale, int max_q,
+                     void* stream) {
+  void *kp, *vp;
+  if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
+  int32_t* table;
+  int max_bps;
+  stb_kv_block_table(pool, &table, &max_bps);
+  if (S <= 0 || T <= 0) return STB_OK;
+  int n_kv, d_head;
+  stb_pool_geometry(pool, &n_kv, &d_head);
+  if (n_q % n_kv) return fail(STB_EINVAL, "attn_prefill: n_q %% n_kv != 0");
+  int g = n_q / n_kv;
+  float qs = scale * kLog2e;
+  auto* qq = (const __nv_bfloat16*)q;
+  auto* oo = (__nv_bfloat16*)out;
+  auto* kk = (const __nv_bfloat16*)kp;
+  auto* vv = (const __nv_bfloat16*)vp;
+  cudaStream_t st = (cudaStream_t)stream;
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, q_start, ctx_lens, S, n_kv, qs, max_q, st
+  if (d_head == 128 && g == 4) return launch_prefill<128, 4>(ARGS);
+  if (d_head == 128 && g == 8) return launch_prefill<128, 8>(ARGS);
+  if (d_head == 128 && g == 1) return launch_prefill<128, 1>(ARGS);
+  if (d_head == 64 && g == 2) return launch_prefill<64, 2>(ARGS);
+  if (d_head == 64 && g == 8) return launch_prefill<64, 8>(ARGS);
+  if (d_head == 64 && g == 4) return launch_prefill<64, 4>(ARGS);
+#undef ARGS
+  return fail(STB_EINVAL, "attn_prefill: unsupported (d_head=%d, group=%d)", d_head, g);
+}
+
+}  // extern "C"

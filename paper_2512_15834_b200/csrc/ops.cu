@@ -1,0 +1,265 @@
+// Small fused row ops around the GEMMs (HBM-bound, one pass each) and K4, the
+// speculation-validation kernel.
+//
+// K4 replaces `validate_draft` (`engine.py:96-111`) and the consume rule
+// (`engine.py:291`): greedy longest-common-prefix of the drafted call ids against
+// the ids the verify pass produced at the same positions, as int32 compares —
+// bit-exact by construction. One warp per sequence: ballot of mismatches, ffs.
+#include <cfloat>
+
+#include "../../include/stb200.h"
+#include "common.cuh"
+
+using namespace stb;
+
+namespace {
+
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
+                             float* __restrict__ x, int n, int d) {
+  int t = blockIdx.x;
+  const __nv_bfloat16* row = table + (int64_t)ids[t] * d;
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    uint4 v = *reinterpret_cast<const uint4*>(row + c);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float4 a, b;
+    float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+    float2 f2 = __bfloat1622float2(h[2]), f3 = __bfloat1622float2(h[3]);
+    a = make_float4(f0.x, f0.y, f1.x, f1.y);
+    b = make_float4(f2.x, f2.y, f3.x, f3.y);
+    *reinterpret_cast<float4*>(x + (int64_t)t * d + c) = a;
+    *reinterpret_cast<float4*>(x + (int64_t)t * d + c + 4) = b;
+  }
+}
+
+// block-wide sum with warp shuffles + one smem hop
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = (l < (int)(blockDim.x >> 5)) ? red[l] : 0.f;
+  t = warp_sum(t);
+  __syncthreads();
+  return t;
+}
+
+// one CTA per row: x (+)= delta; y = bf16(x * rsqrt(mean(x^2) + eps) * w)
+__global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
+                                   const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int d,
+                                   float eps, const int32_t* __restrict__ gather) {
+  __shared__ float red[32];
+  int t = blockIdx.x;
+  int src = gather ? gather[t] : t;
+  float* xr = x + (int64_t)src * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(xr + c);
+    if (delta) {
+      float4 e = *reinterpret_cast<const float4*>(delta + (int64_t)t * d + c);
+      v.x += e.x;
+      v.y += e.y;
+      v.z += e.z;
+      v.w += e.w;
+      *reinterpret_cast<float4*>(xr + c) = v;
+    }
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (!y) return;  // residual add only
+  float inv = rsqrtf(block_sum(ss, red) / d + eps);
+  __nv_bfloat16* yr = y + (int64_t)t * d;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(xr + c);
+    float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c));
+    float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c + 2));
+    uint2 o = make_uint2(pack_bf16(v.x * inv * w01.x, v.y * inv * w01.y), pack_bf16(v.z * inv * w23.x, v.w * inv * w23.y));
+    *reinterpret_cast<uint2*>(yr + c) = o;
+  }
+}
+
+__global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f) {
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  int64_t total = (int64_t)n * f;
+  if (i >= total) return;
+  int64_t t = i / f, c = i % f;
+  const float* row = gu + t * 2 * f;
+  float4 g = *reinterpret_cast<const float4*>(row + c);
+  float4 u = *reinterpret_cast<const float4*>(row + f + c);
+  auto silu = [](float a) { return a / (1.f + __expf(-a)); };
+  uint2 o = make_uint2(pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y), pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w));
+  *reinterpret_cast<uint2*>(y + i) = o;
+}
+
+// one CTA per sampled row: biased argmax over the vocabulary (first index wins ties)
+__global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ target,
+                                     int V, float bias, int32_t* __restrict__ out, int32_t* __restrict__ raw_arg,
+                                     float* __restrict__ raw_max) {
+  __shared__ float sv[32], sb[32];
+  __shared__ int si[32], sbi[32];
+  int r = blockIdx.x;
+  const float* row = logits + (int64_t)r * ld;
+  int tgt = target ? target[r] : -1;
+  float best = -FLT_MAX, bbest = -FLT_MAX;
+  int bi = 0x7fffffff, bbi = 0x7fffffff;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    float v = row[c];
+    if (v > best || (v == best && c < bi)) {
+      best = v;
+      bi = c;
+    }
+    float b = (c == tgt) ? v + bias : v;
+    if (b > bbest || (b == bbest && c < bbi)) {
+      bbest = b;
+      bbi = c;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+    float ob = __shfl_xor_sync(0xffffffffu, bbest, o);
+    int obi = __shfl_xor_sync(0xffffffffu, bbi, o);
+    if (ob > bbest || (ob == bbest && obi < bbi)) {
+      bbest = ob;
+      bbi = obi;
+    }
+  }
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sv[w] = best;
+    si[w] = bi;
+    sb[w] = bbest;
+    sbi[w] = bbi;
+  }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    best = l < nw ? sv[l] : -FLT_MAX;
+    bi = l < nw ? si[l] : 0x7fffffff;
+    bbest = l < nw ? sb[l] : -FLT_MAX;
+    bbi = l < nw ? sbi[l] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+      float ob = __shfl_xor_sync(0xffffffffu, bbest, o);
+      int obi = __shfl_xor_sync(0xffffffffu, bbi, o);
+      if (ob > bbest || (ob == bbest && obi < bbi)) {
+        bbest = ob;
+        bbi = obi;
+      }
+    }
+    if (l == 0) {
+      out[r] = bbi;
+      if (raw_arg) raw_arg[r] = bi;
+      if (raw_max) raw_max[r] = best;
+    }
+  }
+}
+
+// K4: one warp per sequence
+__global__ void spec_validate_kernel(const int32_t* __restrict__ draft, const int32_t* __restrict__ d_off,
+                                     const int32_t* __restrict__ model, const int32_t* __restrict__ m_off,
+                                     const int32_t* __restrict__ span_len, const int32_t* __restrict__ kv_len,
+                                     const int32_t* __restrict__ base_extra, int S, int32_t* __restrict__ accepted,
+                                     int32_t* __restrict__ consume, int32_t* __restrict__ new_len) {
+  int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  int dl = d_off[s + 1] - d_off[s];
+  int ml = m_off[s + 1] - m_off[s];
+  int sl = span_len[s];
+  int n = min(min(dl, ml), sl);
+  const int32_t* d = draft + d_off[s];
+  const int32_t* m = model + m_off[s];
+  int acc = n;
+  for (int base = 0; base < n; base += 32) {
+    int i = base + lane;
+    bool miss = i < n && d[i] != m[i];
+    unsigned bal = __ballot_sync(0xffffffffu, miss);
+    if (bal) {
+      acc = base + __ffs(bal) - 1;
+      break;
+    }
+  }
+  if (lane == 0) {
+    accepted[s] = acc;
+    consume[s] = acc >= sl ? sl : acc + 1;
+    if (new_len) new_len[s] = kv_len[s] + acc + (base_extra ? base_extra[s] : 0);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, void* stream) {
+  if (n <= 0) return STB_OK;
+  if (d % 8) return fail(STB_EINVAL, "embed: d must be a multiple of 8");
+  embed_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(ids, (const __nv_bfloat16*)table, x, n, d);
+  count_launch();
+  STB_CHECK_LAUNCH("embed");
+  return STB_OK;
+}
+
+int stb_add_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps, void* stream) {
+  if (n <= 0) return STB_OK;
+  if (d % 4) return fail(STB_EINVAL, "add_rmsnorm: d must be a multiple of 4");
+  add_rmsnorm_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(x, delta, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, d, eps,
+                                                          nullptr);
+  count_launch();
+  STB_CHECK_LAUNCH("add_rmsnorm");
+  return STB_OK;
+}
+
+int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,
+                       void* stream) {
+  if (n <= 0) return STB_OK;
+  if (d % 4) return fail(STB_EINVAL, "gather_rmsnorm: d must be a multiple of 4");
+  add_rmsnorm_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(const_cast<float*>(x), nullptr, (const __nv_bfloat16*)w,
+                                                          (__nv_bfloat16*)y, d, eps, idx);
+  count_launch();
+  STB_CHECK_LAUNCH("gather_rmsnorm");
+  return STB_OK;
+}
+
+int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream) {
+  if (n <= 0) return STB_OK;
+  if (f % 4) return fail(STB_EINVAL, "silu_mul: f must be a multiple of 4");
+  int64_t total = (int64_t)n * f / 4;
+  silu_mul_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(gu, (__nv_bfloat16*)y, n, f);
+  count_launch();
+  STB_CHECK_LAUNCH("silu_mul");
+  return STB_OK;
+}
+
+int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
+                      int32_t* raw_argmax, float* raw_max, void* stream) {
+  if (R <= 0) return STB_OK;
+  sample_forced_kernel<<<R, 512, 0, (cudaStream_t)stream>>>(logits, ld, target, V, bias, out, raw_argmax, raw_max);
+  count_launch();
+  STB_CHECK_LAUNCH("sample_forced");
+  return STB_OK;
+}
+
+int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t* model, const int32_t* m_off,
+                      const int32_t* span_len, const int32_t* kv_len, const int32_t* base_extra, int S,
+                      int32_t* accepted, int32_t* consume, int32_t* new_len, void* stream) {
+  if (S <= 0) return STB_OK;
+  int threads = 128;
+  int blocks = (S * 32 + threads - 1) / threads;
+  spec_validate_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(draft, d_off, model, m_off, span_len, kv_len,
+                                                                     base_extra, S, accepted, consume, new_len);
+  count_launch();
+  STB_CHECK_LAUNCH("spec_validate");
+  return STB_OK;
+}
+
+}  // extern "C"

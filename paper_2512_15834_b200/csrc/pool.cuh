@@ -1,0 +1,29 @@
+// Internal definition of the paged KV pool handle (opaque in include/stb200.h).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+struct stb_kv_pool {
+  int device, layers, n_kv, d_head, bs, num_blocks, max_slots, max_bps;
+  __nv_bfloat16* pages = nullptr;   // [layers][2][num_blocks][n_kv][bs][d_head]
+  int64_t block_elems = 0;          // n_kv * bs * d_head
+  int64_t half_elems = 0;           // num_blocks * block_elems (K -> V)
+  std::vector<int32_t> free_list;   // stack: back() is the next block handed out
+  std::vector<std::vector<int32_t>> blocks;
+  std::vector<int> len;             // reserved logical length per slot
+  std::vector<int32_t> table;       // host mirror [max_slots][max_bps]
+  int32_t* dev_table = nullptr;
+  // pending device-table updates: (flat index, value) pairs, double-buffered staging
+  std::vector<int32_t> updates;
+  int32_t* staging[2] = {nullptr, nullptr};
+  int32_t* dev_updates[2] = {nullptr, nullptr};
+  int64_t cap[2] = {0, 0};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int flip = 0;
+};
+
+
+extern "C" int stb_pool_geometry(const stb_kv_pool* p, int* n_kv, int* d_head);

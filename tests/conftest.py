@@ -1,0 +1,19 @@
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libstb200.so")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+
+    return json.loads((ROOT / "tests" / "golden" / "reference_control_plane.json").read_text())
