@@ -1,0 +1,296 @@
+"""Kernel-level numerics on the B200, each kernel called through the C ABI and
+compared with a plain PyTorch fp32 restatement of the same op (or, for the
+integer kernels, bit-exactly with the oracle)."""
+
+import ctypes as C
+import math
+import random
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2512_15834_b200.modelcfg import ModelShape  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_15834_b200.runtime import lib as L
+
+    L.load()
+    return L
+
+
+def P(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def rel(a, b):
+    return float((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-12))
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 256), (7, 384, 512), (32, 6144, 4096), (32, 4096, 14336),
+                                   (100, 1000, 256), (300, 640, 1024), (2048, 1024, 4096), (17, 128256, 256)])
+def test_gemm_bf16(lib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (0.05 * torch.randn(N, K, device="cuda", generator=g)).to(torch.bfloat16)
+    c = torch.full((M, N), float("nan"), device="cuda")
+    lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, 0, stream())
+    ref = a.float() @ w.float().T
+    torch.cuda.synchronize()
+    assert rel(c, ref) < 2e-5
+
+
+def test_gemm_explicit_split(lib):
+    M, N, K = 32, 512, 4096
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    ref = a.float() @ w.float().T
+    for split in (1, 2, 5, 64):
+        c = torch.full((M, N), float("nan"), device="cuda")
+        lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, split, stream())
+        assert rel(c, ref) < 2e-5, split
+
+
+def _pool(lib, shape, nb=256, slots=64, bps=512):
+    from paper_2512_15834_b200.runtime.decoder import KVPool
+
+    return KVPool(shape, nb, slots, bps)
+
+
+def test_allocator_matches_oracle(lib):
+    from oracle.kv_alloc import LifoAllocator
+
+    shape = ModelShape("t", 1, 64, 1, 1, 64, 64, 64)
+    pool = _pool(lib, shape, nb=200, slots=8, bps=64)
+    ref = LifoAllocator(200)
+    rng = random.Random(3)
+    for _ in range(2000):
+        slot = rng.randrange(8)
+        op = rng.choice(["res", "res", "trunc", "rel"])
+        n = rng.randrange(0, 300)
+        if op == "res":
+            need = -(-n // 16) - len(ref.blocks(slot))
+            if need > len(ref.free):
+                continue
+            pool.reserve(slot, n)
+            ref.reserve(slot, n)
+        elif op == "trunc":
+            pool.truncate(slot, n)
+            ref.truncate(slot, n)
+        else:
+            pool.release(slot)
+            ref.release(slot)
+        assert pool.blocks(slot) == ref.blocks(slot)
+    assert pool.free_blocks() == len(ref.free)
+
+
+def _dense_kv(pool, layer, slot, n, shape):
+    """Gather a slot's first n rows from the pool via the block table (torch)."""
+    kp, vp = pool.layer_ptrs(layer)
+    nb = pool.num_blocks
+    per = nb * shape.n_kv * 16 * shape.d_head
+    import numpy as np
+
+    kbuf = torch.empty(per, dtype=torch.bfloat16, device="cuda")
+    vbuf = torch.empty(per, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    cudart = torch.cuda.cudart()
+    cudart.cudaMemcpy(kbuf.data_ptr(), kp, per * 2, 3)
+    cudart.cudaMemcpy(vbuf.data_ptr(), vp, per * 2, 3)
+    k = kbuf.view(nb, shape.n_kv, 16, shape.d_head)
+    v = vbuf.view(nb, shape.n_kv, 16, shape.d_head)
+    blocks = torch.tensor(pool.blocks(slot), device="cuda", dtype=torch.long)
+    kd = k[blocks].permute(0, 2, 1, 3).reshape(-1, shape.n_kv, shape.d_head)[:n]
+    vd = v[blocks].permute(0, 2, 1, 3).reshape(-1, shape.n_kv, shape.d_head)[:n]
+    del np
+    return kd, vd
+
+
+def _fill_pool(lib, pool, shape, ctxs, seed=0):
+    """Commit random K/V rows for slots 0..len(ctxs)-1 with stb_kv_commit; returns dense copies."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dense = []
+    for s, n in enumerate(ctxs):
+        pool.reserve(s, n)
+    pool.sync(torch.cuda.current_stream().cuda_stream)
+    for s, n in enumerate(ctxs):
+        k = torch.randn(n, shape.kv_dim, device="cuda", generator=g).to(torch.bfloat16)
+        v = torch.randn(n, shape.kv_dim, device="cuda", generator=g).to(torch.bfloat16)
+        slot_of = torch.full((n,), s, dtype=torch.int32, device="cuda")
+        pos = torch.arange(n, dtype=torch.int32, device="cuda")
+        for layer in range(shape.layers):
+            lib.call("stb_kv_commit", pool.h, layer, P(k), P(v), shape.kv_dim, P(slot_of), P(pos), n, stream())
+        dense.append((k.view(n, shape.n_kv, shape.d_head), v.view(n, shape.n_kv, shape.d_head)))
+    return dense
+
+
+def test_kv_commit_roundtrip(lib):
+    shape = ModelShape("t", 2, 256, 4, 2, 64, 64, 64)
+    pool = _pool(lib, shape)
+    dense = _fill_pool(lib, pool, shape, [1, 15, 16, 17, 100])
+    for s, (k, v) in enumerate(dense):
+        for layer in range(2):
+            kd, vd = _dense_kv(pool, layer, s, k.shape[0], shape)
+            assert torch.equal(kd, k) and torch.equal(vd, v)
+
+
+def _ref_attn(q, k, v, qpos, scale):
+    # q [n, H, D] fp32, k/v [ctx, G, D]; causal: key j visible iff j <= qpos[i]
+    H, G = q.shape[1], k.shape[1]
+    kk = k.float().repeat_interleave(H // G, dim=1)
+    vv = v.float().repeat_interleave(H // G, dim=1)
+    s = torch.einsum("nhd,chd->hnc", q.float(), kk) * scale
+    mask = torch.arange(k.shape[0], device=q.device)[None, :] > qpos[:, None]
+    s = s.masked_fill(mask[None], float("-inf"))
+    return torch.einsum("hnc,chd->nhd", torch.softmax(s, -1), vv)
+
+
+SHAPES = [ModelShape("llama-ish", 1, 4096, 32, 8, 128, 64, 64), ModelShape("tiny", 1, 256, 4, 2, 64, 64, 64),
+          ModelShape("qwen-ish", 1, 5120, 64, 8, 128, 64, 64)]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
+@pytest.mark.parametrize("ctxs", [[1], [5, 16, 17, 33], [4096] * 4 + [100, 2500], [700] * 32])
+def test_attn_decode(lib, shape, ctxs):
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(ctxs), bps=512)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=len(ctxs))
+    B = len(ctxs)
+    q = torch.randn(B, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    slots = torch.arange(B, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.d_head) // 4, device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, max(ctxs), P(ws),
+             stream())
+    for b, (k, v) in enumerate(dense):
+        ref = _ref_attn(q[b:b + 1], k, v, torch.tensor([ctxs[b] - 1], device="cuda"), scale)
+        assert rel(out[b:b + 1], ref) < 1e-2, b
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
+@pytest.mark.parametrize("runs", [[(1, 1)], [(4, 10), (21, 33)], [(300, 300), (33, 1200), (7, 8)]])
+def test_attn_prefill(lib, shape, runs):
+    # runs: (n new queries, ctx incl. them)
+    ctxs = [c for _, c in runs]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(runs), bps=512)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=7)
+    T = sum(n for n, _ in runs)
+    q = torch.randn(T, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out = torch.full_like(q, float("nan"))
+    qs = [0]
+    for n, _ in runs:
+        qs.append(qs[-1] + n)
+    slots = torch.arange(len(runs), dtype=torch.int32, device="cuda")
+    qstart = torch.tensor(qs, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    lib.call("stb_attn_prefill", pool.h, 0, P(q), P(out), P(slots), P(qstart), P(ctx), len(runs), T, shape.n_q,
+             scale, max(n for n, _ in runs), stream())
+    for s, ((n, c), (k, v)) in enumerate(zip(runs, dense)):
+        qpos = torch.arange(c - n, c, device="cuda")
+        ref = _ref_attn(q[qs[s]:qs[s + 1]], k, v, qpos, scale)
+        assert rel(out[qs[s]:qs[s + 1]], ref) < 1e-2, s
+
+
+def test_rope_commit(lib):
+    shape = ModelShape("t", 1, 512, 8, 2, 64, 64, 64, rope_theta=10000.0)
+    pool = _pool(lib, shape)
+    n = 37
+    pool.reserve(0, 200)
+    pool.sync(torch.cuda.current_stream().cuda_stream)
+    qkv = torch.randn(n, (shape.n_q + 2 * shape.n_kv) * shape.d_head, device="cuda")
+    pos = torch.arange(150, 150 + n, dtype=torch.int32, device="cuda")
+    slot_of = torch.zeros(n, dtype=torch.int32, device="cuda")
+    q = torch.empty(n, shape.q_dim, dtype=torch.bfloat16, device="cuda")
+    lib.call("stb_qkv_rope_commit", pool.h, 0, P(qkv), P(q), P(slot_of), P(pos), n, shape.n_q, shape.rope_theta,
+             stream())
+    from oracle.cpu_decoder import CpuDecoder
+
+    dec = CpuDecoder.__new__(CpuDecoder)
+    dec.inv_freq = torch.tensor([1.0 / math.pow(shape.rope_theta, 2.0 * i / shape.d_head)
+                                 for i in range(shape.d_head // 2)], dtype=torch.float32)
+    x = qkv.cpu().view(n, -1, shape.d_head)
+    rq = dec._rope(x[:, :shape.n_q], pos.cpu())
+    rk = dec._rope(x[:, shape.n_q:shape.n_q + shape.n_kv], pos.cpu())
+    assert rel(q.view(n, shape.n_q, -1).cpu(), rq) < 5e-3
+    kd, vd = _dense_kv(pool, 0, 0, 150 + n, shape)
+    assert rel(kd[150:].cpu(), rk) < 5e-3
+    assert rel(vd[150:].cpu(), x[:, shape.n_q + shape.n_kv:]) < 5e-3
+
+
+def test_small_ops(lib):
+    n, d, f, V = 13, 512, 256, 1000
+    ids = torch.randint(0, V, (n,), dtype=torch.int32, device="cuda")
+    table = torch.randn(V, d, device="cuda").to(torch.bfloat16)
+    x = torch.empty(n, d, device="cuda")
+    lib.call("stb_embed", P(ids), P(table), P(x), n, d, stream())
+    assert torch.equal(x, table[ids.long()].float())
+    delta = torch.randn(n, d, device="cuda")
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).to(torch.bfloat16)
+    y = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+    x0 = x.clone()
+    lib.call("stb_add_rmsnorm", P(x), P(delta), P(w), P(y), n, d, 1e-5, stream())
+    xr = x0 + delta
+    ref = xr * torch.rsqrt((xr * xr).mean(-1, keepdim=True) + 1e-5) * w.float()
+    assert torch.allclose(x, xr) and rel(y, ref) < 5e-3
+    gu = torch.randn(n, 2 * f, device="cuda")
+    a = torch.empty(n, f, dtype=torch.bfloat16, device="cuda")
+    lib.call("stb_silu_mul", P(gu), P(a), n, f, stream())
+    assert rel(a, torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]) < 5e-3
+    idx = torch.tensor([3, 0, 12], dtype=torch.int32, device="cuda")
+    rows = torch.empty(3, d, dtype=torch.bfloat16, device="cuda")
+    lib.call("stb_gather_rmsnorm", P(x), P(idx), P(w), P(rows), 3, d, 1e-5, stream())
+    assert rel(rows, ref[idx.long()]) < 5e-3
+
+
+def test_sample_forced(lib):
+    R, V = 9, 128256
+    logits = torch.randn(R, V, device="cuda")
+    target = torch.tensor([5, -1, 77, 128255, 0, -1, 3, 9, 1000], dtype=torch.int32, device="cuda")
+    out = torch.empty(R, dtype=torch.int32, device="cuda")
+    raw = torch.empty(R, dtype=torch.int32, device="cuda")
+    mx = torch.empty(R, device="cuda")
+    lib.call("stb_sample_forced", P(logits), V, P(target), R, V, 1e4, P(out), P(raw), P(mx), stream())
+    am = logits.argmax(-1).int()
+    want = torch.where(target >= 0, target, am)
+    assert torch.equal(out, want) and torch.equal(raw, am)
+    assert torch.equal(mx, logits.max(-1).values)
+
+
+def test_spec_validate(lib):
+    rng = random.Random(0)
+    S = 40
+    drafts, models, spans, d_off, m_off = [], [], [], [0], [0]
+    for _ in range(S):
+        L = rng.randrange(0, 70)
+        dr = [rng.randrange(5) for _ in range(L)]
+        mo = list(dr)
+        if L and rng.random() < 0.7:
+            mo[rng.randrange(L)] += 1
+        mo += [rng.randrange(5) for _ in range(rng.randrange(0, 3))]
+        drafts += dr
+        models += mo
+        spans.append(rng.randrange(1, 80))
+        d_off.append(len(drafts))
+        m_off.append(len(models))
+    t = lambda v: torch.tensor(v if v else [0], dtype=torch.int32, device="cuda")  # noqa: E731
+    acc, con, nl = (torch.empty(S, dtype=torch.int32, device="cuda") for _ in range(3))
+    kv = t([100 * i for i in range(S)])
+    extra = t([i % 2 for i in range(S)])
+    lib.call("stb_spec_validate", P(t(drafts)), P(t(d_off)), P(t(models)), P(t(m_off)), P(t(spans)), P(kv),
+             P(extra), S, P(acc), P(con), P(nl), stream())
+    for s in range(S):
+        dr, mo = drafts[d_off[s]:d_off[s + 1]], models[m_off[s]:m_off[s + 1]]
+        n = min(len(dr), len(mo), spans[s])
+        a = next((i for i in range(n) if dr[i] != mo[i]), n)
+        assert acc[s].item() == a
+        assert con[s].item() == (spans[s] if a >= spans[s] else a + 1)
+        assert nl[s].item() == 100 * s + a + s % 2
