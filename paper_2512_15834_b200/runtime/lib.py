@@ -89,5 +89,16 @@ def check(rc: int, what: str) -> int:
     return rc
 
 
+_DEBUG_SYNC = bool(os.environ.get("STB200_DEBUG_SYNC"))
+
+
 def call(name: str, *args) -> int:
-    return check(getattr(load(), name)(*args), name)
+    rc = check(getattr(load(), name)(*args), name)
+    if _DEBUG_SYNC:  # debugging aid: attribute asynchronous faults to the launching call
+        import torch
+
+        try:
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001
+            raise KernelError(f"{name}: asynchronous fault: {exc}") from exc
+    return rc

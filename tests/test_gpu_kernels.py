@@ -91,26 +91,30 @@ def test_allocator_matches_oracle(lib):
     assert pool.free_blocks() == len(ref.free)
 
 
+class _Raw:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<u2", "data": (ptr, False), "version": 3}
+
+
+def _view(ptr, n):
+    """Zero-copy bf16 view of n elements of library-owned device memory."""
+    return torch.as_tensor(_Raw(ptr, n), device="cuda").view(torch.bfloat16)
+
+
 def _dense_kv(pool, layer, slot, n, shape):
     """Gather a slot's first n rows from the pool via the block table (torch)."""
     kp, vp = pool.layer_ptrs(layer)
     nb = pool.num_blocks
     per = nb * shape.n_kv * 16 * shape.d_head
-    import numpy as np
-
-    kbuf = torch.empty(per, dtype=torch.bfloat16, device="cuda")
-    vbuf = torch.empty(per, dtype=torch.bfloat16, device="cuda")
     torch.cuda.synchronize()
-    cudart = torch.cuda.cudart()
-    cudart.cudaMemcpy(kbuf.data_ptr(), kp, per * 2, 3)
-    cudart.cudaMemcpy(vbuf.data_ptr(), vp, per * 2, 3)
+    kbuf = _view(kp, per)
+    vbuf = _view(vp, per)
     k = kbuf.view(nb, shape.n_kv, 16, shape.d_head)
     v = vbuf.view(nb, shape.n_kv, 16, shape.d_head)
     blocks = torch.tensor(pool.blocks(slot), device="cuda", dtype=torch.long)
     kd = k[blocks].permute(0, 2, 1, 3).reshape(-1, shape.n_kv, shape.d_head)[:n]
     vd = v[blocks].permute(0, 2, 1, 3).reshape(-1, shape.n_kv, shape.d_head)[:n]
-    del np
-    return kd, vd
+    return kd.clone(), vd.clone()
 
 
 def _fill_pool(lib, pool, shape, ctxs, seed=0):
@@ -285,8 +289,8 @@ def test_spec_validate(lib):
     acc, con, nl = (torch.empty(S, dtype=torch.int32, device="cuda") for _ in range(3))
     kv = t([100 * i for i in range(S)])
     extra = t([i % 2 for i in range(S)])
-    lib.call("stb_spec_validate", P(t(drafts)), P(t(d_off)), P(t(models)), P(t(m_off)), P(t(spans)), P(kv),
-             P(extra), S, P(acc), P(con), P(nl), stream())
+    keep = [t(drafts), t(d_off), t(models), t(m_off), t(spans)]  # alive until the kernel ran
+    lib.call("stb_spec_validate", *(P(x) for x in keep), P(kv), P(extra), S, P(acc), P(con), P(nl), stream())
     for s in range(S):
         dr, mo = drafts[d_off[s]:d_off[s + 1]], models[m_off[s]:m_off[s + 1]]
         n = min(len(dr), len(mo), spans[s])
