@@ -1,0 +1,316 @@
+"""Whole-box agent tokens/s of the tool-resident engine (BASELINE.json metric).
+
+Workload (BASELINE config C2): Llama-3-8B-shaped random-init bf16 decoder,
+32 concurrent agents per GPU on the synthetic tool-call trace of
+`runtime/fleet.py` (prompt 2048, reasoning 64-512, 32-token calls, tool
+outputs 64-1024 tokens, tool latency log-uniform 10 ms - 2 s, draft latency
+50 ms, accuracy 0.8), engine-side tool cache on. A *step* is one packed
+forward of the continuous-batching engine over every resident sequence
+(decode tokens + any prefill / verify / in-place ingest runs).
+
+  value  agent tokens emitted in the K timed steps / summed device time of
+         those steps (CUDA events on the engine stream; inputs resident)
+  e2e    the same tokens / wall time of the K steps through the public API:
+         host scheduling, timers, per-step H2D metadata + D2H sampled ids
+  roofline  live CUDA-event timing of the dominant kernel over the timed region
+
+N > 1 (torchrun): sessions are independent, so every rank is a replica with
+its own 32 agents (weak scaling); times are max over ranks, tokens summed.
+
+`--impl reference`: the reference path has no GPU code; its CPU
+restatement (oracle engine + fp32 decoder) is timed on the host cores on a
+bounded sample of the same workload and reported on the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "agent tokens/sec (whole box) at N concurrent agents; tool-resume latency ms"
+REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
+           "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+                mask = int(parts[2], 16)
+            except ValueError:
+                continue
+            for bit, name in enumerate(REASONS):
+                if mask & (1 << bit) and name != "gpu_idle":
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if os.environ.get("BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+    return world, rank, local
+
+
+def reduce(values: list[float], op: str, world: int, device) -> list[float]:
+    if world == 1:
+        return values
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_sample(shape, seconds_budget: float = 20.0, threads: int | None = None) -> dict:
+    """Oracle fp32 CPU decoder on a bounded sample of the workload.
+
+    Time a 2-layer slice of the shape and a 0-layer slice (embed + final norm +
+    LM head), then scale: t_token = t0 + (L/2) * (t2 - t0). Each sample token is
+    a decode step of one sequence at a 2048-token context (the trace's prompt).
+    """
+    import torch
+
+    from oracle.cpu_decoder import CpuDecoder
+
+    threads = threads or os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    res = {}
+    for L in (0, 2):
+        dec = CpuDecoder(shape, seed=0, layers=L)
+        ctx = 2048
+        dec.forward("s", list(range(3, 3 + ctx)), 0, [ctx - 1])
+        n, t0 = 0, time.perf_counter()
+        while n < 3 or (time.perf_counter() - t0 < seconds_budget / 4 and n < 16):
+            dec.forward("s", [5], ctx + n, [0])
+            n += 1
+        res[L] = (time.perf_counter() - t0) / n
+        del dec
+    t_tok = res[0] + shape.layers / 2 * (res[2] - res[0])
+    return {"value": 1.0 / t_tok, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle fp32 CpuDecoder, {shape.name}: decode steps of 1 sequence at ctx 2048, "
+                       f"timed on 0 and 2 layers ({res[0] * 1e3:.1f} / {res[2] * 1e3:.1f} ms/token) and scaled "
+                       f"to {shape.layers} layers")}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2512_15834_b200.modelcfg import SHAPES
+
+    shape = SHAPES[args.shape]
+    base = cpu_sample(shape, seconds_budget=max(8.0, min(60.0, 2.0 * (args.steps + args.warmup))))
+    line = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / base["value"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args), "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args) -> dict:
+    return {"workload": f"C2 {args.shape}-shaped random-init bf16, {args.agents} agents/GPU, tool-call trace "
+                        f"(prompt 2048, reason 64-512, call 32, output 64-1024, tool 10ms-2s log-uniform)",
+            "agents_per_gpu": args.agents, "prompt_tokens": 2048, "draft_latency_s": 0.05, "accept_rate": 0.8,
+            "layers": args.layers, "parallelism": f"replicas x{args.gpus}",
+            "l2": "working set > L2 (16 GB weights + KV streamed every step)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_b200(args, world, rank, local):
+    import torch
+
+    from paper_2512_15834_b200.engine import B200Engine
+    from paper_2512_15834_b200.modelcfg import SHAPES
+    from paper_2512_15834_b200.runtime import lib
+    from paper_2512_15834_b200.runtime.executor import BatchRuntime
+    from paper_2512_15834_b200.runtime.fleet import Fleet, TraceSpec, engine_config
+    from paper_2512_15834_b200.runtime.realtime import RealtimeLoop
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    shape = SHAPES[args.shape]
+    if args.layers:
+        shape = shape.with_layers(args.layers)
+    free, _ = torch.cuda.mem_get_info()
+    block_bytes = 16 * shape.kv_bytes_per_token
+    budget = free - shape.weight_bytes - 24 * (1 << 30)
+    num_blocks = int(max(2048, min(budget // block_bytes, args.agents * 2 * 16384 // 16)))
+    rt = BatchRuntime(shape, init_device="cuda", num_blocks=num_blocks, max_slots=max(256, 4 * args.agents),
+                      max_ctx=16384, max_step_tokens=args.max_step_tokens)
+    loop = RealtimeLoop()
+    engine = B200Engine(loop, engine_config(args.agents), runtime=rt)
+    fleet = Fleet(engine, loop, TraceSpec(seed=args.seed), args.agents, agent_offset=rank * args.agents)
+    fleet.start()
+
+    def one_step(events=None):
+        while True:
+            loop._fire_due()
+            if rt.busy():
+                break
+            time.sleep(0.0005)
+        if events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        rt.step()
+        if events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            events.append((e0, e1))
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    rt.dec.timers = {}
+    events = []
+    h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
+    launches0 = lib.load().stb_launch_count()
+    resume0 = len(engine.resume_latencies)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(events)
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+    barrier(world)
+    emitted = rt.emitted - em0
+    dev_s = sum(a.elapsed_time(b) for a, b in events) / 1e3
+    wall_s = w1 - w0
+    launches = lib.load().stb_launch_count() - launches0
+    resume = engine.resume_latencies[resume0:]
+    timers = rt.dec.timers
+    rt.dec.timers = None
+    kern = {}
+    for name, rows in timers.items():
+        t = sum(a.elapsed_time(b) for a, b, _ in rows) / 1e3
+        w = sum(x for _, _, x in rows)
+        kern[name] = (t, w, len(rows))
+    tot_emit, = reduce([float(emitted)], "sum", world, device)
+    dev_max, wall_max = reduce([dev_s, wall_s], "max", world, device)
+    if rank != 0:
+        return
+    hbm, tf_burst, tf_sus, src = peaks()
+    dominant = max(kern, key=lambda k: kern[k][0]) if kern else None
+    roof = None
+    if dominant:
+        t, w, n = kern[dominant]
+        ach = w / t / 1e9
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": None, "peak_source": src, "launches": n,
+                "avg_us": round(t / n * 1e6, 2), "share_of_device_time": round(t / dev_s, 4)}
+    others = {k: {"achieved_GBps": round(w / t / 1e9, 1), "frac": round(w / t / 1e9 / hbm, 4),
+                  "share_of_device_time": round(t / dev_s, 4), "launches": n}
+              for k, (t, w, n) in kern.items() if k != dominant}
+    cpu = cpu_sample(SHAPES[args.shape], seconds_budget=args.cpu_seconds) if not args.no_cpu else None
+    rs = sorted(resume)
+    line = {
+        "metric": METRIC, "value": round(tot_emit / dev_max, 2), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_max / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, scripted agent trace)", "config": workload_config(args),
+        "e2e": {"value": round(tot_emit / wall_max, 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": int((rt.h2d_bytes - h2d0) / args.steps),
+                "d2h_bytes_per_step": int((rt.d2h_bytes - d2h0) / args.steps)},
+        "tool_resume_ms": {"p50": round(rs[len(rs) // 2] * 1e3, 2) if rs else None,
+                           "p90": round(rs[int(len(rs) * 0.9)] * 1e3, 2) if rs else None, "count": len(rs)},
+        "roofline": roof, "kernels": others, "gpu_launches": int(launches), "clocks": clocks.summary(),
+        "cpu_baseline": cpu, "emitted_tokens": int(tot_emit), "tasks_completed": fleet.completed,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=40)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--agents", type=int, default=32)
+    ap.add_argument("--shape", default="llama3-8b")
+    ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--max-step-tokens", type=int, default=8192)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

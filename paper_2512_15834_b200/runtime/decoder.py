@@ -123,6 +123,7 @@ class Decoder:
         self._cap_r = 0
         self._cap_b = 0
         self.keep_logits = False
+        self.timers: dict[str, list] | None = None  # kernel -> [(ev0, ev1, algorithmic bytes|flops)]
         self.last_logits: torch.Tensor | None = None
         self.last_raw_argmax: torch.Tensor | None = None
 
@@ -193,13 +194,17 @@ class Decoder:
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, st)
         max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
         max_ctx = int(b.dec_ctx.max()) if B else 0
+        # K3 algorithmic bytes per launch: every context row's K and V once + q in + out
+        dec_bytes = (int(b.dec_ctx.sum()) * 2 * s.kv_dim * 2 + 2 * B * s.q_dim * 2) if B else 0
         for i in range(s.layers):
             self.gemm(h, w[f"l{i}.wqkv"], self.qkv[:T], st)
             call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]), _p(m["pos"]),
                  T, s.n_q, s.rope_theta, st)
             if B:
+                ev = self._tick()
                 call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
                      _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
+                self._tock("attn_decode", ev, dec_bytes)
             if S:
                 call("stb_attn_prefill", self.pool.h, i, C.c_void_p(self.q[B:].data_ptr()),
                      C.c_void_p(self.attn[B:].data_ptr()), _p(m["pre_slots"]), _p(m["pre_qstart"]),
@@ -225,7 +230,24 @@ class Decoder:
             self.last_raw_argmax = self.raw_arg[:R].clone()
         return self.sampled[:R]
 
+    def _tick(self):
+        if self.timers is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def _tock(self, name: str, ev0, work: int) -> None:
+        if ev0 is None:
+            return
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record()
+        self.timers.setdefault(name, []).append((ev0, ev1, work))
+
     def gemm(self, a: torch.Tensor, wt: torch.Tensor, out: torch.Tensor, st: C.c_void_p) -> None:
         M, K = a.shape
         N = wt.shape[0]
+        ev = self._tick()
         lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0, st)
+        # K5 algorithmic bytes: weights + activations in + fp32 out (HBM-bound when M is small)
+        self._tock("gemm", ev, N * K * 2 + M * K * 2 + M * N * 4)

@@ -105,6 +105,9 @@ class Runtime:
         self.trace: list[dict] = []     # per forward row: rid, pos, target, sampled, logits (if record)
         self.forwards = 0
         self.tokens_fed = 0
+        self.emitted = 0                # tokens sampled and counted (reference kv_tokens += ...)
+        self.h2d_bytes = 0              # per-step metadata uploads (ids, positions, tables, drafts)
+        self.d2h_bytes = 0              # sampled ids / validation results read back
 
     # -- vocabulary ------------------------------------------------------------
 
@@ -177,6 +180,7 @@ class Runtime:
                 raise KernelError(f"{seq.rid}: sampled {d.pend} but the script says {targets[0]}")
             d.counted = True
             k = 1
+            self.emitted += 1
             self._commit_blocks(d)
         if k == len(targets):
             done(None)
@@ -213,6 +217,7 @@ class Runtime:
             else:
                 d.pend, d.counted = None, False
             self._commit_blocks(d)  # K1 rollback of the rejected rows' blocks
+            self.emitted += consume
             done((accepted, consume))
 
         self._submit_run(Run(seq, inputs, d.kv_len, rows, targets, finish), want_device=True)
@@ -284,6 +289,8 @@ class Runtime:
         lib.call("stb_spec_validate", p(draft_t), p(meta[0:2]), p(model_t), p(meta[2:4]), p(meta[4:5]),
                  p(meta[5:6]), p(meta[6:7]), 1, p(out[0:1]), p(out[1:2]), p(out[2:3]), st)
         a, c, n = out.tolist()
+        self.h2d_bytes += 4 * (len(draft) + 7)
+        self.d2h_bytes += 12
         return a, c, n
 
     # -- forward plumbing ----------------------------------------------------------
@@ -331,6 +338,8 @@ class Runtime:
         self.dec.keep_logits = self.record
         sampled_dev = self.dec.forward(batch)
         sampled = sampled_dev.tolist()
+        self.h2d_bytes += self.dec.h2d_bytes
+        self.d2h_bytes += 4 * batch.R
         self.forwards += 1
         self.tokens_fed += batch.T
         if self.record:
@@ -360,6 +369,7 @@ class Runtime:
             d.kv_len += 1
             d.pend, d.counted = got, True
             j.k += 1
+        self.emitted += len(decodes)
         off = len(decodes)
         results = []
         for r in runs:
