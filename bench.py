@@ -204,32 +204,26 @@ def run_b200(args, world, rank, local):
     num_blocks = int(max(2048, min(budget // block_bytes, args.agents * 2 * 16384 // 16)))
     rt = BatchRuntime(shape, init_device="cuda", num_blocks=num_blocks, max_slots=max(256, 4 * args.agents),
                       max_ctx=16384, max_step_tokens=args.max_step_tokens)
+    rt.precapture(args.agents)
     loop = RealtimeLoop()
     engine = B200Engine(loop, engine_config(args.agents), runtime=rt)
     fleet = Fleet(engine, loop, TraceSpec(seed=args.seed), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
-    def one_step(events=None):
+    def one_step():
         while True:
             loop._fire_due()
             if rt.busy():
                 break
             time.sleep(0.0005)
-        if events is not None:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record()
         rt.step()
-        if events is not None:
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record()
-            events.append((e0, e1))
 
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
     barrier(world)
     rt.dec.timers = {}
-    events = []
+    events = rt.dec.step_events = []
     h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
     launches0 = lib.load().stb_launch_count()
     resume0 = len(engine.resume_latencies)
@@ -237,22 +231,22 @@ def run_b200(args, world, rank, local):
         torch.cuda.synchronize()
         w0 = time.perf_counter()
         for _ in range(args.steps):
-            one_step(events)
+            one_step()
         torch.cuda.synchronize()
         w1 = time.perf_counter()
     barrier(world)
     emitted = rt.emitted - em0
-    dev_s = sum(a.elapsed_time(b) for a, b in events) / 1e3
+    rt.dec.step_events = None
+    per = [(a.elapsed_time(b), g, T) for a, b, g, T in events]
+    dev_s = sum(ms for ms, _, _ in per) / 1e3
+    graphed = [ms for ms, g, _ in per if g]
+    mixed = [(ms, T) for ms, g, T in per if not g]
     wall_s = w1 - w0
     launches = lib.load().stb_launch_count() - launches0
     resume = engine.resume_latencies[resume0:]
     timers = rt.dec.timers
     rt.dec.timers = None
-    kern = {}
-    for name, rows in timers.items():
-        t = sum(a.elapsed_time(b) for a, b, _ in rows) / 1e3
-        w = sum(x for _, _, x in rows)
-        kern[name] = (t, w, len(rows))
+    kern = {name: (ms / 1e3, work, n) for name, (ms, work, n) in timers.items()}
     tot_emit, = reduce([float(emitted)], "sum", world, device)
     dev_max, wall_max = reduce([dev_s, wall_s], "max", world, device)
     if rank != 0:
@@ -283,6 +277,11 @@ def run_b200(args, world, rank, local):
                            "p90": round(rs[int(len(rs) * 0.9)] * 1e3, 2) if rs else None, "count": len(rs)},
         "roofline": roof, "kernels": others, "gpu_launches": int(launches), "clocks": clocks.summary(),
         "cpu_baseline": cpu, "emitted_tokens": int(tot_emit), "tasks_completed": fleet.completed,
+        "graph_replays": rt.dec.graph_replays,
+        "step_mix": {"decode_steps": len(graphed), "decode_ms_avg": round(sum(graphed) / max(1, len(graphed)), 3),
+                     "mixed_steps": len(mixed), "mixed_ms_avg": round(sum(m for m, _ in mixed) / max(1, len(mixed)), 3),
+                     "mixed_tokens_avg": round(sum(t for _, t in mixed) / max(1, len(mixed)), 1),
+                     "wall_ms_per_step": round(wall_s / args.steps * 1e3, 3)},
     }
     print(json.dumps(line), flush=True)
 

@@ -79,7 +79,9 @@ int stb_qkv_rope_commit(stb_kv_pool* pool, int layer, const float* qkv, void* q_
  * Replaces the decode charges engine.py:270,276,302,317. q/out bf16
  * [B][n_q][d_head]; slots/ctx_lens int32 [B]; split-K over the context with
  * a merge pass. `work` is a caller-owned fp32 scratch of
- * stb_attn_decode_workspace(B, n_q, d_head) bytes.                        */
+ * stb_attn_decode_workspace(B, n_q, d_head) bytes. max_ctx > 0 only caps the
+ * split count (>= 4 pages per split); 0 gives a grid that depends on B alone,
+ * which is what a captured CUDA graph needs.                               */
 int64_t stb_attn_decode_workspace(int B, int n_q, int d_head);
 int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                     const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, void* work, void* stream);
@@ -108,7 +110,9 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
 
 /* ---- K5: bf16 tensor-core GEMM (tcgen05 + TMA + TMEM) --------------------
  * C[M][N] (fp32, row stride ldc) = A[M][K] (bf16, lda) * W[N][K]^T (bf16, ldw).
- * split_k > 1 accumulates with fp32 reductions into a zeroed C.            */
+ * Persistent, one CTA per SM. split_k: 0 = automatic schedule; 1 = whole
+ * tiles per CTA (plain stores); >= 2 = stream-K over min(split_k, SMs) CTAs,
+ * partial tiles reduced with fp32 red.add into C (zeroed by the call).    */
 int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
                   int split_k, void* stream);
 

@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int n_kv, float qscale,
-    int pages_per_split, float* __restrict__ o_part, float* __restrict__ lse_part) {
+    float* __restrict__ o_part, float* __restrict__ lse_part) {
+  pdl_wait();
   constexpr int PAGE = 16 * D * 2;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -175,6 +176,9 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   const int n_q = n_kv * G;
   const int ctx = ctx_lens[b];
   const int npages = (ctx + 15) >> 4;
+  // this sequence's pages are divided evenly over the splits (grid shape is
+  // independent of context lengths, so one CUDA graph serves every step of a batch size)
+  const int pages_per_split = (npages + splits - 1) / splits;
   const int p0 = split * pages_per_split;
   const int p1 = min(npages, p0 + pages_per_split);
   const int32_t* row = table + (int64_t)slots[b] * max_bps;
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
 template <int D>
 __global__ void attn_merge_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                                   __nv_bfloat16* __restrict__ out, int rows, int splits) {
+  pdl_wait();
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const float* lse = lse_part + (int64_t)warp * splits;
@@ -309,6 +314,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ q_start, const int32_t* __restrict__ ctx_lens,
     int n_kv, float qscale) {
+  pdl_wait();
   constexpr int PAGE = 16 * D * 2;
   constexpr int QPW = 16 / G;  // queries per warp tile
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -400,19 +406,17 @@ template <int D, int G>
 int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
                   float qscale, int max_ctx, float* work, cudaStream_t st) {
-  int max_pages = (max_ctx + 15) / 16;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // aim for ~3 CTAs per SM in flight; at least 8 pages per split so the merge stays cheap
+  // ~3 CTAs per SM in flight; max_ctx (when known, > 0) caps splits at >= 4 pages each
   int pairs = B * n_kv;
   int splits = (3 * sms + pairs - 1) / pairs;
-  int max_splits = (max_pages + 7) / 8;
-  if (splits > max_splits) splits = max_splits;
+  if (max_ctx > 0) {
+    int cap = ((max_ctx + 15) / 16 + 3) / 4;
+    if (splits > cap) splits = cap;
+  }
   if (splits > 64) splits = 64;
-  if (splits < 1) splits = 1;
-  int pps = (max_pages + splits - 1) / splits;
-  splits = (max_pages + pps - 1) / pps;
   if (splits < 1) splits = 1;
   size_t smem = (size_t)4 * kDecodeStages * 2 * 16 * D * 2;
   size_t red = (size_t)4 * (32 + 16 * D) * 4;
@@ -421,13 +425,11 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   float* o_part = work;
   float* lse_part = work + (size_t)B * n_kv * G * 64 * D;
-  kern<<<dim3(splits, n_kv, B), 128, smem, st>>>(q, out, kp, vp, table, max_bps, slots, ctx, n_kv, qscale, pps, o_part,
+  launch_k(kern, dim3(splits, n_kv, B), dim3(128), smem, st, q, out, kp, vp, table, max_bps, slots, ctx, n_kv, qscale, o_part,
                                                  lse_part);
-  count_launch();
   if (splits > 1) {
     int rows = B * n_kv * G;
-    attn_merge_kernel<D><<<(rows * 32 + 255) / 256, 256, 0, st>>>(o_part, lse_part, out, rows, splits);
-    count_launch();
+    launch_k(attn_merge_kernel<D>, dim3((rows * 32 + 255) / 256), dim3(256), 0, st, o_part, lse_part, out, rows, splits);
   }
   STB_CHECK_LAUNCH("attn_decode");
   return STB_OK;
@@ -442,8 +444,7 @@ int launch_prefill(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat
   auto kern = attn_prefill_kernel<D, G, kPrefillStages>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((max_q + QPC - 1) / QPC, n_kv, S);
-  kern<<<grid, 128, smem, st>>>(q, out, kp, vp, table, max_bps, slots, q_start, ctx, n_kv, qscale);
-  count_launch();
+  launch_k(kern, dim3(grid), dim3(128), smem, st, q, out, kp, vp, table, max_bps, slots, q_start, ctx, n_kv, qscale);
   STB_CHECK_LAUNCH("attn_prefill");
   return STB_OK;
 }
@@ -465,7 +466,6 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
   int max_bps;
   stb_kv_block_table(pool, &table, &max_bps);
   if (B <= 0) return STB_OK;
-  if (max_ctx <= 0) return fail(STB_EINVAL, "attn_decode: max_ctx must be positive");
   int n_kv, d_head;
   stb_pool_geometry(pool, &n_kv, &d_head);
   if (n_q % n_kv) return fail(STB_EINVAL, "attn_decode: n_q %% n_kv != 0");

@@ -24,6 +24,33 @@ void count_launch(int n = 1);
     if (_e != cudaSuccess) return ::stb::fail(-3, "%s: %s", name, cudaGetErrorString(_e)); \
   } while (0)
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel calls pdl_wait() before touching data a previous kernel produced
+// (and before any early exit, so completion stays transitive along the stream);
+// pdl_launch() lets the next kernel's CTAs start their prologue early. Both are
+// no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+
+bool pdl_enabled();
+
+// cudaLaunchKernelEx with programmatic stream serialization (PDL) when enabled
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- small math
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -4,18 +4,37 @@
 // Replaces, with real FLOPs, every `rate x tokens` charge of the reference engine
 // (`engine.py:251,270,296,358`): the QKV / O / gate-up / down / LM-head projections.
 //
-// Weight-stationary tiling: the 128-row MMA "M" side is always 128 weight rows
-// (output features) and the MMA "N" side is BN tokens (16..256). Decode steps
-// (M = batch = 32) then run 128 x 32 UMMAs instead of padding the batch to 128,
-// and prefill/ingest (M = thousands of tokens) run 128 x 256. Operands are
-// K-major and arrive by TMA with 128-byte swizzle into a STAGES-deep smem ring;
-// one elected thread issues tcgen05.mma (kind::f16, fp32 accumulate in TMEM);
-// tcgen05.commit releases ring slots back to the TMA producer; after the last
-// K block all four warps drain their 32 TMEM lanes with tcgen05.ld and store
-// fp32 rows (coalesced across the 32 features a warp owns). When the tile grid
-// is smaller than the SM count the K loop is split and partial tiles are
-// reduced with fp32 red.global.add into a zeroed C (decode-shaped GEMMs are
-// HBM-bound on the weights: the split keeps all 148 SMs streaming).
+// Weight-stationary tiling: the 128-row UMMA "M" side is always 128 weight rows
+// (output features) and the UMMA "N" side is BN tokens (16..256), so decode steps
+// (M = resident batch, e.g. 32) run 128 x 32 UMMAs instead of padding the batch.
+//
+// Persistent, one CTA per SM, warp-specialised (192 threads):
+//   warp 0      TMA producer: W [128 x 64] + X [BN x 64] per stage, 128B swizzle,
+//               into a STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1      MMA issuer: one elected thread, tcgen05.mma kind::f16 (fp32 accum
+//               in TMEM); tcgen05.commit frees ring slots and publishes finished
+//               accumulators; TMEM is double-buffered so the next tile's MMAs run
+//               while the epilogue drains the previous one
+//   warps 2..5  epilogue: tcgen05.ld of their 32-lane TMEM quarter, fp32 stores
+//               (coalesced across the 32 features of a warp)
+//
+// Two schedules over the (tile, K-block) work space:
+//   tiles  tile t -> CTA t mod G, whole K, plain stores (enough tiles to fill
+//          the machine: prefill / ingest / LM head)
+//   stream the tile-major unit range is cut into G equal contiguous pieces
+//          (stream-K); a CTA's piece may end mid-tile, so tiles are reduced with
+//          fp32 red.global.add. C is zeroed inside the kernel: after the
+//          dependency wait every CTA clears a slice of C and arrives on a
+//          self-resetting grid barrier that the epilogue passes before its first
+//          reduction (the barrier completes long before the first tile's MMAs,
+//          so it costs nothing and there is no separate memset node).
+//          Decode-shaped GEMMs (M = 32) are HBM-bound on the weights: this keeps
+//          every SM streaming weights for the whole kernel with no tail wave.
+//
+// Launched with programmatic dependent launch: the producer issues the weight
+// loads of the first ring slots *before* griddepcontrol.wait (weights never
+// depend on the previous kernel), so pipeline fill overlaps the previous
+// kernel's tail; activations are loaded only after the wait.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -30,37 +49,79 @@ namespace {
 
 constexpr int BM = 128;  // weight rows per tile (UMMA M)
 constexpr int BK = 64;   // K per stage: one 128-byte swizzle atom of bf16
+constexpr int kThreads = 192;
 
 template <int BN>
 struct Cfg {
   static constexpr int W_BYTES = BM * BK * 2;
   static constexpr int X_BYTES = BN * BK * 2;
   static constexpr int STAGE = W_BYTES + X_BYTES;
-  static constexpr int STAGES = (196 * 1024 / STAGE) > 8 ? 8 : (196 * 1024 / STAGE);
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int RING = 200 * 1024;
+  static constexpr int STAGES = (RING / STAGE) > 12 ? 12 : (RING / STAGE);
+  static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+struct Sched {
+  int stream;        // 0: tile schedule, 1: stream-K
+  int tiles_n;       // feature tiles (of BM rows)
+  int tiles;         // tiles_n * token tiles
+  int kb;            // K blocks per tile
+  int64_t units;     // tiles * kb
+  unsigned* bar;     // stream-K grid barrier {count, generation}, self-resetting
+};
+
+// Segment iterator: (tile, kb_begin, kb_end) for this CTA, in order.
+struct SegIter {
+  Sched s;
+  int cta, G;
+  int64_t u, u_end;  // stream mode cursor
+  int t;             // tile mode cursor
+  __device__ SegIter(const Sched& sc) : s(sc), cta(blockIdx.x), G(gridDim.x) {
+    if (s.stream) {
+      u = s.units * cta / G;
+      u_end = s.units * (cta + 1) / G;
+    } else {
+      t = cta;
+    }
+  }
+  __device__ __forceinline__ bool next(int& tile, int& k0, int& k1) {
+    if (s.stream) {
+      if (u >= u_end) return false;
+      tile = (int)(u / s.kb);
+      k0 = (int)(u - (int64_t)tile * s.kb);
+      int64_t tile_end = (int64_t)(tile + 1) * s.kb;
+      int64_t e = tile_end < u_end ? tile_end : u_end;
+      k1 = (int)(e - (int64_t)tile * s.kb);
+      u = e;
+      return true;
+    }
+    if (t >= s.tiles) return false;
+    tile = t;
+    k0 = 0;
+    k1 = s.kb;
+    t += G;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
-    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                        float* __restrict__ C, int64_t ldc, int M, int N, int kb_per_split, int kb_total) {
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_persistent(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                         float* __restrict__ C, int64_t ldc, int M, int N, Sched sched) {
   using CF = Cfg<BN>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int f0 = blockIdx.x * BM;
-  const int t0 = blockIdx.y * BN;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int kb1 = min(kb_total, kb0 + kb_per_split);
-  const int nkb = kb1 - kb0;
-
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_w);
     tma_prefetch(&tm_x);
@@ -68,10 +129,13 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+    }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, CF::TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, CF::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -79,73 +143,138 @@ __global__ void __launch_bounds__(128, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // TMA producer
-      for (int i = 0; i < nkb; ++i) {
-        int s = i % STAGES;
-        uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sw = smem + s * CF::STAGE;
-        mbar_expect_tx(&full[s], CF::STAGE);
-        int kx = (kb0 + i) * BK;
-        tma_load_2d(sw, &tm_w, &full[s], kx, f0);
-        tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], kx, t0);
+      // weights first: the ring's first slots fill before the dependency wait
+      SegIter pre(sched);
+      int tile, k0, k1, i = 0;
+      while (i < STAGES && pre.next(tile, k0, k1)) {
+        const int f0 = (tile % sched.tiles_n) * BM;
+        for (int k = k0; k < k1 && i < STAGES; ++k, ++i) {
+          mbar_expect_tx(&full[i], CF::STAGE);
+          tma_load_2d(smem + i * CF::STAGE, &tm_w, &full[i], k * BK, f0);
+        }
+      }
+      const int prefetched = i;
+      pdl_wait();
+      pdl_launch();
+      SegIter it(sched);
+      i = 0;
+      while (it.next(tile, k0, k1)) {
+        const int f0 = (tile % sched.tiles_n) * BM;
+        const int t0 = (tile / sched.tiles_n) * BN;
+        for (int k = k0; k < k1; ++k, ++i) {
+          const int s = i % STAGES;
+          uint8_t* sw = smem + s * CF::STAGE;
+          if (i < prefetched) {
+            tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
+            continue;
+          }
+          mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], CF::STAGE);
+          tma_load_2d(sw, &tm_w, &full[s], k * BK, f0);
+          tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      // MMA issuer: D[128 x BN] += W[128 x 64] * X[BN x 64]^T per stage, 4 UMMA_K=16 steps
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, false, false);
-      for (int i = 0; i < nkb; ++i) {
-        int s = i % STAGES;
-        uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      SegIter it(sched);
+      int tile, k0, k1, i = 0, j = 0;
+      while (it.next(tile, k0, k1)) {
+        const int buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        uint32_t wa = smem_u32(smem + s * CF::STAGE);
-        uint32_t xa = wa + CF::W_BYTES;
+        const uint32_t d = tmem + buf * BN;
+        for (int k = k0; k < k1; ++k, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t wa = smem_u32(smem + s * CF::STAGE);
+          const uint32_t xa = wa + CF::W_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          uint64_t da = umma_desc_kmajor_sw128(wa + k * 32, 1024);
-          uint64_t db = umma_desc_kmajor_sw128(xa + k * 32, 1024);
-          umma_f16_ss(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            umma_f16_ss(d, umma_desc_kmajor_sw128(wa + kk * 32, 1024), umma_desc_kmajor_sw128(xa + kk * 32, 1024),
+                        idesc, (k > k0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&acc_full[buf]);
+        ++j;
       }
-      umma_commit(done);
     }
     __syncwarp();
-  }
-
-  // epilogue: every warp drains its 32 TMEM lanes (= 32 weight rows / output features)
-  if (nkb > 0) {
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int feat = f0 + warp * 32 + lane;
-    const bool split = gridDim.z > 1;
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarters 2,3,0,1
+    pdl_wait();
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // row of the 128-row tile this thread owns
+    const bool atomic = sched.stream != 0;
+    unsigned gen = 0;
+    if (atomic) {
+      // clear this CTA's slice of C, then arrive on the grid barrier
+      const int G = gridDim.x;
+      if (threadIdx.x == 64) gen = *(volatile unsigned*)(sched.bar + 1);
+      const int64_t total = (int64_t)M * N;
+      const int64_t lo = total * blockIdx.x / G, hi = total * (blockIdx.x + 1) / G;
+      for (int64_t e = lo + (threadIdx.x - 64); e < hi; e += 128) C[(e / N) * ldc + (e % N)] = 0.f;
+      __threadfence();
+      epi_bar();
+      if (threadIdx.x == 64) {
+        if (atomicAdd(sched.bar, 1u) == (unsigned)G - 1) {
+          *(volatile unsigned*)sched.bar = 0u;
+          __threadfence();
+          atomicAdd(sched.bar + 1, 1u);
+        }
+      }
+    }
+    bool passed = !atomic;
+    SegIter it(sched);
+    int tile, k0, k1, j = 0;
+    while (it.next(tile, k0, k1)) {
+      const int buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      if (!passed) {  // every slice of C is zero before the first reduction lands
+        if (threadIdx.x == 64)
+          while (*(volatile unsigned*)(sched.bar + 1) == gen) __nanosleep(64);
+        epi_bar();
+        __threadfence();
+        passed = true;
+      }
+      const int feat = (tile % sched.tiles_n) * BM + row;
+      const int t0 = (tile / sched.tiles_n) * BN;
+      const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
 #pragma unroll 1
-    for (int c = 0; c < BN / 16; ++c) {
-      uint32_t r[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c * 16, r);
-      tmem_ld_wait();
-      if (feat < N) {
+      for (int c = 0; c < BN / 16; ++c) {
+        uint32_t r[16];
+        tmem_ld16(base + c * 16, r);
+        tmem_ld_wait();
+        if (feat < N) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          int tok = t0 + c * 16 + j;
-          if (tok < M) {
-            float v = __uint_as_float(r[j]);
-            float* dst = C + (int64_t)tok * ldc + feat;
-            if (split)
-              atomicAdd(dst, v);
-            else
-              *dst = v;
+          for (int q = 0; q < 16; ++q) {
+            const int tok = t0 + c * 16 + q;
+            if (tok < M) {
+              float* dst = C + (int64_t)tok * ldc + feat;
+              if (atomic)
+                atomicAdd(dst, __uint_as_float(r[q]));
+              else
+                *dst = __uint_as_float(r[q]);
+            }
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      ++j;
     }
+    if (!passed && threadIdx.x == 64)  // no segment: still let the barrier complete before exiting
+      while (*(volatile unsigned*)(sched.bar + 1) == gen) __nanosleep(64);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_free(tmem, CF::TMEM_COLS);
+  if (warp == 1) tmem_free(tmem, CF::TMEM_COLS);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -201,45 +330,66 @@ int cached_map(CUtensorMap* out, const void* base, int64_t rows, int64_t cols, i
     return STB_OK;
   }
   if (int rc = make_map(out, base, rows, cols, ld, box_rows)) return rc;
-  if (cache.size() > 4096) cache.clear();
+  if (cache.size() > 8192) cache.clear();
   cache.emplace(key, *out);
   return STB_OK;
 }
 
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+// stream-K grid barrier state {arrivals, generation}: zeroed once, self-resetting
+unsigned* grid_barrier() {
+  static unsigned* bar = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cudaMalloc(&bar, 2 * sizeof(unsigned)) == cudaSuccess) cudaMemset(bar, 0, 2 * sizeof(unsigned));
+  });
+  return bar;
+}
+
 template <int BN>
 int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
-           int split_k, cudaStream_t st) {
+           int mode, cudaStream_t st) {
   using CF = Cfg<BN>;
   CUtensorMap tw, tx;
   if (int rc = cached_map(&tw, W, N, K, ldw, BM)) return rc;
   if (int rc = cached_map(&tx, X, M, K, lda, BN)) return rc;
-  int kb_total = (K + BK - 1) / BK;
-  int tiles = ((N + BM - 1) / BM) * ((M + BN - 1) / BN);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int splits = split_k;
-  if (splits <= 0) {
-    splits = 1;
-    if (tiles < sms) splits = (2 * sms + tiles - 1) / tiles;  // ~2 waves of K slices
-    int max_s = kb_total / 4 > 0 ? kb_total / 4 : 1;          // keep >= 4 K blocks per slice
-    if (splits > max_s) splits = max_s;
+  Sched s;
+  s.tiles_n = (N + BM - 1) / BM;
+  s.tiles = s.tiles_n * ((M + BN - 1) / BN);
+  s.kb = (K + BK - 1) / BK;
+  s.units = (int64_t)s.tiles * s.kb;
+  const int sms = sm_count();
+  // tile schedule when the tiles alone fill the machine several times over; stream-K otherwise
+  s.stream = mode == 1 ? 0 : (mode >= 2 ? 1 : ((s.tiles >= 4 * sms || (M > 128 && s.tiles >= sms)) ? 0 : 1));
+  int grid = s.stream ? sms : (s.tiles < sms ? s.tiles : sms);
+  if (mode >= 2 && mode < grid) grid = mode;
+  if (s.stream && s.units < grid) grid = (int)s.units;
+  s.bar = grid_barrier();
+  if (!s.bar) return fail(STB_ENOMEM, "gemm_bf16: barrier state");
+  auto kern = gemm_bf16_persistent<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    attr_set = true;
   }
-  if (splits > kb_total) splits = kb_total;
-  int kbps = (kb_total + splits - 1) / splits;
-  splits = (kb_total + kbps - 1) / kbps;
-  if (splits > 1) cudaMemsetAsync(C, 0, sizeof(float) * ((size_t)(M - 1) * ldc + N), st);
-  auto kern = gemm_bf16_tn_kernel<BN>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-  dim3 grid((N + BM - 1) / BM, (M + BN - 1) / BN, splits);
-  kern<<<grid, 128, CF::SMEM, st>>>(tw, tx, C, ldc, M, N, kbps, kb_total);
-  count_launch();
-  STB_CHECK_LAUNCH("gemm_bf16");
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), CF::SMEM, st, tw, tx, C, ldc, M, N, s);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "gemm_bf16 launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
 
 }  // namespace
 
+// split_k: 0 = automatic schedule, 1 = tile schedule (no reductions), >= 2 = stream-K over
+// min(split_k, SMs) CTAs (tests use it to force mid-tile splits).
 extern "C" int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M,
                              int N, int K, int split_k, void* stream) {
   if (M <= 0 || N <= 0) return STB_OK;

@@ -9,6 +9,7 @@
 // ceil(len/16) blocks; truncate frees from the tail, so the next pop reuses the
 // lowest freed logical block first. oracle/kv_alloc.py restates this policy.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -33,6 +34,14 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 void count_launch(int n) { __atomic_fetch_add(&g_launches, (int64_t)n, __ATOMIC_RELAXED); }
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STB200_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
 
 }  // namespace stb
 
@@ -47,6 +56,7 @@ static void table_set(stb_kv_pool* p, int slot, int idx, int32_t value) {
 }
 
 __global__ void apply_updates_kernel(const int32_t* __restrict__ upd, int n, int32_t* __restrict__ table) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) table[upd[2 * i]] = upd[2 * i + 1];
 }
@@ -57,6 +67,7 @@ __global__ void kv_commit_kernel(const __nv_bfloat16* __restrict__ k, const __nv
                                  const int32_t* __restrict__ slot_of, const int32_t* __restrict__ pos_of, int n,
                                  const int32_t* __restrict__ table, int max_bps, __nv_bfloat16* __restrict__ kpages,
                                  __nv_bfloat16* __restrict__ vpages, int n_kv, int d_head) {
+  pdl_wait();
   const int chunks = n_kv * d_head / 8;  // 8 bf16 per 16 bytes
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)n * 2 * chunks;
@@ -76,6 +87,7 @@ __global__ void kv_commit_kernel(const __nv_bfloat16* __restrict__ k, const __nv
 __global__ void kv_copy_blocks_kernel(__nv_bfloat16* __restrict__ pages, const int32_t* __restrict__ src,
                                       const int32_t* __restrict__ dst, int n, int64_t block_elems, int64_t half_elems,
                                       int layers) {
+  pdl_wait();
   // grid.y = block pair, grid.z = layer*2 + {K,V}; threads stride the block in 16B vectors
   int pair = blockIdx.y;
   int lz = blockIdx.z;
@@ -93,6 +105,7 @@ __global__ void qkv_rope_commit_kernel(const float* __restrict__ qkv, __nv_bfloa
                                        int n_q, int n_kv, int d_head, const float* __restrict__ inv_freq,
                                        const int32_t* __restrict__ table, int max_bps,
                                        __nv_bfloat16* __restrict__ kpages, __nv_bfloat16* __restrict__ vpages) {
+  pdl_wait();
   const int half = d_head / 2;
   const int groups = half / 8;
   const int heads = n_q + 2 * n_kv;
@@ -285,8 +298,7 @@ int stb_kv_sync(stb_kv_pool* p, void* stream) {
   p->updates.clear();
   cudaMemcpyAsync(p->dev_updates[i], p->staging[i], n * sizeof(int32_t), cudaMemcpyHostToDevice, st);
   int pairs = (int)(n / 2);
-  apply_updates_kernel<<<(pairs + 255) / 256, 256, 0, st>>>(p->dev_updates[i], pairs, p->dev_table);
-  count_launch();
+  launch_k(apply_updates_kernel, dim3((pairs + 255) / 256), dim3(256), 0, st, p->dev_updates[i], pairs, p->dev_table);
   cudaEventRecord(p->done[i], st);
   STB_CHECK_LAUNCH("kv_sync");
   return STB_OK;
@@ -316,10 +328,9 @@ int stb_kv_commit(stb_kv_pool* p, int layer, const void* k, const void* v, int64
   stb_kv_layer_ptrs(p, layer, &kp, &vp);
   int64_t total = (int64_t)n * 2 * (p->n_kv * p->d_head / 8);
   int threads = 256;
-  kv_commit_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+  launch_k(kv_commit_kernel, dim3((unsigned)((total + threads - 1) / threads)), dim3(threads), 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, ld, slot_of, pos_of, n, p->dev_table, p->max_bps,
       (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, p->n_kv, p->d_head);
-  count_launch();
   STB_CHECK_LAUNCH("kv_commit");
   return STB_OK;
 }
@@ -329,9 +340,8 @@ int stb_kv_copy_blocks(stb_kv_pool* p, const int32_t* src, const int32_t* dst, i
   if (n <= 0) return STB_OK;
   if (n > 65535) return fail(STB_EINVAL, "kv_copy_blocks: at most 65535 pairs per call");
   dim3 grid(4, n, p->layers * 2);
-  kv_copy_blocks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p->pages, src, dst, n, p->block_elems, p->half_elems,
+  launch_k(kv_copy_blocks_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, p->pages, src, dst, n, p->block_elems, p->half_elems,
                                                                  p->layers);
-  count_launch();
   STB_CHECK_LAUNCH("kv_copy_blocks");
   return STB_OK;
 }
@@ -362,10 +372,9 @@ int stb_qkv_rope_commit(stb_kv_pool* p, int layer, const float* qkv, void* q_out
   if (p->d_head % 16 != 0) return fail(STB_EINVAL, "qkv_rope_commit: d_head must be a multiple of 16");
   int64_t total = (int64_t)n * (n_q + 2 * p->n_kv) * (p->d_head / 16);
   int threads = 256;
-  qkv_rope_commit_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+  launch_k(qkv_rope_commit_kernel, dim3((unsigned)((total + threads - 1) / threads)), dim3(threads), 0, (cudaStream_t)stream, 
       qkv, (__nv_bfloat16*)q_out, slot_of, pos_of, n, n_q, p->n_kv, p->d_head, inv, p->dev_table, p->max_bps,
       (__nv_bfloat16*)kp, (__nv_bfloat16*)vp);
-  count_launch();
   STB_CHECK_LAUNCH("qkv_rope_commit");
   return STB_OK;
 }

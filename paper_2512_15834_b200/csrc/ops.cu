@@ -16,6 +16,7 @@ namespace {
 
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
                              float* __restrict__ x, int n, int d) {
+  pdl_wait();
   int t = blockIdx.x;
   const __nv_bfloat16* row = table + (int64_t)ids[t] * d;
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
@@ -47,6 +48,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int d,
                                    float eps, const int32_t* __restrict__ gather) {
+  pdl_wait();
   __shared__ float red[32];
   int t = blockIdx.x;
   int src = gather ? gather[t] : t;
@@ -77,6 +79,7 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restric
 }
 
 __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f) {
+  pdl_wait();
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   int64_t total = (int64_t)n * f;
   if (i >= total) return;
@@ -89,78 +92,102 @@ __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __r
   *reinterpret_cast<uint2*>(y + i) = o;
 }
 
-// one CTA per sampled row: biased argmax over the vocabulary (first index wins ties)
-__global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ target,
-                                     int V, float bias, int32_t* __restrict__ out, int32_t* __restrict__ raw_arg,
-                                     float* __restrict__ raw_max) {
-  __shared__ float sv[32], sb[32];
-  __shared__ int si[32], sbi[32];
-  int r = blockIdx.x;
-  const float* row = logits + (int64_t)r * ld;
-  int tgt = target ? target[r] : -1;
-  float best = -FLT_MAX, bbest = -FLT_MAX;
-  int bi = 0x7fffffff, bbi = 0x7fffffff;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    float v = row[c];
-    if (v > best || (v == best && c < bi)) {
-      best = v;
-      bi = c;
-    }
-    float b = (c == tgt) ? v + bias : v;
-    if (b > bbest || (b == bbest && c < bbi)) {
-      bbest = b;
-      bbi = c;
-    }
+// Script-forced greedy sampling, split over the vocabulary: grid = R rows x CH chunks.
+// Each CTA reduces its chunk to (max, argmax) of the raw and of the biased logits
+// (first index wins ties), publishes a partial, and the last CTA of a row to
+// finish (atomic ticket) reduces the row's CH partials; the ticket self-resets.
+struct ArgPart {
+  float best, bbest;
+  int bi, bbi;
+};
+
+__device__ __forceinline__ void arg_merge(float& v, int& i, float ov, int oi) {
+  if (ov > v || (ov == v && oi < i)) {
+    v = ov;
+    i = oi;
   }
+}
+
+__device__ __forceinline__ void block_arg(float& best, int& bi, float& bbest, int& bbi, ArgPart* sm) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     float ov = __shfl_xor_sync(0xffffffffu, best, o);
     int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) {
-      best = ov;
-      bi = oi;
-    }
     float ob = __shfl_xor_sync(0xffffffffu, bbest, o);
     int obi = __shfl_xor_sync(0xffffffffu, bbi, o);
-    if (ob > bbest || (ob == bbest && obi < bbi)) {
-      bbest = ob;
-      bbi = obi;
-    }
+    arg_merge(best, bi, ov, oi);
+    arg_merge(bbest, bbi, ob, obi);
   }
   int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    sv[w] = best;
-    si[w] = bi;
-    sb[w] = bbest;
-    sbi[w] = bbi;
-  }
+  if (l == 0) sm[w] = {best, bbest, bi, bbi};
   __syncthreads();
   if (w == 0) {
     int nw = blockDim.x >> 5;
-    best = l < nw ? sv[l] : -FLT_MAX;
-    bi = l < nw ? si[l] : 0x7fffffff;
-    bbest = l < nw ? sb[l] : -FLT_MAX;
-    bbi = l < nw ? sbi[l] : 0x7fffffff;
+    ArgPart p = l < nw ? sm[l] : ArgPart{-FLT_MAX, -FLT_MAX, 0x7fffffff, 0x7fffffff};
+    best = p.best, bi = p.bi, bbest = p.bbest, bbi = p.bbi;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       float ov = __shfl_xor_sync(0xffffffffu, best, o);
       int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) {
-        best = ov;
-        bi = oi;
-      }
       float ob = __shfl_xor_sync(0xffffffffu, bbest, o);
       int obi = __shfl_xor_sync(0xffffffffu, bbi, o);
-      if (ob > bbest || (ob == bbest && obi < bbi)) {
-        bbest = ob;
-        bbi = obi;
+      arg_merge(best, bi, ov, oi);
+      arg_merge(bbest, bbi, ob, obi);
+    }
+  }
+}
+
+__global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ target,
+                                     int V, float bias, int CH, ArgPart* __restrict__ parts,
+                                     int* __restrict__ tickets, int32_t* __restrict__ out,
+                                     int32_t* __restrict__ raw_arg, float* __restrict__ raw_max) {
+  pdl_wait();
+  __shared__ ArgPart sm[32];
+  __shared__ int last;
+  const int r = blockIdx.x / CH, ch = blockIdx.x % CH;
+  const float* row = logits + (int64_t)r * ld;
+  const int tgt = target ? target[r] : -1;
+  const int span = ((V + CH - 1) / CH + 3) & ~3;
+  const int lo = ch * span, hi = min(V, lo + span);
+  float best = -FLT_MAX, bbest = -FLT_MAX;
+  int bi = 0x7fffffff, bbi = 0x7fffffff;
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0);
+  if (vec) {
+    for (int c = lo + threadIdx.x * 4; c < hi; c += blockDim.x * 4) {
+      float4 v4 = *reinterpret_cast<const float4*>(row + c);
+      float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int idx = c + q;
+        if (idx < hi) {
+          arg_merge(best, bi, vv[q], idx);
+          arg_merge(bbest, bbi, idx == tgt ? vv[q] + bias : vv[q], idx);
+        }
       }
     }
-    if (l == 0) {
-      out[r] = bbi;
-      if (raw_arg) raw_arg[r] = bi;
-      if (raw_max) raw_max[r] = best;
+  } else {
+    for (int c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+      arg_merge(best, bi, row[c], c);
+      arg_merge(bbest, bbi, c == tgt ? row[c] + bias : row[c], c);
     }
+  }
+  block_arg(best, bi, bbest, bbi, sm);
+  if (threadIdx.x == 0) {
+    parts[blockIdx.x] = {best, bbest, bi, bbi};
+    __threadfence();
+    last = atomicAdd(&tickets[r], 1) == CH - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  ArgPart p = threadIdx.x < CH ? parts[r * CH + threadIdx.x] : ArgPart{-FLT_MAX, -FLT_MAX, 0x7fffffff, 0x7fffffff};
+  best = p.best, bi = p.bi, bbest = p.bbest, bbi = p.bbi;
+  block_arg(best, bi, bbest, bbi, sm);
+  if (threadIdx.x == 0) {
+    out[r] = bbi;
+    if (raw_arg) raw_arg[r] = bi;
+    if (raw_max) raw_max[r] = best;
+    tickets[r] = 0;
   }
 }
 
@@ -170,6 +197,7 @@ __global__ void spec_validate_kernel(const int32_t* __restrict__ draft, const in
                                      const int32_t* __restrict__ span_len, const int32_t* __restrict__ kv_len,
                                      const int32_t* __restrict__ base_extra, int S, int32_t* __restrict__ accepted,
                                      int32_t* __restrict__ consume, int32_t* __restrict__ new_len) {
+  pdl_wait();
   int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (s >= S) return;
@@ -203,8 +231,7 @@ extern "C" {
 int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, void* stream) {
   if (n <= 0) return STB_OK;
   if (d % 8) return fail(STB_EINVAL, "embed: d must be a multiple of 8");
-  embed_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(ids, (const __nv_bfloat16*)table, x, n, d);
-  count_launch();
+  launch_k(embed_kernel, dim3(n), dim3(128), 0, (cudaStream_t)stream, ids, (const __nv_bfloat16*)table, x, n, d);
   STB_CHECK_LAUNCH("embed");
   return STB_OK;
 }
@@ -212,9 +239,8 @@ int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, voi
 int stb_add_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps, void* stream) {
   if (n <= 0) return STB_OK;
   if (d % 4) return fail(STB_EINVAL, "add_rmsnorm: d must be a multiple of 4");
-  add_rmsnorm_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(x, delta, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, d, eps,
+  launch_k(add_rmsnorm_kernel, dim3(n), dim3(256), 0, (cudaStream_t)stream, x, delta, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, d, eps,
                                                           nullptr);
-  count_launch();
   STB_CHECK_LAUNCH("add_rmsnorm");
   return STB_OK;
 }
@@ -223,9 +249,8 @@ int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* 
                        void* stream) {
   if (n <= 0) return STB_OK;
   if (d % 4) return fail(STB_EINVAL, "gather_rmsnorm: d must be a multiple of 4");
-  add_rmsnorm_kernel<<<n, 256, 0, (cudaStream_t)stream>>>(const_cast<float*>(x), nullptr, (const __nv_bfloat16*)w,
+  launch_k(add_rmsnorm_kernel, dim3(n), dim3(256), 0, (cudaStream_t)stream, const_cast<float*>(x), nullptr, (const __nv_bfloat16*)w,
                                                           (__nv_bfloat16*)y, d, eps, idx);
-  count_launch();
   STB_CHECK_LAUNCH("gather_rmsnorm");
   return STB_OK;
 }
@@ -234,8 +259,7 @@ int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream) {
   if (n <= 0) return STB_OK;
   if (f % 4) return fail(STB_EINVAL, "silu_mul: f must be a multiple of 4");
   int64_t total = (int64_t)n * f / 4;
-  silu_mul_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(gu, (__nv_bfloat16*)y, n, f);
-  count_launch();
+  launch_k(silu_mul_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, gu, (__nv_bfloat16*)y, n, f);
   STB_CHECK_LAUNCH("silu_mul");
   return STB_OK;
 }
@@ -243,8 +267,19 @@ int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream) {
 int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
                       int32_t* raw_argmax, float* raw_max, void* stream) {
   if (R <= 0) return STB_OK;
-  sample_forced_kernel<<<R, 512, 0, (cudaStream_t)stream>>>(logits, ld, target, V, bias, out, raw_argmax, raw_max);
-  count_launch();
+  constexpr int CH = 32;  // vocabulary chunks per row (<= 32: one warp reduces the partials)
+  constexpr int kMaxRows = 65536;
+  if (R > kMaxRows) return fail(STB_EINVAL, "sample_forced: at most %d rows per call", kMaxRows);
+  // persistent scratch: partials + self-resetting tickets (allocated once, before any graph capture)
+  static ArgPart* parts = nullptr;
+  static int* tickets = nullptr;
+  if (!parts) {
+    if (cudaMalloc(&parts, sizeof(ArgPart) * (size_t)kMaxRows * CH) != cudaSuccess ||
+        cudaMalloc(&tickets, sizeof(int) * kMaxRows) != cudaSuccess || cudaMemset(tickets, 0, sizeof(int) * kMaxRows))
+      return fail(STB_ENOMEM, "sample_forced: scratch allocation failed");
+  }
+  launch_k(sample_forced_kernel, dim3(R * CH), dim3(256), 0, (cudaStream_t)stream, logits, ld, target, V, bias, CH, parts, tickets, out,
+                                                                 raw_argmax, raw_max);
   STB_CHECK_LAUNCH("sample_forced");
   return STB_OK;
 }
@@ -255,9 +290,8 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
   if (S <= 0) return STB_OK;
   int threads = 128;
   int blocks = (S * 32 + threads - 1) / threads;
-  spec_validate_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(draft, d_off, model, m_off, span_len, kv_len,
+  launch_k(spec_validate_kernel, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, draft, d_off, model, m_off, span_len, kv_len,
                                                                      base_extra, S, accepted, consume, new_len);
-  count_launch();
   STB_CHECK_LAUNCH("spec_validate");
   return STB_OK;
 }

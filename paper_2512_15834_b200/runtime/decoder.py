@@ -9,10 +9,15 @@ each a contiguous token range. Per layer:
   K5 O GEMM -> residual + rmsnorm -> K5 gate-up GEMM -> SiLU*up -> K5 down GEMM
 
 then the final norm on the R sampled rows only, the K5 LM-head GEMM on those
-rows, and script-forced greedy sampling. Everything is launched through the
-C ABI on the current torch stream; the only torch ops are buffer allocation
-and the metadata H2D copy. Host metadata for a step is one pinned int32
-buffer, uploaded with a single async copy.
+rows, and script-forced greedy sampling. Every launch goes through the C ABI
+on the current torch stream.
+
+Step metadata (ids, positions, slots, contexts, sample rows, targets) is one
+int32 record written into a pinned host buffer and copied with a single H2D
+into a static device buffer. Decode-only steps (the common case) replay a
+CUDA graph captured once per batch size: all launch parameters of such a step
+depend on B alone (the K3 split count is B-derived, GEMM tensor maps point at
+static buffers), so the graph is valid for every step of that size.
 """
 
 from __future__ import annotations
@@ -108,24 +113,40 @@ class StepBatch:
         return int(self.sample_rows.shape[0])
 
 
-def _p(t: torch.Tensor | None) -> C.c_void_p:
-    return C.c_void_p(0 if t is None else t.data_ptr())
+FIELDS = ("ids", "pos", "slot_of", "dec_slots", "dec_ctx", "pre_slots", "pre_qstart", "pre_ctx", "sample_rows",
+          "targets")
+
+
+def _p(t) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(0)
+    return C.c_void_p(t if isinstance(t, int) else t.data_ptr())
 
 
 class Decoder:
-    def __init__(self, shape: ModelShape, weights: dict[str, torch.Tensor], pool: KVPool, device: str = "cuda"):
+    META_CAP = 1 << 20  # int32 entries of the static step record
+
+    def __init__(self, shape: ModelShape, weights: dict[str, torch.Tensor], pool: KVPool, device: str = "cuda",
+                 use_graphs: bool = True):
         self.shape = shape
         self.w = weights
         self.pool = pool
         self.device = device
         self.scale = 1.0 / math.sqrt(shape.d_head)
-        self._cap_t = 0
-        self._cap_r = 0
-        self._cap_b = 0
+        self._cap_t = self._cap_r = self._cap_b = 0
         self.keep_logits = False
-        self.timers: dict[str, list] | None = None  # kernel -> [(ev0, ev1, algorithmic bytes|flops)]
+        self.use_graphs = use_graphs
+        self.graphs: dict[tuple, tuple] = {}
+        self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
+        self._pending: list | None = []             # (name, ev0, ev1, work) awaiting a sync
+        self._graph_timed = False
         self.last_logits: torch.Tensor | None = None
         self.last_raw_argmax: torch.Tensor | None = None
+        self.meta_host = torch.empty(self.META_CAP, dtype=torch.int32, pin_memory=True)
+        self.meta_dev = torch.empty(self.META_CAP, dtype=torch.int32, device=device)
+        self.h2d_bytes = 0
+        self.graph_replays = 0
+        self.step_events: list | None = None  # (ev0, ev1, graphed, T) bracketing each step's kernels
 
     # -- buffers ----------------------------------------------------------------
 
@@ -143,61 +164,105 @@ class Decoder:
             self.gu = torch.empty(cap, 2 * s.d_ff, dtype=f32, device=dev)
             self.act = torch.empty(cap, s.d_ff, dtype=bf, device=dev)
             self._cap_t = cap
+            self.graphs.clear()  # captured graphs point at the old buffers
         if R > self._cap_r:
-            cap = max(R, 2 * self._cap_r, 16)
+            cap = max(R, 2 * self._cap_r, 64)
             self.rows = torch.empty(cap, s.d_model, dtype=torch.bfloat16, device=dev)
             self.logits = torch.empty(cap, s.vocab, dtype=torch.float32, device=dev)
             self.sampled = torch.empty(cap, dtype=torch.int32, device=dev)
             self.raw_arg = torch.empty(cap, dtype=torch.int32, device=dev)
             self.raw_max = torch.empty(cap, dtype=torch.float32, device=dev)
             self._cap_r = cap
+            self.graphs.clear()
         if B > self._cap_b:
-            cap = max(B, 2 * self._cap_b, 16)
+            cap = max(B, 2 * self._cap_b, 64)
             nbytes = lib.load().stb_attn_decode_workspace(cap, s.n_q, s.d_head)
             self.work = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
             self._cap_b = cap
+            self.graphs.clear()
 
-    def _upload(self, b: StepBatch) -> dict[str, torch.Tensor]:
-        parts = [("ids", b.ids), ("pos", b.pos), ("slot_of", b.slot_of), ("dec_slots", b.dec_slots),
-                 ("dec_ctx", b.dec_ctx), ("pre_slots", b.pre_slots), ("pre_qstart", b.pre_qstart),
-                 ("pre_ctx", b.pre_ctx), ("sample_rows", b.sample_rows), ("targets", b.targets)]
-        total = sum(int(a.shape[0]) for _, a in parts)
-        host = torch.empty(max(total, 1), dtype=torch.int32, pin_memory=True)
-        hv = host.numpy()
-        off = 0
-        spans = {}
-        for name, a in parts:
+    def _upload(self, b: StepBatch) -> dict[str, int]:
+        """Write the step record into pinned memory, one async H2D into the static buffer."""
+        hv = self.meta_host.numpy()
+        off, spans = 0, {}
+        for name in FIELDS:
+            a = getattr(b, name)
             n = int(a.shape[0])
             hv[off:off + n] = a
-            spans[name] = (off, n)
+            spans[name] = off
             off += n
-        dev = host.to(self.device, non_blocking=True)
-        self._pinned = host  # keep alive until the copy lands
-        self.h2d_bytes = 4 * total
-        return {k: dev[o:o + n] for k, (o, n) in spans.items()}
+        if off > self.META_CAP:
+            raise ValueError("step record exceeds the static metadata buffer")
+        self.meta_dev[:off].copy_(self.meta_host[:off], non_blocking=True)
+        self.h2d_bytes = 4 * off
+        base = self.meta_dev.data_ptr()
+        return {k: base + 4 * o for k, o in spans.items()}
 
     # -- forward ----------------------------------------------------------------
 
     def forward(self, b: StepBatch) -> torch.Tensor:
         """Run one packed step; returns the sampled ids [R] (device int32)."""
-        s, w = self.shape, self.w
         T, R, B, S = b.T, b.R, b.B_dec, b.S
         self._ensure(T, R, B)
         stream = torch.cuda.current_stream().cuda_stream
-        st = C.c_void_p(stream)
         self.pool.sync(stream)
         m = self._upload(b)
+        dec_bytes = (int(b.dec_ctx.sum()) * 2 * self.shape.kv_dim * 2 + 2 * B * self.shape.q_dim * 2) if B else 0
+        graphable = self.use_graphs and S == 0 and B > 0 and not self.keep_logits
+        if self.step_events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        if not graphable:
+            max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
+            self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
+        else:
+            timed = self.timers is not None
+            key = (B, timed)
+            if key not in self.graphs:
+                self._capture(key, m, B)
+            graph, events = self.graphs[key]
+            graph.replay()
+            self.graph_replays += 1
+            if timed:
+                for name, a0, a1, work in events:
+                    self._pending.append((name, a0, a1, dec_bytes if name == "attn_decode" else work))
+        if self.step_events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self.step_events.append((e0, e1, graphable, T))
+        if self.keep_logits:
+            self.last_logits = self.logits[:R].clone()
+            self.last_raw_argmax = self.raw_arg[:R].clone()
+        return self.sampled[:R]
+
+    def _capture(self, key, m: dict[str, int], B: int) -> None:
+        timed = key[1]
+        saved, saved_timers = self._pending, self.timers
+        # warm once eagerly (first-call allocations, tensor-map encodes, attributes); untimed
+        self.timers, self._pending = None, []
+        self._launch(m, B, B, B, 0, 0, 0, 0)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        events: list = []
+        self._pending = events
+        self._graph_timed = timed
+        with torch.cuda.graph(graph):
+            self._launch(m, B, B, B, 0, 0, 0, 0)
+        self._pending, self.timers = saved, saved_timers
+        self._graph_timed = False
+        self.graphs[key] = (graph, events)
+
+    def _launch(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
+                dec_bytes: int) -> None:
+        s, w = self.shape, self.w
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         d = s.d_model
-        x, h = self.x[:T], self.h[:T]
+        x, h = self.x, self.h
         call = lib.call
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, st)
-        max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
-        max_ctx = int(b.dec_ctx.max()) if B else 0
-        # K3 algorithmic bytes per launch: every context row's K and V once + q in + out
-        dec_bytes = (int(b.dec_ctx.sum()) * 2 * s.kv_dim * 2 + 2 * B * s.q_dim * 2) if B else 0
         for i in range(s.layers):
-            self.gemm(h, w[f"l{i}.wqkv"], self.qkv[:T], st)
+            self.gemm(h[:T], w[f"l{i}.wqkv"], self.qkv[:T], st)
             call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]), _p(m["pos"]),
                  T, s.n_q, s.rope_theta, st)
             if B:
@@ -206,12 +271,12 @@ class Decoder:
                      _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
                 self._tock("attn_decode", ev, dec_bytes)
             if S:
-                call("stb_attn_prefill", self.pool.h, i, C.c_void_p(self.q[B:].data_ptr()),
-                     C.c_void_p(self.attn[B:].data_ptr()), _p(m["pre_slots"]), _p(m["pre_qstart"]),
-                     _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q, st)
+                call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
+                     _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
+                     st)
             self.gemm(self.attn[:T], w[f"l{i}.wo"], self.proj[:T], st)
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, st)
-            self.gemm(h, w[f"l{i}.w_gate_up"], self.gu[:T], st)
+            self.gemm(h[:T], w[f"l{i}.w_gate_up"], self.gu[:T], st)
             call("stb_silu_mul", _p(self.gu), _p(self.act), T, s.d_ff, st)
             self.gemm(self.act[:T], w[f"l{i}.w_down"], self.proj[:T], st)
             if i + 1 < s.layers:
@@ -225,24 +290,32 @@ class Decoder:
         self.gemm(rows, w["lm_head"], logits, st)
         call("stb_sample_forced", _p(logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
              _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), st)
-        if self.keep_logits:
-            self.last_logits = logits.clone()
-            self.last_raw_argmax = self.raw_arg[:R].clone()
-        return self.sampled[:R]
+
+    # -- timing (CUDA events on the launching stream; graph-safe) ----------------
 
     def _tick(self):
-        if self.timers is None:
+        if self.timers is None and not self._graph_timed:
             return None
-        ev = torch.cuda.Event(enable_timing=True)
+        ev = torch.cuda.Event(enable_timing=True, external=True)
         ev.record()
         return ev
 
     def _tock(self, name: str, ev0, work: int) -> None:
         if ev0 is None:
             return
-        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True, external=True)
         ev1.record()
-        self.timers.setdefault(name, []).append((ev0, ev1, work))
+        self._pending.append((name, ev0, ev1, work))
+
+    def collect(self) -> None:
+        """Fold finished event pairs into `timers` (call after the step synchronised)."""
+        if self.timers is not None:
+            for name, e0, e1, work in self._pending:
+                t = self.timers.setdefault(name, [0.0, 0, 0])
+                t[0] += e0.elapsed_time(e1)
+                t[1] += work
+                t[2] += 1
+        self._pending = []
 
     def gemm(self, a: torch.Tensor, wt: torch.Tensor, out: torch.Tensor, st: C.c_void_p) -> None:
         M, K = a.shape

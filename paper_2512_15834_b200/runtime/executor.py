@@ -141,6 +141,26 @@ class Runtime:
     def block_ids(self, seq) -> list[int]:
         return self.pool.blocks(seq.dev.slot)
 
+    def precapture(self, max_batch: int) -> None:
+        """Capture the decode-step CUDA graphs for B = 1..max_batch up front (timed and
+        untimed variants) against a scratch slot, so no capture lands in a timed run."""
+        scratch = self._free_slots.pop(0)  # highest slot id: the last one handed out
+        self.pool.reserve(scratch, 16)
+        z = np.zeros
+        for B in range(1, max_batch + 1):
+            one = np.full(B, scratch, dtype=np.int32)
+            batch = StepBatch(z(B, np.int32), z(B, np.int32), one, one, np.ones(B, np.int32), z(0, np.int32),
+                              z(1, np.int32), z(0, np.int32), np.arange(B, dtype=np.int32), np.full(B, -1, np.int32))
+            saved = self.dec.timers
+            for timers in (None, {}):
+                self.dec.timers = timers
+                self.dec.forward(batch)
+                torch.cuda.synchronize()
+                self.dec.collect()
+            self.dec.timers = saved
+        self.pool.release(scratch)
+        self._free_slots.insert(0, scratch)
+
     # -- phase entry points (called by B200Engine) ------------------------------
 
     def prefill(self, seq, cached: int, next_turn: int, done) -> None:
@@ -338,6 +358,7 @@ class Runtime:
         self.dec.keep_logits = self.record
         sampled_dev = self.dec.forward(batch)
         sampled = sampled_dev.tolist()
+        self.dec.collect()
         self.h2d_bytes += self.dec.h2d_bytes
         self.d2h_bytes += 4 * batch.R
         self.forwards += 1

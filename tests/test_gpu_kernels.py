@@ -52,7 +52,7 @@ def test_gemm_explicit_split(lib):
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     w = torch.randn(N, K, device="cuda").to(torch.bfloat16)
     ref = a.float() @ w.float().T
-    for split in (1, 2, 5, 64):
+    for split in (1, 2, 5, 64, 148):
         c = torch.full((M, N), float("nan"), device="cuda")
         lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, split, stream())
         assert rel(c, ref) < 2e-5, split

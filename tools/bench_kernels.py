@@ -1,0 +1,121 @@
+"""Kernel microbenchmarks (CUDA events, cold operands cycled past L2).
+
+GEMM: the decode- and prefill-shaped projections of a model shape.
+Decode attention: B sequences at a context length, K3 alone.
+Prints achieved GB/s (HBM-bound) or TFLOP/s against MEASURED_PEAKS.json.
+"""
+
+import argparse
+import ctypes as C
+import json
+import math
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_2512_15834_b200.modelcfg import SHAPES  # noqa: E402
+from paper_2512_15834_b200.runtime import lib  # noqa: E402
+
+PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {
+    "hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def P(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def st():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def time_it(fn, iters=40, warm=3):
+    """Device time per call: the loop is captured in a CUDA graph (no host launch cost)."""
+    for i in range(warm):
+        fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(iters):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters * 1e3  # us
+
+
+def bench_gemm(shape, M, split=0):
+    s = shape
+    gemms = {"qkv": (s.q_dim + 2 * s.kv_dim, s.d_model), "o": (s.d_model, s.q_dim),
+             "gate_up": (2 * s.d_ff, s.d_model), "down": (s.d_model, s.d_ff), "lm_head": (s.vocab, s.d_model)}
+    out = {}
+    for name, (N, K) in gemms.items():
+        copies = max(2, int(math.ceil(400e6 / (N * K * 2))))
+        ws = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) for _ in range(copies)]
+        a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+        c = torch.empty(M, N, device="cuda")
+        us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(ws[i % copies]), K, P(c), N, M, N, K, split, st()))
+        byts = N * K * 2 + M * K * 2 + M * N * 4
+        fl = 2 * M * N * K
+        out[name] = (us, byts / us / 1e3, fl / us / 1e6)
+        print(f"  M={M:5d} {name:8s} N={N:6d} K={K:5d}: {us:8.1f} us  {byts / us / 1e3:7.0f} GB/s "
+              f"({byts / us / 1e3 / PEAK['hbm_gbs']:.2f})  {fl / us / 1e6:7.1f} TF/s "
+              f"({fl / us / 1e6 / PEAK['bf16_tflops']:.2f})")
+        del ws
+    tot = sum(v[0] for v in out.values())
+    print(f"  M={M}: sum {tot:.1f} us")
+    return out
+
+
+def bench_attn(shape, B, ctx, reps=4):
+    from paper_2512_15834_b200.runtime.decoder import KVPool
+
+    s = shape
+    pages = B * (ctx // 16 + 1)
+    pools = []
+    for r in range(reps):  # several pools cycled so K/V are cold in L2
+        pool = KVPool(s.with_layers(1), pages + 16, B, ctx // 16 + 2)
+        for b in range(B):
+            pool.reserve(b, ctx)
+        pool.sync(torch.cuda.current_stream().cuda_stream)
+        pools.append(pool)
+    q = torch.randn(B, s.n_q, s.d_head, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty_like(q)
+    slots = torch.arange(B, dtype=torch.int32, device="cuda")
+    ctxs = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.load().stb_attn_decode_workspace(B, s.n_q, s.d_head) // 4, device="cuda")
+    sc = 1 / math.sqrt(s.d_head)
+    us = time_it(lambda i: lib.call("stb_attn_decode", pools[i % reps].h, 0, P(q), P(o), P(slots), P(ctxs), B, s.n_q,
+                                    sc, 0, P(ws), st()))
+    byts = B * ctx * 2 * s.kv_dim * 2 + 2 * B * s.q_dim * 2
+    print(f"  attn_decode B={B:3d} ctx={ctx:6d}: {us:8.1f} us  {byts / us / 1e3:7.0f} GB/s "
+          f"({byts / us / 1e3 / PEAK['hbm_gbs']:.2f})")
+    return us
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="llama3-8b")
+    ap.add_argument("--what", default="gemm,attn")
+    ap.add_argument("--M", default="32,2080")
+    ap.add_argument("--split", type=int, default=0)
+    args = ap.parse_args()
+    lib.load()
+    shape = SHAPES[args.shape]
+    if "gemm" in args.what:
+        for M in [int(x) for x in args.M.split(",")]:
+            bench_gemm(shape, M, args.split)
+    if "attn" in args.what:
+        for B, ctx in [(32, 2048), (32, 4096), (16, 32768), (1, 4096), (64, 4096)]:
+            bench_attn(shape, B, ctx)
+
+
+if __name__ == "__main__":
+    main()

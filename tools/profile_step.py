@@ -1,0 +1,78 @@
+"""Steady-state decode steps of the B200 engine, for ncu and kernel timing.
+
+Builds the engine on a shape, admits `--batch` requests whose script is one
+long reasoning turn, prefills them to `--ctx`, then runs decode steps. With
+`--profile`, cudaProfilerStart/Stop bracket the last `--profile-steps` steps so
+`ncu --profile-from-start off` captures only those launches.
+
+    ncu --profile-from-start off --metrics gpu__time_duration.sum --csv \
+        python tools/profile_step.py --profile
+"""
+
+import argparse
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+from paper_2512_15834_b200.domain import EOS, Token, TokenKind  # noqa: E402
+from paper_2512_15834_b200.engine import B200Engine, EngineConfig  # noqa: E402
+from paper_2512_15834_b200.mocks import GenerationScript  # noqa: E402
+from paper_2512_15834_b200.modelcfg import SHAPES  # noqa: E402
+from paper_2512_15834_b200.runtime.executor import BatchRuntime  # noqa: E402
+from paper_2512_15834_b200.runtime.realtime import RealtimeLoop  # noqa: E402
+
+
+class Quiet:
+    def on_turn_start(self, *a): pass
+    def on_emit(self, *a): pass
+    def on_ingest(self, *a): pass
+    def on_final(self, *a): pass
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="llama3-8b")
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--ctx", type=int, default=2048)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=3)
+    args = ap.parse_args()
+    shape = SHAPES[args.shape]
+    if args.layers:
+        shape = shape.with_layers(args.layers)
+    nb = args.batch * (args.ctx + 4096) // 16 + 64
+    rt = BatchRuntime(shape, init_device="cuda", num_blocks=nb, max_slots=max(64, args.batch),
+                      max_ctx=args.ctx + 8192, max_step_tokens=16384)
+    loop = RealtimeLoop()
+    eng = B200Engine(loop, EngineConfig(prefill_rate=0, decode_rate=0, batch_size=max(64, args.batch)), runtime=rt)
+    script = GenerationScript([[Token(TokenKind.TEXT, "mull ")] * 8000 + [EOS]])
+    for b in range(args.batch):
+        eng.submit_request(f"r{b}", script, args.ctx, Quiet())
+    while rt.runs:  # prefill
+        rt.step()
+    torch.cuda.synchronize()
+    times = []
+    for i in range(args.steps):
+        last = i >= args.steps - args.profile_steps
+        if args.profile and i == args.steps - args.profile_steps:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
+        t0 = time.perf_counter()
+        rt.step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        if args.profile and last and i == args.steps - 1:
+            torch.cuda.profiler.stop()
+    ms = sorted(times[len(times) // 3:])
+    print(f"{shape.name} B={args.batch} ctx~{args.ctx}: median step {ms[len(ms) // 2] * 1e3:.3f} ms "
+          f"({args.batch / ms[len(ms) // 2]:.0f} tok/s)")
+
+
+if __name__ == "__main__":
+    main()
