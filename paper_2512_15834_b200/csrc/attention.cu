@@ -140,6 +140,102 @@ __device__ __forceinline__ void page_step(const uint32_t (*qf)[4], uint32_t ks, 
   }
 }
 
+// NP consecutive pages (16*NP keys) per online-softmax update: S for all pages,
+// one max / exp / rescale, then P V over NP k-steps. `lim0/lim1` count the valid
+// keys of the chunk for the two rows this lane holds; full chunks skip masking.
+template <int D, int NP>
+__device__ __forceinline__ void chunk_step(const uint32_t (*qf)[4], uint32_t ks0, int lim0, int lim1, RowState<D>& st,
+                                           int lane) {
+  constexpr int PAGE = 16 * D * 2;
+  // pages past both rows' limits were never loaded: no S, no P V for them
+  const int lim = lim0 > lim1 ? lim0 : lim1;
+  float s[2 * NP][4];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const uint32_t ks = ks0 + p * 2 * PAGE;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      float* acc = s[p * 2 + nt];
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+      if (p > 0 && lim <= 16 * p) continue;
+#pragma unroll
+      for (int c0 = 0; c0 < D / 8; c0 += 4) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(ks + swz<D>(nt * 8 + (lane & 7), c0 + (lane >> 3)), b0, b1, b2, b3);
+        mma_bf16_16816(acc, qf[c0 / 2], b0, b1);
+        mma_bf16_16816(acc, qf[c0 / 2 + 1], b2, b3);
+      }
+    }
+  }
+  const int kc = (lane & 3) * 2;
+  if (lim0 < 16 * NP || lim1 < 16 * NP) {
+#pragma unroll
+    for (int t = 0; t < 2 * NP; ++t)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int k = t * 8 + kc + j;
+        if (k >= lim0) s[t][j] = -INFINITY;
+        if (k >= lim1) s[t][2 + j] = -INFINITY;
+      }
+  }
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < 2 * NP; ++t) {
+    mx0 = fmaxf(mx0, fmaxf(s[t][0], s[t][1]));
+    mx1 = fmaxf(mx1, fmaxf(s[t][2], s[t][3]));
+  }
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  const float mn0 = fmaxf(st.m[0], mx0), mn1 = fmaxf(st.m[1], mx1);
+  const float ref0 = mn0 == -INFINITY ? 0.f : mn0, ref1 = mn1 == -INFINITY ? 0.f : mn1;
+  const float a0 = exp2f(st.m[0] - ref0), a1 = exp2f(st.m[1] - ref1);
+  st.m[0] = mn0;
+  st.m[1] = mn1;
+  float rs0 = 0.f, rs1 = 0.f;
+  uint32_t pf[NP][4];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      float* v = s[p * 2 + nt];
+      v[0] = exp2f(v[0] - ref0);
+      v[1] = exp2f(v[1] - ref0);
+      v[2] = exp2f(v[2] - ref1);
+      v[3] = exp2f(v[3] - ref1);
+      rs0 += v[0] + v[1];
+      rs1 += v[2] + v[3];
+      pf[p][nt * 2 + 0] = pack_bf16(v[0], v[1]);
+      pf[p][nt * 2 + 1] = pack_bf16(v[2], v[3]);
+    }
+  }
+  st.l[0] = st.l[0] * a0 + rs0;
+  st.l[1] = st.l[1] * a1 + rs1;
+  if (a0 != 1.f || a1 != 1.f) {
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      st.o[n][0] *= a0;
+      st.o[n][1] *= a0;
+      st.o[n][2] *= a1;
+      st.o[n][3] *= a1;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    if (p > 0 && lim <= 16 * p) continue;
+    const uint32_t vs = ks0 + p * 2 * PAGE + PAGE;
+#pragma unroll
+    for (int d0 = 0; d0 < D / 8; d0 += 2) {
+      const int m = lane >> 3;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(vs + swz<D>((m & 1) * 8 + (lane & 7), d0 + (m >> 1)), b0, b1, b2, b3);
+      mma_bf16_16816(st.o[d0], pf[p], b0, b1);
+      mma_bf16_16816(st.o[d0 + 1], pf[p], b2, b3);
+    }
+  }
+}
+
 // Load a 16 x D query tile into A fragments; row r -> (src row pointer or null)
 template <int D>
 __device__ __forceinline__ void load_q(uint32_t (*qf)[4], const __nv_bfloat16* row_lo, const __nv_bfloat16* row_hi,
@@ -160,148 +256,208 @@ __device__ __forceinline__ void load_q(uint32_t (*qf)[4], const __nv_bfloat16* r
 }
 
 // ------------------------------------------------------------------ K3 decode
-// grid: (splits, n_kv, B); 4 warps; warp w walks pages start+w, start+w+4, ...
+// Stream-K over pages: the units (b, kv-head, page) of the whole step are laid
+// out b-major and cut into W equal contiguous ranges, one per warp (W = grid x 4,
+// grid = 2 x SMs, persistent). A warp streams its pages through a private
+// STAGES-deep cp.async ring *across* segment boundaries, keeping an online
+// softmax per (b, kv-head) segment. A segment that covers its whole pair is
+// written out directly; a pair split across warps gets a partial (o/l, lse)
+// from each contributor and the last one to finish (ticket) merges them, so no
+// separate merge launch and no wave tail, whatever the context lengths.
+constexpr int kMaxB = 1024;
+constexpr int kChunkPages = 2;  // pages (16 keys each) per online-softmax update
+constexpr int kMinChunks = 4;   // fewest chunks a warp is given (bounds merge fan-in)
+
+__device__ __forceinline__ int warp_of(int64_t u, int64_t U, int W) {
+  return (int)(((u + 1) * W + U - 1) / U) - 1;  // largest w with floor(U*w/W) <= u
+}
+
 template <int D, int G, int STAGES>
 __global__ void __launch_bounds__(128) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
-    const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int n_kv, float qscale,
-    float* __restrict__ o_part, float* __restrict__ lse_part) {
+    const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
+    float* __restrict__ o_part, float* __restrict__ lse_part, int* __restrict__ tickets) {
   pdl_wait();
   constexpr int PAGE = 16 * D * 2;
+  constexpr int NP = kChunkPages;
+  constexpr int STAGE = NP * 2 * PAGE;  // K and V of NP pages
   extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ int64_t prefix[kMaxB + 1];  // chunk units before sequence b
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, kh = blockIdx.y, b = blockIdx.z;
-  const int splits = gridDim.x;
   const int n_q = n_kv * G;
-  const int ctx = ctx_lens[b];
-  const int npages = (ctx + 15) >> 4;
-  // this sequence's pages are divided evenly over the splits (grid shape is
-  // independent of context lengths, so one CUDA graph serves every step of a batch size)
-  const int pages_per_split = (npages + splits - 1) / splits;
-  const int p0 = split * pages_per_split;
-  const int p1 = min(npages, p0 + pages_per_split);
-  const int32_t* row = table + (int64_t)slots[b] * max_bps;
-
-  uint32_t qf[D / 16][4];
-  {
-    int r0 = lane >> 2, r1 = r0 + 8;
-    const __nv_bfloat16* base = q + ((int64_t)b * n_q + kh * G) * D;
-    load_q<D>(qf, r0 < G ? base + r0 * D : nullptr, r1 < G ? base + r1 * D : nullptr, qscale, lane);
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int b = 0; b < B; ++b) {
+      prefix[b] = acc;
+      acc += (int64_t)n_kv * ((ctx_lens[b] + 16 * NP - 1) / (16 * NP));
+    }
+    prefix[B] = acc;
   }
-  RowState<D> st;
-  st.init();
+  __syncthreads();
+  pdl_launch();
+  const int64_t U = prefix[B];
+  const int W = (int)max((int64_t)1, min((int64_t)gridDim.x * 4, U / kMinChunks));
+  const int w = blockIdx.x * 4 + warp;
+  if (w >= W) return;
+  const int64_t u0 = U * w / W, u1 = U * (w + 1) / W;
+  const int n = (int)(u1 - u0);
+  if (n <= 0) return;
 
-  const uint32_t wbase = smem_u32(smem) + warp * STAGES * 2 * PAGE;
-  auto page_ptr = [&](int p, const __nv_bfloat16* pages) {
-    return pages + (((int64_t)row[p] * n_kv + kh) * 16) * D;
+  // cursor over (b, kh, chunk) — located once by binary search, then incremented
+  struct Cur {
+    int b, kh, c, chunks;
   };
-  // per-warp software pipeline over this warp's pages
-  int mine = p1 > p0 + warp ? (p1 - p0 - warp + 3) / 4 : 0;
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < mine) {
-      int p = p0 + warp + 4 * s;
-      load_page<D>(wbase + s * 2 * PAGE, wbase + s * 2 * PAGE + PAGE, page_ptr(p, kpages), page_ptr(p, vpages), lane);
+  auto locate = [&](int64_t u) {
+    int lo = 0, hi = B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= u) lo = mid; else hi = mid - 1;
     }
-    cp_async_commit();
-  }
-  for (int i = 0; i < mine; ++i) {
-    cp_async_wait<STAGES - 2>();
-    __syncwarp();
-    int stage = i % STAGES;
-    int p = p0 + warp + 4 * i;
-    int lim = ctx - p * 16;
-    page_step<D>(qf, wbase + stage * 2 * PAGE, wbase + stage * 2 * PAGE + PAGE, lim, lim, st, lane);
-    __syncwarp();
-    int nx = i + STAGES - 1;
-    if (nx < mine) {
-      int pn = p0 + warp + 4 * nx;
-      int sn = nx % STAGES;
-      load_page<D>(wbase + sn * 2 * PAGE, wbase + sn * 2 * PAGE + PAGE, page_ptr(pn, kpages), page_ptr(pn, vpages),
-                   lane);
-    }
-    cp_async_commit();
-  }
-  cp_async_wait<0>();
-  // quad-reduce row sums (lanes of a quad hold disjoint keys)
+    Cur r;
+    r.b = lo;
+    r.chunks = (ctx_lens[lo] + 16 * NP - 1) / (16 * NP);
+    const int rem = (int)(u - prefix[lo]);
+    r.kh = rem / r.chunks;
+    r.c = rem - r.kh * r.chunks;
+    return r;
+  };
+  auto advance = [&](Cur& r) {
+    if (++r.c < r.chunks) return;
+    r.c = 0;
+    if (++r.kh < n_kv) return;
+    r.kh = 0;
+    do {
+      ++r.b;
+      r.chunks = r.b < B ? (ctx_lens[r.b] + 16 * NP - 1) / (16 * NP) : 1;
+    } while (r.b < B && r.chunks == 0);
+  };
+  const uint32_t wbase = smem_u32(smem) + warp * STAGES * STAGE;
+  auto issue = [&](const Cur& r, int i) {
+    const int32_t* row = table + (int64_t)slots[r.b] * max_bps;
+    const int npages = (ctx_lens[r.b] + 15) >> 4;
+    const uint32_t sb = wbase + (i % STAGES) * STAGE;
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    st.l[j] += __shfl_xor_sync(0xffffffffu, st.l[j], 1);
-    st.l[j] += __shfl_xor_sync(0xffffffffu, st.l[j], 2);
-  }
-  __syncthreads();
-  // merge the 4 warps: smem[w] = {m[16], l[16], o[16][D]}
-  float* red = reinterpret_cast<float*>(smem);
-  constexpr int WSTRIDE = 32 + 16 * D;
-  float* mine_red = red + warp * WSTRIDE;
-  if ((lane & 3) == 0) {
-    mine_red[lane >> 2] = st.m[0];
-    mine_red[(lane >> 2) + 8] = st.m[1];
-    mine_red[16 + (lane >> 2)] = st.l[0];
-    mine_red[16 + (lane >> 2) + 8] = st.l[1];
-  }
-#pragma unroll
-  for (int n = 0; n < D / 8; ++n) {
-    int r = lane >> 2, c = n * 8 + (lane & 3) * 2;
-    mine_red[32 + r * D + c] = st.o[n][0];
-    mine_red[32 + r * D + c + 1] = st.o[n][1];
-    mine_red[32 + (r + 8) * D + c] = st.o[n][2];
-    mine_red[32 + (r + 8) * D + c + 1] = st.o[n][3];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
-    int r = e / D, d = e % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[w * WSTRIDE + r]);
-    float L = 0.f, acc = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        float wt = exp2f(red[w * WSTRIDE + r] - M);
-        L += wt * red[w * WSTRIDE + 16 + r];
-        acc += wt * red[w * WSTRIDE + 32 + r * D + d];
+    for (int p = 0; p < NP; ++p) {
+      const int page = r.c * NP + p;
+      if (page < npages) {
+        const int64_t off = (((int64_t)row[page] * n_kv + r.kh) * 16) * D;
+        load_page<D>(sb + p * 2 * PAGE, sb + p * 2 * PAGE + PAGE, kpages + off, vpages + off, lane);
       }
     }
-    int h = kh * G + r;
-    if (splits == 1) {
-      out[((int64_t)b * n_q + h) * D + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
-    } else {
-      int64_t idx = ((int64_t)b * n_q + h) * splits + split;
-      o_part[idx * D + d] = L > 0.f ? acc / L : 0.f;
-      if (d == 0) lse_part[idx] = L > 0.f ? M + log2f(L) : -INFINITY;
+  };
+  Cur ld = locate(u0);
+#pragma unroll
+  for (int s2 = 0; s2 < STAGES - 1; ++s2) {
+    if (s2 < n) {
+      issue(ld, s2);
+      advance(ld);
     }
+    cp_async_commit();
   }
-}
-
-// merge split partials: one warp per (b, head)
-template <int D>
-__global__ void attn_merge_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
-                                  __nv_bfloat16* __restrict__ out, int rows, int splits) {
-  pdl_wait();
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const float* lse = lse_part + (int64_t)warp * splits;
-  float M = -INFINITY;
-  for (int s = lane; s < splits; s += 32) M = fmaxf(M, lse[s]);
-  M = warp_max(M);
-  float acc[D / 32];
-#pragma unroll
-  for (int j = 0; j < D / 32; ++j) acc[j] = 0.f;
-  float L = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < splits; ++s) {
-      float w = exp2f(lse[s] - M);
-      L += w;
-      const float* o = o_part + ((int64_t)warp * splits + s) * D;
-#pragma unroll
-      for (int j = 0; j < D / 32; ++j) acc[j] += w * o[j * 32 + lane];
+  Cur cu = locate(u0);
+  uint32_t qf[D / 16][4];
+  RowState<D> st;
+  bool open = false;
+  int seg_first = 0, seg_ctx = 0;
+  int64_t seg_start = u0;
+  for (int i = 0; i < n; ++i) {
+    if (!open) {
+      open = true;
+      seg_first = cu.c;
+      seg_ctx = ctx_lens[cu.b];
+      seg_start = u0 + i;
+      const int r0 = lane >> 2, r1 = r0 + 8;
+      const __nv_bfloat16* qb = q + ((int64_t)cu.b * n_q + cu.kh * G) * D;
+      load_q<D>(qf, r0 < G ? qb + r0 * D : nullptr, r1 < G ? qb + r1 * D : nullptr, qscale, lane);
+      st.init();
     }
-  }
+    cp_async_wait<STAGES - 2>();
+    __syncwarp();
+    const int lim = seg_ctx - cu.c * 16 * NP;
+    chunk_step<D, NP>(qf, wbase + (i % STAGES) * STAGE, lim, lim, st, lane);
+    __syncwarp();
+    if (i + STAGES - 1 < n) {
+      issue(ld, i + STAGES - 1);
+      advance(ld);
+    }
+    cp_async_commit();
+    const bool pair_end = cu.c == cu.chunks - 1;
+    if (pair_end || i == n - 1) {
+      // close the segment of pair (cu.b, cu.kh)
+      float l0 = st.l[0], l1 = st.l[1];
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+      const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+      const int r0 = lane >> 2, r1 = r0 + 8;
+      const int sb = cu.b, skh = cu.kh;
+      if (seg_first == 0 && pair_end) {
 #pragma unroll
-  for (int j = 0; j < D / 32; ++j)
-    out[(int64_t)warp * D + j * 32 + lane] = __float2bfloat16_rn(L > 0.f ? acc[j] / L : 0.f);
+        for (int nd = 0; nd < D / 8; ++nd) {
+          const int c = nd * 8 + (lane & 3) * 2;
+          if (r0 < G)
+            *reinterpret_cast<uint32_t*>(out + ((int64_t)sb * n_q + skh * G + r0) * D + c) =
+                pack_bf16(st.o[nd][0] * inv0, st.o[nd][1] * inv0);
+          if (r1 < G)
+            *reinterpret_cast<uint32_t*>(out + ((int64_t)sb * n_q + skh * G + r1) * D + c) =
+                pack_bf16(st.o[nd][2] * inv1, st.o[nd][3] * inv1);
+        }
+      } else {
+        const int slot = w * 2 + (seg_start == u0 ? 0 : 1);
+        float* op = o_part + (int64_t)slot * G * D;
+#pragma unroll
+        for (int nd = 0; nd < D / 8; ++nd) {
+          const int c = nd * 8 + (lane & 3) * 2;
+          if (r0 < G)
+            __stcg(reinterpret_cast<float2*>(op + r0 * D + c), make_float2(st.o[nd][0] * inv0, st.o[nd][1] * inv0));
+          if (r1 < G)
+            __stcg(reinterpret_cast<float2*>(op + r1 * D + c), make_float2(st.o[nd][2] * inv1, st.o[nd][3] * inv1));
+        }
+        if ((lane & 3) == 0) {
+          if (r0 < G) __stcg(lse_part + slot * G + r0, l0 > 0.f ? st.m[0] + log2f(l0) : -INFINITY);
+          if (r1 < G) __stcg(lse_part + slot * G + r1, l1 > 0.f ? st.m[1] + log2f(l1) : -INFINITY);
+        }
+        __threadfence();
+        __syncwarp();
+        const int64_t pstart = prefix[sb] + (int64_t)skh * cu.chunks;
+        const int wf = warp_of(pstart, U, W), wl = warp_of(pstart + cu.chunks - 1, U, W);
+        int last = 0;
+        if (lane == 0) last = atomicAdd(&tickets[sb * n_kv + skh], 1) == wl - wf;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();
+          for (int r = 0; r < G; ++r) {
+            float M = -INFINITY;
+            for (int c = wf; c <= wl; ++c) {
+              const int sl = c * 2 + ((c == wf && (U * c / W) < pstart) ? 1 : 0);
+              M = fmaxf(M, __ldcg(lse_part + sl * G + r));
+            }
+            float L = 0.f, acc[D / 32];
+#pragma unroll
+            for (int j = 0; j < D / 32; ++j) acc[j] = 0.f;
+            if (M != -INFINITY) {
+              for (int c = wf; c <= wl; ++c) {
+                const int sl = c * 2 + ((c == wf && (U * c / W) < pstart) ? 1 : 0);
+                const float wt = exp2f(__ldcg(lse_part + sl * G + r) - M);
+                L += wt;
+#pragma unroll
+                for (int j = 0; j < D / 32; ++j) acc[j] += wt * __ldcg(o_part + ((int64_t)sl * G + r) * D + j * 32 + lane);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < D / 32; ++j)
+              out[((int64_t)sb * n_q + skh * G + r) * D + j * 32 + lane] = __float2bfloat16_rn(L > 0.f ? acc[j] / L : 0.f);
+          }
+          if (lane == 0) tickets[sb * n_kv + skh] = 0;
+        }
+      }
+      open = false;
+    }
+    advance(cu);
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------- short-run prefill
@@ -315,6 +471,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
     const int32_t* __restrict__ slots, const int32_t* __restrict__ q_start, const int32_t* __restrict__ ctx_lens,
     int n_kv, float qscale) {
   pdl_wait();
+  pdl_launch();
   constexpr int PAGE = 16 * D * 2;
   constexpr int QPW = 16 / G;  // queries per warp tile
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -402,36 +559,55 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
 constexpr int kDecodeStages = 3;
 constexpr int kPrefillStages = 3;
 
+struct DecodeScratch {
+  float* part = nullptr;  // [W*2][G][D] partial o + [W*2][G] lse
+  int* tickets = nullptr;
+  size_t floats = 0;
+  int n_tickets = 0;
+};
+
 template <int D, int G>
 int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
-                  float qscale, int max_ctx, float* work, cudaStream_t st) {
+                  float qscale, cudaStream_t st) {
+  static DecodeScratch sc;
+  if (B > kMaxB) return fail(STB_EINVAL, "attn_decode: at most %d sequences per step", kMaxB);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // ~3 CTAs per SM in flight; max_ctx (when known, > 0) caps splits at >= 4 pages each
-  int pairs = B * n_kv;
-  int splits = (3 * sms + pairs - 1) / pairs;
-  if (max_ctx > 0) {
-    int cap = ((max_ctx + 15) / 16 + 3) / 4;
-    if (splits > cap) splits = cap;
+  const int grid = (2 * (4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 8 * (kMaxB + 1)) <= 220 * 1024 ? 2 : 1) * sms;
+  const int W = grid * 4;
+  const size_t need = (size_t)W * 2 * G * (D + 1);
+  const int pairs = B * n_kv;
+  if (need > sc.floats || pairs > sc.n_tickets) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      return fail(STB_EINVAL, "attn_decode: scratch growth during graph capture");
+    if (need > sc.floats) {
+      if (sc.part) cudaFree(sc.part);
+      if (cudaMalloc(&sc.part, need * sizeof(float)) != cudaSuccess) return fail(STB_ENOMEM, "attn_decode scratch");
+      sc.floats = need;
+    }
+    if (pairs > sc.n_tickets) {
+      if (sc.tickets) cudaFree(sc.tickets);
+      int nt = pairs * 2 + 256;
+      if (cudaMalloc(&sc.tickets, nt * sizeof(int)) != cudaSuccess || cudaMemset(sc.tickets, 0, nt * sizeof(int)))
+        return fail(STB_ENOMEM, "attn_decode tickets");
+      sc.n_tickets = nt;
+    }
   }
-  if (splits > 64) splits = 64;
-  if (splits < 1) splits = 1;
-  size_t smem = (size_t)4 * kDecodeStages * 2 * 16 * D * 2;
-  size_t red = (size_t)4 * (32 + 16 * D) * 4;
-  if (red > smem) smem = red;
+  constexpr size_t smem = (size_t)4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
   auto kern = attn_decode_kernel<D, G, kDecodeStages>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  float* o_part = work;
-  float* lse_part = work + (size_t)B * n_kv * G * 64 * D;
-  launch_k(kern, dim3(splits, n_kv, B), dim3(128), smem, st, q, out, kp, vp, table, max_bps, slots, ctx, n_kv, qscale, o_part,
-                                                 lse_part);
-  if (splits > 1) {
-    int rows = B * n_kv * G;
-    launch_k(attn_merge_kernel<D>, dim3((rows * 32 + 255) / 256), dim3(256), 0, st, o_part, lse_part, out, rows, splits);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
   }
-  STB_CHECK_LAUNCH("attn_decode");
+  float* o_part = sc.part;
+  float* lse_part = sc.part + (size_t)W * 2 * G * D;
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(128), smem, st, q, out, kp, vp, table, max_bps, slots, ctx, B, n_kv,
+                           qscale, o_part, lse_part, sc.tickets);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "attn_decode launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
 
@@ -476,7 +652,7 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
   auto* kk = (const __nv_bfloat16*)kp;
   auto* vv = (const __nv_bfloat16*)vp;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, max_ctx, (float*)work, st
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, st
   if (d_head == 128 && g == 4) return launch_decode<128, 4>(ARGS);
   if (d_head == 128 && g == 8) return launch_decode<128, 8>(ARGS);
   if (d_head == 128 && g == 1) return launch_decode<128, 1>(ARGS);

@@ -57,6 +57,7 @@ static void table_set(stb_kv_pool* p, int slot, int idx, int32_t value) {
 
 __global__ void apply_updates_kernel(const int32_t* __restrict__ upd, int n, int32_t* __restrict__ table) {
   pdl_wait();
+  pdl_launch();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) table[upd[2 * i]] = upd[2 * i + 1];
 }
@@ -68,6 +69,7 @@ __global__ void kv_commit_kernel(const __nv_bfloat16* __restrict__ k, const __nv
                                  const int32_t* __restrict__ table, int max_bps, __nv_bfloat16* __restrict__ kpages,
                                  __nv_bfloat16* __restrict__ vpages, int n_kv, int d_head) {
   pdl_wait();
+  pdl_launch();
   const int chunks = n_kv * d_head / 8;  // 8 bf16 per 16 bytes
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)n * 2 * chunks;
@@ -88,6 +90,7 @@ __global__ void kv_copy_blocks_kernel(__nv_bfloat16* __restrict__ pages, const i
                                       const int32_t* __restrict__ dst, int n, int64_t block_elems, int64_t half_elems,
                                       int layers) {
   pdl_wait();
+  pdl_launch();
   // grid.y = block pair, grid.z = layer*2 + {K,V}; threads stride the block in 16B vectors
   int pair = blockIdx.y;
   int lz = blockIdx.z;
@@ -106,6 +109,7 @@ __global__ void qkv_rope_commit_kernel(const float* __restrict__ qkv, __nv_bfloa
                                        const int32_t* __restrict__ table, int max_bps,
                                        __nv_bfloat16* __restrict__ kpages, __nv_bfloat16* __restrict__ vpages) {
   pdl_wait();
+  pdl_launch();
   const int half = d_head / 2;
   const int groups = half / 8;
   const int heads = n_q + 2 * n_kv;
@@ -181,6 +185,8 @@ int stb_kv_pool_create(int device, int layers, int n_kv, int d_head, int block_s
     cudaGetLastError();
     return fail(STB_ENOMEM, "kv_pool_create: cannot allocate %zu bytes of pages", bytes);
   }
+  // zeroed once so rows never written (page tails) are finite for masked P*V
+  cudaMemset(p->pages, 0, bytes);
   size_t tbytes = (size_t)max_slots * max_blocks_per_slot * sizeof(int32_t);
   if (cudaMalloc(&p->dev_table, tbytes) != cudaSuccess || cudaMemset(p->dev_table, 0, tbytes) != cudaSuccess) {
     cudaFree(p->pages);

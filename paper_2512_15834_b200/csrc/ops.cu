@@ -17,6 +17,7 @@ namespace {
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
                              float* __restrict__ x, int n, int d) {
   pdl_wait();
+  pdl_launch();
   int t = blockIdx.x;
   const __nv_bfloat16* row = table + (int64_t)ids[t] * d;
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
@@ -49,6 +50,7 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restric
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int d,
                                    float eps, const int32_t* __restrict__ gather) {
   pdl_wait();
+  pdl_launch();
   __shared__ float red[32];
   int t = blockIdx.x;
   int src = gather ? gather[t] : t;
@@ -80,6 +82,7 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restric
 
 __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f) {
   pdl_wait();
+  pdl_launch();
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   int64_t total = (int64_t)n * f;
   if (i >= total) return;
@@ -142,6 +145,7 @@ __global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t l
                                      int* __restrict__ tickets, int32_t* __restrict__ out,
                                      int32_t* __restrict__ raw_arg, float* __restrict__ raw_max) {
   pdl_wait();
+  pdl_launch();
   __shared__ ArgPart sm[32];
   __shared__ int last;
   const int r = blockIdx.x / CH, ch = blockIdx.x % CH;
@@ -198,6 +202,7 @@ __global__ void spec_validate_kernel(const int32_t* __restrict__ draft, const in
                                      const int32_t* __restrict__ base_extra, int S, int32_t* __restrict__ accepted,
                                      int32_t* __restrict__ consume, int32_t* __restrict__ new_len) {
   pdl_wait();
+  pdl_launch();
   int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (s >= S) return;
