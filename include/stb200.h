@@ -98,15 +98,17 @@ int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, con
 
 /* ---- K4: speculation validation (greedy LCP, bit-exact int32) -----------
  * Replaces validate_draft (engine.py:96-111) + the consume rule (engine.py:291).
- * For sequence s: draft ids [d_off[s], d_off[s+1]), model ids (what the
- * verify pass sampled at each draft position) [m_off[s], m_off[s+1]),
- * span_len[s]. accepted = LCP(draft, model) clamped to span_len;
+ * For sequence s: draft ids [d_off[s], d_off[s+1]); the model's ids at the
+ * draft positions are model_first[s] (if >= 0: a token sampled by an earlier
+ * step) followed by the verify pass's samples model[m_off[s] .. m_off[s+1]);
+ * span_len[s]. accepted = LCP(draft, model ids) clamped to span_len;
  * consume = span_len if accepted == span_len else accepted + 1;
  * new_len[s] = kv_len[s] + accepted + base_extra[s] (KV rows that survive
- * rollback). */
+ * rollback). model_first may be NULL. */
 int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t* model, const int32_t* m_off,
-                      const int32_t* span_len, const int32_t* kv_len, const int32_t* base_extra, int S,
-                      int32_t* accepted, int32_t* consume, int32_t* new_len, void* stream);
+                      const int32_t* model_first, const int32_t* span_len, const int32_t* kv_len,
+                      const int32_t* base_extra, int S, int32_t* accepted, int32_t* consume, int32_t* new_len,
+                      void* stream);
 
 /* ---- K5: bf16 tensor-core GEMM (tcgen05 + TMA + TMEM) --------------------
  * C[M][N] (fp32, row stride ldc) = A[M][K] (bf16, lda) * W[N][K]^T (bf16, ldw).

@@ -12,6 +12,8 @@
 // query heads that share a kv head are rows of one 16-row MMA tile, so each K/V
 // page is read from HBM exactly once per step for the whole group. Softmax is
 // online (exp2 domain) with quad shuffles; rows of one warp live in one quad.
+#include <cstdlib>
+
 #include "../../include/stb200.h"
 #include "common.cuh"
 #include "pool.cuh"
@@ -672,6 +674,13 @@ int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, con
   int max_bps;
   stb_kv_block_table(pool, &table, &max_bps);
   if (S <= 0 || T <= 0) return STB_OK;
+  // tcgen05/TMEM path unless explicitly pinned to the warp-MMA kernel (A/B checks)
+  static int use_mma = -1;
+  if (use_mma < 0) {
+    const char* e = getenv("STB200_PREFILL");
+    use_mma = (e && e[0] == 'm') ? 1 : 0;
+  }
+  if (!use_mma) return stb_attn_prefill_tc(pool, layer, q, out, slots, q_start, ctx_lens, S, T, n_q, scale, max_q, stream);
   int n_kv, d_head;
   stb_pool_geometry(pool, &n_kv, &d_head);
   if (n_q % n_kv) return fail(STB_EINVAL, "attn_prefill: n_q %% n_kv != 0");

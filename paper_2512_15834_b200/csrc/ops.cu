@@ -198,6 +198,7 @@ __global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t l
 // K4: one warp per sequence
 __global__ void spec_validate_kernel(const int32_t* __restrict__ draft, const int32_t* __restrict__ d_off,
                                      const int32_t* __restrict__ model, const int32_t* __restrict__ m_off,
+                                     const int32_t* __restrict__ model_first,
                                      const int32_t* __restrict__ span_len, const int32_t* __restrict__ kv_len,
                                      const int32_t* __restrict__ base_extra, int S, int32_t* __restrict__ accepted,
                                      int32_t* __restrict__ consume, int32_t* __restrict__ new_len) {
@@ -207,7 +208,9 @@ __global__ void spec_validate_kernel(const int32_t* __restrict__ draft, const in
   int lane = threadIdx.x & 31;
   if (s >= S) return;
   int dl = d_off[s + 1] - d_off[s];
-  int ml = m_off[s + 1] - m_off[s];
+  const int first = model_first ? model_first[s] : -1;
+  const int lead = first >= 0 ? 1 : 0;
+  int ml = m_off[s + 1] - m_off[s] + lead;
   int sl = span_len[s];
   int n = min(min(dl, ml), sl);
   const int32_t* d = draft + d_off[s];
@@ -215,7 +218,8 @@ __global__ void spec_validate_kernel(const int32_t* __restrict__ draft, const in
   int acc = n;
   for (int base = 0; base < n; base += 32) {
     int i = base + lane;
-    bool miss = i < n && d[i] != m[i];
+    bool miss = false;
+    if (i < n) miss = d[i] != (i < lead ? first : m[i - lead]);
     unsigned bal = __ballot_sync(0xffffffffu, miss);
     if (bal) {
       acc = base + __ffs(bal) - 1;
@@ -290,12 +294,13 @@ int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, in
 }
 
 int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t* model, const int32_t* m_off,
-                      const int32_t* span_len, const int32_t* kv_len, const int32_t* base_extra, int S,
-                      int32_t* accepted, int32_t* consume, int32_t* new_len, void* stream) {
+                      const int32_t* model_first, const int32_t* span_len, const int32_t* kv_len,
+                      const int32_t* base_extra, int S, int32_t* accepted, int32_t* consume, int32_t* new_len,
+                      void* stream) {
   if (S <= 0) return STB_OK;
   int threads = 128;
   int blocks = (S * 32 + threads - 1) / threads;
-  launch_k(spec_validate_kernel, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, draft, d_off, model, m_off, span_len, kv_len,
+  launch_k(spec_validate_kernel, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream, draft, d_off, model, m_off, model_first, span_len, kv_len,
                                                                      base_extra, S, accepted, consume, new_len);
   STB_CHECK_LAUNCH("spec_validate");
   return STB_OK;

@@ -142,10 +142,15 @@ class Decoder:
         self._graph_timed = False
         self.last_logits: torch.Tensor | None = None
         self.last_raw_argmax: torch.Tensor | None = None
-        self.meta_host = torch.empty(self.META_CAP, dtype=torch.int32, pin_memory=True)
+        # double-buffered pinned step records: the runtime keeps one step in flight, so the
+        # record of step k+1 is written while step k's upload may still be pending
+        self.meta_host = [torch.empty(self.META_CAP, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self.meta_ev: list = [None, None]
+        self.meta_flip = 0
         self.meta_dev = torch.empty(self.META_CAP, dtype=torch.int32, device=device)
         self.h2d_bytes = 0
         self.graph_replays = 0
+        self._timed_parity = 0
         self.step_events: list | None = None  # (ev0, ev1, graphed, T) bracketing each step's kernels
 
     # -- buffers ----------------------------------------------------------------
@@ -183,7 +188,11 @@ class Decoder:
 
     def _upload(self, b: StepBatch) -> dict[str, int]:
         """Write the step record into pinned memory, one async H2D into the static buffer."""
-        hv = self.meta_host.numpy()
+        k = self.meta_flip
+        self.meta_flip ^= 1
+        if self.meta_ev[k] is not None:
+            self.meta_ev[k].synchronize()
+        hv = self.meta_host[k].numpy()
         off, spans = 0, {}
         for name in FIELDS:
             a = getattr(b, name)
@@ -193,7 +202,10 @@ class Decoder:
             off += n
         if off > self.META_CAP:
             raise ValueError("step record exceeds the static metadata buffer")
-        self.meta_dev[:off].copy_(self.meta_host[:off], non_blocking=True)
+        self.meta_dev[:off].copy_(self.meta_host[k][:off], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.meta_ev[k] = ev
         self.h2d_bytes = 4 * off
         base = self.meta_dev.data_ptr()
         return {k: base + 4 * o for k, o in spans.items()}
@@ -217,7 +229,13 @@ class Decoder:
             self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
         else:
             timed = self.timers is not None
-            key = (B, timed)
+            # timed graphs carry their own event nodes: two copies alternate so a step's
+            # events are not re-recorded while the runtime still has that step in flight
+            par = 0
+            if timed:
+                par = self._timed_parity
+                self._timed_parity ^= 1
+            key = (B, timed, par)
             if key not in self.graphs:
                 self._capture(key, m, B)
             graph, events = self.graphs[key]
@@ -307,15 +325,23 @@ class Decoder:
         ev1.record()
         self._pending.append((name, ev0, ev1, work))
 
-    def collect(self) -> None:
-        """Fold finished event pairs into `timers` (call after the step synchronised)."""
-        if self.timers is not None:
-            for name, e0, e1, work in self._pending:
-                t = self.timers.setdefault(name, [0.0, 0, 0])
+    def take_pending(self) -> list:
+        """Detach the event pairs of the step just launched (completed later)."""
+        pend, self._pending = self._pending, []
+        return pend
+
+    def fold(self, pending: list, sink: dict | None = None) -> None:
+        """Fold finished event pairs into `sink` (default `timers`) after their step synchronised."""
+        sink = self.timers if sink is None else sink
+        if sink is not None:
+            for name, e0, e1, work in pending:
+                t = sink.setdefault(name, [0.0, 0, 0])
                 t[0] += e0.elapsed_time(e1)
                 t[1] += work
                 t[2] += 1
-        self._pending = []
+
+    def collect(self) -> None:
+        self.fold(self.take_pending())
 
     def gemm(self, a: torch.Tensor, wt: torch.Tensor, out: torch.Tensor, st: C.c_void_p) -> None:
         M, K = a.shape

@@ -15,14 +15,21 @@ Phase work (what each reference charge becomes):
   emit     n tokens: an uncounted pend is emitted for free, every other token
            is one decode step (feed pend, sample the next scripted token)
   verify   one append-prefill over [pend?] + draft -> sampled ids at every
-           draft position -> K4 LCP -> rollback (truncate) of rejected rows
+           draft position -> K4 LCP on the device -> rollback (truncate) of the
+           rejected rows' blocks
   ingest   one append-prefill over [pend?] + tool-output ids, in place
   evict    truncate to the retained prefix (prefix cache) or release
 
-`EagerRuntime` runs each phase to completion immediately, one sequence per
-forward (virtual-time parity mode). `BatchRuntime` queues phases as jobs and
-`step()` packs every runnable job of every resident sequence into one forward
-(wall-clock continuous batching; decode jobs advance one token per step).
+Every forward is a *flight*: `_launch` packs the step, enqueues the forward,
+the K4 validation of its verify runs and one async D2H of the sampled ids
+(+ K4 results) into pinned memory; `_complete` waits for that copy, checks
+every forced sample against its script target and fires the phase
+callbacks. `EagerRuntime` completes each flight at once (virtual-time parity
+mode, one sequence per forward). `BatchRuntime` keeps one flight in the air:
+decode tokens advance optimistically at launch (their targets are the
+script; the completion check raises on any mismatch), so step k+1 is packed
+and launched while step k runs; a sequence with a run in flight (prefill /
+verify / ingest) sits out until that run completes.
 """
 
 from __future__ import annotations
@@ -52,6 +59,7 @@ class SeqDev:
     counted: bool = False
     hist: list[int] = field(default_factory=list)  # id fed at each physical row
     replay: list[int] = field(default_factory=list)
+    busy: bool = False                              # a run of this sequence is in flight
 
     @property
     def kv_tokens(self) -> int:
@@ -68,13 +76,18 @@ def _turn_first(seq, turn: int, table: TokenTable) -> int:
 # ------------------------------------------------------------------- jobs
 
 class Run:
-    """A contiguous run of input ids appended at `start`; samples some rows."""
+    """A contiguous run of input ids appended at `start`; samples some rows.
 
-    __slots__ = ("seq", "ids", "start", "rows", "targets", "on_done")
+    With `verify` = (draft ids, span_len, lead, model_first) the run is a
+    validation pass: K4 compares the draft with the model's ids (model_first
+    if >= 0, then the sampled rows) and `on_done` receives
+    (accepted, consume, new_len, sampled rows)."""
 
-    def __init__(self, seq, ids: list[int], start: int, rows: list[int], targets: list[int], on_done):
+    __slots__ = ("seq", "ids", "start", "rows", "targets", "on_done", "verify")
+
+    def __init__(self, seq, ids, start, rows, targets, on_done, verify=None):
         self.seq, self.ids, self.start = seq, ids, start
-        self.rows, self.targets, self.on_done = rows, targets, on_done
+        self.rows, self.targets, self.on_done, self.verify = rows, targets, on_done, verify
 
 
 class Decode:
@@ -86,8 +99,13 @@ class Decode:
         self.seq, self.targets, self.k, self.on_done = seq, targets, 0, on_done
 
 
+class Flight:
+    __slots__ = ("batch", "decodes", "runs", "event", "host", "n_sampled", "n_verify", "logits", "raw", "finished",
+                 "timers")
+
+
 class Runtime:
-    """Common state machine; subclasses decide when forwards run."""
+    """Common state machine; subclasses decide when flights complete."""
 
     def __init__(self, shape: ModelShape, *, seed: int = 0, num_blocks: int = 4096, max_slots: int = 1024,
                  max_ctx: int = 8192, init_device: str = "cpu", weights: dict | None = None,
@@ -102,12 +120,19 @@ class Runtime:
         self.max_ctx = max_ctx
         self._free_slots = list(range(max_slots - 1, -1, -1))
         self.record = record
-        self.trace: list[dict] = []     # per forward row: rid, pos, target, sampled, logits (if record)
+        self.trace: list[dict] = []     # per sampled row: rid, pos, fed, target, sampled, logits (record mode)
         self.forwards = 0
         self.tokens_fed = 0
         self.emitted = 0                # tokens sampled and counted (reference kv_tokens += ...)
         self.h2d_bytes = 0              # per-step metadata uploads (ids, positions, tables, drafts)
         self.d2h_bytes = 0              # sampled ids / validation results read back
+        # double-buffered pinned results (one flight may be in the air) + K4 staging
+        self._host = [torch.empty(1 << 16, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self._vstage = [torch.empty(1 << 16, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self._host_ev: list = [None, None]
+        self._flip = 0
+        self._vdev = torch.empty(1 << 16, dtype=torch.int32, device="cuda")   # K4 inputs
+        self._vout = torch.empty(3 * 4096, dtype=torch.int32, device="cuda")  # K4 outputs
 
     # -- vocabulary ------------------------------------------------------------
 
@@ -152,7 +177,7 @@ class Runtime:
             batch = StepBatch(z(B, np.int32), z(B, np.int32), one, one, np.ones(B, np.int32), z(0, np.int32),
                               z(1, np.int32), z(0, np.int32), np.arange(B, dtype=np.int32), np.full(B, -1, np.int32))
             saved = self.dec.timers
-            for timers in (None, {}):
+            for timers in (None, {}, {}):  # untimed + both timed parities
                 self.dec.timers = timers
                 self.dec.forward(batch)
                 torch.cuda.synchronize()
@@ -221,26 +246,26 @@ class Runtime:
         # is pend (uncounted case, i == 0) or the sample of the row feeding slot i-1
         off = 0 if d.counted else 1
         targets = [span[j + off] if j + off < len(span) else -1 for j in range(len(inputs))]
-        rows = list(range(len(inputs)))
-        pend_uncounted = None if d.counted else d.pend
+        first = -1 if d.counted else d.pend
+        start = d.kv_len
 
-        def finish(sampled: list[int], dev_sampled: torch.Tensor) -> None:
-            model = ([pend_uncounted] if pend_uncounted is not None else []) + sampled
-            accepted, consume, new_len = self._validate(d, draft, model, len(span), len(lead), dev_sampled,
-                                                        pend_uncounted)
-            valid = len(lead) + accepted
-            d.kv_len = d.kv_len - len(inputs) + valid  # kv_len was advanced by the whole run
-            assert d.kv_len == new_len, (d.kv_len, new_len)
-            del d.hist[len(d.hist) - (len(inputs) - valid):]
+        def finish(res) -> None:
+            accepted, consume, new_len, rows = res
+            if new_len != start + len(lead) + accepted:
+                raise KernelError(f"{seq.rid}: K4 kept {new_len} rows, expected {start + len(lead) + accepted}")
+            d.kv_len = new_len
+            del d.hist[new_len:]
             if accepted < len(span):
-                d.pend, d.counted = model[accepted], True
+                model = ([first] if first >= 0 else []) + rows
+                d.pend, d.counted = model[accepted], True  # the correction token, emitted
             else:
                 d.pend, d.counted = None, False
             self._commit_blocks(d)  # K1 rollback of the rejected rows' blocks
             self.emitted += consume
             done((accepted, consume))
 
-        self._submit_run(Run(seq, inputs, d.kv_len, rows, targets, finish), want_device=True)
+        self._submit_run(Run(seq, inputs, start, list(range(len(inputs))), targets, finish,
+                             verify=(draft, len(span), len(lead), first)))
 
     def ingest(self, seq, n_out: int, next_turn: int, done) -> None:
         d = seq.dev
@@ -293,41 +318,18 @@ class Runtime:
         d.kv_len -= 1
         d.pend, d.counted = d.hist.pop(), True
 
-    def _validate(self, d, draft, model, span_len, lead, dev_sampled, pend_uncounted):
-        """K4 on the device: LCP(draft, model ids) clamped to the span."""
-        dev = self.dec.device
-        draft_t = torch.tensor(draft if draft else [0], dtype=torch.int32, device=dev)[: len(draft)]
-        if pend_uncounted is not None:
-            model_t = torch.cat([torch.tensor([pend_uncounted], dtype=torch.int32, device=dev), dev_sampled])
-        else:
-            model_t = dev_sampled
-        meta = torch.tensor([0, len(draft), 0, int(model_t.shape[0]), span_len, d.kv_len - len(draft) - lead, lead],
-                            dtype=torch.int32, device=dev)
-        out = torch.empty(3, dtype=torch.int32, device=dev)
-        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-        p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
-        lib.call("stb_spec_validate", p(draft_t), p(meta[0:2]), p(model_t), p(meta[2:4]), p(meta[4:5]),
-                 p(meta[5:6]), p(meta[6:7]), 1, p(out[0:1]), p(out[1:2]), p(out[2:3]), st)
-        a, c, n = out.tolist()
-        self.h2d_bytes += 4 * (len(draft) + 7)
-        self.d2h_bytes += 12
-        return a, c, n
-
-    # -- forward plumbing ----------------------------------------------------------
+    # -- flights -----------------------------------------------------------------
 
     def _build(self, decodes: list[Decode], runs: list[Run]) -> StepBatch:
-        ids, pos, slot_of = [], [], []
-        dec_slots, dec_ctx = [], []
-        for j in decodes:
-            d = j.seq.dev
-            ids.append(d.pend)
-            pos.append(d.kv_len)
-            slot_of.append(d.slot)
-            dec_slots.append(d.slot)
-            dec_ctx.append(d.kv_len + 1)
+        nd = len(decodes)
+        ids = [j.seq.dev.pend for j in decodes]
+        pos = [j.seq.dev.kv_len for j in decodes]
+        slots = [j.seq.dev.slot for j in decodes]
+        ctx = [p + 1 for p in pos]
+        targets = [j.targets[j.k] for j in decodes]
+        slot_of = list(slots)
         pre_slots, qstart, pre_ctx = [], [0], []
-        sample_rows, targets = list(range(len(decodes))), [j.targets[j.k] for j in decodes]
-        base = len(decodes)
+        sample_rows = list(range(nd))
         for r in runs:
             d = r.seq.dev
             n = len(r.ids)
@@ -336,16 +338,18 @@ class Runtime:
             slot_of.extend([d.slot] * n)
             pre_slots.append(d.slot)
             pre_ctx.append(r.start + n)
-            sample_rows.extend(base + qstart[-1] + x for x in r.rows)
+            base = nd + qstart[-1]
+            sample_rows.extend(base + x for x in r.rows)
             targets.extend(r.targets)
             qstart.append(qstart[-1] + n)
         a = lambda v: np.asarray(v, dtype=np.int32)  # noqa: E731
-        return StepBatch(a(ids), a(pos), a(slot_of), a(dec_slots), a(dec_ctx), a(pre_slots), a(qstart),
-                         a(pre_ctx), a(sample_rows), a(targets))
+        return StepBatch(a(ids), a(pos), a(slot_of), a(slots), a(ctx), a(pre_slots), a(qstart), a(pre_ctx),
+                         a(sample_rows), a(targets))
 
-    def _run_now(self, runs: list[Run], decodes: list[Decode] = (), want_device: bool = False):
-        """One forward over `decodes` (one token each) + `runs`; applies results."""
+    def _launch(self, runs: list[Run], decodes=()) -> Flight:
+        """Pack and enqueue one forward (+ K4, + D2H); advance decode rows optimistically."""
         decodes = list(decodes)
+        runs = sorted(runs, key=lambda r: r.verify is None)  # verify runs first: their samples are contiguous
         for j in decodes:
             d = j.seq.dev
             self.pool.reserve(d.slot, d.kv_len + 1)
@@ -356,57 +360,123 @@ class Runtime:
             self.pool.reserve(d.slot, r.start + len(r.ids))
         batch = self._build(decodes, runs)
         self.dec.keep_logits = self.record
-        sampled_dev = self.dec.forward(batch)
-        sampled = sampled_dev.tolist()
-        self.dec.collect()
+        k = self._flip
+        self._flip ^= 1
+        if self._host_ev[k] is not None:  # the pinned buffers of two flights ago are free again
+            self._host_ev[k].synchronize()
+        sampled = self.dec.forward(batch)
+        R = batch.R
+        nv = self._launch_validate(decodes, runs, sampled, k)
+        host = self._host[k]
+        host[:R].copy_(sampled, non_blocking=True)
+        if nv:
+            host[R:R + 3 * nv].copy_(self._vout[:3 * nv], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._host_ev[k] = ev
+        f = Flight()
+        f.batch, f.decodes, f.runs, f.n_sampled, f.n_verify = batch, decodes, runs, R, nv
+        f.event, f.host, f.finished = ev, host, []
+        f.timers = (self.dec.take_pending(), self.dec.timers)
+        f.logits = self.dec.last_logits if self.record else None
+        f.raw = self.dec.last_raw_argmax if self.record else None
         self.h2d_bytes += self.dec.h2d_bytes
-        self.d2h_bytes += 4 * batch.R
+        self.d2h_bytes += 4 * (R + 3 * nv)
         self.forwards += 1
         self.tokens_fed += batch.T
-        if self.record:
-            logits = self.dec.last_logits.float().cpu()
-            raw = self.dec.last_raw_argmax.cpu().tolist()
-            for i in range(batch.R):
-                row = int(batch.sample_rows[i])
-                seq = (decodes[row].seq if row < len(decodes) else None)
-                if seq is None:
-                    acc = len(decodes)
-                    for r in runs:
-                        if row < acc + len(r.ids):
-                            seq = r.seq
-                            break
-                        acc += len(r.ids)
-                self.trace.append({"rid": seq.rid, "pos": int(batch.pos[row]), "fed": int(batch.ids[row]),
-                                   "target": int(batch.targets[i]), "sampled": sampled[i], "raw_argmax": raw[i],
-                                   "logits": logits[i]})
-        # apply decode results
-        for i, j in enumerate(decodes):
+        # optimistic state: decode rows take their scripted target, checked at completion
+        for j in decodes:
             d = j.seq.dev
-            got, want = sampled[i], j.targets[j.k]
-            if want >= 0 and got != want:
-                raise KernelError(f"{j.seq.rid}: forced sample {got} != scripted {want}")
             del d.hist[d.kv_len:]
             d.hist.append(d.pend)
             d.kv_len += 1
-            d.pend, d.counted = got, True
+            d.pend, d.counted = j.targets[j.k], True
             j.k += 1
         self.emitted += len(decodes)
-        off = len(decodes)
-        results = []
         for r in runs:
             d = r.seq.dev
             del d.hist[r.start:]
             d.hist.extend(r.ids)
             d.kv_len = r.start + len(r.ids)
+            d.busy = True
+        return f
+
+    def _launch_validate(self, decodes, runs, sampled: torch.Tensor, k: int) -> int:
+        """K4 for the flight's verify runs (the first runs), on the device, after the forward."""
+        vr = [r for r in runs if r.verify is not None]
+        if not vr:
+            return 0
+        nv = len(vr)
+        drafts, d_off, m_off, firsts, spans, kvs, extra = [], [0], [len(decodes)], [], [], [], []
+        for r in vr:
+            draft, span_len, lead, first = r.verify
+            drafts.extend(draft)
+            d_off.append(len(drafts))
+            m_off.append(m_off[-1] + len(r.rows))
+            firsts.append(first)
+            spans.append(span_len)
+            kvs.append(r.start)
+            extra.append(lead)
+        parts = [drafts, d_off, m_off, firsts, spans, kvs, extra]
+        host = self._vstage[k].numpy()
+        offs, o = [], 0
+        for p in parts:
+            offs.append(o)
+            host[o:o + len(p)] = p
+            o += len(p)
+        self._vdev[:o].copy_(self._vstage[k][:o], non_blocking=True)
+        base = self._vdev.data_ptr()
+        ptr = [C.c_void_p(base + 4 * x) for x in offs]
+        out = self._vout.data_ptr()
+        lib.call("stb_spec_validate", ptr[0], ptr[1], C.c_void_p(sampled.data_ptr()), ptr[2], ptr[3], ptr[4],
+                 ptr[5], ptr[6], nv, C.c_void_p(out), C.c_void_p(out + 4 * nv), C.c_void_p(out + 8 * nv),
+                 C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        self.h2d_bytes += 4 * o
+        return nv
+
+    def _complete(self, f: Flight) -> None:
+        """Wait for the flight's results, check every forced sample, fire callbacks."""
+        f.event.synchronize()
+        R, nv = f.n_sampled, f.n_verify
+        sampled = f.host[:R].tolist()
+        vres = f.host[R:R + 3 * nv].tolist() if nv else []
+        self.dec.fold(*f.timers)
+        b = f.batch
+        if self.record:
+            logits = f.logits.float().cpu()
+            raw = f.raw.cpu().tolist()
+            owners = [j.seq for j in f.decodes]
+            for r in f.runs:
+                owners.extend([r.seq] * len(r.ids))
+            for i in range(R):
+                row = int(b.sample_rows[i])
+                self.trace.append({"rid": owners[row].rid, "pos": int(b.pos[row]), "fed": int(b.ids[row]),
+                                   "target": int(b.targets[i]), "sampled": sampled[i], "raw_argmax": raw[i],
+                                   "logits": logits[i]})
+        for i, j in enumerate(f.decodes):
+            want = int(b.targets[i])
+            if want >= 0 and sampled[i] != want:
+                raise KernelError(f"{j.seq.rid}: forced sample {sampled[i]} != scripted {want}")
+        off, kv = len(f.decodes), 0
+        done_runs = []
+        for r in f.runs:
             got = sampled[off:off + len(r.rows)]
             for g, t in zip(got, r.targets):
                 if t >= 0 and g != t:
                     raise KernelError(f"{r.seq.rid}: forced sample {g} != scripted {t}")
-            results.append((r, got, sampled_dev[off:off + len(r.rows)] if want_device else None))
+            r.seq.dev.busy = False
+            if r.verify is not None:
+                done_runs.append((r, (vres[kv], vres[nv + kv], vres[2 * nv + kv], got)))
+                kv += 1
+            else:
+                done_runs.append((r, got))
             off += len(r.rows)
-        return results
+        for j in f.finished:
+            j.on_done()
+        for r, res in done_runs:
+            r.on_done(res)
 
-    def _submit_run(self, run: Run, want_device: bool = False) -> None:
+    def _submit_run(self, run: Run) -> None:
         raise NotImplementedError
 
     def _submit_decode(self, job: Decode) -> None:
@@ -416,68 +486,72 @@ class Runtime:
 class EagerRuntime(Runtime):
     """Parity mode: each phase runs to completion now, batch of one."""
 
-    def _submit_run(self, run: Run, want_device: bool = False) -> None:
-        ((r, got, dev),) = self._run_now([run], want_device=want_device)
-        if want_device:
-            r.on_done(got, dev)
-        else:
-            r.on_done(got)
+    def _submit_run(self, run: Run) -> None:
+        self._complete(self._launch([run]))
 
     def _submit_decode(self, job: Decode) -> None:
         while job.k < len(job.targets):
-            d = job.seq.dev
-            self._run_now([], [job])
-            self._commit_blocks(d)
+            f = self._launch([], [job])
+            self._commit_blocks(job.seq.dev)
+            self._complete(f)
         job.on_done()
 
 
 class BatchRuntime(Runtime):
-    """Throughput mode: jobs queue up; `step()` runs one packed forward."""
+    """Throughput mode: jobs queue up; `step()` launches one packed forward and then
+    completes the previous one (one flight in the air)."""
 
-    def __init__(self, *a, max_step_tokens: int = 8192, **kw):
+    def __init__(self, *a, max_step_tokens: int = 8192, pipeline: bool = True, **kw):
         super().__init__(*a, **kw)
         self.max_step_tokens = max_step_tokens
+        self.pipeline = pipeline
         self.runs: deque = deque()
         self.decodes: list[Decode] = []
-        self.step_tokens_emitted = 0
+        self.flight: Flight | None = None
 
-    def _submit_run(self, run: Run, want_device: bool = False) -> None:
-        self.runs.append((run, want_device))
+    def _submit_run(self, run: Run) -> None:
+        self.runs.append(run)
 
     def _submit_decode(self, job: Decode) -> None:
         self.decodes.append(job)
 
     def busy(self) -> bool:
-        return bool(self.runs or self.decodes)
+        return bool(self.runs or self.decodes or self.flight is not None)
 
-    def step(self) -> int:
-        """One packed forward over every decode job + as many runs as fit."""
-        decodes = list(self.decodes)
+    def _pack(self):
+        decodes = [j for j in self.decodes if not j.seq.dev.busy]
         budget = self.max_step_tokens - len(decodes)
         runs = []
-        while self.runs and (not runs or len(self.runs[0][0].ids) <= budget):
-            r, wd = self.runs.popleft()
+        while self.runs and (not runs or len(self.runs[0].ids) <= budget):
+            r = self.runs.popleft()
             budget -= len(r.ids)
-            runs.append((r, wd))
-        if not decodes and not runs:
-            return 0
-        want = any(wd for _, wd in runs)
-        results = self._run_now([r for r, _ in runs], decodes, want_device=want)
-        emitted = len(decodes)
-        self.decodes = []
-        for j in decodes:
-            self._commit_blocks(j.seq.dev)
-            if j.k < len(j.targets):
-                self.decodes.append(j)
-        for j in decodes:
-            if j.k >= len(j.targets):
-                j.on_done()
-        for (r, got, dev), (_, wd) in zip(results, runs):
-            if wd:
-                r.on_done(got, dev)
+            runs.append(r)
+        return decodes, runs
+
+    def step(self) -> int:
+        """Launch the next packed forward (if any work), then complete the previous one."""
+        prev, self.flight = self.flight, None
+        decodes, runs = self._pack()
+        emitted = 0
+        if decodes or runs:
+            f = self._launch(runs, decodes)
+            emitted = len(decodes)
+            for j in decodes:
+                self._commit_blocks(j.seq.dev)
+            f.finished = [j for j in decodes if j.k >= len(j.targets)]
+            self.decodes = [j for j in self.decodes if j.k < len(j.targets)]
+            if self.pipeline:
+                self.flight = f
             else:
-                r.on_done(got)
+                self._complete(f)
+        if prev is not None:
+            self._complete(prev)
         return emitted
+
+    def drain(self) -> None:
+        if self.flight is not None:
+            f, self.flight = self.flight, None
+            self._complete(f)
 
 
 def default_runtime(config, shape: ModelShape = TINY, **kw) -> Runtime:

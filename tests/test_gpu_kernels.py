@@ -289,10 +289,13 @@ def test_spec_validate(lib):
     acc, con, nl = (torch.empty(S, dtype=torch.int32, device="cuda") for _ in range(3))
     kv = t([100 * i for i in range(S)])
     extra = t([i % 2 for i in range(S)])
-    keep = [t(drafts), t(d_off), t(models), t(m_off), t(spans)]  # alive until the kernel ran
+    firsts = [rng.choice([-1, 0, 1, 2]) for _ in range(S)]
+    keep = [t(drafts), t(d_off), t(models), t(m_off), t(firsts), t(spans)]  # alive until the kernel ran
     lib.call("stb_spec_validate", *(P(x) for x in keep), P(kv), P(extra), S, P(acc), P(con), P(nl), stream())
     for s in range(S):
         dr, mo = drafts[d_off[s]:d_off[s + 1]], models[m_off[s]:m_off[s + 1]]
+        if firsts[s] >= 0:
+            mo = [firsts[s]] + mo
         n = min(len(dr), len(mo), spans[s])
         a = next((i for i in range(n) if dr[i] != mo[i]), n)
         assert acc[s].item() == a

@@ -100,10 +100,37 @@ def bench_attn(shape, B, ctx, reps=4):
     return us
 
 
+def bench_prefill(shape, S, n, ctx, reps=2):
+    """K2 append-prefill: S runs of n new queries at context ctx (incl. the new rows)."""
+    from paper_2512_15834_b200.runtime.decoder import KVPool
+
+    s = shape
+    pools = []
+    for r in range(reps):
+        pool = KVPool(s.with_layers(1), S * (ctx // 16 + 1) + 16, S, ctx // 16 + 2)
+        for b in range(S):
+            pool.reserve(b, ctx)
+        pool.sync(torch.cuda.current_stream().cuda_stream)
+        pools.append(pool)
+    T = S * n
+    q = torch.randn(T, s.n_q, s.d_head, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty_like(q)
+    slots = torch.arange(S, dtype=torch.int32, device="cuda")
+    qs = torch.arange(0, T + 1, n, dtype=torch.int32, device="cuda")
+    ctxs = torch.full((S,), ctx, dtype=torch.int32, device="cuda")
+    sc = 1 / math.sqrt(s.d_head)
+    us = time_it(lambda i: lib.call("stb_attn_prefill", pools[i % reps].h, 0, P(q), P(o), P(slots), P(qs), P(ctxs), S,
+                                    T, s.n_q, sc, n, st()), iters=10)
+    prev = ctx - n
+    fl = S * 4 * s.n_q * s.d_head * (n * prev + n * (n + 1) / 2)
+    print(f"  attn_prefill S={S:3d} n={n:5d} ctx={ctx:6d}: {us:9.1f} us  {fl / us / 1e6:7.1f} TF/s "
+          f"({fl / us / 1e6 / PEAK['bf16_tflops']:.2f})")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="llama3-8b")
-    ap.add_argument("--what", default="gemm,attn")
+    ap.add_argument("--what", default="gemm,attn,prefill")
     ap.add_argument("--M", default="32,2080")
     ap.add_argument("--split", type=int, default=0)
     args = ap.parse_args()
@@ -112,6 +139,9 @@ def main():
     if "gemm" in args.what:
         for M in [int(x) for x in args.M.split(",")]:
             bench_gemm(shape, M, args.split)
+    if "prefill" in args.what:
+        for S, n, ctx in [(4, 2048, 2048), (1, 2048, 34816), (8, 512, 4096), (32, 33, 4096)]:
+            bench_prefill(shape, S, n, ctx)
     if "attn" in args.what:
         for B, ctx in [(32, 2048), (32, 4096), (16, 32768), (1, 4096), (64, 4096)]:
             bench_attn(shape, B, ctx)

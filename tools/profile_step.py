@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--timers", action="store_true", help="per-kernel CUDA-event times inside the step")
     args = ap.parse_args()
     shape = SHAPES[args.shape]
     if args.layers:
@@ -58,6 +59,8 @@ def main():
         rt.step()
     torch.cuda.synchronize()
     times = []
+    if args.timers:
+        rt.dec.timers = {}
     for i in range(args.steps):
         last = i >= args.steps - args.profile_steps
         if args.profile and i == args.steps - args.profile_steps:
@@ -65,10 +68,15 @@ def main():
             torch.cuda.profiler.start()
         t0 = time.perf_counter()
         rt.step()
+        rt.drain()
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
         if args.profile and last and i == args.steps - 1:
             torch.cuda.profiler.stop()
+    rt.drain()
+    if args.timers:
+        for name, (t, work, n) in rt.dec.timers.items():
+            print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e9:8.1f} GB/s algorithmic")
     ms = sorted(times[len(times) // 3:])
     print(f"{shape.name} B={args.batch} ctx~{args.ctx}: median step {ms[len(ms) // 2] * 1e3:.3f} ms "
           f"({args.batch / ms[len(ms) // 2]:.0f} tok/s)")
