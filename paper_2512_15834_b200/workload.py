@@ -185,7 +185,9 @@ def engine_config_for(config: WorkloadConfig, **extra) -> EngineConfig:
                         tool_cache=config.mode == "engine_spec", **extra)
 
 
-def _execute(config: WorkloadConfig, engine_factory=None, sim=None) -> WorkloadRun:
+def _execute(config: WorkloadConfig, engine_factory=None, sim=None, agent_ids=None) -> WorkloadRun:
+    """Run the fleet; `agent_ids` restricts it to a shard of the agents (replicas:
+    sessions are independent, so a shard's agents behave exactly as in the full run)."""
     if config.backend != "engine":
         raise ConfigError("only the engine backend is part of the B200 hot path")
     library = build_task_library(config.seed)
@@ -198,7 +200,8 @@ def _execute(config: WorkloadConfig, engine_factory=None, sim=None) -> WorkloadR
     usage: list = []
     results: dict[str, AgentResult] = {}
     fates: dict[str, list[str]] = {}
-    plan = [(a, f"a{a}_s{s}", library[task_assignment(a, s)]) for a in range(config.agents)
+    agent_ids = list(range(config.agents)) if agent_ids is None else list(agent_ids)
+    plan = [(a, f"a{a}_s{s}", library[task_assignment(a, s)]) for a in agent_ids
             for s in range(config.tasks_per_agent)]
     engine = (engine_factory or default_engine_factory)(sim, engine_config_for(config))
 
@@ -221,12 +224,12 @@ def _execute(config: WorkloadConfig, engine_factory=None, sim=None) -> WorkloadR
             yield result.completion
             fates[task_id] = list(engine.sequences[task_id].fates)
 
-    for a in range(config.agents):
+    for a in agent_ids:
         spawn(agent_loop(a))
     sim.run_until_idle()
 
     agents = []
-    for a in range(config.agents):
+    for a in agent_ids:
         mine = [results[t] for ag, t, _ in plan if ag == a]
         if not all(r.done for r in mine):
             raise ConfigError(f"agent {a} did not finish all tasks")
