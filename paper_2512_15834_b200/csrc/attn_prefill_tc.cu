@@ -4,20 +4,23 @@
 // (`engine.py:251,296,358`): n new query tokens of a resident sequence attend
 // causally to its whole paged context (the new rows already committed by K1).
 //
-// One CTA per (tile of 128 packed query rows, kv head, sequence). GQA packing:
-// row r = (query r / G, head r % G) so the G heads sharing a kv head share every
-// K/V tile. Warp roles (192 threads):
-//   warp 4  TMA producer: Q once (4-D map over [T][n_kv][G][D]), then per KV tile
-//           of 128 keys the 8 K pages and 8 V pages through the block table
-//           (2-D maps over the page pool, 16 x 64 boxes, 128B swizzle) into a
-//           2-stage ring
-//   warp 5  MMA issuer: S = Q K^T (M=128, N=128 keys, K=D) into TMEM; after the
-//           softmax wrote P, O_tile = P V (M=128, N=D, K=128 keys; V is an
-//           MN-major B operand) into a second TMEM region
-//   warps 0-3  softmax: thread = row (TMEM lane), two passes over its S row
-//           (max, then exp2 / sum / bf16 pack into the swizzled P tile), then
-//           O = O * alpha + O_tile in registers; final O / l to global
-// TMEM: 128 columns S + D columns O_tile.
+// One CTA per (two tiles of 128 packed query rows, kv head, sequence). GQA
+// packing: row r = (query r / G, head r % G), so the G heads sharing a kv head
+// share every K/V tile, and both query tiles share it too. Warp roles (320 thr):
+//   warp 8     TMA producer: Q tiles A and B once (4-D map over [T][n_kv][G][D]),
+//              then per KV tile of 128 keys the 8 K and 8 V pages through the
+//              block table (2-D maps over the page pool, 16 x 64 boxes, 128B
+//              swizzle) into a 2-stage ring
+//   warp 9     MMA issuer (one thread), ping-pong over the two tiles:
+//              S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
+//              S = Q K^T into TMEM (M=128, N=128 keys, K=D); O += P V with P read
+//              from TMEM (A operand) and V an MN-major B operand from smem
+//   warps 0-3  softmax of tile A, warps 4-7 softmax of tile B: thread = row; one
+//              pass over its S row (128 TMEM columns -> registers), exp2, row sum,
+//              P packed to bf16 and stored back over S; O (in TMEM) is rescaled
+//              only when a warp's running max moved. While one warpgroup does its
+//              softmax the tensor core runs the other tile's MMAs.
+// TMEM (512 columns): S/P_A | S/P_B | O_A | O_B.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -31,24 +34,22 @@ using namespace stb;
 
 namespace {
 
-constexpr int ROWS = 128;   // packed query rows per CTA (UMMA M)
+constexpr int ROWS = 128;   // packed query rows per tile (UMMA M)
 constexpr int KT = 128;     // keys per KV tile (UMMA N of S, K of P V)
 constexpr int KV_STAGES = 2;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
 struct TcCfg {
   static constexpr int HALVES = D / 64;              // 64-column swizzle atoms along d
-  static constexpr int Q_BYTES = ROWS * D * 2;       // [half][128 rows][64]
+  static constexpr int Q_BYTES = ROWS * D * 2;       // per tile: [half][128 rows][64]
   static constexpr int KV_BYTES = KT * D * 2;        // one of K or V: [half][128 keys][64]
-  static constexpr int P_BYTES = ROWS * KT * 2;      // [key half][128 rows][64 keys]
   static constexpr int STAGE = 2 * KV_BYTES;
-  static constexpr int SMEM = Q_BYTES + KV_STAGES * STAGE + P_BYTES + 1024 + 256;
-  static constexpr int TMEM_COLS = (KT + D) <= 256 ? 256 : 512;
+  static constexpr int SMEM = 2 * Q_BYTES + KV_STAGES * STAGE + 1024 + 256;
+  static constexpr int TMEM_COLS = 512;
 };
 
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -57,6 +58,22 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+
+// 2^x for x <= 0 on the FMA pipe (Cody-Waite split + cubic minimax on [0,1), max
+// relative error 2.6e-4 — below bf16 P's 3.9e-3): offloads a share of the softmax
+// exponentials from the MUFU unit, which otherwise paces the softmax.
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -127.f);
+  const float xi = floorf(x);
+  const float f = x - xi;
+  const float p = fmaf(fmaf(fmaf(0.0755871f, f, 0.22877206f), f, 0.69511613f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
+}
+
+#ifndef STB_EXP_FMA_EVERY
+#define STB_EXP_FMA_EVERY 0  // 0: all exponentials on MUFU (measured fastest: the softmax is latency-bound)
+#endif
+constexpr float kRescaleSlack = 8.f;  // lazy rescale: keep the stale max until the row max grows by > 2^8
 
 template <int D, int G>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -68,19 +85,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   using CF = TcCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = sQ + CF::Q_BYTES;
-  uint8_t* sP = sKV + KV_STAGES * CF::STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + CF::P_BYTES);
+  uint8_t* sQ = smem;  // tile A, then tile B
+  uint8_t* sKV = sQ + 2 * CF::Q_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + KV_STAGES * CF::STAGE);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;             // [KV_STAGES]
-  uint64_t* kv_empty = kv_full + KV_STAGES; // [KV_STAGES]
-  uint64_t* s_full = kv_empty + KV_STAGES;
-  uint64_t* s_free = s_full + 1;
-  uint64_t* p_full = s_free + 1;
-  uint64_t* pv_full = p_full + 1;
-  uint64_t* pv_free = pv_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_free + 1);
+  uint64_t* kv_full = bars + 1;              // [KV_STAGES]
+  uint64_t* kv_empty = kv_full + KV_STAGES;  // [KV_STAGES]
+  uint64_t* s_full = kv_empty + KV_STAGES;   // [2] per tile
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_done = p_full + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = blockIdx.z, kh = blockIdx.y;
@@ -88,13 +102,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
   pdl_launch();
   const int t0 = q_start[s], n = q_start[s + 1] - t0;
-  const int qi0 = blockIdx.x * QPT;
+  const int qi0 = blockIdx.x * 2 * QPT;
   if (qi0 >= n) return;
+  const bool has_b = qi0 + QPT < n;
   const int ctx = ctx_lens[s];
-  const int pos0 = ctx - n;                            // absolute position of query 0
-  const int q_last = min(n, qi0 + QPT) - 1;            // last query of this tile
-  const int n_tiles = (pos0 + q_last) / KT + 1;        // KV tiles the tile needs (causal)
-  const int full_tiles = (pos0 + qi0 + 1) / KT;        // tiles visible to every row of the tile
+  const int pos0 = ctx - n;  // absolute position of query 0
+  const int q_last = min(n, qi0 + 2 * QPT) - 1;
+  const int n_tiles = (pos0 + q_last) / KT + 1;  // KV tiles the CTA needs (causal)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -102,31 +116,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 128);
-    mbar_init(p_full, 128);
-    mbar_init(pv_full, 1);
-    mbar_init(pv_free, 128);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, CF::TMEM_COLS);
+  if (warp == 9) tmem_alloc(tmem_slot, CF::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + KT;
+  // column map: S/P of tile t at t*KT, O of tile t at 2*KT + t*D
+  auto tS = [&](int t) { return tmem + t * KT; };
+  auto tO = [&](int t) { return tmem + 2 * KT + t * D; };
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ---------------- TMA producer
+    const int32_t* row = table + (int64_t)slots[s] * max_bps;
     if (lane == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
-      mbar_expect_tx(q_full, CF::Q_BYTES);
+      mbar_expect_tx(q_full, 2 * CF::Q_BYTES);
 #pragma unroll
-      for (int h = 0; h < CF::HALVES; ++h)
-        tma_load_4d(sQ + h * ROWS * 128, &tm_q, q_full, h * 64, 0, kh, t0 + qi0);
-      const int32_t* row = table + (int64_t)slots[s] * max_bps;
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int h = 0; h < CF::HALVES; ++h)
+          tma_load_4d(sQ + t * CF::Q_BYTES + h * ROWS * 128, &tm_q, q_full, h * 64, 0, kh, t0 + qi0 + t * QPT);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % KV_STAGES;
         mbar_wait(&kv_empty[st], ((j / KV_STAGES) & 1) ^ 1);
@@ -147,134 +165,164 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
-    // ---------------- MMA issuer
+  } else if (warp == 9) {
+    // ---------------- MMA issuer (ping-pong)
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(ROWS, KT, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(ROWS, D, false, true);
+      const int ntile_q = has_b ? 2 : 1;
       mbar_wait(q_full, 0);
-      const uint32_t qa = smem_u32(sQ);
-      const uint32_t pa = smem_u32(sP);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % KV_STAGES;
-        const uint32_t ka = smem_u32(sKV + st * CF::STAGE);
-        const uint32_t va = ka + CF::KV_BYTES;
-        mbar_wait(&kv_full[st], (j / KV_STAGES) & 1);
-        mbar_wait(s_free, (j & 1) ^ 1);  // softmax finished reading S of tile j-1
-        tc_fence_after();
+      auto issue_s = [&](int t, int j) {
+        const uint32_t ka = smem_u32(sKV + (j % KV_STAGES) * CF::STAGE);
+        const uint32_t qa = smem_u32(sQ + t * CF::Q_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk / 4) * ROWS * 128 + (kk % 4) * 32;
-          umma_f16_ss(tS, umma_desc_kmajor_sw128(qa + off, 1024),
+          umma_f16_ss(tS(t), umma_desc_kmajor_sw128(qa + off, 1024),
                       umma_desc_kmajor_sw128(ka + (kk / 4) * KT * 128 + (kk % 4) * 32, 1024), idesc_s, kk > 0);
         }
-        umma_commit(s_full);
-        mbar_wait(p_full, j & 1);         // P of tile j is in smem
-        mbar_wait(pv_free, (j & 1) ^ 1);  // O_tile of tile j-1 consumed
-        tc_fence_after();
+        umma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t va = smem_u32(sKV + (j % KV_STAGES) * CF::STAGE) + CF::KV_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk) {
-          // A = P (K-major over keys), B = V (MN-major: rows = keys, 64-wide d halves LBO apart)
-          umma_f16_ss(tO, umma_desc_kmajor_sw128(pa + (kk / 4) * ROWS * 128 + (kk % 4) * 32, 1024),
-                      umma_desc_mnmajor_sw128(va + kk * 16 * 128, KT * 128, 1024), idesc_o, kk > 0);
+        for (int kk = 0; kk < KT / 16; ++kk)  // P: 16 keys = 8 packed bf16x2 columns per k-step
+          umma_f16_ts(tO(t), tS(t) + kk * 8, umma_desc_mnmajor_sw128(va + kk * 16 * 128, KT * 128, 1024), idesc_o,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&o_done[t]);
+      };
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      if (ntile_q > 1) issue_s(1, 0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const bool more = j + 1 < n_tiles;
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (more) {
+          mbar_wait(&kv_full[(j + 1) % KV_STAGES], ((j + 1) / KV_STAGES) & 1);
+          tc_fence_after();
+          issue_s(0, j + 1);
         }
-        umma_commit(pv_full);
-        umma_commit(&kv_empty[st]);
+        if (ntile_q > 1) {
+          mbar_wait(&p_full[1], j & 1);
+          tc_fence_after();
+          issue_pv(1, j);
+          if (more) issue_s(1, j + 1);
+        }
+        umma_commit(&kv_empty[j % KV_STAGES]);
       }
     }
     __syncwarp();
   } else {
-    // ---------------- softmax / output warps: thread = row
-    const int r = warp * 32 + lane;
-    const int qi = qi0 + r / G;
+    // ---------------- softmax warpgroups: warps 0-3 tile A, 4-7 tile B; thread = row
+    const int t = warp >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const bool tile_live = t == 0 || has_b;
+    const int qi = qi0 + t * QPT + r / G;
     const int g = r % G;
-    const bool live = qi < n;
-    const int qpos = pos0 + qi;  // keys <= qpos are visible
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    float o[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) o[c] = 0.f;
+    const bool live = tile_live && qi < n;
+    const int qpos = pos0 + qi;                               // keys <= qpos are visible
+    const int full_tiles = (pos0 + qi0 + t * QPT + 1) / KT;   // tiles visible to every row of this tile
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      const int kbase = j * KT;
-      const bool full = j < full_tiles;
-      // pass 1: row max
-      float mx = -INFINITY;
+    if (tile_live) {
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        uint32_t v[KT];
 #pragma unroll
-      for (int c = 0; c < KT; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(tS + lane_base + c, v);
+        for (int c = 0; c < KT; c += 32) tmem_ld32(tS(t) + lane_base + c, v + c);
         tmem_ld_wait();
+        const int kbase = j * KT;
+        if (!(j < full_tiles && live)) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          float x = __uint_as_float(v[q]) * qscale;
-          if (!full && (kbase + c + q > qpos || !live)) x = -INFINITY;
-          mx = fmaxf(mx, x);
+          for (int c = 0; c < KT; ++c)
+            if (!live || kbase + c > qpos) v[c] = __float_as_uint(-INFINITY);
         }
-      }
-      const float mn = fmaxf(m, mx);
-      const float ref = mn == -INFINITY ? 0.f : mn;
-      const float alpha = exp2f(m - ref);
-      m = mn;
-      // pass 2: p = exp2(s - m), row sum, bf16 P tile (wait until P V of tile j-1 read P)
-      if (j > 0) mbar_wait(pv_full, (j - 1) & 1);
-      float rs = 0.f;
+        // tree-reduced row max (8 independent chains)
+        float mx8[8];
 #pragma unroll
-      for (int c = 0; c < KT; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(tS + lane_base + c, v);
-        tmem_ld_wait();
-        uint32_t pk[8];
+        for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(v[q]);
 #pragma unroll
-        for (int q = 0; q < 16; q += 2) {
-          float x0 = __uint_as_float(v[q]) * qscale, x1 = __uint_as_float(v[q + 1]) * qscale;
-          if (!full && (kbase + c + q > qpos || !live)) x0 = -INFINITY;
-          if (!full && (kbase + c + q + 1 > qpos || !live)) x1 = -INFINITY;
-          const float e0 = exp2f(x0 - ref), e1 = exp2f(x1 - ref);
-          rs += e0 + e1;
-          pk[q / 2] = pack_bf16(e0, e1);
+        for (int c = 8; c < KT; c += 8)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], __uint_as_float(v[c + q]));
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * qscale;
+        // lazy rescale (FA4): exponentiate against a stale reference while the row max stays
+        // within 2^8 of it; exact because O and l always share the reference
+        float alpha = 1.f;
+        if (mx > m + kRescaleSlack || m == -INFINITY) {
+          const float mn = fmaxf(m, mx);
+          alpha = (m == -INFINITY || mn == -INFINITY) ? (m == -INFINITY ? 0.f : 1.f) : exp2f(m - mn);
+          m = mn;
         }
-        // 32 bytes of row r, keys c..c+15 -> two swizzled 16B chunks of the K-major P tile
-        const int half = c / 64, ch = (c % 64) / 8;
-        uint8_t* prow = sP + half * ROWS * 128 + r * 128;
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(prow + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        const float ref = m == -INFINITY ? 0.f : m;
+        float rs8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rs8[q] = 0.f;
+        uint32_t pk[KT / 2];
+#pragma unroll
+        for (int c = 0; c < KT; c += 2) {
+          const float x0 = fmaf(__uint_as_float(v[c]), qscale, -ref);
+          const float x1 = fmaf(__uint_as_float(v[c + 1]), qscale, -ref);
+          const bool fma_pipe = STB_EXP_FMA_EVERY > 0 && ((c / 2) % (STB_EXP_FMA_EVERY > 0 ? STB_EXP_FMA_EVERY : 1)) == STB_EXP_FMA_EVERY - 1;
+          const float e0 = fma_pipe ? exp2_fma(x0) : exp2f(x0);
+          const float e1 = fma_pipe ? exp2_fma(x1) : exp2f(x1);
+          rs8[(c / 2) % 8] += e0 + e1;
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        l = l * alpha + rs;
+        // P (bf16 pairs) over the S columns just read: the A operand of P V
+#pragma unroll
+        for (int c = 0; c < KT / 2; c += 32) tmem_st32(tS(t) + lane_base + c, pk + c);
+        // rescale O (in TMEM) when this warp's running max moved and O holds earlier tiles
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare with the lazy reference
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tO(t) + lane_base + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+            tmem_st32(tO(t) + lane_base + c, o);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
       }
-      l = l * alpha + rs;
-      tc_fence_before();
-      mbar_arrive(s_free);   // S region may be overwritten by the next tile's QK^T
-      fence_async_smem();    // make the P stores visible to the tensor core (async proxy)
-      mbar_arrive(p_full);
-      // O = O * alpha + P V
-      mbar_wait(pv_full, j & 1);
+      // final: O / l
+      mbar_wait(&o_done[t], (n_tiles - 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < D; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(tO + lane_base + c, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int q = 0; q < 16; ++q) o[c + q] = o[c + q] * alpha + __uint_as_float(v[q]);
-      }
-      tc_fence_before();
-      mbar_arrive(pv_free);
-    }
-    if (live) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
       __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D;
 #pragma unroll
-      for (int c = 0; c < D; c += 8) {
-        *reinterpret_cast<uint4*>(dst + c) =
-            make_uint4(pack_bf16(o[c] * inv, o[c + 1] * inv), pack_bf16(o[c + 2] * inv, o[c + 3] * inv),
-                       pack_bf16(o[c + 4] * inv, o[c + 5] * inv), pack_bf16(o[c + 6] * inv, o[c + 7] * inv));
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO(t) + lane_base + c, o);
+        tmem_ld_wait();
+        if (live) {
+#pragma unroll
+          for (int q = 0; q < 32; q += 8)
+            *reinterpret_cast<uint4*>(dst + c + q) = make_uint4(
+                pack_bf16(__uint_as_float(o[q]) * inv, __uint_as_float(o[q + 1]) * inv),
+                pack_bf16(__uint_as_float(o[q + 2]) * inv, __uint_as_float(o[q + 3]) * inv),
+                pack_bf16(__uint_as_float(o[q + 4]) * inv, __uint_as_float(o[q + 5]) * inv),
+                pack_bf16(__uint_as_float(o[q + 6]) * inv, __uint_as_float(o[q + 7]) * inv));
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_free(tmem, CF::TMEM_COLS);
+  if (warp == 9) tmem_free(tmem, CF::TMEM_COLS);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
@@ -344,7 +392,7 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr = true;
   }
-  dim3 grid((max_q + ROWS / G - 1) / (ROWS / G), n_kv, S);
+  dim3 grid((max_q + 2 * ROWS / G - 1) / (2 * ROWS / G), n_kv, S);
   cudaError_t e = launch_k(kern, grid, dim3(kThreads), CF::SMEM, st, mp.q, mp.k, mp.v, (__nv_bfloat16*)out,
                            pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill_tc launch: %s", cudaGetErrorString(e));
