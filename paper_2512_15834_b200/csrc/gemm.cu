@@ -56,7 +56,7 @@ struct Cfg {
   static constexpr int W_BYTES = BM * BK * 2;
   static constexpr int X_BYTES = BN * BK * 2;
   static constexpr int STAGE = W_BYTES + X_BYTES;
-  static constexpr int RING = 200 * 1024;
+  static constexpr int RING = 200 * 1024;  // measured best: bytes in flight beat SM co-residence
   static constexpr int STAGES = (RING / STAGE) > 12 ? 12 : (RING / STAGE);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
@@ -110,7 +110,8 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_persistent(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                         float* __restrict__ C, int64_t ldc, int M, int N, Sched sched) {
+                         float* __restrict__ C, int64_t ldc, int M, int N, Sched sched, int bn) {
+  // bn: token-tile height actually used (<= BN, multiple of 16); BN sizes the smem ring
   using CF = Cfg<BN>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (i < STAGES && pre.next(tile, k0, k1)) {
         const int f0 = (tile % sched.tiles_n) * BM;
         for (int k = k0; k < k1 && i < STAGES; ++k, ++i) {
-          mbar_expect_tx(&full[i], CF::STAGE);
+          mbar_expect_tx(&full[i], CF::W_BYTES + bn * BK * 2);
           tma_load_2d(smem + i * CF::STAGE, &tm_w, &full[i], k * BK, f0);
         }
       }
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       i = 0;
       while (it.next(tile, k0, k1)) {
         const int f0 = (tile % sched.tiles_n) * BM;
-        const int t0 = (tile / sched.tiles_n) * BN;
+        const int t0 = (tile / sched.tiles_n) * bn;
         for (int k = k0; k < k1; ++k, ++i) {
           const int s = i % STAGES;
           uint8_t* sw = smem + s * CF::STAGE;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-          mbar_expect_tx(&full[s], CF::STAGE);
+          mbar_expect_tx(&full[s], CF::W_BYTES + bn * BK * 2);
           tma_load_2d(sw, &tm_w, &full[s], k * BK, f0);
           tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
         }
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, false, false);
+      const uint32_t idesc = umma_idesc_bf16(BM, bn, false, false);
       SegIter it(sched);
       int tile, k0, k1, i = 0, j = 0;
       while (it.next(tile, k0, k1)) {
@@ -243,10 +244,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         passed = true;
       }
       const int feat = (tile % sched.tiles_n) * BM + row;
-      const int t0 = (tile / sched.tiles_n) * BN;
+      const int t0 = (tile / sched.tiles_n) * bn;
       const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 16; ++c) {
+      for (int c = 0; c < bn / 16; ++c) {
         uint32_t r[16];
         tmem_ld16(base + c * 16, r);
         tmem_ld_wait();
@@ -361,10 +362,13 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   using CF = Cfg<BN>;
   CUtensorMap tw, tx;
   if (int rc = cached_map(&tw, W, N, K, ldw, BM)) return rc;
-  if (int rc = cached_map(&tx, X, M, K, lda, BN)) return rc;
+  // token tile: BN for M <= BN; above, split M into ceil(M/BN) near-equal tiles (multiple of 16)
+  const int nt = (M + BN - 1) / BN;
+  const int bn = nt == 1 ? BN : (((M + nt - 1) / nt + 15) / 16) * 16;
+  if (int rc = cached_map(&tx, X, M, K, lda, bn)) return rc;
   Sched s;
   s.tiles_n = (N + BM - 1) / BM;
-  s.tiles = s.tiles_n * ((M + BN - 1) / BN);
+  s.tiles = s.tiles_n * ((M + bn - 1) / bn);
   s.kb = (K + BK - 1) / BK;
   s.units = (int64_t)s.tiles * s.kb;
   const int sms = sm_count();
@@ -381,7 +385,7 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr_set = true;
   }
-  cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), CF::SMEM, st, tw, tx, C, ldc, M, N, s);
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), CF::SMEM, st, tw, tx, C, ldc, M, N, s, bn);
   if (e != cudaSuccess) return fail(STB_ECUDA, "gemm_bf16 launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }

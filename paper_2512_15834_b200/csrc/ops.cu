@@ -45,39 +45,68 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// one CTA per row: x (+)= delta; y = bf16(x * rsqrt(mean(x^2) + eps) * w)
+// one CTA per row, the row held in registers (VPT float4 per thread, blockDim*4*VPT == d):
+// x (+)= delta; y = bf16(x * rsqrt(mean(x^2) + eps) * w). One global read of x (and
+// delta), one write of x and y, a single block reduction.
+template <int VPT>
 __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int d,
                                    float eps, const int32_t* __restrict__ gather) {
   pdl_wait();
   pdl_launch();
   __shared__ float red[32];
-  int t = blockIdx.x;
-  int src = gather ? gather[t] : t;
+  const int t = blockIdx.x;
+  const int src = gather ? gather[t] : t;
   float* xr = x + (int64_t)src * d;
+  float4 v[VPT];
   float ss = 0.f;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<float4*>(xr + c);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    v[i] = *reinterpret_cast<const float4*>(xr + c);
     if (delta) {
-      float4 e = *reinterpret_cast<const float4*>(delta + (int64_t)t * d + c);
-      v.x += e.x;
-      v.y += e.y;
-      v.z += e.z;
-      v.w += e.w;
-      *reinterpret_cast<float4*>(xr + c) = v;
+      const float4 e = *reinterpret_cast<const float4*>(delta + (int64_t)t * d + c);
+      v[i].x += e.x;
+      v[i].y += e.y;
+      v[i].z += e.z;
+      v[i].w += e.w;
+      *reinterpret_cast<float4*>(xr + c) = v[i];
     }
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
   }
   if (!y) return;  // residual add only
-  float inv = rsqrtf(block_sum(ss, red) / d + eps);
+  const float inv = rsqrtf(block_sum(ss, red) / d + eps);
   __nv_bfloat16* yr = y + (int64_t)t * d;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<float4*>(xr + c);
-    float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c));
-    float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c + 2));
-    uint2 o = make_uint2(pack_bf16(v.x * inv * w01.x, v.y * inv * w01.y), pack_bf16(v.z * inv * w23.x, v.w * inv * w23.y));
-    *reinterpret_cast<uint2*>(yr + c) = o;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c));
+    const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c + 2));
+    *reinterpret_cast<uint2*>(yr + c) = make_uint2(pack_bf16(v[i].x * inv * w01.x, v[i].y * inv * w01.y),
+                                                   pack_bf16(v[i].z * inv * w23.x, v[i].w * inv * w23.y));
   }
+}
+
+// d = threads * 4 * VPT with threads a multiple of 32 and <= 1024
+int launch_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps,
+                   const int32_t* gather, cudaStream_t st) {
+  if (d % 128) return fail(STB_EINVAL, "rmsnorm: d must be a multiple of 128");
+  const int v4 = d / 4;
+  int vpt = 1;
+  while (v4 / vpt > 1024 || (v4 % vpt)) vpt *= 2;
+  if (vpt > 8) return fail(STB_EINVAL, "rmsnorm: d too large");
+  const int threads = v4 / vpt;
+  const auto* wb = (const __nv_bfloat16*)w;
+  auto* yb = (__nv_bfloat16*)y;
+  cudaError_t e;
+  switch (vpt) {
+    case 1: e = launch_k(add_rmsnorm_kernel<1>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
+    case 2: e = launch_k(add_rmsnorm_kernel<2>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
+    case 4: e = launch_k(add_rmsnorm_kernel<4>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
+    default: e = launch_k(add_rmsnorm_kernel<8>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
+  }
+  if (e != cudaSuccess) return fail(STB_ECUDA, "rmsnorm launch: %s", cudaGetErrorString(e));
+  return STB_OK;
 }
 
 __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f) {
@@ -247,21 +276,13 @@ int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, voi
 
 int stb_add_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps, void* stream) {
   if (n <= 0) return STB_OK;
-  if (d % 4) return fail(STB_EINVAL, "add_rmsnorm: d must be a multiple of 4");
-  launch_k(add_rmsnorm_kernel, dim3(n), dim3(256), 0, (cudaStream_t)stream, x, delta, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, d, eps,
-                                                          nullptr);
-  STB_CHECK_LAUNCH("add_rmsnorm");
-  return STB_OK;
+  return launch_rmsnorm(x, delta, w, y, n, d, eps, nullptr, (cudaStream_t)stream);
 }
 
 int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,
                        void* stream) {
   if (n <= 0) return STB_OK;
-  if (d % 4) return fail(STB_EINVAL, "gather_rmsnorm: d must be a multiple of 4");
-  launch_k(add_rmsnorm_kernel, dim3(n), dim3(256), 0, (cudaStream_t)stream, const_cast<float*>(x), nullptr, (const __nv_bfloat16*)w,
-                                                          (__nv_bfloat16*)y, d, eps, idx);
-  STB_CHECK_LAUNCH("gather_rmsnorm");
-  return STB_OK;
+  return launch_rmsnorm(const_cast<float*>(x), nullptr, w, y, n, d, eps, idx, (cudaStream_t)stream);
 }
 
 int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream) {

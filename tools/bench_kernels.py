@@ -127,6 +127,30 @@ def bench_prefill(shape, S, n, ctx, reps=2):
           f"({fl / us / 1e6 / PEAK['bf16_tflops']:.2f})")
 
 
+def bench_pdl(shape, M=32):
+    """rmsnorm -> QKV GEMM pairs in one graph: is the GEMM's weight prefetch overlapping?"""
+    s = shape
+    N, K = s.q_dim + 2 * s.kv_dim, s.d_model
+    copies = 8
+    ws = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) for _ in range(copies)]
+    x = torch.randn(M, K, device="cuda")
+    h = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
+    nw = torch.ones(K, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(M, N, device="cuda")
+
+    def norm(i):
+        lib.call("stb_add_rmsnorm", P(x), None, P(nw), P(h), M, K, 1e-5, st())
+
+    def gemm(i):
+        lib.call("stb_gemm_bf16", P(h), K, P(ws[i % copies]), K, P(c), N, M, N, K, 0, st())
+
+    t_norm = time_it(norm)
+    t_gemm = time_it(gemm)
+    t_pair = time_it(lambda i: (norm(i), gemm(i)))
+    print(f"  pdl probe M={M}: rmsnorm {t_norm:.1f} us, qkv gemm {t_gemm:.1f} us, pair {t_pair:.1f} us "
+          f"(overlap {t_norm + t_gemm - t_pair:.1f} us)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="llama3-8b")
@@ -139,6 +163,8 @@ def main():
     if "gemm" in args.what:
         for M in [int(x) for x in args.M.split(",")]:
             bench_gemm(shape, M, args.split)
+    if "pdl" in args.what:
+        bench_pdl(shape)
     if "prefill" in args.what:
         for S, n, ctx in [(4, 2048, 2048), (1, 2048, 34816), (8, 512, 4096), (32, 33, 4096)]:
             bench_prefill(shape, S, n, ctx)

@@ -43,12 +43,13 @@ def main():
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--timers", action="store_true", help="per-kernel CUDA-event times inside the step")
+    ap.add_argument("--mix", default="", help="NxL: N new L-token prefills packed into every step")
     args = ap.parse_args()
     shape = SHAPES[args.shape]
     if args.layers:
         shape = shape.with_layers(args.layers)
-    nb = args.batch * (args.ctx + 4096) // 16 + 64
-    rt = BatchRuntime(shape, init_device="cuda", num_blocks=nb, max_slots=max(64, args.batch),
+    nb = args.batch * (args.ctx + 4096) // 16 + 64 + 4096
+    rt = BatchRuntime(shape, init_device="cuda", num_blocks=nb, max_slots=max(64, args.batch) + 1024,
                       max_ctx=args.ctx + 8192, max_step_tokens=16384)
     loop = RealtimeLoop()
     eng = B200Engine(loop, EngineConfig(prefill_rate=0, decode_rate=0, batch_size=max(64, args.batch)), runtime=rt)
@@ -58,6 +59,15 @@ def main():
     while rt.runs:  # prefill
         rt.step()
     torch.cuda.synchronize()
+    mix_n, mix_l = (int(x) for x in args.mix.split("x")) if args.mix else (0, 0)
+    short = GenerationScript([[Token(TokenKind.TEXT, "mull ")] * 2 + [EOS]])
+    extra = [0]
+
+    def inject():
+        for _ in range(mix_n):
+            eng.submit_request(f"x{extra[0]}", short, mix_l, Quiet())
+            extra[0] += 1
+
     times = []
     if args.timers:
         rt.dec.timers = {}
@@ -66,6 +76,7 @@ def main():
         if args.profile and i == args.steps - args.profile_steps:
             torch.cuda.synchronize()
             torch.cuda.profiler.start()
+        inject()
         t0 = time.perf_counter()
         rt.step()
         rt.drain()
@@ -78,7 +89,7 @@ def main():
         for name, (t, work, n) in rt.dec.timers.items():
             print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e9:8.1f} GB/s algorithmic")
     ms = sorted(times[len(times) // 3:])
-    print(f"{shape.name} B={args.batch} ctx~{args.ctx}: median step {ms[len(ms) // 2] * 1e3:.3f} ms "
+    print(f"{shape.name} B={args.batch} ctx~{args.ctx} mix={args.mix or '-'}: median step {ms[len(ms) // 2] * 1e3:.3f} ms "
           f"({args.batch / ms[len(ms) // 2]:.0f} tok/s)")
 
 
