@@ -105,3 +105,36 @@ class CpuDecoder:
             x = x + (torch.nn.functional.silu(g) * u) @ w["dn"].T
         sel = x[torch.tensor(rows, dtype=torch.long)]
         return self._norm(sel, self.fn) @ self.head.T
+
+
+def decode_batch(dec: CpuDecoder, caches: list, ids: list[int], positions: list[int]) -> torch.Tensor:
+    """One batched decode step (bench CPU baseline only): B sequences, one new token each.
+
+    `caches[b][layer]` = (K, V) fp32 [ctx, n_kv, d]; GEMMs run batched over B (as a CPU
+    server would), attention per sequence. Returns logits [B, V]."""
+    s = dec.s
+    H, G, D = s.n_q, s.n_kv, s.d_head
+    B = len(ids)
+    pos = torch.tensor(positions)
+    x = dec.embed[torch.tensor(ids, dtype=torch.long)]
+    for i, w in enumerate(dec.layers):
+        h = dec._norm(x, w["an"])
+        qkv = h @ w["qkv"].T
+        q = dec._rope(qkv[:, : H * D].view(B, H, D), pos)
+        k = dec._rope(qkv[:, H * D: (H + G) * D].view(B, G, D), pos)
+        v = qkv[:, (H + G) * D:].view(B, G, D)
+        outs = []
+        for b in range(B):
+            kc, vc = caches[b][i]
+            kc = torch.cat([kc, k[b:b + 1]])
+            vc = torch.cat([vc, v[b:b + 1]])
+            caches[b][i] = (kc, vc)
+            kk = kc.repeat_interleave(H // G, dim=1)
+            vv = vc.repeat_interleave(H // G, dim=1)
+            p = torch.softmax(torch.einsum("hd,nhd->hn", q[b], kk) / math.sqrt(D), dim=-1)
+            outs.append(torch.einsum("hn,nhd->hd", p, vv).reshape(H * D))
+        x = x + torch.stack(outs) @ w["o"].T
+        h = dec._norm(x, w["mn"])
+        gu = h @ w["gu"].T
+        x = x + (torch.nn.functional.silu(gu[:, : s.d_ff]) * gu[:, s.d_ff:]) @ w["dn"].T
+    return dec._norm(x, dec.fn) @ dec.head.T
