@@ -71,9 +71,11 @@ int stb_kv_copy_blocks(stb_kv_pool* pool, const int32_t* src, const int32_t* dst
 
 /* ---- fused QKV epilogue: RoPE on q/k + K1 commit of k/v -----------------
  * qkv fp32 [n][(n_q + 2 n_kv) d_head] from the QKV GEMM; writes q bf16
- * [n][n_q d_head] (rotated) and commits rotated k and v into the pool. */
-int stb_qkv_rope_commit(stb_kv_pool* pool, int layer, const float* qkv, void* q_out, const int32_t* slot_of,
-                        const int32_t* pos_of, int n, int n_q, float rope_theta, void* stream);
+ * [n][n_q d_head] (rotated) and commits rotated k and v into the pool.
+ * Rows < clear_rows of qkv are zeroed after they are read (so the next
+ * stream-K GEMM into qkv can accumulate without a memset).               */
+int stb_qkv_rope_commit(stb_kv_pool* pool, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                        const int32_t* pos_of, int n, int n_q, float rope_theta, int clear_rows, void* stream);
 
 /* ---- K3: paged decode attention (one query per sequence) ----------------
  * Replaces the decode charges engine.py:270,276,302,317. q/out bf16
@@ -114,24 +116,32 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
  * C[M][N] (fp32, row stride ldc) = A[M][K] (bf16, lda) * W[N][K]^T (bf16, ldw).
  * Persistent, one CTA per SM. split_k: 0 = automatic schedule; 1 = whole
  * tiles per CTA (plain stores); >= 2 = stream-K over min(split_k, SMs) CTAs,
- * partial tiles reduced with fp32 red.add into C (zeroed by the call).    */
+ * partial tiles reduced with fp32 red.add into C. C is zeroed by the call
+ * unless flags has STB_GEMM_C_ZEROED (the caller guarantees C == 0, e.g.
+ * because the consumer of the previous product cleared the rows it read). */
+#define STB_GEMM_C_ZEROED 1
+/* 1 if the automatic schedule runs this shape stream-K (C accumulated with reductions) */
+int stb_gemm_is_stream(int M, int N, int K);
 int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
-                  int split_k, void* stream);
+                  int split_k, int flags, void* stream);
 
 /* ---- small fused ops (HBM-bound elementwise / row ops) ------------------ */
 /* x fp32 [n][d] <- table bf16 [ids[i]][d] */
 int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, void* stream);
-/* x += delta (if delta != NULL); y bf16 = rmsnorm(x) * w */
-int stb_add_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps, void* stream);
-/* y bf16 [n][f] = silu(gu[:, :f]) * gu[:, f:]  (gu fp32 [n][2f]) */
-int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream);
+/* x += delta (if delta != NULL); y bf16 = rmsnorm(x) * w; delta rows < clear_rows
+ * are zeroed after reading (see stb_qkv_rope_commit) */
+int stb_add_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d, float eps, int clear_rows,
+                    void* stream);
+/* y bf16 [n][f] = silu(gu[:, :f]) * gu[:, f:]  (gu fp32 [n][2f]); gu rows < clear_rows zeroed after reading */
+int stb_silu_mul(float* gu, void* y, int n, int f, int clear_rows, void* stream);
 /* rows[i] = x[idx[i]] as bf16 after rmsnorm: final norm fused with row gather */
 int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,
                        void* stream);
 /* script-forced greedy sampling: out[r] = argmax(logits[r] + bias * onehot(target[r]))
- * (target < 0: plain argmax); raw_argmax[r] / raw_max[r] = unbiased argmax / max */
-int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
-                      int32_t* raw_argmax, float* raw_max, void* stream);
+ * (target < 0: plain argmax); raw_argmax[r] / raw_max[r] = unbiased argmax / max;
+ * clear != 0 zeroes the logits rows after reading */
+int stb_sample_forced(float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
+                      int32_t* raw_argmax, float* raw_max, int clear, void* stream);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,9 @@
 //               accumulators; TMEM is double-buffered so the next tile's MMAs run
 //               while the epilogue drains the previous one
 //   warps 2..5  epilogue: tcgen05.ld of their 32-lane TMEM quarter, fp32 stores
-//               (coalesced across the 32 features of a warp)
+//               (coalesced across the 32 features of a warp; stream-K partial
+//               sums as red.global.add — TMA bulk reductions through an smem
+//               stage measured no faster)
 //
 // Two schedules over the (tile, K-block) work space:
 //   tiles  tile t -> CTA t mod G, whole K, plain stores (enough tiles to fill
@@ -69,6 +71,7 @@ struct Sched {
   int kb;            // K blocks per tile
   int64_t units;     // tiles * kb
   unsigned* bar;     // stream-K grid barrier {count, generation}, self-resetting
+  int c_zeroed;      // stream-K: the caller guarantees C == 0 (no in-kernel zeroing, no barrier)
 };
 
 // Segment iterator: (tile, kb_begin, kb_end) for this CTA, in order.
@@ -209,16 +212,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue warps 2..5 -> TMEM lane quarters 2,3,0,1
     pdl_wait();
     const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;  // row of the 128-row tile this thread owns
     const bool atomic = sched.stream != 0;
+    const bool zero_here = atomic && !sched.c_zeroed;
     unsigned gen = 0;
-    if (atomic) {
-      // clear this CTA's slice of C, then arrive on the grid barrier
+    if (zero_here) {
+      // clear this CTA's slice of C (rows split across CTAs, float4 when the row is aligned),
+      // then arrive on the grid barrier
       const int G = gridDim.x;
       if (threadIdx.x == 64) gen = *(volatile unsigned*)(sched.bar + 1);
-      const int64_t total = (int64_t)M * N;
-      const int64_t lo = total * blockIdx.x / G, hi = total * (blockIdx.x + 1) / G;
-      for (int64_t e = lo + (threadIdx.x - 64); e < hi; e += 128) C[(e / N) * ldc + (e % N)] = 0.f;
+      const int et = threadIdx.x - 64;
+      const bool vec = (N % 4 == 0) && (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+      const int per_row = vec ? N / 4 : N;
+      const int total = M * per_row;
+      const int lo = (int)((int64_t)total * blockIdx.x / G), hi = (int)((int64_t)total * (blockIdx.x + 1) / G);
+      for (int e = lo + et; e < hi; e += 128) {
+        const int r = e / per_row, cidx = e - r * per_row;
+        if (vec)
+          reinterpret_cast<float4*>(C + (int64_t)r * ldc)[cidx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        else
+          C[(int64_t)r * ldc + cidx] = 0.f;
+      }
       __threadfence();
       epi_bar();
       if (threadIdx.x == 64) {
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    bool passed = !atomic;
+    bool passed = !zero_here;
     SegIter it(sched);
     int tile, k0, k1, j = 0;
     while (it.next(tile, k0, k1)) {
@@ -243,7 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         passed = true;
       }
-      const int feat = (tile % sched.tiles_n) * BM + row;
+      const int slab = (tile % sched.tiles_n) * BM + quarter * 32;  // this warp's 32 features
+      const int feat = slab + lane;
       const int t0 = (tile / sched.tiles_n) * bn;
       const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
 #pragma unroll 1
@@ -358,7 +372,7 @@ unsigned* grid_barrier() {
 
 template <int BN>
 int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
-           int mode, cudaStream_t st) {
+           int mode, int flags, cudaStream_t st) {
   using CF = Cfg<BN>;
   CUtensorMap tw, tx;
   if (int rc = cached_map(&tw, W, N, K, ldw, BM)) return rc;
@@ -377,6 +391,7 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   int grid = s.stream ? sms : (s.tiles < sms ? s.tiles : sms);
   if (mode >= 2 && mode < grid) grid = mode;
   if (s.stream && s.units < grid) grid = (int)s.units;
+  s.c_zeroed = (flags & STB_GEMM_C_ZEROED) ? 1 : 0;
   s.bar = grid_barrier();
   if (!s.bar) return fail(STB_ENOMEM, "gemm_bf16: barrier state");
   auto kern = gemm_bf16_persistent<BN>;
@@ -392,19 +407,30 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
 
 }  // namespace
 
+// 1 when stb_gemm_bf16(split_k = 0) would run this shape stream-K (reductions into C)
+extern "C" int stb_gemm_is_stream(int M, int N, int K) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  const int BNs = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+  const int nt = (M + BNs - 1) / BNs;
+  const int bn = nt == 1 ? BNs : (((M + nt - 1) / nt + 15) / 16) * 16;
+  const int tiles = ((N + BM - 1) / BM) * ((M + bn - 1) / bn);
+  const int sms = sm_count();
+  return (tiles >= 4 * sms || (M > 128 && tiles >= sms)) ? 0 : 1;
+}
+
 // split_k: 0 = automatic schedule, 1 = tile schedule (no reductions), >= 2 = stream-K over
 // min(split_k, SMs) CTAs (tests use it to force mid-tile splits).
 extern "C" int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M,
-                             int N, int K, int split_k, void* stream) {
+                             int N, int K, int split_k, int flags, void* stream) {
   if (M <= 0 || N <= 0) return STB_OK;
   if (K <= 0 || K % 8 != 0) return fail(STB_EINVAL, "gemm_bf16: K must be a positive multiple of 8");
   if (lda % 8 != 0 || ldw % 8 != 0) return fail(STB_EINVAL, "gemm_bf16: row strides must be multiples of 8");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
     return fail(STB_EINVAL, "gemm_bf16: operands must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  if (M <= 16) return launch<16>(A, lda, W, ldw, C, ldc, M, N, K, split_k, st);
-  if (M <= 32) return launch<32>(A, lda, W, ldw, C, ldc, M, N, K, split_k, st);
-  if (M <= 64) return launch<64>(A, lda, W, ldw, C, ldc, M, N, K, split_k, st);
-  if (M <= 128) return launch<128>(A, lda, W, ldw, C, ldc, M, N, K, split_k, st);
-  return launch<256>(A, lda, W, ldw, C, ldc, M, N, K, split_k, st);
+  if (M <= 16) return launch<16>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
+  if (M <= 32) return launch<32>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
+  if (M <= 64) return launch<64>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
+  if (M <= 128) return launch<128>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
+  return launch<256>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
 }

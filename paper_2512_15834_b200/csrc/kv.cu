@@ -103,11 +103,12 @@ __global__ void kv_copy_blocks_kernel(__nv_bfloat16* __restrict__ pages, const i
 
 // Fused QKV epilogue: rotate q and k (rotate-half RoPE), write q as bf16, commit k and v.
 // thread -> (token, head among n_q + 2*n_kv, group of 8 rotation pairs); every store is 16 bytes.
-__global__ void qkv_rope_commit_kernel(const float* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
+__global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
                                        const int32_t* __restrict__ slot_of, const int32_t* __restrict__ pos_of, int n,
                                        int n_q, int n_kv, int d_head, const float* __restrict__ inv_freq,
                                        const int32_t* __restrict__ table, int max_bps,
-                                       __nv_bfloat16* __restrict__ kpages, __nv_bfloat16* __restrict__ vpages) {
+                                       __nv_bfloat16* __restrict__ kpages, __nv_bfloat16* __restrict__ vpages,
+                                       int clear_rows) {
   pdl_wait();
   pdl_launch();
   const int half = d_head / 2;
@@ -118,11 +119,18 @@ __global__ void qkv_rope_commit_kernel(const float* __restrict__ qkv, __nv_bfloa
   int g = gid % groups;
   int h = (gid / groups) % heads;
   int t = gid / ((int64_t)groups * heads);
-  const float* row = qkv + ((int64_t)t * heads + h) * d_head;
+  float* row = qkv + ((int64_t)t * heads + h) * d_head;
   float4 a0 = *reinterpret_cast<const float4*>(row + g * 8);
   float4 a1 = *reinterpret_cast<const float4*>(row + g * 8 + 4);
   float4 b0 = *reinterpret_cast<const float4*>(row + half + g * 8);
   float4 b1 = *reinterpret_cast<const float4*>(row + half + g * 8 + 4);
+  if (t < clear_rows) {  // leave the GEMM accumulator zeroed for the next stream-K product
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(row + g * 8) = z;
+    *reinterpret_cast<float4*>(row + g * 8 + 4) = z;
+    *reinterpret_cast<float4*>(row + half + g * 8) = z;
+    *reinterpret_cast<float4*>(row + half + g * 8 + 4) = z;
+  }
   float x1[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
   float x2[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
   float y1[8], y2[8];
@@ -352,8 +360,8 @@ int stb_kv_copy_blocks(stb_kv_pool* p, const int32_t* src, const int32_t* dst, i
   return STB_OK;
 }
 
-int stb_qkv_rope_commit(stb_kv_pool* p, int layer, const float* qkv, void* q_out, const int32_t* slot_of,
-                        const int32_t* pos_of, int n, int n_q, float rope_theta, void* stream) {
+int stb_qkv_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                        const int32_t* pos_of, int n, int n_q, float rope_theta, int clear_rows, void* stream) {
   if (!p || layer < 0 || layer >= p->layers) return fail(STB_EINVAL, "qkv_rope_commit: bad layer");
   if (n <= 0) return STB_OK;
   // inverse frequencies are a pure function of (theta, d_head): cache one device table per pair
@@ -380,7 +388,7 @@ int stb_qkv_rope_commit(stb_kv_pool* p, int layer, const float* qkv, void* q_out
   int threads = 256;
   launch_k(qkv_rope_commit_kernel, dim3((unsigned)((total + threads - 1) / threads)), dim3(threads), 0, (cudaStream_t)stream, 
       qkv, (__nv_bfloat16*)q_out, slot_of, pos_of, n, n_q, p->n_kv, p->d_head, inv, p->dev_table, p->max_bps,
-      (__nv_bfloat16*)kp, (__nv_bfloat16*)vp);
+      (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, clear_rows);
   STB_CHECK_LAUNCH("qkv_rope_commit");
   return STB_OK;
 }

@@ -49,9 +49,9 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // x (+)= delta; y = bf16(x * rsqrt(mean(x^2) + eps) * w). One global read of x (and
 // delta), one write of x and y, a single block reduction.
 template <int VPT>
-__global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
+__global__ void add_rmsnorm_kernel(float* __restrict__ x, float* __restrict__ delta,
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int d,
-                                   float eps, const int32_t* __restrict__ gather) {
+                                   float eps, const int32_t* __restrict__ gather, int clear_rows) {
   pdl_wait();
   pdl_launch();
   __shared__ float red[32];
@@ -65,7 +65,9 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restric
     const int c = (i * blockDim.x + threadIdx.x) * 4;
     v[i] = *reinterpret_cast<const float4*>(xr + c);
     if (delta) {
-      const float4 e = *reinterpret_cast<const float4*>(delta + (int64_t)t * d + c);
+      float4* dp = reinterpret_cast<float4*>(delta + (int64_t)t * d + c);
+      const float4 e = *dp;
+      if (t < clear_rows) *dp = make_float4(0.f, 0.f, 0.f, 0.f);  // GEMM accumulator back to zero
       v[i].x += e.x;
       v[i].y += e.y;
       v[i].z += e.z;
@@ -88,8 +90,8 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, const float* __restric
 }
 
 // d = threads * 4 * VPT with threads a multiple of 32 and <= 1024
-int launch_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps,
-                   const int32_t* gather, cudaStream_t st) {
+int launch_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d, float eps,
+                   const int32_t* gather, int clear_rows, cudaStream_t st) {
   if (d % 128) return fail(STB_EINVAL, "rmsnorm: d must be a multiple of 128");
   const int v4 = d / 4;
   int vpt = 1;
@@ -100,25 +102,29 @@ int launch_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, 
   auto* yb = (__nv_bfloat16*)y;
   cudaError_t e;
   switch (vpt) {
-    case 1: e = launch_k(add_rmsnorm_kernel<1>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
-    case 2: e = launch_k(add_rmsnorm_kernel<2>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
-    case 4: e = launch_k(add_rmsnorm_kernel<4>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
-    default: e = launch_k(add_rmsnorm_kernel<8>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather); break;
+    case 1: e = launch_k(add_rmsnorm_kernel<1>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
+    case 2: e = launch_k(add_rmsnorm_kernel<2>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
+    case 4: e = launch_k(add_rmsnorm_kernel<4>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
+    default: e = launch_k(add_rmsnorm_kernel<8>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
   }
   if (e != cudaSuccess) return fail(STB_ECUDA, "rmsnorm launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
 
-__global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f) {
+__global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f, int clear_rows) {
   pdl_wait();
   pdl_launch();
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   int64_t total = (int64_t)n * f;
   if (i >= total) return;
   int64_t t = i / f, c = i % f;
-  const float* row = gu + t * 2 * f;
+  float* row = gu + t * 2 * f;
   float4 g = *reinterpret_cast<const float4*>(row + c);
   float4 u = *reinterpret_cast<const float4*>(row + f + c);
+  if (t < clear_rows) {
+    *reinterpret_cast<float4*>(row + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(row + f + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   auto silu = [](float a) { return a / (1.f + __expf(-a)); };
   uint2 o = make_uint2(pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y), pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w));
   *reinterpret_cast<uint2*>(y + i) = o;
@@ -169,16 +175,16 @@ __device__ __forceinline__ void block_arg(float& best, int& bi, float& bbest, in
   }
 }
 
-__global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ target,
+__global__ void sample_forced_kernel(float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ target,
                                      int V, float bias, int CH, ArgPart* __restrict__ parts,
                                      int* __restrict__ tickets, int32_t* __restrict__ out,
-                                     int32_t* __restrict__ raw_arg, float* __restrict__ raw_max) {
+                                     int32_t* __restrict__ raw_arg, float* __restrict__ raw_max, int clear) {
   pdl_wait();
   pdl_launch();
   __shared__ ArgPart sm[32];
   __shared__ int last;
   const int r = blockIdx.x / CH, ch = blockIdx.x % CH;
-  const float* row = logits + (int64_t)r * ld;
+  float* row = logits + (int64_t)r * ld;
   const int tgt = target ? target[r] : -1;
   const int span = ((V + CH - 1) / CH + 3) & ~3;
   const int lo = ch * span, hi = min(V, lo + span);
@@ -188,6 +194,7 @@ __global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t l
   if (vec) {
     for (int c = lo + threadIdx.x * 4; c < hi; c += blockDim.x * 4) {
       float4 v4 = *reinterpret_cast<const float4*>(row + c);
+      if (clear) *reinterpret_cast<float4*>(row + c) = make_float4(0.f, 0.f, 0.f, 0.f);
       float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -200,8 +207,10 @@ __global__ void sample_forced_kernel(const float* __restrict__ logits, int64_t l
     }
   } else {
     for (int c = lo + threadIdx.x; c < hi; c += blockDim.x) {
-      arg_merge(best, bi, row[c], c);
-      arg_merge(bbest, bbi, c == tgt ? row[c] + bias : row[c], c);
+      const float x = row[c];
+      if (clear) row[c] = 0.f;
+      arg_merge(best, bi, x, c);
+      arg_merge(bbest, bbi, c == tgt ? x + bias : x, c);
     }
   }
   block_arg(best, bi, bbest, bbi, sm);
@@ -274,28 +283,29 @@ int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, voi
   return STB_OK;
 }
 
-int stb_add_rmsnorm(float* x, const float* delta, const void* w, void* y, int n, int d, float eps, void* stream) {
+int stb_add_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d, float eps, int clear_rows,
+                    void* stream) {
   if (n <= 0) return STB_OK;
-  return launch_rmsnorm(x, delta, w, y, n, d, eps, nullptr, (cudaStream_t)stream);
+  return launch_rmsnorm(x, delta, w, y, n, d, eps, nullptr, clear_rows, (cudaStream_t)stream);
 }
 
 int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,
                        void* stream) {
   if (n <= 0) return STB_OK;
-  return launch_rmsnorm(const_cast<float*>(x), nullptr, w, y, n, d, eps, idx, (cudaStream_t)stream);
+  return launch_rmsnorm(const_cast<float*>(x), nullptr, w, y, n, d, eps, idx, 0, (cudaStream_t)stream);
 }
 
-int stb_silu_mul(const float* gu, void* y, int n, int f, void* stream) {
+int stb_silu_mul(float* gu, void* y, int n, int f, int clear_rows, void* stream) {
   if (n <= 0) return STB_OK;
   if (f % 4) return fail(STB_EINVAL, "silu_mul: f must be a multiple of 4");
   int64_t total = (int64_t)n * f / 4;
-  launch_k(silu_mul_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, gu, (__nv_bfloat16*)y, n, f);
+  launch_k(silu_mul_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, gu, (__nv_bfloat16*)y, n, f, clear_rows);
   STB_CHECK_LAUNCH("silu_mul");
   return STB_OK;
 }
 
-int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
-                      int32_t* raw_argmax, float* raw_max, void* stream) {
+int stb_sample_forced(float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
+                      int32_t* raw_argmax, float* raw_max, int clear, void* stream) {
   if (R <= 0) return STB_OK;
   constexpr int CH = 32;  // vocabulary chunks per row (<= 32: one warp reduces the partials)
   constexpr int kMaxRows = 65536;
@@ -309,7 +319,7 @@ int stb_sample_forced(const float* logits, int64_t ld, const int32_t* target, in
       return fail(STB_ENOMEM, "sample_forced: scratch allocation failed");
   }
   launch_k(sample_forced_kernel, dim3(R * CH), dim3(256), 0, (cudaStream_t)stream, logits, ld, target, V, bias, CH, parts, tickets, out,
-                                                                 raw_argmax, raw_max);
+                                                                 raw_argmax, raw_max, clear);
   STB_CHECK_LAUNCH("sample_forced");
   return STB_OK;
 }

@@ -33,6 +33,8 @@ from ..modelcfg import ModelShape
 from . import lib
 
 FORCE_BIAS = 1.0e4  # >> any logit spread of the random-init models (|logit| < 10)
+GEMM_C_ZEROED = 1   # include/stb200.h STB_GEMM_C_ZEROED
+CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
 
 
 class KVPool:
@@ -152,6 +154,9 @@ class Decoder:
         self.graph_replays = 0
         self._timed_parity = 0
         self.step_events: list | None = None  # (ev0, ev1, graphed, T) bracketing each step's kernels
+        # leading rows of each GEMM output that may be non-zero (rows at and past it are zero)
+        self._dirty = {"qkv": 0, "proj": 0, "gu": 0, "logits": 0}
+        self._stream_cache: dict = {}
 
     # -- buffers ----------------------------------------------------------------
 
@@ -162,22 +167,26 @@ class Decoder:
             f32, bf = torch.float32, torch.bfloat16
             self.x = torch.empty(cap, s.d_model, dtype=f32, device=dev)
             self.h = torch.empty(cap, s.d_model, dtype=bf, device=dev)
-            self.qkv = torch.empty(cap, s.q_dim + 2 * s.kv_dim, dtype=f32, device=dev)
+            # GEMM outputs start zeroed and are cleared by their consumers, so decode-shaped
+            # (stream-K) GEMMs accumulate into them with no memset (see _dirty)
+            self.qkv = torch.zeros(cap, s.q_dim + 2 * s.kv_dim, dtype=f32, device=dev)
             self.q = torch.empty(cap, s.q_dim, dtype=bf, device=dev)
             self.attn = torch.empty(cap, s.q_dim, dtype=bf, device=dev)
-            self.proj = torch.empty(cap, s.d_model, dtype=f32, device=dev)
-            self.gu = torch.empty(cap, 2 * s.d_ff, dtype=f32, device=dev)
+            self.proj = torch.zeros(cap, s.d_model, dtype=f32, device=dev)
+            self.gu = torch.zeros(cap, 2 * s.d_ff, dtype=f32, device=dev)
             self.act = torch.empty(cap, s.d_ff, dtype=bf, device=dev)
             self._cap_t = cap
+            self._dirty.update(qkv=0, proj=0, gu=0)
             self.graphs.clear()  # captured graphs point at the old buffers
         if R > self._cap_r:
             cap = max(R, 2 * self._cap_r, 64)
             self.rows = torch.empty(cap, s.d_model, dtype=torch.bfloat16, device=dev)
-            self.logits = torch.empty(cap, s.vocab, dtype=torch.float32, device=dev)
+            self.logits = torch.zeros(cap, s.vocab, dtype=torch.float32, device=dev)
             self.sampled = torch.empty(cap, dtype=torch.int32, device=dev)
             self.raw_arg = torch.empty(cap, dtype=torch.int32, device=dev)
             self.raw_max = torch.empty(cap, dtype=torch.float32, device=dev)
             self._cap_r = cap
+            self._dirty["logits"] = 0
             self.graphs.clear()
         if B > self._cap_b:
             cap = max(B, 2 * self._cap_b, 64)
@@ -228,6 +237,11 @@ class Decoder:
             max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
             self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
         else:
+            # decode graphs assume (and leave) every GEMM output zeroed
+            for name, rows in self._dirty.items():
+                if rows:
+                    getattr(self, name)[:rows].zero_()
+                    self._dirty[name] = 0
             timed = self.timers is not None
             # timed graphs carry their own event nodes: two copies alternate so a step's
             # events are not re-recorded while the runtime still has that step in flight
@@ -250,6 +264,8 @@ class Decoder:
             self.step_events.append((e0, e1, graphable, T))
         if self.keep_logits:
             self.last_logits = self.logits[:R].clone()
+            self.logits[:R].zero_()
+            self._dirty["logits"] = 0
             self.last_raw_argmax = self.raw_arg[:R].clone()
         return self.sampled[:R]
 
@@ -278,11 +294,13 @@ class Decoder:
         x, h = self.x, self.h
         call = lib.call
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
-        call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, st)
+        call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
+        clr = T if T <= CLEAR_MAX else 0
         for i in range(s.layers):
-            self.gemm(h[:T], w[f"l{i}.wqkv"], self.qkv[:T], st)
+            self.gemm(h[:T], w[f"l{i}.wqkv"], "qkv", st)
             call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]), _p(m["pos"]),
-                 T, s.n_q, s.rope_theta, st)
+                 T, s.n_q, s.rope_theta, clr, st)
+            self._cleared("qkv", clr)
             if B:
                 ev = self._tick()
                 call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
@@ -292,22 +310,30 @@ class Decoder:
                 call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                      _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                      st)
-            self.gemm(self.attn[:T], w[f"l{i}.wo"], self.proj[:T], st)
-            call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, st)
-            self.gemm(h[:T], w[f"l{i}.w_gate_up"], self.gu[:T], st)
-            call("stb_silu_mul", _p(self.gu), _p(self.act), T, s.d_ff, st)
-            self.gemm(self.act[:T], w[f"l{i}.w_down"], self.proj[:T], st)
+            self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st)
+            call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
+            self._cleared("proj", clr)
+            self.gemm(h[:T], w[f"l{i}.w_gate_up"], "gu", st)
+            call("stb_silu_mul", _p(self.gu), _p(self.act), T, s.d_ff, clr, st)
+            self._cleared("gu", clr)
+            self.gemm(self.act[:T], w[f"l{i}.w_down"], "proj", st)
             if i + 1 < s.layers:
                 call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i + 1}.attn_norm"]), _p(h), T, d,
-                     s.rms_eps, st)
+                     s.rms_eps, clr, st)
             else:  # residual add only; the final norm runs on the sampled rows
-                call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w["final_norm"]), None, T, d, s.rms_eps, st)
+                call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w["final_norm"]), None, T, d, s.rms_eps, clr, st)
+            self._cleared("proj", clr)
         rows = self.rows[:R]
         call("stb_gather_rmsnorm", _p(x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows), R, d, s.rms_eps, st)
-        logits = self.logits[:R]
-        self.gemm(rows, w["lm_head"], logits, st)
-        call("stb_sample_forced", _p(logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
-             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), st)
+        self.gemm(rows, w["lm_head"], "logits", st)
+        call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
+             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), 0 if self.keep_logits else 1, st)
+        if not self.keep_logits:
+            self._cleared("logits", R)
+
+    def _cleared(self, name: str, rows: int) -> None:
+        if rows >= self._dirty[name]:
+            self._dirty[name] = 0
 
     # -- timing (CUDA events on the launching stream; graph-safe) ----------------
 
@@ -343,10 +369,18 @@ class Decoder:
     def collect(self) -> None:
         self.fold(self.take_pending())
 
-    def gemm(self, a: torch.Tensor, wt: torch.Tensor, out: torch.Tensor, st: C.c_void_p) -> None:
+    def gemm(self, a: torch.Tensor, wt: torch.Tensor, out_name: str, st: C.c_void_p) -> None:
         M, K = a.shape
         N = wt.shape[0]
+        out = getattr(self, out_name)[:M]
+        key = (M, N, K)
+        stream = self._stream_cache.get(key)
+        if stream is None:
+            stream = self._stream_cache[key] = bool(lib.load().stb_gemm_is_stream(M, N, K))
+        flags = GEMM_C_ZEROED if (stream and self._dirty[out_name] == 0) else 0
         ev = self._tick()
-        lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0, st)
+        lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0,
+                 flags, st)
+        self._dirty[out_name] = max(self._dirty[out_name], M)
         # K5 algorithmic bytes: weights + activations in + fp32 out (HBM-bound when M is small)
         self._tock("gemm", ev, N * K * 2 + M * K * 2 + M * N * 4)

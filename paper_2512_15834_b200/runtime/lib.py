@@ -38,17 +38,18 @@ SIGNATURES: dict[str, tuple] = {
     "stb_kv_block_table": (I32, [P, C.POINTER(P), C.POINTER(I32)]),
     "stb_kv_commit": (I32, [P, I32, P, P, I64, P, P, I32, P]),
     "stb_kv_copy_blocks": (I32, [P, P, P, I32, P]),
-    "stb_qkv_rope_commit": (I32, [P, I32, P, P, P, P, I32, I32, F32, P]),
+    "stb_qkv_rope_commit": (I32, [P, I32, P, P, P, P, I32, I32, F32, I32, P]),
     "stb_attn_decode_workspace": (I64, [I32, I32, I32]),
     "stb_attn_decode": (I32, [P, I32, P, P, P, P, I32, I32, F32, I32, P, P]),
     "stb_attn_prefill": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, P]),
     "stb_spec_validate": (I32, [P, P, P, P, P, P, P, P, I32, P, P, P, P]),
-    "stb_gemm_bf16": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, I32, P]),
+    "stb_gemm_bf16": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, I32, I32, P]),
+    "stb_gemm_is_stream": (I32, [I32, I32, I32]),
     "stb_embed": (I32, [P, P, P, I32, I32, P]),
-    "stb_add_rmsnorm": (I32, [P, P, P, P, I32, I32, F32, P]),
-    "stb_silu_mul": (I32, [P, P, I32, I32, P]),
+    "stb_add_rmsnorm": (I32, [P, P, P, P, I32, I32, F32, I32, P]),
+    "stb_silu_mul": (I32, [P, P, I32, I32, I32, P]),
     "stb_gather_rmsnorm": (I32, [P, P, P, P, I32, I32, F32, P]),
-    "stb_sample_forced": (I32, [P, I64, P, I32, I32, F32, P, P, P, P]),
+    "stb_sample_forced": (I32, [P, I64, P, I32, I32, F32, P, P, P, I32, P]),
 }
 
 STATUS_CAPACITY = -4

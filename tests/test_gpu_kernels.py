@@ -41,10 +41,26 @@ def test_gemm_bf16(lib, M, N, K):
     a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     w = (0.05 * torch.randn(N, K, device="cuda", generator=g)).to(torch.bfloat16)
     c = torch.full((M, N), float("nan"), device="cuda")
-    lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, 0, stream())
+    lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, 0, 0, stream())
     ref = a.float() @ w.float().T
     torch.cuda.synchronize()
     assert rel(c, ref) < 2e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 256), (32, 6144, 4096), (64, 4096, 14336), (300, 640, 1024)])
+def test_gemm_c_zeroed(lib, M, N, K):
+    """STB_GEMM_C_ZEROED: a stream-K GEMM accumulates into a caller-zeroed C (no memset,
+    no grid barrier); tile-mode shapes ignore the flag."""
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (0.05 * torch.randn(N, K, device="cuda")).to(torch.bfloat16)
+    c = torch.zeros(M, N, device="cuda")
+    for _ in range(3):  # repeated launches stay exact because the caller re-zeroes
+        lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, 0, 1, stream())
+        ref = a.float() @ w.float().T
+        assert rel(c, ref) < 2e-5
+        c.zero_()
+    lib.load().stb_gemm_is_stream.restype  # exported
+    assert lib.load().stb_gemm_is_stream(32, 6144, 4096) in (0, 1)
 
 
 def test_gemm_explicit_split(lib):
@@ -54,7 +70,7 @@ def test_gemm_explicit_split(lib):
     ref = a.float() @ w.float().T
     for split in (1, 2, 5, 64, 148):
         c = torch.full((M, N), float("nan"), device="cuda")
-        lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, split, stream())
+        lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), N, M, N, K, split, 0, stream())
         assert rel(c, ref) < 2e-5, split
 
 
@@ -214,8 +230,11 @@ def test_rope_commit(lib):
     pos = torch.arange(150, 150 + n, dtype=torch.int32, device="cuda")
     slot_of = torch.zeros(n, dtype=torch.int32, device="cuda")
     q = torch.empty(n, shape.q_dim, dtype=torch.bfloat16, device="cuda")
+    qkv0 = qkv.clone()
     lib.call("stb_qkv_rope_commit", pool.h, 0, P(qkv), P(q), P(slot_of), P(pos), n, shape.n_q, shape.rope_theta,
-             stream())
+             20, stream())
+    assert not qkv[:20].any() and torch.equal(qkv[20:], qkv0[20:])  # consumer clears rows < clear_rows
+    qkv = qkv0
     from oracle.cpu_decoder import CpuDecoder
 
     dec = CpuDecoder.__new__(CpuDecoder)
@@ -241,14 +260,20 @@ def test_small_ops(lib):
     w = (1 + 0.1 * torch.randn(d, device="cuda")).to(torch.bfloat16)
     y = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
     x0 = x.clone()
-    lib.call("stb_add_rmsnorm", P(x), P(delta), P(w), P(y), n, d, 1e-5, stream())
-    xr = x0 + delta
+    delta0 = delta.clone()
+    lib.call("stb_add_rmsnorm", P(x), P(delta), P(w), P(y), n, d, 1e-5, n, stream())
+    assert not delta.any()
+    xr = x0 + delta0
     ref = xr * torch.rsqrt((xr * xr).mean(-1, keepdim=True) + 1e-5) * w.float()
     assert torch.allclose(x, xr) and rel(y, ref) < 5e-3
     gu = torch.randn(n, 2 * f, device="cuda")
     a = torch.empty(n, f, dtype=torch.bfloat16, device="cuda")
-    lib.call("stb_silu_mul", P(gu), P(a), n, f, stream())
+    gu0 = gu.clone()
+    lib.call("stb_silu_mul", P(gu), P(a), n, f, 0, stream())
     assert rel(a, torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]) < 5e-3
+    lib.call("stb_silu_mul", P(gu), P(a), n, f, 5, stream())
+    assert not gu[:5].any() and torch.equal(gu[5:], gu0[5:])
+    assert rel(a, torch.nn.functional.silu(gu0[:, :f]) * gu0[:, f:]) < 5e-3
     idx = torch.tensor([3, 0, 12], dtype=torch.int32, device="cuda")
     rows = torch.empty(3, d, dtype=torch.bfloat16, device="cuda")
     lib.call("stb_gather_rmsnorm", P(x), P(idx), P(w), P(rows), 3, d, 1e-5, stream())
@@ -262,11 +287,14 @@ def test_sample_forced(lib):
     out = torch.empty(R, dtype=torch.int32, device="cuda")
     raw = torch.empty(R, dtype=torch.int32, device="cuda")
     mx = torch.empty(R, device="cuda")
-    lib.call("stb_sample_forced", P(logits), V, P(target), R, V, 1e4, P(out), P(raw), P(mx), stream())
     am = logits.argmax(-1).int()
     want = torch.where(target >= 0, target, am)
-    assert torch.equal(out, want) and torch.equal(raw, am)
-    assert torch.equal(mx, logits.max(-1).values)
+    top = logits.max(-1).values
+    for clear in (0, 1):
+        lib.call("stb_sample_forced", P(logits), V, P(target), R, V, 1e4, P(out), P(raw), P(mx), clear, stream())
+        assert torch.equal(out, want) and torch.equal(raw, am)
+        assert torch.equal(mx, top)
+    assert not logits.any()
 
 
 def test_spec_validate(lib):

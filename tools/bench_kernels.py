@@ -61,7 +61,9 @@ def bench_gemm(shape, M, split=0):
         ws = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) for _ in range(copies)]
         a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
         c = torch.empty(M, N, device="cuda")
-        us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(ws[i % copies]), K, P(c), N, M, N, K, split, st()))
+        flags = 1 if lib.load().stb_gemm_is_stream(M, N, K) else 0  # as the decoder runs it
+        us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(ws[i % copies]), K, P(c), N, M, N, K, split,
+                                        flags, st()))
         byts = N * K * 2 + M * K * 2 + M * N * 4
         fl = 2 * M * N * K
         out[name] = (us, byts / us / 1e3, fl / us / 1e6)
@@ -139,16 +141,31 @@ def bench_pdl(shape, M=32):
     c = torch.empty(M, N, device="cuda")
 
     def norm(i):
-        lib.call("stb_add_rmsnorm", P(x), None, P(nw), P(h), M, K, 1e-5, st())
+        lib.call("stb_add_rmsnorm", P(x), None, P(nw), P(h), M, K, 1e-5, 0, st())
 
     def gemm(i):
-        lib.call("stb_gemm_bf16", P(h), K, P(ws[i % copies]), K, P(c), N, M, N, K, 0, st())
+        lib.call("stb_gemm_bf16", P(h), K, P(ws[i % copies]), K, P(c), N, M, N, K, 0, 0, st())
 
     t_norm = time_it(norm)
     t_gemm = time_it(gemm)
     t_pair = time_it(lambda i: (norm(i), gemm(i)))
     print(f"  pdl probe M={M}: rmsnorm {t_norm:.1f} us, qkv gemm {t_gemm:.1f} us, pair {t_pair:.1f} us "
           f"(overlap {t_norm + t_gemm - t_pair:.1f} us)")
+
+
+def bench_gemm_sweep(M=32, N=148 * 128):
+    """Fixed cost of a decode-shaped GEMM: time vs weight bytes at one tile per SM."""
+    for K in (64, 256, 1024, 4096, 8192):
+        copies = max(2, int(math.ceil(400e6 / (N * K * 2))))
+        ws = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) for _ in range(copies)]
+        a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+        c = torch.empty(M, N, device="cuda")
+        for split, flags in ((0, 0), (0, 1), (1, 0)):  # flags=1: caller-zeroed C (no memset/barrier)
+            us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(ws[i % copies]), K, P(c), N, M, N, K, split,
+                                            flags, st()))
+            print(f"  sweep M={M} N={N} K={K:5d} split={split} flags={flags}: {us:7.2f} us  "
+                  f"{N * K * 2 / us / 1e3:7.0f} GB/s")
+        del ws
 
 
 def main():
@@ -163,6 +180,8 @@ def main():
     if "gemm" in args.what:
         for M in [int(x) for x in args.M.split(",")]:
             bench_gemm(shape, M, args.split)
+    if "sweep" in args.what:
+        bench_gemm_sweep()
     if "pdl" in args.what:
         bench_pdl(shape)
     if "prefill" in args.what:
