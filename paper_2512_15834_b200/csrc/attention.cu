@@ -40,8 +40,9 @@ __device__ __forceinline__ void load_page(uint32_t ks, uint32_t vs, const __nv_b
   for (int i = 0; i < PER; ++i) {
     int idx = i * 32 + lane;
     int r = idx / CH, c = idx % CH;
-    cp_async16(ks + swz<D>(r, c), kp + r * D + c * 8);
-    cp_async16(vs + swz<D>(r, c), vp + r * D + c * 8);
+    // pages are pre-swizzled in HBM (pool.cuh): a linear copy lands them swizzled
+    cp_async16(ks + (r * CH + c) * 16, kp + r * D + c * 8);
+    cp_async16(vs + (r * CH + c) * 16, vp + r * D + c * 8);
   }
 }
 
@@ -192,7 +193,7 @@ __device__ __forceinline__ void chunk_step(const uint32_t (*qf)[4], uint32_t ks0
   mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
   const float mn0 = fmaxf(st.m[0], mx0), mn1 = fmaxf(st.m[1], mx1);
   const float ref0 = mn0 == -INFINITY ? 0.f : mn0, ref1 = mn1 == -INFINITY ? 0.f : mn1;
-  const float a0 = exp2f(st.m[0] - ref0), a1 = exp2f(st.m[1] - ref1);
+  const float a0 = fast_exp2(st.m[0] - ref0), a1 = fast_exp2(st.m[1] - ref1);
   st.m[0] = mn0;
   st.m[1] = mn1;
   float rs0 = 0.f, rs1 = 0.f;
@@ -202,10 +203,10 @@ __device__ __forceinline__ void chunk_step(const uint32_t (*qf)[4], uint32_t ks0
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       float* v = s[p * 2 + nt];
-      v[0] = exp2f(v[0] - ref0);
-      v[1] = exp2f(v[1] - ref0);
-      v[2] = exp2f(v[2] - ref1);
-      v[3] = exp2f(v[3] - ref1);
+      v[0] = fast_exp2(v[0] - ref0);
+      v[1] = fast_exp2(v[1] - ref0);
+      v[2] = fast_exp2(v[2] - ref1);
+      v[3] = fast_exp2(v[3] - ref1);
       rs0 += v[0] + v[1];
       rs1 += v[2] + v[3];
       pf[p][nt * 2 + 0] = pack_bf16(v[0], v[1]);
@@ -286,9 +287,12 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   constexpr int STAGE = NP * 2 * PAGE;  // K and V of NP pages
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int64_t prefix[kMaxB + 1];  // chunk units before sequence b
+  __shared__ __align__(8) uint64_t full_bars[4 * STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = n_kv * G;
   if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < 4 * STAGES; ++s2) mbar_init(&full_bars[s2], 1);
+    fence_mbar_init();
     int64_t acc = 0;
     for (int b = 0; b < B; ++b) {
       prefix[b] = acc;
@@ -306,9 +310,16 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   const int n = (int)(u1 - u0);
   if (n <= 0) return;
 
-  // cursor over (b, kh, chunk) — located once by binary search, then incremented
+  // cursor over (b, kh, chunk) — located once by binary search, then incremented;
+  // the pair's block-table row and length are cached when the cursor enters it
   struct Cur {
-    int b, kh, c, chunks;
+    int b, kh, c, chunks, ctx;
+    const int32_t* row;
+  };
+  auto enter = [&](Cur& r) {
+    r.ctx = ctx_lens[r.b];
+    r.chunks = (r.ctx + 16 * NP - 1) / (16 * NP);
+    r.row = table + (int64_t)slots[r.b] * max_bps;
   };
   auto locate = [&](int64_t u) {
     int lo = 0, hi = B - 1;
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     }
     Cur r;
     r.b = lo;
-    r.chunks = (ctx_lens[lo] + 16 * NP - 1) / (16 * NP);
+    enter(r);
     const int rem = (int)(u - prefix[lo]);
     r.kh = rem / r.chunks;
     r.c = rem - r.kh * r.chunks;
@@ -331,31 +342,49 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     r.kh = 0;
     do {
       ++r.b;
-      r.chunks = r.b < B ? (ctx_lens[r.b] + 16 * NP - 1) / (16 * NP) : 1;
+      if (r.b < B) enter(r);
     } while (r.b < B && r.chunks == 0);
   };
+  // K/V pages arrive by bulk copy (one lane, 4 KiB each) into a per-warp STAGES ring;
+  // full[s] counts the bytes. Page ids are fetched one chunk ahead of their copy.
   const uint32_t wbase = smem_u32(smem) + warp * STAGES * STAGE;
-  auto issue = [&](const Cur& r, int i) {
-    const int32_t* row = table + (int64_t)slots[r.b] * max_bps;
-    const int npages = (ctx_lens[r.b] + 15) >> 4;
-    const uint32_t sb = wbase + (i % STAGES) * STAGE;
+  uint64_t* full = full_bars + warp * STAGES;
+  int pid[NP];
+  auto fetch = [&](const Cur& r) {
+    const int npages = (r.ctx + 15) >> 4;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const int page = r.c * NP + p;
-      if (page < npages) {
-        const int64_t off = (((int64_t)row[page] * n_kv + r.kh) * 16) * D;
-        load_page<D>(sb + p * 2 * PAGE, sb + p * 2 * PAGE + PAGE, kpages + off, vpages + off, lane);
+      pid[p] = page < npages ? __ldg(r.row + page) : -1;
+    }
+  };
+  auto issue = [&](const Cur& r, int i) {  // lane 0
+    const uint32_t sb = wbase + (i % STAGES) * STAGE;
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) bytes += pid[p] >= 0 ? 2 * PAGE : 0;
+    uint64_t* bar = full + (i % STAGES);
+    mbar_expect_tx(bar, bytes);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if (pid[p] >= 0) {
+        const int64_t off = (((int64_t)pid[p] * n_kv + r.kh) * 16) * D;
+        bulk_load(sb + p * 2 * PAGE, kpages + off, PAGE, bar);
+        bulk_load(sb + p * 2 * PAGE + PAGE, vpages + off, PAGE, bar);
       }
     }
   };
   Cur ld = locate(u0);
+  if (lane == 0) {
+    fetch(ld);
 #pragma unroll
-  for (int s2 = 0; s2 < STAGES - 1; ++s2) {
-    if (s2 < n) {
-      issue(ld, s2);
-      advance(ld);
+    for (int s2 = 0; s2 < STAGES - 1; ++s2) {
+      if (s2 < n) {
+        issue(ld, s2);
+        advance(ld);
+        fetch(ld);
+      }
     }
-    cp_async_commit();
   }
   Cur cu = locate(u0);
   uint32_t qf[D / 16][4];
@@ -367,23 +396,23 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     if (!open) {
       open = true;
       seg_first = cu.c;
-      seg_ctx = ctx_lens[cu.b];
+      seg_ctx = cu.ctx;
       seg_start = u0 + i;
       const int r0 = lane >> 2, r1 = r0 + 8;
       const __nv_bfloat16* qb = q + ((int64_t)cu.b * n_q + cu.kh * G) * D;
       load_q<D>(qf, r0 < G ? qb + r0 * D : nullptr, r1 < G ? qb + r1 * D : nullptr, qscale, lane);
       st.init();
     }
-    cp_async_wait<STAGES - 2>();
-    __syncwarp();
+    mbar_wait(full + (i % STAGES), (uint32_t)(i / STAGES) & 1u);
     const int lim = seg_ctx - cu.c * 16 * NP;
     chunk_step<D, NP>(qf, wbase + (i % STAGES) * STAGE, lim, lim, st, lane);
-    __syncwarp();
-    if (i + STAGES - 1 < n) {
+    __syncwarp();  // every lane's ldmatrix reads of the slot refilled below are done
+    if (lane == 0 && i + STAGES - 1 < n) {
+      fence_proxy_async_smem();
       issue(ld, i + STAGES - 1);
       advance(ld);
+      fetch(ld);
     }
-    cp_async_commit();
     const bool pair_end = cu.c == cu.chunks - 1;
     if (pair_end || i == n - 1) {
       // close the segment of pair (cu.b, cu.kh)
@@ -430,28 +459,58 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
           __threadfence();
-          for (int r = 0; r < G; ++r) {
-            float M = -INFINITY;
-            for (int c = wf; c <= wl; ++c) {
-              const int sl = c * 2 + ((c == wf && (U * c / W) < pstart) ? 1 : 0);
-              M = fmaxf(M, __ldcg(lse_part + sl * G + r));
-            }
-            float L = 0.f, acc[D / 32];
+          // merge the nc partials of this pair: lanes own contributors for the LSE
+          // reductions, then every lane accumulates D/32 dims of all G rows with the
+          // contributor loop unrolled so the partial loads overlap
+          const int nc = wl - wf + 1;
+          auto part = [&](int c) { return c * 2 + ((c == wf && (U * c / W) < pstart) ? 1 : 0); };
+          float M[G], L[G], wt_l[G];
 #pragma unroll
-            for (int j = 0; j < D / 32; ++j) acc[j] = 0.f;
-            if (M != -INFINITY) {
-              for (int c = wf; c <= wl; ++c) {
-                const int sl = c * 2 + ((c == wf && (U * c / W) < pstart) ? 1 : 0);
-                const float wt = exp2f(__ldcg(lse_part + sl * G + r) - M);
-                L += wt;
+          for (int r = 0; r < G; ++r) M[r] = -INFINITY, L[r] = 0.f, wt_l[r] = 0.f;
+          for (int j = lane; j < nc; j += 32) {
+            const int sl = part(wf + j);
 #pragma unroll
-                for (int j = 0; j < D / 32; ++j) acc[j] += wt * __ldcg(o_part + ((int64_t)sl * G + r) * D + j * 32 + lane);
-              }
+            for (int r = 0; r < G; ++r) M[r] = fmaxf(M[r], __ldcg(lse_part + sl * G + r));
+          }
+#pragma unroll
+          for (int r = 0; r < G; ++r)
+#pragma unroll
+            for (int o = 16; o; o >>= 1) M[r] = fmaxf(M[r], __shfl_xor_sync(0xffffffffu, M[r], o));
+          for (int j = lane; j < nc; j += 32) {
+            const int sl = part(wf + j);
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+              const float wt = M[r] == -INFINITY ? 0.f : exp2f(__ldcg(lse_part + sl * G + r) - M[r]);
+              L[r] += wt;
+              if (j < 32) wt_l[r] = wt;
             }
+          }
+#pragma unroll
+          for (int r = 0; r < G; ++r)
+#pragma unroll
+            for (int o = 16; o; o >>= 1) L[r] += __shfl_xor_sync(0xffffffffu, L[r], o);
+          float acc[G][D / 32];
+#pragma unroll
+          for (int r = 0; r < G; ++r)
+#pragma unroll
+            for (int j = 0; j < D / 32; ++j) acc[r][j] = 0.f;
+#pragma unroll 4
+          for (int c = 0; c < nc; ++c) {
+            const int sl = part(wf + c);
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+              float wt = __shfl_sync(0xffffffffu, wt_l[r], c & 31);
+              if (c >= 32) wt = M[r] == -INFINITY ? 0.f : exp2f(__ldcg(lse_part + sl * G + r) - M[r]);
+#pragma unroll
+              for (int j = 0; j < D / 32; ++j) acc[r][j] += wt * __ldcg(o_part + ((int64_t)sl * G + r) * D + j * 32 + lane);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < G; ++r)
 #pragma unroll
             for (int j = 0; j < D / 32; ++j)
-              out[((int64_t)sb * n_q + skh * G + r) * D + j * 32 + lane] = __float2bfloat16_rn(L > 0.f ? acc[j] / L : 0.f);
-          }
+              out[((int64_t)sb * n_q + skh * G + r) * D + j * 32 + lane] =
+                  __float2bfloat16_rn(L[r] > 0.f ? acc[r][j] / L[r] : 0.f);
           if (lane == 0) tickets[sb * n_kv + skh] = 0;
         }
       }
@@ -459,7 +518,6 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     }
     advance(cu);
   }
-  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------- short-run prefill
@@ -515,8 +573,8 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
     uint32_t ks = base + stage * 2 * PAGE, vs = ks + PAGE;
     for (int idx = threadIdx.x; idx < 16 * CH; idx += 128) {
       int r = idx / CH, c = idx % CH;
-      cp_async16(ks + swz<D>(r, c), kp + r * D + c * 8);
-      cp_async16(vs + swz<D>(r, c), vp + r * D + c * 8);
+      cp_async16(ks + (r * D / 8 + c) * 16, kp + r * D + c * 8);  // pre-swizzled pages: linear copy
+      cp_async16(vs + (r * D / 8 + c) * 16, vp + r * D + c * 8);
     }
   };
 #pragma unroll

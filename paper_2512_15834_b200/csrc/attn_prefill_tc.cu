@@ -339,12 +339,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 }
 
 int encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-           const cuuint32_t* box) {
+           const cuuint32_t* box, CUtensorMapSwizzle swizzle) {
   auto fn = encode_tiled();
   if (!fn) return fail(STB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(STB_ECUDA, "attn_prefill_tc: tensor map encode failed (%d)", (int)r);
   return STB_OK;
@@ -375,13 +375,13 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
       cuuint64_t qd[4] = {(cuuint64_t)D, (cuuint64_t)G, (cuuint64_t)n_kv, (cuuint64_t)T};
       cuuint64_t qs[3] = {(cuuint64_t)D * 2, (cuuint64_t)G * D * 2, (cuuint64_t)n_kv * G * D * 2};
       cuuint32_t qb[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)(ROWS / G)};
-      if (int rc = encode(&mp.q, q, 4, qd, qs, qb)) return rc;
+      if (int rc = encode(&mp.q, q, 4, qd, qs, qb, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
       const cuuint64_t rows = (cuuint64_t)pool->num_blocks * n_kv * 16;
       cuuint64_t kd[2] = {(cuuint64_t)D, rows};
       cuuint64_t ks[1] = {(cuuint64_t)D * 2};
       cuuint32_t kb[2] = {64, 16};
-      if (int rc = encode(&mp.k, kp, 2, kd, ks, kb)) return rc;
-      if (int rc = encode(&mp.v, vp, 2, kd, ks, kb)) return rc;
+      if (int rc = encode(&mp.k, kp, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return rc;
+      if (int rc = encode(&mp.v, vp, 2, kd, ks, kb, CU_TENSOR_MAP_SWIZZLE_NONE)) return rc;
       if (cache.size() > 4096) cache.clear();
       cache.emplace(key, mp);
     }

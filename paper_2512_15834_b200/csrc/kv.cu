@@ -80,7 +80,7 @@ __global__ void kv_commit_kernel(const __nv_bfloat16* __restrict__ k, const __nv
   int pos = pos_of[t];
   int blk = table[(int64_t)slot_of[t] * max_bps + (pos >> 4)];
   int h = (c * 8) / d_head, dd = (c * 8) % d_head;
-  int64_t dst = (((int64_t)blk * n_kv + h) * 16 + (pos & 15)) * d_head + dd;
+  int64_t dst = (((int64_t)blk * n_kv + h) * 16 + (pos & 15)) * d_head + kv_phys_chunk(pos & 15, dd / 8) * 8;
   const __nv_bfloat16* src = (which ? v : k) + (int64_t)t * ld + c * 8;
   __nv_bfloat16* pages = which ? vpages : kpages;
   *reinterpret_cast<uint4*>(pages + dst) = *reinterpret_cast<const uint4*>(src);
@@ -150,6 +150,7 @@ __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* _
   uint4 lo = make_uint4(pack_bf16(y1[0], y1[1]), pack_bf16(y1[2], y1[3]), pack_bf16(y1[4], y1[5]), pack_bf16(y1[6], y1[7]));
   uint4 hi = make_uint4(pack_bf16(y2[0], y2[1]), pack_bf16(y2[2], y2[3]), pack_bf16(y2[4], y2[5]), pack_bf16(y2[6], y2[7]));
   __nv_bfloat16* dst;
+  int c_lo = g, c_hi = half / 8 + g;  // 16-byte chunks of the row
   if (h < n_q) {
     dst = q_out + ((int64_t)t * n_q + h) * d_head;
   } else {
@@ -157,9 +158,11 @@ __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* _
     __nv_bfloat16* pages = (h < n_q + n_kv) ? kpages : vpages;
     int blk = table[(int64_t)slot_of[t] * max_bps + (pos >> 4)];
     dst = pages + (((int64_t)blk * n_kv + kvh) * 16 + (pos & 15)) * d_head;
+    c_lo = kv_phys_chunk(pos & 15, c_lo);  // pre-swizzled page layout (pool.cuh)
+    c_hi = kv_phys_chunk(pos & 15, c_hi);
   }
-  *reinterpret_cast<uint4*>(dst + g * 8) = lo;
-  *reinterpret_cast<uint4*>(dst + half + g * 8) = hi;
+  *reinterpret_cast<uint4*>(dst + c_lo * 8) = lo;
+  *reinterpret_cast<uint4*>(dst + c_hi * 8) = hi;
 }
 
 // ------------------------------------------------------------------- C ABI

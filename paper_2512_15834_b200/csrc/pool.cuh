@@ -26,6 +26,13 @@ struct stb_kv_pool {
 };
 
 
+// Pages are stored pre-swizzled: within each 128-byte half-row of a [16][d_head] page,
+// logical 16-byte chunk c of token row r sits at chunk (c ^ r) & 7. That is exactly the
+// layout TMA SWIZZLE_128B / the ldmatrix XOR swizzle produce in shared memory, so a
+// page is moved HBM -> smem with plain bulk copies (no per-lane swizzle, no tensor-map
+// swizzle) and consumed in place.
+__host__ __device__ __forceinline__ int kv_phys_chunk(int row, int c) { return (c & ~7) | ((c ^ row) & 7); }
+
 extern "C" int stb_pool_geometry(const stb_kv_pool* p, int* n_kv, int* d_head);
 extern "C" int stb_kv_layer_ptrs(const stb_kv_pool* pool, int layer, void** k_pages, void** v_pages);
 // K2 tensor-core path (attn_prefill_tc.cu), dispatched from stb_attn_prefill

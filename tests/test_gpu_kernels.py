@@ -125,8 +125,13 @@ def _dense_kv(pool, layer, slot, n, shape):
     torch.cuda.synchronize()
     kbuf = _view(kp, per)
     vbuf = _view(vp, per)
-    k = kbuf.view(nb, shape.n_kv, 16, shape.d_head)
-    v = vbuf.view(nb, shape.n_kv, 16, shape.d_head)
+    # pages are pre-swizzled (csrc/pool.cuh kv_phys_chunk): logical chunk c of row r is
+    # stored at chunk (c & ~7) | ((c ^ r) & 7)
+    ch = shape.d_head // 8
+    perm = torch.tensor([[(c & ~7) | ((c ^ r) & 7) for c in range(ch)] for r in range(16)], device="cuda")
+    idx = perm.view(1, 1, 16, ch, 1).expand(nb, shape.n_kv, 16, ch, 8)
+    k = kbuf.view(nb, shape.n_kv, 16, ch, 8).gather(3, idx).view(nb, shape.n_kv, 16, shape.d_head)
+    v = vbuf.view(nb, shape.n_kv, 16, ch, 8).gather(3, idx).view(nb, shape.n_kv, 16, shape.d_head)
     blocks = torch.tensor(pool.blocks(slot), device="cuda", dtype=torch.long)
     kd = k[blocks].permute(0, 2, 1, 3).reshape(-1, shape.n_kv, shape.d_head)[:n]
     vd = v[blocks].permute(0, 2, 1, 3).reshape(-1, shape.n_kv, shape.d_head)[:n]
@@ -177,7 +182,7 @@ SHAPES = [ModelShape("llama-ish", 1, 4096, 32, 8, 128, 64, 64), ModelShape("tiny
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
-@pytest.mark.parametrize("ctxs", [[1], [5, 16, 17, 33], [4096] * 4 + [100, 2500], [700] * 32])
+@pytest.mark.parametrize("ctxs", [[1], [5, 16, 17, 33], [4096] * 4 + [100, 2500], [700] * 32, [8000], [8000, 2]])
 def test_attn_decode(lib, shape, ctxs):
     pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(ctxs), bps=512)
     dense = _fill_pool(lib, pool, shape, ctxs, seed=len(ctxs))
