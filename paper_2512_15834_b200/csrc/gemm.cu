@@ -67,12 +67,28 @@ struct Cfg {
 struct Sched {
   int stream;        // 0: tile schedule, 1: stream-K
   int tiles_n;       // feature tiles (of BM rows)
-  int tiles;         // tiles_n * token tiles
+  int tiles_m;       // token tiles (of bn rows)
+  int tiles;         // tiles_n * tiles_m, ordered feature-major: the tiles_m token tiles
+                     // that share a weight slice are adjacent, so they run concurrently and
+                     // the slice is read from HBM once (L2 serves the others)
   int kb;            // K blocks per tile
   int64_t units;     // tiles * kb
   unsigned* bar;     // stream-K grid barrier {count, generation}, self-resetting
   int c_zeroed;      // stream-K: the caller guarantees C == 0 (no in-kernel zeroing, no barrier)
+  int tag;           // launch sequence number (debug trace only)
 };
+
+// Debug timeline (stb_debug_gemm_trace): per CTA {tag, t_last_epilogue, sm, t_entry,
+// t_dep_wait, t_first_stage, t_last_mma_issue, t_exit} in %globaltimer ns. Off (null) in
+// production; %globaltimer ticks at ~1 us here, so read medians over CTAs, not deltas.
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned int g_trace_n = 0;
+__device__ unsigned int g_trace_cap = 0;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Segment iterator: (tile, kb_begin, kb_end) for this CTA, in order.
 struct SegIter {
@@ -124,6 +140,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + STAGES;   // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  __shared__ unsigned long long tt[5];
+  const bool tracing = g_trace != nullptr;
+  if (tracing && threadIdx.x == 0) tt[0] = gtime();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -151,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       SegIter pre(sched);
       int tile, k0, k1, i = 0;
       while (i < STAGES && pre.next(tile, k0, k1)) {
-        const int f0 = (tile % sched.tiles_n) * BM;
+        const int f0 = (tile / sched.tiles_m) * BM;
         for (int k = k0; k < k1 && i < STAGES; ++k, ++i) {
           mbar_expect_tx(&full[i], CF::W_BYTES + bn * BK * 2);
           tma_load_2d(smem + i * CF::STAGE, &tm_w, &full[i], k * BK, f0);
@@ -159,12 +178,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int prefetched = i;
       pdl_wait();
+      if (tracing) tt[1] = gtime();
       pdl_launch();
       SegIter it(sched);
       i = 0;
       while (it.next(tile, k0, k1)) {
-        const int f0 = (tile % sched.tiles_n) * BM;
-        const int t0 = (tile / sched.tiles_n) * bn;
+        const int f0 = (tile / sched.tiles_m) * BM;
+        const int t0 = (tile % sched.tiles_m) * bn;
         for (int k = k0; k < k1; ++k, ++i) {
           const int s = i % STAGES;
           uint8_t* sw = smem + s * CF::STAGE;
@@ -193,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = k0; k < k1; ++k, ++i) {
           const int s = i % STAGES;
           mbar_wait(&full[s], (i / STAGES) & 1);
+          if (tracing && i == 0) tt[2] = gtime();
           tc_fence_after();
           const uint32_t wa = smem_u32(smem + s * CF::STAGE);
           const uint32_t xa = wa + CF::W_BYTES;
@@ -206,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&acc_full[buf]);
         ++j;
       }
+      if (tracing) tt[3] = gtime();
     }
     __syncwarp();
   } else {
@@ -248,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (it.next(tile, k0, k1)) {
       const int buf = j & 1;
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      if (tracing && threadIdx.x == 64) tt[4] = gtime();
       tc_fence_after();
       if (!passed) {  // every slice of C is zero before the first reduction lands
         if (threadIdx.x == 64)
@@ -256,9 +279,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         passed = true;
       }
-      const int slab = (tile % sched.tiles_n) * BM + quarter * 32;  // this warp's 32 features
+      const int slab = (tile / sched.tiles_m) * BM + quarter * 32;  // this warp's 32 features
       const int feat = slab + lane;
-      const int t0 = (tile / sched.tiles_n) * bn;
+      const int t0 = (tile % sched.tiles_m) * bn;
       const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
 #pragma unroll 1
       for (int c = 0; c < bn / 16; ++c) {
@@ -290,6 +313,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_free(tmem, CF::TMEM_COLS);
+  if (tracing && threadIdx.x == 64) {
+    const unsigned slot = atomicAdd(&g_trace_n, 1u);
+    if (slot < g_trace_cap) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      unsigned long long* r = g_trace + (size_t)slot * 8;
+      r[0] = (unsigned long long)sched.tag;
+      r[1] = tt[4];
+      r[2] = sm;
+      r[3] = tt[0];
+      r[4] = tt[1];
+      r[5] = tt[2];
+      r[6] = tt[3];
+      r[7] = gtime();
+    }
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -370,28 +409,69 @@ unsigned* grid_barrier() {
   return bar;
 }
 
+int bn_template(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
+
+// Token-tile height and schedule for an M x N product.
+//  M <= 128 (decode: HBM-bound on the weights): one token tile; tile schedule only when
+//    the tiles fill the machine several times over, stream-K otherwise so every SM
+//    streams weights for the whole kernel.
+//  M > 128 (prefill / ingest: tensor-bound): pick the number of token tiles that
+//    minimises waves x (bn + fixed per-tile cost) — wave quantisation dominates at a few
+//    hundred tokens — and use whole tiles unless they would leave most SMs idle.
+struct Plan {
+  int bn, tiles_m, stream;
+};
+Plan plan(int M, int N, int sms) {
+  const int BN = bn_template(M);
+  const int tiles_n = (N + BM - 1) / BM;
+  Plan p{BN, 1, 0};
+  if (M <= 128) {
+    p.stream = tiles_n >= 4 * sms ? 0 : 1;
+    return p;
+  }
+  constexpr int kTileCost = 48;  // per-tile fill/epilogue + smaller-tile inefficiency, in token columns
+  long best = -1;
+  for (int nt = (M + 255) / 256; nt <= (M + 63) / 64; ++nt) {
+    const int bn = (((M + nt - 1) / nt + 15) / 16) * 16;
+    if (bn > 256) continue;
+    const int tm = (M + bn - 1) / bn;
+    const long tiles = (long)tiles_n * tm;
+    const long cost = ((tiles + sms - 1) / sms) * (long)(bn + kTileCost);
+    if (best < 0 || cost < best) {
+      best = cost;
+      p.bn = bn;
+      p.tiles_m = tm;
+    }
+  }
+  const long tiles = (long)tiles_n * p.tiles_m;
+  const long waves = (tiles + sms - 1) / sms;
+  p.stream = 2 * tiles < waves * sms ? 1 : 0;  // whole tiles would leave most SMs idle
+  return p;
+}
+
 template <int BN>
 int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
            int mode, int flags, cudaStream_t st) {
   using CF = Cfg<BN>;
   CUtensorMap tw, tx;
   if (int rc = cached_map(&tw, W, N, K, ldw, BM)) return rc;
-  // token tile: BN for M <= BN; above, split M into ceil(M/BN) near-equal tiles (multiple of 16)
-  const int nt = (M + BN - 1) / BN;
-  const int bn = nt == 1 ? BN : (((M + nt - 1) / nt + 15) / 16) * 16;
+  const int sms = sm_count();
+  const Plan pl = plan(M, N, sms);
+  const int bn = pl.bn;
   if (int rc = cached_map(&tx, X, M, K, lda, bn)) return rc;
   Sched s;
   s.tiles_n = (N + BM - 1) / BM;
-  s.tiles = s.tiles_n * ((M + bn - 1) / bn);
+  s.tiles_m = pl.tiles_m;
+  s.tiles = s.tiles_n * s.tiles_m;
   s.kb = (K + BK - 1) / BK;
   s.units = (int64_t)s.tiles * s.kb;
-  const int sms = sm_count();
-  // tile schedule when the tiles alone fill the machine several times over; stream-K otherwise
-  s.stream = mode == 1 ? 0 : (mode >= 2 ? 1 : ((s.tiles >= 4 * sms || (M > 128 && s.tiles >= sms)) ? 0 : 1));
+  s.stream = mode == 1 ? 0 : (mode >= 2 ? 1 : pl.stream);
   int grid = s.stream ? sms : (s.tiles < sms ? s.tiles : sms);
   if (mode >= 2 && mode < grid) grid = mode;
   if (s.stream && s.units < grid) grid = (int)s.units;
   s.c_zeroed = (flags & STB_GEMM_C_ZEROED) ? 1 : 0;
+  static int launch_seq = 0;
+  s.tag = launch_seq++;
   s.bar = grid_barrier();
   if (!s.bar) return fail(STB_ENOMEM, "gemm_bf16: barrier state");
   auto kern = gemm_bf16_persistent<BN>;
@@ -410,16 +490,24 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
 // 1 when stb_gemm_bf16(split_k = 0) would run this shape stream-K (reductions into C)
 extern "C" int stb_gemm_is_stream(int M, int N, int K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
-  const int BNs = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
-  const int nt = (M + BNs - 1) / BNs;
-  const int bn = nt == 1 ? BNs : (((M + nt - 1) / nt + 15) / 16) * 16;
-  const int tiles = ((N + BM - 1) / BM) * ((M + bn - 1) / bn);
-  const int sms = sm_count();
-  return (tiles >= 4 * sms || (M > 128 && tiles >= sms)) ? 0 : 1;
+  return plan(M, N, sm_count()).stream;
 }
 
 // split_k: 0 = automatic schedule, 1 = tile schedule (no reductions), >= 2 = stream-K over
 // min(split_k, SMs) CTAs (tests use it to force mid-tile splits).
+// Debug only (not part of include/stb200.h): record per-CTA GEMM timelines into
+// buf[cap][8] (device memory) — buf = NULL turns tracing off. Returns records written.
+extern "C" int stb_debug_gemm_trace(void* buf, int cap) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
+  unsigned long long* p = (unsigned long long*)buf;
+  unsigned int c = (unsigned int)cap, z = 0;
+  cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+  cudaMemcpyToSymbol(g_trace_cap, &c, sizeof(c));
+  cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z));
+  return (int)n;
+}
+
 extern "C" int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M,
                              int N, int K, int split_k, int flags, void* stream) {
   if (M <= 0 || N <= 0) return STB_OK;

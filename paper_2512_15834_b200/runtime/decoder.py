@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,6 +34,9 @@ from ..modelcfg import ModelShape
 from . import lib
 
 FORCE_BIAS = 1.0e4  # >> any logit spread of the random-init models (|logit| < 10)
+# timing experiments only: comma-separated C-ABI entry points the step does not launch
+# (outputs are garbage; tools/profile_step.py uses it to attribute in-step time under PDL)
+_SKIP = frozenset(k for k in os.environ.get("STB200_SKIP_KERNELS", "").split(",") if k)
 GEMM_C_ZEROED = 1   # include/stb200.h STB_GEMM_C_ZEROED
 CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
 
@@ -292,12 +296,12 @@ class Decoder:
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         d = s.d_model
         x, h = self.x, self.h
-        call = lib.call
+        call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
         clr = T if T <= CLEAR_MAX else 0
         for i in range(s.layers):
-            self.gemm(h[:T], w[f"l{i}.wqkv"], "qkv", st)
+            self.gemm(h[:T], w[f"l{i}.wqkv"], "qkv", st, "wqkv")
             call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]), _p(m["pos"]),
                  T, s.n_q, s.rope_theta, clr, st)
             self._cleared("qkv", clr)
@@ -310,13 +314,13 @@ class Decoder:
                 call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                      _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                      st)
-            self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st)
+            self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
             self._cleared("proj", clr)
-            self.gemm(h[:T], w[f"l{i}.w_gate_up"], "gu", st)
+            self.gemm(h[:T], w[f"l{i}.w_gate_up"], "gu", st, "w_gate_up")
             call("stb_silu_mul", _p(self.gu), _p(self.act), T, s.d_ff, clr, st)
             self._cleared("gu", clr)
-            self.gemm(self.act[:T], w[f"l{i}.w_down"], "proj", st)
+            self.gemm(self.act[:T], w[f"l{i}.w_down"], "proj", st, "w_down")
             if i + 1 < s.layers:
                 call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i + 1}.attn_norm"]), _p(h), T, d,
                      s.rms_eps, clr, st)
@@ -325,7 +329,7 @@ class Decoder:
             self._cleared("proj", clr)
         rows = self.rows[:R]
         call("stb_gather_rmsnorm", _p(x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows), R, d, s.rms_eps, st)
-        self.gemm(rows, w["lm_head"], "logits", st)
+        self.gemm(rows, w["lm_head"], "logits", st, "lm_head")
         call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
              _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), 0 if self.keep_logits else 1, st)
         if not self.keep_logits:
@@ -369,7 +373,7 @@ class Decoder:
     def collect(self) -> None:
         self.fold(self.take_pending())
 
-    def gemm(self, a: torch.Tensor, wt: torch.Tensor, out_name: str, st: C.c_void_p) -> None:
+    def gemm(self, a: torch.Tensor, wt: torch.Tensor, out_name: str, st: C.c_void_p, tag: str = "") -> None:
         M, K = a.shape
         N = wt.shape[0]
         out = getattr(self, out_name)[:M]
@@ -378,6 +382,8 @@ class Decoder:
         if stream is None:
             stream = self._stream_cache[key] = bool(lib.load().stb_gemm_is_stream(M, N, K))
         flags = GEMM_C_ZEROED if (stream and self._dirty[out_name] == 0) else 0
+        if "stb_gemm_bf16" in _SKIP or f"gemm:{tag}" in _SKIP:
+            return
         ev = self._tick()
         lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0,
                  flags, st)

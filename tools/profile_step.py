@@ -44,6 +44,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--timers", action="store_true", help="per-kernel CUDA-event times inside the step")
     ap.add_argument("--mix", default="", help="NxL: N new L-token prefills packed into every step")
+    ap.add_argument("--gemm-trace", action="store_true",
+                    help="per-CTA %%globaltimer timeline of every GEMM launch in the last step")
     args = ap.parse_args()
     shape = SHAPES[args.shape]
     if args.layers:
@@ -85,12 +87,52 @@ def main():
         if args.profile and last and i == args.steps - 1:
             torch.cuda.profiler.stop()
     rt.drain()
+    if args.gemm_trace:
+        gemm_trace(rt)
     if args.timers:
         for name, (t, work, n) in rt.dec.timers.items():
             print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e9:8.1f} GB/s algorithmic")
     ms = sorted(times[len(times) // 3:])
     print(f"{shape.name} B={args.batch} ctx~{args.ctx} mix={args.mix or '-'}: median step {ms[len(ms) // 2] * 1e3:.3f} ms "
           f"({args.batch / ms[len(ms) // 2]:.0f} tok/s)")
+
+
+def gemm_trace(rt):
+    """One more decode step with GEMM tracing on: per launch, the CTA-median entry,
+    dependency-wait, first-stage and last-MMA times and the last CTA exit (us, from
+    the first GEMM entry), plus the idle gap since the previous GEMM's last exit."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2512_15834_b200.runtime import lib
+
+    cap = 1 << 16
+    buf = torch.zeros(cap * 8, dtype=torch.int64, device="cuda")
+    fn = lib.load().stb_debug_gemm_trace
+    fn.argtypes, fn.restype = [C.c_void_p, C.c_int], C.c_int
+    torch.cuda.synchronize()
+    fn(C.c_void_p(buf.data_ptr()), cap)
+    rt.step()
+    rt.drain()
+    torch.cuda.synchronize()
+    n = fn(None, 0)
+    rec = buf[:n * 8].view(n, 8).cpu().numpy().astype(np.int64)
+    t_base = rec[:, 3].min()
+    prev_end = None
+    print(f"  GEMM trace: {n} CTA records")
+    print("   (us from entry of the launch; p50/max over CTAs)")
+    print("   tag  gap  | wait p50 | first p50 | mma-issued p50/max | epi-start p50/max | exit p50/max | dur")
+    for tag in np.unique(rec[:, 0]):
+        r = rec[rec[:, 0] == tag]
+        e0 = r[:, 3].min()
+        q = lambda col, f: (f(r[:, col]) - e0) / 1e3  # noqa: E731
+        end = r[:, 7].max()
+        gap = (e0 - prev_end) / 1e3 if prev_end is not None else 0.0
+        print(f"  {tag:4d} {gap:5.1f} | {q(4, np.median):6.1f} | {q(5, np.median):6.1f} | "
+              f"{q(6, np.median):6.1f} {q(6, np.max):6.1f} | {q(1, np.median):6.1f} {q(1, np.max):6.1f} | "
+              f"{q(7, np.median):6.1f} {q(7, np.max):6.1f} | {(end - e0) / 1e3:6.1f}")
+        prev_end = end
 
 
 if __name__ == "__main__":
