@@ -39,6 +39,7 @@
 // kernel's tail; activations are loaded only after the wait.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -76,6 +77,8 @@ struct Sched {
   unsigned* bar;     // stream-K grid barrier {count, generation}, self-resetting
   int c_zeroed;      // stream-K: the caller guarantees C == 0 (no in-kernel zeroing, no barrier)
   int tag;           // launch sequence number (debug trace only)
+  int load_debug;    // timing experiments (STB200_GEMM_LOAD_DEBUG): after the first ring fill
+                     // 1 = skip X loads, 2 = skip W loads, 3 = skip both (results are garbage)
 };
 
 // Debug timeline (stb_debug_gemm_trace): per CTA {tag, t_last_epilogue, sm, t_entry,
@@ -193,6 +196,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+          if (sched.load_debug && i >= STAGES) {
+            const bool lw = !(sched.load_debug & 2), lx = !(sched.load_debug & 1);
+            const uint32_t b = (lw ? CF::W_BYTES : 0) + (lx ? bn * BK * 2 : 0);
+            if (b) {
+              mbar_expect_tx(&full[s], b);
+              if (lw) tma_load_2d(sw, &tm_w, &full[s], k * BK, f0);
+              if (lx) tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
+            } else {
+              mbar_arrive(&full[s]);
+            }
+            continue;
+          }
           mbar_expect_tx(&full[s], CF::W_BYTES + bn * BK * 2);
           tma_load_2d(sw, &tm_w, &full[s], k * BK, f0);
           tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
@@ -201,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (elect_one()) {
       const uint32_t idesc = umma_idesc_bf16(BM, bn, false, false);
       SegIter it(sched);
       int tile, k0, k1, i = 0, j = 0;
@@ -283,23 +298,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int feat = slab + lane;
       const int t0 = (tile % sched.tiles_m) * bn;
       const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
+      // 32 tokens per TMEM load (one wait per 32), a 16-token load for the remainder; the
+      // warp-collective loads run on every lane, stores only for features < N; full
+      // in-range chunks store without per-token predicates
+      const int ntok = min(bn, M - t0);
+      const bool fok = feat < N;
+      float* crow = C + (int64_t)t0 * ldc + feat;
+      auto put = [&](int q, uint32_t v) {
+        float* dst = crow + (int64_t)q * ldc;
+        if (atomic) atomicAdd(dst, __uint_as_float(v));
+        else *dst = __uint_as_float(v);
+      };
+      int c = 0;
 #pragma unroll 1
-      for (int c = 0; c < bn / 16; ++c) {
-        uint32_t r[16];
-        tmem_ld16(base + c * 16, r);
+      for (; c + 32 <= bn; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(base + c, r);
         tmem_ld_wait();
-        if (feat < N) {
+        if (fok) {
+          if (c + 32 <= ntok) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int tok = t0 + c * 16 + q;
-            if (tok < M) {
-              float* dst = C + (int64_t)tok * ldc + feat;
-              if (atomic)
-                atomicAdd(dst, __uint_as_float(r[q]));
-              else
-                *dst = __uint_as_float(r[q]);
-            }
+            for (int q = 0; q < 32; ++q) put(c + q, r[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (c + q < ntok) put(c + q, r[q]);
           }
+        }
+      }
+      if (c < bn) {  // bn is a multiple of 16
+        uint32_t r[16];
+        tmem_ld16(base + c, r);
+        tmem_ld_wait();
+        if (fok) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c + q < ntok) put(c + q, r[q]);
         }
       }
       tc_fence_before();
@@ -472,6 +506,8 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   s.c_zeroed = (flags & STB_GEMM_C_ZEROED) ? 1 : 0;
   static int launch_seq = 0;
   s.tag = launch_seq++;
+  static const int load_debug = getenv("STB200_GEMM_LOAD_DEBUG") ? atoi(getenv("STB200_GEMM_LOAD_DEBUG")) : 0;
+  s.load_debug = load_debug;
   s.bar = grid_barrier();
   if (!s.bar) return fail(STB_ENOMEM, "gemm_bf16: barrier state");
   auto kern = gemm_bf16_persistent<BN>;
