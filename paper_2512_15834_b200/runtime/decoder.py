@@ -297,6 +297,8 @@ class Decoder:
         d = s.d_model
         x, h = self.x, self.h
         call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
+        for _ in range(2):  # empty pairs: the timers' own overhead, subtracted by the reader
+            self._tock("event_overhead", self._tick(), 0)
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
         clr = T if T <= CLEAR_MAX else 0
@@ -388,5 +390,7 @@ class Decoder:
         lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0,
                  flags, st)
         self._dirty[out_name] = max(self._dirty[out_name], M)
-        # K5 algorithmic bytes: weights + activations in + fp32 out (HBM-bound when M is small)
-        self._tock("gemm", ev, N * K * 2 + M * K * 2 + M * N * 4)
+        if M <= 128:  # decode-shaped: HBM-bound on the weights; work = algorithmic bytes
+            self._tock("gemm_decode", ev, N * K * 2 + M * K * 2 + M * N * 4)
+        else:  # prefill / ingest: tensor-bound; work = FLOPs
+            self._tock("gemm_prefill", ev, 2 * M * N * K)

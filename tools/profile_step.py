@@ -90,8 +90,15 @@ def main():
     if args.gemm_trace:
         gemm_trace(rt)
     if args.timers:
+        ov_t, _, ov_n = rt.dec.timers.pop("event_overhead", (0.0, 0, 0))
+        ov = ov_t / ov_n if ov_n else 0.0
+        print(f"  (event-pair overhead {ov * 1e3:.2f} us per launch subtracted)")
         for name, (t, work, n) in rt.dec.timers.items():
-            print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e9:8.1f} GB/s algorithmic")
+            t = max(t - n * ov, 1e-3 * t)
+            if name == "gemm_prefill":
+                print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e12:8.1f} TFLOP/s")
+            else:
+                print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e9:8.1f} GB/s algorithmic")
     ms = sorted(times[len(times) // 3:])
     print(f"{shape.name} B={args.batch} ctx~{args.ctx} mix={args.mix or '-'}: median step {ms[len(ms) // 2] * 1e3:.3f} ms "
           f"({args.batch / ms[len(ms) // 2]:.0f} tok/s)")
