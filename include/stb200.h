@@ -120,6 +120,11 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
  * unless flags has STB_GEMM_C_ZEROED (the caller guarantees C == 0, e.g.
  * because the consumer of the previous product cleared the rows it read). */
 #define STB_GEMM_C_ZEROED 1
+/* fused SiLU-gate epilogue (tile schedule only, else STB_EINVAL): W rows hold (gate,
+ * up) pairs interleaved (row 2i = gate_i, row 2i+1 = up_i); C is then bf16
+ * act[M][N/2] (row stride ldc elements) = silu(gate) * up, computed in fp32 exactly
+ * as stb_silu_mul does */
+#define STB_GEMM_SILU_MUL 2
 /* 1 if the automatic schedule runs this shape stream-K (C accumulated with reductions) */
 int stb_gemm_is_stream(int M, int N, int K);
 int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
@@ -132,7 +137,8 @@ int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, voi
  * are zeroed after reading (see stb_qkv_rope_commit) */
 int stb_add_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d, float eps, int clear_rows,
                     void* stream);
-/* y bf16 [n][f] = silu(gu[:, :f]) * gu[:, f:]  (gu fp32 [n][2f]); gu rows < clear_rows zeroed after reading */
+/* y bf16 [n][f] = silu(gate) * up with gu fp32 [n][2f] holding (gate_i, up_i) pairs
+ * interleaved (gu[t][2i], gu[t][2i+1]); gu rows < clear_rows zeroed after reading */
 int stb_silu_mul(float* gu, void* y, int n, int f, int clear_rows, void* stream);
 /* rows[i] = x[idx[i]] as bf16 after rmsnorm: final norm fused with row gather */
 int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,

@@ -281,7 +281,6 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
     float* __restrict__ o_part, float* __restrict__ lse_part, int* __restrict__ tickets) {
-  pdl_wait();
   constexpr int PAGE = 16 * D * 2;
   constexpr int NP = kChunkPages;
   constexpr int STAGE = NP * 2 * PAGE;  // K and V of NP pages
@@ -358,33 +357,53 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
       pid[p] = page < npages ? __ldg(r.row + page) : -1;
     }
   };
-  auto issue = [&](const Cur& r, int i) {  // lane 0
+  auto issue = [&](const Cur& r, int i, const int* ids) {  // lane 0
     const uint32_t sb = wbase + (i % STAGES) * STAGE;
     uint32_t bytes = 0;
 #pragma unroll
-    for (int p = 0; p < NP; ++p) bytes += pid[p] >= 0 ? 2 * PAGE : 0;
+    for (int p = 0; p < NP; ++p) bytes += ids[p] >= 0 ? 2 * PAGE : 0;
     uint64_t* bar = full + (i % STAGES);
     mbar_expect_tx(bar, bytes);
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      if (pid[p] >= 0) {
-        const int64_t off = (((int64_t)pid[p] * n_kv + r.kh) * 16) * D;
+      if (ids[p] >= 0) {
+        const int64_t off = (((int64_t)ids[p] * n_kv + r.kh) * 16) * D;
         bulk_load(sb + p * 2 * PAGE, kpages + off, PAGE, bar);
         bulk_load(sb + p * 2 * PAGE + PAGE, vpages + off, PAGE, bar);
       }
     }
   };
+  // Prologue before the dependency wait: every page except the one K1 writes in this
+  // layer (the last page of each pair, inside the pair's last chunk) was final before
+  // the preceding kernel started, so those copies overlap its tail; chunks holding a
+  // pair's last page are issued after griddepcontrol.wait.
   Cur ld = locate(u0);
+  Cur dcur[STAGES - 1];
+  int dpid[STAGES - 1][NP];
+  int deferred = 0;
   if (lane == 0) {
     fetch(ld);
 #pragma unroll
     for (int s2 = 0; s2 < STAGES - 1; ++s2) {
       if (s2 < n) {
-        issue(ld, s2);
+        if (ld.c == ld.chunks - 1) {
+          deferred |= 1 << s2;
+          dcur[s2] = ld;
+#pragma unroll
+          for (int p = 0; p < NP; ++p) dpid[s2][p] = pid[p];
+        } else {
+          issue(ld, s2, pid);
+        }
         advance(ld);
         fetch(ld);
       }
     }
+  }
+  pdl_wait();  // q and this layer's newest K/V rows come from the preceding kernel
+  if (lane == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < STAGES - 1; ++s2)
+      if (deferred & (1 << s2)) issue(dcur[s2], s2, dpid[s2]);
   }
   Cur cu = locate(u0);
   uint32_t qf[D / 16][4];
@@ -409,7 +428,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     __syncwarp();  // every lane's ldmatrix reads of the slot refilled below are done
     if (lane == 0 && i + STAGES - 1 < n) {
       fence_proxy_async_smem();
-      issue(ld, i + STAGES - 1);
+      issue(ld, i + STAGES - 1, pid);
       advance(ld);
       fetch(ld);
     }

@@ -9,8 +9,9 @@
 // share every K/V tile, and both query tiles share it too. Warp roles (320 thr):
 //   warp 8     TMA producer: Q tiles A and B once (4-D map over [T][n_kv][G][D]),
 //              then per KV tile of 128 keys the 8 K and 8 V pages through the
-//              block table (2-D maps over the page pool, 16 x 64 boxes, 128B
-//              swizzle) into a 2-stage ring
+//              block table (2-D maps over the page pool, 16 x 64 boxes; pages are
+//              stored pre-swizzled, so the boxes land in the 128B-swizzle layout
+//              with no tensor-map swizzle) into a 2-stage ring
 //   warp 9     MMA issuer (one thread), ping-pong over the two tiles:
 //              S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
 //              S = Q K^T into TMEM (M=128, N=128 keys, K=D); O += P V with P read
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) {
     // ---------------- TMA producer
     const int32_t* row = table + (int64_t)slots[s] * max_bps;
-    if (lane == 0) {
+    if (elect_one()) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 9) {
     // ---------------- MMA issuer (ping-pong)
-    if (lane == 0) {
+    if (elect_one()) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(ROWS, KT, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(ROWS, D, false, true);
       const int ntile_q = has_b ? 2 : 1;

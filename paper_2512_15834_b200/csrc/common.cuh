@@ -98,6 +98,9 @@ __device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// silu(g) * u in fp32 — shared by stb_silu_mul and the fused GEMM epilogue (bit-identical)
+__device__ __forceinline__ float silu_gate(float g, float u) { return g / (1.f + __expf(-g)) * u; }
+
 // one lane of the (converged) warp; nvcc knows the predicate selects a single thread, so
 // tcgen05 operands go straight to uniform registers instead of a per-lane waterfall loop
 __device__ __forceinline__ bool elect_one() {

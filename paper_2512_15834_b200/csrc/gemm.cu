@@ -76,6 +76,7 @@ struct Sched {
   int64_t units;     // tiles * kb
   unsigned* bar;     // stream-K grid barrier {count, generation}, self-resetting
   int c_zeroed;      // stream-K: the caller guarantees C == 0 (no in-kernel zeroing, no barrier)
+  int silu;          // tile schedule: fused SiLU-gate epilogue, C is bf16 act[M][N/2]
   int tag;           // launch sequence number (debug trace only)
   int load_debug;    // timing experiments (STB200_GEMM_LOAD_DEBUG): after the first ring fill
                      // 1 = skip X loads, 2 = skip W loads, 3 = skip both (results are garbage)
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       // weights first: the ring's first slots fill before the dependency wait
       SegIter pre(sched);
       int tile, k0, k1, i = 0;
@@ -309,6 +310,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (atomic) atomicAdd(dst, __uint_as_float(v));
         else *dst = __uint_as_float(v);
       };
+      if (sched.silu) {
+        // (gate, up) of output feature feat/2 sit in lanes (2i, 2i+1): one xor-shuffle
+        // per token pair; the even lane emits the first half of each chunk, the odd lane
+        // the second half
+        __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)t0 * ldc + (feat >> 1);
+        const bool odd = lane & 1;
+        auto emit = [&](int tok, float g, float u) {
+          if (fok && tok < ntok) act[(int64_t)tok * ldc] = __float2bfloat16_rn(silu_gate(g, u));
+        };
+        int c = 0;
+#pragma unroll 1
+        for (; c + 32 <= bn; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(base + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float mine = __uint_as_float(odd ? r[16 + q] : r[q]);
+            const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? r[q] : r[16 + q]), 1);
+            if (odd) emit(c + 16 + q, other, mine);
+            else emit(c + q, mine, other);
+          }
+        }
+        if (c < bn) {
+          uint32_t r[16];
+          tmem_ld16(base + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float mine = __uint_as_float(odd ? r[8 + q] : r[q]);
+            const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? r[q] : r[8 + q]), 1);
+            if (odd) emit(c + 8 + q, other, mine);
+            else emit(c + q, mine, other);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        ++j;
+        continue;
+      }
       int c = 0;
 #pragma unroll 1
       for (; c + 32 <= bn; c += 32) {
@@ -504,6 +546,9 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   if (mode >= 2 && mode < grid) grid = mode;
   if (s.stream && s.units < grid) grid = (int)s.units;
   s.c_zeroed = (flags & STB_GEMM_C_ZEROED) ? 1 : 0;
+  s.silu = (flags & STB_GEMM_SILU_MUL) ? 1 : 0;
+  if (s.silu && (s.stream || N % 2))
+    return fail(STB_EINVAL, "gemm_bf16: the SiLU-gate epilogue needs the tile schedule and even N");
   static int launch_seq = 0;
   s.tag = launch_seq++;
   static const int load_debug = getenv("STB200_GEMM_LOAD_DEBUG") ? atoi(getenv("STB200_GEMM_LOAD_DEBUG")) : 0;

@@ -111,6 +111,8 @@ int launch_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d,
   return STB_OK;
 }
 
+// (gate, up) pairs are interleaved in gu (the gate-up weight rows are interleaved at load,
+// so the fused GEMM epilogue finds each pair in adjacent TMEM lanes)
 __global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restrict__ y, int n, int f, int clear_rows) {
   pdl_wait();
   pdl_launch();
@@ -118,15 +120,15 @@ __global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restric
   int64_t total = (int64_t)n * f;
   if (i >= total) return;
   int64_t t = i / f, c = i % f;
-  float* row = gu + t * 2 * f;
-  float4 g = *reinterpret_cast<const float4*>(row + c);
-  float4 u = *reinterpret_cast<const float4*>(row + f + c);
+  float* p = gu + t * 2 * f + 2 * c;
+  float4 a = *reinterpret_cast<const float4*>(p);      // g0 u0 g1 u1
+  float4 b = *reinterpret_cast<const float4*>(p + 4);  // g2 u2 g3 u3
   if (t < clear_rows) {
-    *reinterpret_cast<float4*>(row + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(row + f + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  auto silu = [](float a) { return a / (1.f + __expf(-a)); };
-  uint2 o = make_uint2(pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y), pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w));
+  uint2 o = make_uint2(pack_bf16(silu_gate(a.x, a.y), silu_gate(a.z, a.w)),
+                       pack_bf16(silu_gate(b.x, b.y), silu_gate(b.z, b.w)));
   *reinterpret_cast<uint2*>(y + i) = o;
 }
 

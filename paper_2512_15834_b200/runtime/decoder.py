@@ -37,7 +37,18 @@ FORCE_BIAS = 1.0e4  # >> any logit spread of the random-init models (|logit| < 1
 # timing experiments only: comma-separated C-ABI entry points the step does not launch
 # (outputs are garbage; tools/profile_step.py uses it to attribute in-step time under PDL)
 _SKIP = frozenset(k for k in os.environ.get("STB200_SKIP_KERNELS", "").split(",") if k)
-GEMM_C_ZEROED = 1   # include/stb200.h STB_GEMM_C_ZEROED
+GEMM_C_ZEROED = 1
+GEMM_SILU_MUL = 2   # include/stb200.h STB_GEMM_SILU_MUL
+
+
+def interleave_gate_up(w: torch.Tensor, d_ff: int) -> None:
+    """In place: rows [gate_0..gate_F-1, up_0..up_F-1] -> [gate_0, up_0, gate_1, up_1, ...]
+    (stb_silu_mul / STB_GEMM_SILU_MUL layout). Idempotent per tensor object (marked, not
+    keyed by address: the caching allocator reuses addresses of freed weights)."""
+    if getattr(w, "_stb_gate_up_interleaved", False):
+        return
+    w.copy_(w.view(2, d_ff, -1).transpose(0, 1).reshape(2 * d_ff, -1))
+    w._stb_gate_up_interleaved = True   # include/stb200.h STB_GEMM_C_ZEROED
 CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
 
 
@@ -136,6 +147,8 @@ class Decoder:
                  use_graphs: bool = True):
         self.shape = shape
         self.w = weights
+        for i in range(shape.layers):  # (gate, up) pairs in adjacent rows: fused SiLU epilogue
+            interleave_gate_up(weights[f"l{i}.w_gate_up"], shape.d_ff)
         self.pool = pool
         self.device = device
         self.scale = 1.0 / math.sqrt(shape.d_head)
@@ -319,9 +332,9 @@ class Decoder:
             self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
             self._cleared("proj", clr)
-            self.gemm(h[:T], w[f"l{i}.w_gate_up"], "gu", st, "w_gate_up")
-            call("stb_silu_mul", _p(self.gu), _p(self.act), T, s.d_ff, clr, st)
-            self._cleared("gu", clr)
+            if not self.gemm(h[:T], w[f"l{i}.w_gate_up"], "gu", st, "w_gate_up", fuse_silu=True):
+                call("stb_silu_mul", _p(self.gu), _p(self.act), T, s.d_ff, clr, st)
+                self._cleared("gu", clr)
             self.gemm(self.act[:T], w[f"l{i}.w_down"], "proj", st, "w_down")
             if i + 1 < s.layers:
                 call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i + 1}.attn_norm"]), _p(h), T, d,
@@ -375,22 +388,30 @@ class Decoder:
     def collect(self) -> None:
         self.fold(self.take_pending())
 
-    def gemm(self, a: torch.Tensor, wt: torch.Tensor, out_name: str, st: C.c_void_p, tag: str = "") -> None:
+    def gemm(self, a: torch.Tensor, wt: torch.Tensor, out_name: str, st: C.c_void_p, tag: str = "",
+             fuse_silu: bool = False) -> bool:
+        """Launch K5; returns True when the SiLU-gate epilogue was fused (output in self.act)."""
         M, K = a.shape
         N = wt.shape[0]
-        out = getattr(self, out_name)[:M]
         key = (M, N, K)
         stream = self._stream_cache.get(key)
         if stream is None:
             stream = self._stream_cache[key] = bool(lib.load().stb_gemm_is_stream(M, N, K))
-        flags = GEMM_C_ZEROED if (stream and self._dirty[out_name] == 0) else 0
+        fused = fuse_silu and not stream  # whole tiles: the epilogue sees finished sums
+        if fused:
+            out, flags = self.act[:M], GEMM_SILU_MUL
+        else:
+            out = getattr(self, out_name)[:M]
+            flags = GEMM_C_ZEROED if (stream and self._dirty[out_name] == 0) else 0
         if "stb_gemm_bf16" in _SKIP or f"gemm:{tag}" in _SKIP:
-            return
+            return fused
         ev = self._tick()
         lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0,
                  flags, st)
-        self._dirty[out_name] = max(self._dirty[out_name], M)
+        if not fused:
+            self._dirty[out_name] = max(self._dirty[out_name], M)
         if M <= 128:  # decode-shaped: HBM-bound on the weights; work = algorithmic bytes
             self._tock("gemm_decode", ev, N * K * 2 + M * K * 2 + M * N * 4)
         else:  # prefill / ingest: tensor-bound; work = FLOPs
             self._tock("gemm_prefill", ev, 2 * M * N * K)
+        return fused

@@ -63,6 +63,27 @@ def test_gemm_c_zeroed(lib, M, N, K):
     assert lib.load().stb_gemm_is_stream(32, 6144, 4096) in (0, 1)
 
 
+@pytest.mark.parametrize("M,F,K", [(300, 1024, 512), (608, 2048, 1024), (2080, 512, 256), (200, 14336, 4096)])
+def test_gemm_silu_fused(lib, M, F, K):
+    """STB_GEMM_SILU_MUL: tile-schedule epilogue emits bf16 silu(gate)*up from interleaved
+    (gate, up) weight rows — bit-identical to the fp32 GEMM followed by stb_silu_mul."""
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (0.05 * torch.randn(2 * F, K, device="cuda")).to(torch.bfloat16)
+    act = torch.full((M, F), float("nan"), device="cuda").to(torch.bfloat16)
+    lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(act), F, M, 2 * F, K, 1, 2, stream())
+    c = torch.zeros(M, 2 * F, device="cuda")
+    lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(c), 2 * F, M, 2 * F, K, 1, 0, stream())
+    ref = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    lib.call("stb_silu_mul", P(c), P(ref), M, F, 0, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(act, ref)
+    full = a.float() @ w.float().T
+    assert rel(act, torch.nn.functional.silu(full[:, 0::2]) * full[:, 1::2]) < 1e-2
+    if lib.load().stb_gemm_is_stream(32, 2 * F, K):  # fused epilogue refuses the stream-K schedule
+        with pytest.raises(Exception):
+            lib.call("stb_gemm_bf16", P(a), K, P(w), K, P(act), F, 32, 2 * F, K, 0, 2, stream())
+
+
 def test_gemm_explicit_split(lib):
     M, N, K = 32, 512, 4096
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
@@ -274,11 +295,12 @@ def test_small_ops(lib):
     gu = torch.randn(n, 2 * f, device="cuda")
     a = torch.empty(n, f, dtype=torch.bfloat16, device="cuda")
     gu0 = gu.clone()
+    gate, up = gu0[:, 0::2], gu0[:, 1::2]  # (gate_i, up_i) interleaved
     lib.call("stb_silu_mul", P(gu), P(a), n, f, 0, stream())
-    assert rel(a, torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]) < 5e-3
+    assert rel(a, torch.nn.functional.silu(gate) * up) < 5e-3
     lib.call("stb_silu_mul", P(gu), P(a), n, f, 5, stream())
     assert not gu[:5].any() and torch.equal(gu[5:], gu0[5:])
-    assert rel(a, torch.nn.functional.silu(gu0[:, :f]) * gu0[:, f:]) < 5e-3
+    assert rel(a, torch.nn.functional.silu(gate) * up) < 5e-3
     idx = torch.tensor([3, 0, 12], dtype=torch.int32, device="cuda")
     rows = torch.empty(3, d, dtype=torch.bfloat16, device="cuda")
     lib.call("stb_gather_rmsnorm", P(x), P(idx), P(w), P(rows), 3, d, 1e-5, stream())

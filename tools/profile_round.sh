@@ -1,14 +1,21 @@
 #!/bin/bash
-# One GPU call's worth of evidence for profiles/: launch list of steady-state decode
-# steps, full ncu captures of the hot kernels, and a kernel microbenchmark table.
+# One GPU call's worth of evidence for profiles/: launch lists of steady-state decode and
+# mixed (prefill + decode) steps at the bench's context, full ncu captures of the hot
+# kernels, and a kernel microbenchmark table. Usage: bash tools/profile_round.sh [outdir]
 set -x
 OUT=${1:-gpurun_out}
+CTX=${CTX:-2048}
 mkdir -p $OUT
 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file $OUT/launches_decode.csv python tools/profile_step.py --profile --steps 8 --profile-steps 2 --ctx 4096 > /dev/null 2>&1
+  --log-file $OUT/launches_decode.csv python tools/profile_step.py --profile --steps 8 --profile-steps 2 --ctx $CTX > /dev/null 2>&1
 python tools/launch_table.py $OUT/launches_decode.csv 2 > $OUT/launches_decode.txt
+timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $OUT/launches_mixed.csv python tools/profile_step.py --profile --steps 8 --profile-steps 2 --ctx $CTX --mix 1x576 > /dev/null 2>&1
+python tools/launch_table.py $OUT/launches_mixed.csv 2 > $OUT/launches_mixed.txt
 timeout 400 ncu --profile-from-start off --set full --clock-control none --import-source on \
-  -k regex:"attn_decode|gemm_bf16" -c 6 -o $OUT/full_decode python tools/profile_step.py --profile --steps 6 --profile-steps 1 --ctx 4096 > /dev/null 2>&1
+  -k regex:"attn_decode|gemm_bf16" -c 6 -o $OUT/full_decode python tools/profile_step.py --profile --steps 6 --profile-steps 1 --ctx $CTX > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm -c 1 -s 2 \
+  -o $OUT/full_gemm_prefill python tools/gemm_once.py --M 608 --N 28672 --K 4096 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:attn_prefill_tc -c 2 \
   -o $OUT/full_prefill python tools/bench_kernels.py --what prefill > /dev/null 2>&1
 timeout 300 python tools/bench_kernels.py > $OUT/kernels.txt 2>&1
