@@ -194,16 +194,29 @@ __global__ void sample_forced_kernel(float* __restrict__ logits, int64_t ld, con
   int bi = 0x7fffffff, bbi = 0x7fffffff;
   const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0);
   if (vec) {
-    for (int c = lo + threadIdx.x * 4; c < hi; c += blockDim.x * 4) {
-      float4 v4 = *reinterpret_cast<const float4*>(row + c);
-      if (clear) *reinterpret_cast<float4*>(row + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+    // 4 float4 loads in flight per thread before any compare
+    constexpr int U = 4;
+    const int step = blockDim.x * 4;
+    for (int c0 = lo + threadIdx.x * 4; c0 < hi; c0 += U * step) {
+      float4 v4[U];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int idx = c + q;
-        if (idx < hi) {
-          arg_merge(best, bi, vv[q], idx);
-          arg_merge(bbest, bbi, idx == tgt ? vv[q] + bias : vv[q], idx);
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * step;
+        v4[u] = c < hi ? __ldcs(reinterpret_cast<const float4*>(row + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * step;
+        if (c >= hi) break;
+        if (clear) *reinterpret_cast<float4*>(row + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int idx = c + q;
+          if (idx < hi) {
+            arg_merge(best, bi, vv[q], idx);
+            arg_merge(bbest, bbi, idx == tgt ? vv[q] + bias : vv[q], idx);
+          }
         }
       }
     }

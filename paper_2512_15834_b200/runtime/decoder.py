@@ -254,9 +254,14 @@ class Decoder:
             max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
             self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
         else:
-            # decode graphs assume (and leave) every GEMM output zeroed
+            # decode graphs assume (and leave) zeroed every GEMM output they accumulate into
+            # (stream-K); a whole-tile LM head overwrites the logits, so those stay as they are
+            V, d = self.shape.vocab, self.shape.d_model
+            lm_stream = self._stream_cache.get((B, V, d))
+            if lm_stream is None:
+                lm_stream = self._stream_cache[(B, V, d)] = bool(lib.load().stb_gemm_is_stream(B, V, d))
             for name, rows in self._dirty.items():
-                if rows:
+                if rows and (name != "logits" or lm_stream):
                     getattr(self, name)[:rows].zero_()
                     self._dirty[name] = 0
             timed = self.timers is not None
@@ -345,9 +350,12 @@ class Decoder:
         rows = self.rows[:R]
         call("stb_gather_rmsnorm", _p(x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows), R, d, s.rms_eps, st)
         self.gemm(rows, w["lm_head"], "logits", st, "lm_head")
+        # the sampler re-zeroes the logits only when the LM head accumulated them (stream-K);
+        # whole-tile LM heads (any decode batch) overwrite them with plain stores
+        clear = 0 if self.keep_logits or not self._stream_cache[(R, s.vocab, d)] else 1
         call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
-             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), 0 if self.keep_logits else 1, st)
-        if not self.keep_logits:
+             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)
+        if clear:
             self._cleared("logits", R)
 
     def _cleared(self, name: str, rows: int) -> None:

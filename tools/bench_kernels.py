@@ -168,6 +168,31 @@ def bench_gemm_sweep(M=32, N=148 * 128):
         del ws
 
 
+def bench_small(shape):
+    """Row ops of a decode step at B=32: add+RMSNorm, SiLU-gate, forced sampler (HBM-bound)."""
+    B, d, f, V = 32, shape.d_model, shape.d_ff, shape.vocab
+    x = torch.randn(B, d, device="cuda")
+    delta = torch.randn(B, d, device="cuda")
+    nw = torch.ones(d, device="cuda", dtype=torch.bfloat16)
+    h = torch.empty(B, d, device="cuda", dtype=torch.bfloat16)
+    us = time_it(lambda i: lib.call("stb_add_rmsnorm", P(x), P(delta), P(nw), P(h), B, d, 1e-5, 0, st()))
+    print(f"  add_rmsnorm B={B} d={d}: {us:6.2f} us  {B * d * 14 / us / 1e3:6.0f} GB/s")
+    gu = torch.randn(B, 2 * f, device="cuda")
+    a = torch.empty(B, f, device="cuda", dtype=torch.bfloat16)
+    us = time_it(lambda i: lib.call("stb_silu_mul", P(gu), P(a), B, f, 0, st()))
+    print(f"  silu_mul B={B} f={f}: {us:6.2f} us  {B * f * 10 / us / 1e3:6.0f} GB/s")
+    logits = torch.randn(B, V, device="cuda")
+    tgt = torch.randint(0, V, (B,), device="cuda", dtype=torch.int32)
+    o = torch.empty(B, device="cuda", dtype=torch.int32)
+    ra = torch.empty(B, device="cuda", dtype=torch.int32)
+    rm = torch.empty(B, device="cuda")
+    for clear in (0, 1):
+        us = time_it(lambda i: lib.call("stb_sample_forced", P(logits), V, P(tgt), B, V, 1e4, P(o), P(ra), P(rm),
+                                        clear, st()))
+        print(f"  sample_forced R={B} V={V} clear={clear}: {us:6.2f} us  "
+              f"{B * V * 4 * (1 + clear) / us / 1e3:6.0f} GB/s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="llama3-8b")
@@ -187,6 +212,8 @@ def main():
     if "prefill" in args.what:
         for S, n, ctx in [(4, 2048, 2048), (1, 2048, 34816), (8, 512, 4096), (32, 33, 4096)]:
             bench_prefill(shape, S, n, ctx)
+    if "small" in args.what:
+        bench_small(shape)
     if "attn" in args.what:
         for B, ctx in [(32, 2048), (32, 4096), (16, 32768), (1, 4096), (64, 4096)]:
             bench_attn(shape, B, ctx)
