@@ -20,7 +20,12 @@
 //              pass over its S row (128 TMEM columns -> registers), exp2, row sum,
 //              P packed to bf16 and stored back over S; O (in TMEM) is rescaled
 //              only when a warp's running max moved. While one warpgroup does its
-//              softmax the tensor core runs the other tile's MMAs.
+//              softmax the tensor core runs the other tile's MMAs. The softmax is
+//              the pacing resource (16 MUFU ex2/clk/SM vs 1024 MMA clocks per tile):
+//              scale/subtract and the row sum are packed f32x2 (FFMA2/FADD2), ex2
+//              is the ftz SFU form, and 2 of every 8 column pairs are exponentiated
+//              on the FMA pipe (exp2_emu2) on unmasked tiles.
+// CTAs are issued longest-first (causal work grows with the query-tile index).
 // TMEM (512 columns): S/P_A | S/P_B | O_A | O_B.
 #include <cudaTypedefs.h>
 
@@ -60,21 +65,55 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// 2^x for x <= 0 on the FMA pipe (Cody-Waite split + cubic minimax on [0,1), max
-// relative error 2.6e-4 — below bf16 P's 3.9e-3): offloads a share of the softmax
-// exponentials from the MUFU unit, which otherwise paces the softmax.
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -127.f);
-  const float xi = floorf(x);
-  const float f = x - xi;
-  const float p = fmaf(fmaf(fmaf(0.0755871f, f, 0.22877206f), f, 0.69511613f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (static_cast<int>(xi) << 23));
+// 2^x for a pair of x in [-126, 8] on the FMA pipe (FA4-style offload from the MUFU unit,
+// which otherwise paces the softmax: 16 ex2/clk/SM against 8192 bf16 flop/clk/SM of MMA).
+// Round-to-nearest split x = k + f with the 1.5*2^23 shifter (f in [-0.5, 0.5]), a cubic
+// minimax for 2^f (max relative error 7.5e-5, far below the 3.9e-3 of the bf16 P it feeds),
+// and k added straight into the exponent field: the shifter's low mantissa bits hold k, so
+// bits(j) << 23 == k << 23 (mod 2^32).
+__device__ __forceinline__ float2 exp2_emu2(float2 x) {
+  const float2 shift = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 j = __fadd2_rn(x, shift);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(shift, make_float2(-j.x, -j.y)));
+  float2 p = __ffma2_rn(make_float2(0.0551716117f, 0.0551716117f), f, make_float2(0.24261117f, 0.24261117f));
+  p = __ffma2_rn(p, f, make_float2(0.693261001f, 0.693261001f));
+  p = __ffma2_rn(p, f, make_float2(0.999928071f, 0.999928071f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 
-#ifndef STB_EXP_FMA_EVERY
-#define STB_EXP_FMA_EVERY 0  // 0: all exponentials on MUFU (measured fastest: the softmax is latency-bound)
+#ifndef STB_EXP_EMU
+#define STB_EXP_EMU 2  // column pairs in every 8 exponentiated on the FMA pipe (unmasked tiles)
 #endif
 constexpr float kRescaleSlack = 8.f;  // lazy rescale: keep the stale max until the row max grows by > 2^8
+
+// One S row (KT fp32 scores in registers, already masked) -> bf16 P pairs + row sum.
+// Scale-and-subtract and the row sum run as packed f32x2 (FFMA2 / FADD2); exponentials
+// on MUFU (ex2.approx.ftz) except STB_EXP_EMU of every 8 pairs when EMU.
+template <bool EMU>
+__device__ __forceinline__ float exp_row(const uint32_t* v, uint32_t* pk, float qscale, float ref) {
+  const float2 sc = make_float2(qscale, qscale), nr = make_float2(-ref, -ref);
+  float2 acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < KT; c += 2) {
+    const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), sc, nr);
+    float2 e;
+    if (EMU && ((c / 2) % 8) < STB_EXP_EMU) {
+      e = exp2_emu2(x);
+    } else {
+      e.x = fast_exp2(x.x);
+      e.y = fast_exp2(x.y);
+    }
+    acc[(c / 2) % 4] = __fadd2_rn(acc[(c / 2) % 4], e);
+    pk[c / 2] = pack_bf16(e.x, e.y);
+  }
+  const float2 a = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+  return a.x + a.y;
+}
 
 template <int D, int G>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -98,12 +137,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.z, kh = blockIdx.y;
+  // longest-first order: the causal work of a CTA grows with its query-tile index, so the
+  // linear launch order walks query tiles from the last down (all heads and runs of one
+  // index before the next) and the short diagonal CTAs fill the tail of the last wave
+  const int nyz = gridDim.y * gridDim.z;
+  const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int bx = gridDim.x - 1 - lin / nyz;
+  const int kh = (lin % nyz) % gridDim.y, s = (lin % nyz) / gridDim.y;
   constexpr int QPT = ROWS / G;  // queries per tile
   pdl_wait();
   pdl_launch();
   const int t0 = q_start[s], n = q_start[s + 1] - t0;
-  const int qi0 = blockIdx.x * 2 * QPT;
+  const int qi0 = bx * 2 * QPT;
   if (qi0 >= n) return;
   const bool has_b = qi0 + QPT < n;
   const int ctx = ctx_lens[s];
@@ -238,7 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < KT; c += 32) tmem_ld32(tS(t) + lane_base + c, v + c);
         tmem_ld_wait();
         const int kbase = j * KT;
-        if (!(j < full_tiles && live)) {
+        const bool masked = !(j < full_tiles && live);
+        if (masked) {
 #pragma unroll
           for (int c = 0; c < KT; ++c)
             if (!live || kbase + c > qpos) v[c] = __float_as_uint(-INFINITY);
@@ -262,21 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = mn;
         }
         const float ref = m == -INFINITY ? 0.f : m;
-        float rs8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) rs8[q] = 0.f;
         uint32_t pk[KT / 2];
-#pragma unroll
-        for (int c = 0; c < KT; c += 2) {
-          const float x0 = fmaf(__uint_as_float(v[c]), qscale, -ref);
-          const float x1 = fmaf(__uint_as_float(v[c + 1]), qscale, -ref);
-          const bool fma_pipe = STB_EXP_FMA_EVERY > 0 && ((c / 2) % (STB_EXP_FMA_EVERY > 0 ? STB_EXP_FMA_EVERY : 1)) == STB_EXP_FMA_EVERY - 1;
-          const float e0 = fma_pipe ? exp2_fma(x0) : exp2f(x0);
-          const float e1 = fma_pipe ? exp2_fma(x1) : exp2f(x1);
-          rs8[(c / 2) % 8] += e0 + e1;
-          pk[c / 2] = pack_bf16(e0, e1);
-        }
-        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        const float rs = masked ? exp_row<false>(v, pk, qscale, ref) : exp_row<true>(v, pk, qscale, ref);
         l = l * alpha + rs;
         // P (bf16 pairs) over the S columns just read: the A operand of P V
 #pragma unroll

@@ -13,7 +13,8 @@ from pathlib import Path
 
 from ..errors import KernelError, KVCapacityError
 
-LIB_PATH = Path(__file__).resolve().parent.parent / "lib" / "libstb200.so"
+# STB200_LIB selects a tuning variant built by tools/build_variant.sh (same ABI)
+LIB_PATH = Path(os.environ.get("STB200_LIB") or Path(__file__).resolve().parent.parent / "lib" / "libstb200.so")
 
 P = C.c_void_p
 I32 = C.c_int
@@ -77,7 +78,7 @@ def load() -> C.CDLL:
 
         if not torch.cuda.is_available():
             raise KernelError("B200 runtime needs CUDA; no device visible (there is no CPU fallback)")
-        _lib = load_raw(os.environ.get("STB200_LIB", LIB_PATH))
+        _lib = load_raw(LIB_PATH)
     return _lib
 
 

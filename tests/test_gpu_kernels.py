@@ -223,13 +223,16 @@ def test_attn_decode(lib, shape, ctxs):
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
 @pytest.mark.parametrize("runs", [[(1, 1)], [(4, 10), (21, 33)], [(300, 300), (33, 1200), (7, 8)]])
-def test_attn_prefill(lib, shape, runs):
+@pytest.mark.parametrize("amp", [1.0, 40.0], ids=["unit", "spiky"])
+def test_attn_prefill(lib, shape, runs, amp):
+    # amp scales q: "spiky" scores span hundreds of log2 units, exercising the lazy
+    # rescale and the clamped FMA-pipe exponentials
     # runs: (n new queries, ctx incl. them)
     ctxs = [c for _, c in runs]
     pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(runs), bps=512)
     dense = _fill_pool(lib, pool, shape, ctxs, seed=7)
     T = sum(n for n, _ in runs)
-    q = torch.randn(T, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    q = (torch.randn(T, shape.n_q, shape.d_head, device="cuda") * amp).to(torch.bfloat16)
     out = torch.full_like(q, float("nan"))
     qs = [0]
     for n, _ in runs:

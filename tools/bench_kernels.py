@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--what", default="gemm,attn,prefill")
     ap.add_argument("--M", default="32,2080")
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--prefill-cases", default="4x2048x2048,1x2048x34816,8x512x4096,32x33x4096",
+                    help="SxNxCTX list for --what prefill")
     args = ap.parse_args()
     lib.load()
     shape = SHAPES[args.shape]
@@ -210,7 +212,8 @@ def main():
     if "pdl" in args.what:
         bench_pdl(shape)
     if "prefill" in args.what:
-        for S, n, ctx in [(4, 2048, 2048), (1, 2048, 34816), (8, 512, 4096), (32, 33, 4096)]:
+        for case in args.prefill_cases.split(","):
+            S, n, ctx = (int(x) for x in case.split("x"))
             bench_prefill(shape, S, n, ctx)
     if "small" in args.what:
         bench_small(shape)
