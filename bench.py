@@ -15,7 +15,9 @@ forward of the continuous-batching engine over every resident sequence
   roofline  live CUDA-event timing of the dominant kernel over the timed region
 
 N > 1 (torchrun): sessions are independent, so every rank is a replica with
-its own 32 agents (weak scaling); times are max over ranks, tokens summed.
+its own agents (C2/C5: a fixed count per GPU, weak scaling; C3: the config's
+64 agents split over the replicas, strong scaling); times are max over ranks,
+tokens summed. `--config c3|c5` selects the other single-node BASELINE configs.
 
 `--impl reference`: the reference path has no GPU code; its CPU
 restatement (oracle engine + fp32 decoder) is timed on the host cores on a
@@ -172,21 +174,50 @@ def run_reference(args, world, rank):
     from paper_2512_15834_b200.modelcfg import SHAPES
 
     shape = SHAPES[args.shape]
-    base = cpu_sample(shape, seconds_budget=max(8.0, min(60.0, 2.0 * (args.steps + args.warmup))), batch=args.agents)
+    base = cpu_sample(shape, seconds_budget=max(8.0, min(60.0, 2.0 * (args.steps + args.warmup))), batch=args.agents,
+                      ctx=args.trace.get("prompt_tokens", 2048))
     line = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / base["value"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args), "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# BASELINE.json configs this bench can run on one node (C1 is the CPU parity config, C4 needs
+# TP/EP — out of scope). agents: per GPU (weak scaling) or whole box (strong).
+CONFIGS = {
+    "c2": {"shape": "llama3-8b", "agents": 32, "per_gpu": True, "max_ctx": 16384, "trace": {},
+           "label": "C2 llama3-8b-shaped random-init bf16, 32 agents/GPU, tool-call trace (prompt 2048, reason "
+                    "64-512, call 32, output 64-1024, tool 10ms-2s log-uniform)"},
+    "c3": {"shape": "qwen3-32b", "agents": 64, "per_gpu": False, "max_ctx": 16384, "trace": {},
+           "label": "C3 qwen3-32b-shaped (qk-norm) random-init bf16, 64 agents sharded over the replicas, "
+                    "tool-call trace as C2"},
+    "c5": {"shape": "llama3-8b", "agents": 16, "per_gpu": True, "max_ctx": 49152,
+           "trace": {"prompt_tokens": 32768, "output": (2048, 2048)},
+           "label": "C5 KV-pressure: llama3-8b-shaped random-init bf16, 16 agents/GPU, 32k-token resident "
+                    "contexts, 2k-token tool outputs"},
+}
+
+
+def resolve(args, world: int) -> None:
+    """Fill shape / agents / trace from --config unless given explicitly."""
+    c = CONFIGS[args.config]
+    args.shape = args.shape or c["shape"]
+    if not args.agents:
+        args.agents = c["agents"] if c["per_gpu"] else max(1, c["agents"] // world)
+    args.scaling = "weak" if c["per_gpu"] else "strong"
+    args.trace = dict(c["trace"])
+    args.max_ctx = c["max_ctx"]
+
+
 def workload_config(args) -> dict:
-    return {"workload": f"C2 {args.shape}-shaped random-init bf16, {args.agents} agents/GPU, tool-call trace "
-                        f"(prompt 2048, reason 64-512, call 32, output 64-1024, tool 10ms-2s log-uniform)",
-            "agents_per_gpu": args.agents, "prompt_tokens": 2048, "draft_latency_s": 0.05, "accept_rate": 0.8,
+    c = CONFIGS[args.config]
+    prompt = args.trace.get("prompt_tokens", 2048)
+    return {"workload": c["label"], "config_id": args.config, "shape": args.shape,
+            "agents_per_gpu": args.agents, "prompt_tokens": prompt, "draft_latency_s": 0.05, "accept_rate": 0.8,
             "layers": args.layers, "parallelism": f"replicas x{args.gpus}",
-            "l2": "working set > L2 (16 GB weights + KV streamed every step)"}
+            "l2": "working set > L2 (weights + KV streamed every step)"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -208,13 +239,13 @@ def run_b200(args, world, rank, local):
     free, _ = torch.cuda.mem_get_info()
     block_bytes = 16 * shape.kv_bytes_per_token
     budget = free - shape.weight_bytes - 24 * (1 << 30)
-    num_blocks = int(max(2048, min(budget // block_bytes, args.agents * 2 * 16384 // 16)))
+    num_blocks = int(max(2048, min(budget // block_bytes, args.agents * 2 * args.max_ctx // 16)))
     rt = BatchRuntime(shape, init_device="cuda", num_blocks=num_blocks, max_slots=max(256, 4 * args.agents),
-                      max_ctx=16384, max_step_tokens=args.max_step_tokens)
+                      max_ctx=args.max_ctx, max_step_tokens=args.max_step_tokens)
     rt.precapture(args.agents)
     loop = RealtimeLoop()
     engine = B200Engine(loop, engine_config(args.agents), runtime=rt)
-    fleet = Fleet(engine, loop, TraceSpec(seed=args.seed), args.agents, agent_offset=rank * args.agents)
+    fleet = Fleet(engine, loop, TraceSpec(seed=args.seed, **args.trace), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
     state = {"i": 0, "timed": None}
@@ -296,12 +327,13 @@ def run_b200(args, world, rank, local):
         bound, ach, peak, unit = rate(k)
         others[k] = {"bound": bound, "achieved": round(ach, 1), "unit": unit, "frac": round(ach / peak, 4),
                      "share_of_device_time": round(t / dev_s * TIMER_STRIDE, 4), "launches": n}
-    cpu = cpu_sample(SHAPES[args.shape], seconds_budget=args.cpu_seconds, batch=args.agents) if not args.no_cpu else None
+    cpu = (cpu_sample(SHAPES[args.shape], seconds_budget=args.cpu_seconds, batch=args.agents,
+                      ctx=args.trace.get("prompt_tokens", 2048)) if not args.no_cpu else None)
     rs = sorted(resume)
     line = {
         "metric": METRIC, "value": round(tot_emit / dev_max, 2), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_max / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, scripted agent trace)", "config": workload_config(args),
         "e2e": {"value": round(tot_emit / wall_max, 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": int((rt.h2d_bytes - h2d0) / args.steps),
@@ -325,8 +357,10 @@ def main():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=40)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--agents", type=int, default=32)
-    ap.add_argument("--shape", default="llama3-8b")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="BASELINE config: c2 (default, the metric's config), c3, c5")
+    ap.add_argument("--agents", type=int, default=0, help="override the config's agent count (per GPU)")
+    ap.add_argument("--shape", default="", help="override the config's model shape")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--max-step-tokens", type=int, default=8192)
@@ -334,6 +368,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_setup()
+    resolve(args, world)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

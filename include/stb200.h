@@ -76,6 +76,13 @@ int stb_kv_copy_blocks(stb_kv_pool* pool, const int32_t* src, const int32_t* dst
  * stream-K GEMM into qkv can accumulate without a memset).               */
 int stb_qkv_rope_commit(stb_kv_pool* pool, int layer, float* qkv, void* q_out, const int32_t* slot_of,
                         const int32_t* pos_of, int n, int n_q, float rope_theta, int clear_rows, void* stream);
+/* Same, with Qwen3 qk-norm (config C3): each q and k head row is RMS-normalised over
+ * d_head and scaled by q_norm / k_norm (bf16 [d_head]) before RoPE. The reference
+ * has no decoder; this is part of the self-defined model of the
+ * charges at engine.py:251,270,296,358. NULL norms = stb_qkv_rope_commit.       */
+int stb_qkv_norm_rope_commit(stb_kv_pool* pool, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                             const int32_t* pos_of, int n, int n_q, float rope_theta, const void* q_norm,
+                             const void* k_norm, float eps, int clear_rows, void* stream);
 
 /* ---- K3: paged decode attention (one query per sequence) ----------------
  * Replaces the decode charges engine.py:270,276,302,317. q/out bf16

@@ -3,7 +3,8 @@ engine runs (the reference has none: its phases are virtual-time charges,
 engine.py:251,270,296,358). Same random-init weights (the product's bf16 draw,
 upcast to fp32), standard Llama math: RMSNorm, rotate-half RoPE (theta,
 fp32 inverse frequencies from a float64 pow, fp32 angle pos*inv_freq), GQA
-causal attention, SwiGLU MLP, untied LM head. Each sequence keeps a
+causal attention, SwiGLU MLP, untied LM head; Qwen3 qk-norm (per-head RMSNorm of q
+and k before RoPE) for qk_norm shapes. Each sequence keeps a
 contiguous fp32 K/V cache; `forward` appends rows at `start` and returns the
 logits of the requested rows.
 """
@@ -45,6 +46,9 @@ class CpuDecoder:
                 "gu": draw((2 * shape.d_ff, d), seed, f"l{i}.w_gate_up", False),
                 "dn": draw((d, shape.d_ff), seed, f"l{i}.w_down", False),
             })
+            if shape.qk_norm:  # Qwen3: per-head RMSNorm of q and k before RoPE
+                self.layers[-1]["qn"] = draw((shape.d_head,), seed, f"l{i}.q_norm", True)
+                self.layers[-1]["kn"] = draw((shape.d_head,), seed, f"l{i}.k_norm", True)
         self.fn = draw((d,), seed, "final_norm", True)
         self.head = draw((V, d), seed, "lm_head", False)
         half = shape.d_head // 2
@@ -54,6 +58,11 @@ class CpuDecoder:
 
     def _norm(self, x, w):
         return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps) * w
+
+    def _qk(self, w, q, k):
+        if "qn" in w:
+            q, k = self._norm(q, w["qn"]), self._norm(k, w["kn"])
+        return q, k
 
     def _rope(self, x, pos):
         # x [T, H, D]; pos [T]
@@ -84,6 +93,7 @@ class CpuDecoder:
             q = qkv[:, : H * D].view(T, H, D)
             k = qkv[:, H * D: (H + G) * D].view(T, G, D)
             v = qkv[:, (H + G) * D:].view(T, G, D)
+            q, k = self._qk(w, q, k)
             q, k = self._rope(q, pos), self._rope(k, pos)
             kc, vc = cache[i]
             kc = torch.cat([kc[:start], k])
@@ -120,8 +130,8 @@ def decode_batch(dec: CpuDecoder, caches: list, ids: list[int], positions: list[
     for i, w in enumerate(dec.layers):
         h = dec._norm(x, w["an"])
         qkv = h @ w["qkv"].T
-        q = dec._rope(qkv[:, : H * D].view(B, H, D), pos)
-        k = dec._rope(qkv[:, H * D: (H + G) * D].view(B, G, D), pos)
+        q, k = dec._qk(w, qkv[:, : H * D].view(B, H, D), qkv[:, H * D: (H + G) * D].view(B, G, D))
+        q, k = dec._rope(q, pos), dec._rope(k, pos)
         v = qkv[:, (H + G) * D:].view(B, G, D)
         outs = []
         for b in range(B):

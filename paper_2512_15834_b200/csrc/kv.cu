@@ -101,38 +101,64 @@ __global__ void kv_copy_blocks_kernel(__nv_bfloat16* __restrict__ pages, const i
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) d[i] = s[i];
 }
 
-// Fused QKV epilogue: rotate q and k (rotate-half RoPE), write q as bf16, commit k and v.
-// thread -> (token, head among n_q + 2*n_kv, group of 8 rotation pairs); every store is 16 bytes.
+// Fused QKV epilogue: (optional per-head RMSNorm of q and k — Qwen3 qk-norm), rotate q
+// and k (rotate-half RoPE), write q as bf16, commit k and v into the pool pages.
+// thread -> (token, head among n_q + 2*n_kv, group of 8 rotation pairs); every store is 16
+// bytes. The d_head/16 threads of one head row are adjacent lanes of one warp, so the
+// qk-norm row reduction is a few xor-shuffles (no early return before them).
 __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
                                        const int32_t* __restrict__ slot_of, const int32_t* __restrict__ pos_of, int n,
                                        int n_q, int n_kv, int d_head, const float* __restrict__ inv_freq,
                                        const int32_t* __restrict__ table, int max_bps,
                                        __nv_bfloat16* __restrict__ kpages, __nv_bfloat16* __restrict__ vpages,
-                                       int clear_rows) {
+                                       int clear_rows, const __nv_bfloat16* __restrict__ q_norm,
+                                       const __nv_bfloat16* __restrict__ k_norm, float eps) {
   pdl_wait();
   pdl_launch();
   const int half = d_head / 2;
   const int groups = half / 8;
   const int heads = n_q + 2 * n_kv;
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)n * heads * groups) return;
-  int g = gid % groups;
-  int h = (gid / groups) % heads;
-  int t = gid / ((int64_t)groups * heads);
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = gid < (int64_t)n * heads * groups;
+  const int g = gid % groups;
+  const int h = (gid / groups) % heads;
+  const int t = valid ? (int)(gid / ((int64_t)groups * heads)) : 0;
+  float x1[8], x2[8];
   float* row = qkv + ((int64_t)t * heads + h) * d_head;
-  float4 a0 = *reinterpret_cast<const float4*>(row + g * 8);
-  float4 a1 = *reinterpret_cast<const float4*>(row + g * 8 + 4);
-  float4 b0 = *reinterpret_cast<const float4*>(row + half + g * 8);
-  float4 b1 = *reinterpret_cast<const float4*>(row + half + g * 8 + 4);
-  if (t < clear_rows) {  // leave the GEMM accumulator zeroed for the next stream-K product
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(row + g * 8) = z;
-    *reinterpret_cast<float4*>(row + g * 8 + 4) = z;
-    *reinterpret_cast<float4*>(row + half + g * 8) = z;
-    *reinterpret_cast<float4*>(row + half + g * 8 + 4) = z;
+  if (valid) {
+    const float4 a0 = *reinterpret_cast<const float4*>(row + g * 8);
+    const float4 a1 = *reinterpret_cast<const float4*>(row + g * 8 + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(row + half + g * 8);
+    const float4 b1 = *reinterpret_cast<const float4*>(row + half + g * 8 + 4);
+    x1[0] = a0.x, x1[1] = a0.y, x1[2] = a0.z, x1[3] = a0.w, x1[4] = a1.x, x1[5] = a1.y, x1[6] = a1.z, x1[7] = a1.w;
+    x2[0] = b0.x, x2[1] = b0.y, x2[2] = b0.z, x2[3] = b0.w, x2[4] = b1.x, x2[5] = b1.y, x2[6] = b1.z, x2[7] = b1.w;
+    if (t < clear_rows) {  // leave the GEMM accumulator zeroed for the next stream-K product
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(row + g * 8) = z;
+      *reinterpret_cast<float4*>(row + g * 8 + 4) = z;
+      *reinterpret_cast<float4*>(row + half + g * 8) = z;
+      *reinterpret_cast<float4*>(row + half + g * 8 + 4) = z;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x1[j] = x2[j] = 0.f;
   }
-  float x1[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-  float x2[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  if (q_norm != nullptr) {  // uniform over the launch: every lane takes the shuffles
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss = fmaf(x1[j], x1[j], fmaf(x2[j], x2[j], ss));
+    for (int o = 1; o < groups; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (h < n_q + n_kv) {
+      const float r = rsqrtf(ss / (float)d_head + eps);
+      const __nv_bfloat16* w = h < n_q ? q_norm : k_norm;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x1[j] = x1[j] * r * __bfloat162float(w[g * 8 + j]);
+        x2[j] = x2[j] * r * __bfloat162float(w[half + g * 8 + j]);
+      }
+    }
+  }
+  if (!valid) return;
   float y1[8], y2[8];
   int pos = pos_of[t];
   if (h < n_q + n_kv) {
@@ -363,8 +389,10 @@ int stb_kv_copy_blocks(stb_kv_pool* p, const int32_t* src, const int32_t* dst, i
   return STB_OK;
 }
 
-int stb_qkv_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
-                        const int32_t* pos_of, int n, int n_q, float rope_theta, int clear_rows, void* stream) {
+int stb_qkv_norm_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                             const int32_t* pos_of, int n, int n_q, float rope_theta, const void* q_norm,
+                             const void* k_norm, float eps, int clear_rows, void* stream) {
+  if ((q_norm == nullptr) != (k_norm == nullptr)) return fail(STB_EINVAL, "qkv_rope_commit: q_norm and k_norm go together");
   if (!p || layer < 0 || layer >= p->layers) return fail(STB_EINVAL, "qkv_rope_commit: bad layer");
   if (n <= 0) return STB_OK;
   // inverse frequencies are a pure function of (theta, d_head): cache one device table per pair
@@ -391,9 +419,16 @@ int stb_qkv_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, cons
   int threads = 256;
   launch_k(qkv_rope_commit_kernel, dim3((unsigned)((total + threads - 1) / threads)), dim3(threads), 0, (cudaStream_t)stream, 
       qkv, (__nv_bfloat16*)q_out, slot_of, pos_of, n, n_q, p->n_kv, p->d_head, inv, p->dev_table, p->max_bps,
-      (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, clear_rows);
+      (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, clear_rows, (const __nv_bfloat16*)q_norm,
+      (const __nv_bfloat16*)k_norm, eps);
   STB_CHECK_LAUNCH("qkv_rope_commit");
   return STB_OK;
+}
+
+int stb_qkv_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                        const int32_t* pos_of, int n, int n_q, float rope_theta, int clear_rows, void* stream) {
+  return stb_qkv_norm_rope_commit(p, layer, qkv, q_out, slot_of, pos_of, n, n_q, rope_theta, nullptr, nullptr, 0.f,
+                                  clear_rows, stream);
 }
 
 }  // extern "C"

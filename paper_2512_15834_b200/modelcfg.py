@@ -24,6 +24,7 @@ class ModelShape:
     vocab: int
     rope_theta: float = 10000.0
     rms_eps: float = 1e-5
+    qk_norm: bool = False  # Qwen3: per-head RMSNorm of q and k (weights [d_head]) before RoPE
 
     @property
     def q_dim(self) -> int:
@@ -42,11 +43,12 @@ class ModelShape:
     def weight_bytes(self) -> int:
         d = self.d_model
         per_layer = d * (self.q_dim + 2 * self.kv_dim) + self.q_dim * d + 3 * d * self.d_ff + 2 * d
+        per_layer += 2 * self.d_head if self.qk_norm else 0
         return 2 * (self.layers * per_layer + 2 * self.vocab * d + d)
 
     def with_layers(self, layers: int) -> "ModelShape":
         return ModelShape(f"{self.name}[L={layers}]", layers, self.d_model, self.n_q, self.n_kv,
-                          self.d_head, self.d_ff, self.vocab, self.rope_theta, self.rms_eps)
+                          self.d_head, self.d_ff, self.vocab, self.rope_theta, self.rms_eps, self.qk_norm)
 
 
 # C1: the reference CPU run's "tiny random-init decoder (2 layers, d=256)"
@@ -54,8 +56,12 @@ TINY = ModelShape("tiny-c1", layers=2, d_model=256, n_q=4, n_kv=2, d_head=64, d_
 # C2: Llama-3-8B shape
 LLAMA3_8B = ModelShape("llama3-8b", layers=32, d_model=4096, n_q=32, n_kv=8, d_head=128,
                        d_ff=14336, vocab=128256, rope_theta=500000.0)
-# C3: Qwen3-32B shape (qk-norm not modelled yet)
+# C3: Qwen3-32B shape, qk-norm included
 QWEN3_32B = ModelShape("qwen3-32b", layers=64, d_model=5120, n_q=64, n_kv=8, d_head=128,
-                       d_ff=25600, vocab=151936, rope_theta=1000000.0, rms_eps=1e-6)
+                       d_ff=25600, vocab=151936, rope_theta=1000000.0, rms_eps=1e-6, qk_norm=True)
+# C3 family at CPU-oracle size (parity tests): Qwen3 attention geometry (d_head 128, GQA 8,
+# qk-norm), two layers
+QWEN3_MINI = ModelShape("qwen3-mini", layers=2, d_model=1024, n_q=16, n_kv=2, d_head=128,
+                        d_ff=2048, vocab=1024, rope_theta=1000000.0, rms_eps=1e-6, qk_norm=True)
 
-SHAPES = {s.name: s for s in (TINY, LLAMA3_8B, QWEN3_32B)}
+SHAPES = {s.name: s for s in (TINY, LLAMA3_8B, QWEN3_32B, QWEN3_MINI)}

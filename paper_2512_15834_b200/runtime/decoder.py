@@ -322,8 +322,13 @@ class Decoder:
         clr = T if T <= CLEAR_MAX else 0
         for i in range(s.layers):
             self.gemm(h[:T], w[f"l{i}.wqkv"], "qkv", st, "wqkv")
-            call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]), _p(m["pos"]),
-                 T, s.n_q, s.rope_theta, clr, st)
+            if s.qk_norm:
+                call("stb_qkv_norm_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]),
+                     _p(m["pos"]), T, s.n_q, s.rope_theta, _p(w[f"l{i}.q_norm"]), _p(w[f"l{i}.k_norm"]), s.rms_eps,
+                     clr, st)
+            else:
+                call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]),
+                     _p(m["pos"]), T, s.n_q, s.rope_theta, clr, st)
             self._cleared("qkv", clr)
             if B:
                 ev = self._tick()

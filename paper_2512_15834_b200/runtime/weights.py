@@ -8,8 +8,9 @@ CPU draw of 8B values would dominate start-up); both are bf16 in HBM.
 
 Layout (rows = output features, so every projection is X @ W^T, K-major):
   embed [V][d]; per layer: attn_norm [d], wqkv [(n_q+2n_kv)*dh][d] (q rows,
-  then k rows, then v rows), wo [d][n_q*dh], mlp_norm [d], w_gate_up [2ff][d]
-  (gate rows, then up rows), w_down [d][ff]; final_norm [d]; lm_head [V][d].
+  then k rows, then v rows), q_norm / k_norm [dh] (qk-norm shapes only),
+  wo [d][n_q*dh], mlp_norm [d], w_gate_up [2ff][d] (gate rows, then up rows),
+  w_down [d][ff]; final_norm [d]; lm_head [V][d].
 """
 
 from __future__ import annotations
@@ -42,6 +43,9 @@ def tensor_specs(shape: ModelShape):
     for i in range(shape.layers):
         yield f"l{i}.attn_norm", (d,), True
         yield f"l{i}.wqkv", (shape.q_dim + 2 * shape.kv_dim, d), False
+        if shape.qk_norm:
+            yield f"l{i}.q_norm", (shape.d_head,), True
+            yield f"l{i}.k_norm", (shape.d_head,), True
         yield f"l{i}.wo", (d, shape.q_dim), False
         yield f"l{i}.mlp_norm", (d,), True
         yield f"l{i}.w_gate_up", (2 * shape.d_ff, d), False

@@ -249,29 +249,40 @@ def test_attn_prefill(lib, shape, runs, amp):
         assert rel(out[qs[s]:qs[s + 1]], ref) < 1e-2, s
 
 
-def test_rope_commit(lib):
-    shape = ModelShape("t", 1, 512, 8, 2, 64, 64, 64, rope_theta=10000.0)
+@pytest.mark.parametrize("qk_norm", [False, True], ids=["llama", "qwen3-qknorm"])
+@pytest.mark.parametrize("d_head", [64, 128])
+def test_rope_commit(lib, qk_norm, d_head):
+    shape = ModelShape("t", 1, 512, 8, 2, d_head, 64, 64, rope_theta=10000.0, rms_eps=1e-6, qk_norm=qk_norm)
     pool = _pool(lib, shape)
     n = 37
     pool.reserve(0, 200)
     pool.sync(torch.cuda.current_stream().cuda_stream)
-    qkv = torch.randn(n, (shape.n_q + 2 * shape.n_kv) * shape.d_head, device="cuda")
+    qkv = torch.randn(n, (shape.n_q + 2 * shape.n_kv) * shape.d_head, device="cuda") * 3.0
     pos = torch.arange(150, 150 + n, dtype=torch.int32, device="cuda")
     slot_of = torch.zeros(n, dtype=torch.int32, device="cuda")
     q = torch.empty(n, shape.q_dim, dtype=torch.bfloat16, device="cuda")
+    qn = (1.0 + 0.1 * torch.randn(d_head, device="cuda")).to(torch.bfloat16)
+    kn = (1.0 + 0.1 * torch.randn(d_head, device="cuda")).to(torch.bfloat16)
     qkv0 = qkv.clone()
-    lib.call("stb_qkv_rope_commit", pool.h, 0, P(qkv), P(q), P(slot_of), P(pos), n, shape.n_q, shape.rope_theta,
-             20, stream())
+    if qk_norm:
+        lib.call("stb_qkv_norm_rope_commit", pool.h, 0, P(qkv), P(q), P(slot_of), P(pos), n, shape.n_q,
+                 shape.rope_theta, P(qn), P(kn), shape.rms_eps, 20, stream())
+    else:
+        lib.call("stb_qkv_rope_commit", pool.h, 0, P(qkv), P(q), P(slot_of), P(pos), n, shape.n_q,
+                 shape.rope_theta, 20, stream())
     assert not qkv[:20].any() and torch.equal(qkv[20:], qkv0[20:])  # consumer clears rows < clear_rows
     qkv = qkv0
     from oracle.cpu_decoder import CpuDecoder
 
     dec = CpuDecoder.__new__(CpuDecoder)
+    dec.s = shape
     dec.inv_freq = torch.tensor([1.0 / math.pow(shape.rope_theta, 2.0 * i / shape.d_head)
                                  for i in range(shape.d_head // 2)], dtype=torch.float32)
     x = qkv.cpu().view(n, -1, shape.d_head)
-    rq = dec._rope(x[:, :shape.n_q], pos.cpu())
-    rk = dec._rope(x[:, shape.n_q:shape.n_q + shape.n_kv], pos.cpu())
+    xq, xk = x[:, :shape.n_q], x[:, shape.n_q:shape.n_q + shape.n_kv]
+    w = {"qn": qn.float().cpu(), "kn": kn.float().cpu()} if qk_norm else {}
+    xq, xk = dec._qk(w, xq, xk)
+    rq, rk = dec._rope(xq, pos.cpu()), dec._rope(xk, pos.cpu())
     assert rel(q.view(n, shape.n_q, -1).cpu(), rq) < 5e-3
     kd, vd = _dense_kv(pool, 0, 0, 150 + n, shape)
     assert rel(kd[150:].cpu(), rk) < 5e-3
