@@ -270,7 +270,7 @@ def run_b200(args, world, rank, local):
     state["timed"] = {}
     events = rt.dec.step_events = []
     h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
-    launches0 = lib.load().stb_launch_count()
+    launches0 = lib.load().stb_launch_count() + rt.dec.graph_kernels
     resume0 = len(engine.resume_latencies)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
@@ -289,7 +289,7 @@ def run_b200(args, world, rank, local):
     graphed = [ms for ms, g, _ in per if g]
     mixed = [(ms, T) for ms, g, T in per if not g]
     wall_s = w1 - w0
-    launches = lib.load().stb_launch_count() - launches0
+    launches = lib.load().stb_launch_count() + rt.dec.graph_kernels - launches0  # eager + graph-replayed
     resume = engine.resume_latencies[resume0:]
     timers = state["timed"]
     rt.dec.timers = None
@@ -307,7 +307,7 @@ def run_b200(args, world, rank, local):
 
     def rate(name):  # (bound, achieved, peak, unit) — tensor-bound kernels count FLOPs, the rest bytes
         t, w, _ = kern[name]
-        if name == "gemm_prefill":  # timed inside long steps: the sustained tensor peak
+        if name in ("gemm_prefill", "attn_prefill"):  # timed inside long steps: the sustained tensor peak
             return "tensor", w / t / 1e12, tf_sus, "TFLOP/s"
         return "hbm", w / t / 1e9, hbm, "GB/s"
 

@@ -132,6 +132,17 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
  * act[M][N/2] (row stride ldc elements) = silu(gate) * up, computed in fp32 exactly
  * as stb_silu_mul does */
 #define STB_GEMM_SILU_MUL 2
+/* W is in the tiled HBM layout written by stb_weight_tile (ldw ignored): every
+ * 128-row x 64-column weight tile is one contiguous 16 KiB block, already in the
+ * 128-byte-swizzled order the tensor core reads, so each pipeline stage is one
+ * linear bulk copy (whole DRAM pages) instead of 128 strided 128-byte rows */
+#define STB_GEMM_W_TILED 4
+/* elements of the tiled copy of an N x K weight (N padded to 128, K to 64) */
+int64_t stb_weight_tiled_elems(int N, int K);
+/* out (bf16, stb_weight_tiled_elems(N, K)) = W[N][K] (row stride ldw) in the tiled
+ * layout: tile (n, k) at ((n * ceil(K/64)) + k) * 8192 elements, row r of the tile
+ * at r * 64, 16-byte chunk c of the row stored at chunk c ^ (r & 7); padding = 0 */
+int stb_weight_tile(const void* W, int64_t ldw, int N, int K, void* out, void* stream);
 /* 1 if the automatic schedule runs this shape stream-K (C accumulated with reductions) */
 int stb_gemm_is_stream(int M, int N, int K);
 int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,

@@ -276,7 +276,7 @@ __device__ __forceinline__ int warp_of(int64_t u, int64_t U, int W) {
 }
 
 template <int D, int G, int STAGES>
-__global__ void __launch_bounds__(128) attn_decode_kernel(
+__global__ void __launch_bounds__(128, 2) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
@@ -285,19 +285,49 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   constexpr int NP = kChunkPages;
   constexpr int STAGE = NP * 2 * PAGE;  // K and V of NP pages
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ int64_t prefix[kMaxB + 1];  // chunk units before sequence b
+  __shared__ int prefix[kMaxB + 1];  // chunk units before sequence b (< 2^31: B * n_kv * ctx/32)
+  __shared__ int s_ctx[kMaxB], s_slot[kMaxB];
+  __shared__ int s_wsum[4];
   __shared__ __align__(8) uint64_t full_bars[4 * STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = n_kv * G;
   if (threadIdx.x == 0) {
     for (int s2 = 0; s2 < 4 * STAGES; ++s2) mbar_init(&full_bars[s2], 1);
     fence_mbar_init();
-    int64_t acc = 0;
-    for (int b = 0; b < B; ++b) {
-      prefix[b] = acc;
-      acc += (int64_t)n_kv * ((ctx_lens[b] + 16 * NP - 1) / (16 * NP));
+  }
+  {
+    // step metadata (host-uploaded, not produced by the preceding kernel): all threads load
+    // ctx / slot in parallel (a serial loop would chain B global-load latencies in front of
+    // the first page copy), then a block scan gives the unit prefix
+    const int per = (B + 127) >> 7, b0 = threadIdx.x * per;
+    int local = 0;
+    for (int j = 0; j < per; ++j) {
+      const int b = b0 + j;
+      if (b < B) {
+        const int c = ctx_lens[b];
+        s_ctx[b] = c;
+        s_slot[b] = slots[b];
+        local += n_kv * ((c + 16 * NP - 1) / (16 * NP));
+      }
     }
-    prefix[B] = acc;
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    int run = incl - local;
+    for (int w2 = 0; w2 < warp; ++w2) run += s_wsum[w2];
+    for (int j = 0; j < per; ++j) {
+      const int b = b0 + j;
+      if (b < B) {
+        prefix[b] = run;
+        run += n_kv * ((s_ctx[b] + 16 * NP - 1) / (16 * NP));
+      }
+    }
+    if (threadIdx.x == 127) prefix[B] = run;
   }
   __syncthreads();
   pdl_launch();
@@ -316,9 +346,9 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     const int32_t* row;
   };
   auto enter = [&](Cur& r) {
-    r.ctx = ctx_lens[r.b];
+    r.ctx = s_ctx[r.b];
     r.chunks = (r.ctx + 16 * NP - 1) / (16 * NP);
-    r.row = table + (int64_t)slots[r.b] * max_bps;
+    r.row = table + (int64_t)s_slot[r.b] * max_bps;
   };
   auto locate = [&](int64_t u) {
     int lo = 0, hi = B - 1;
@@ -654,7 +684,7 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (2 * (4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 8 * (kMaxB + 1)) <= 220 * 1024 ? 2 : 1) * sms;
+  const int grid = (2 * (4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 4 * (3 * kMaxB + 1)) <= 220 * 1024 ? 2 : 1) * sms;
   const int W = grid * 4;
   const size_t need = (size_t)W * 2 * G * (D + 1);
   const int pairs = B * n_kv;

@@ -39,7 +39,9 @@
 // kernel's tail; activations are loaded only after the wait.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -133,7 +135,9 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_persistent(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                         float* __restrict__ C, int64_t ldc, int M, int N, Sched sched, int bn) {
+                         float* __restrict__ C, int64_t ldc, int M, int N, Sched sched, int bn,
+                         const __nv_bfloat16* __restrict__ w_tiled) {
+  // w_tiled != nullptr: W in the stb_weight_tile layout, one 16 KiB bulk copy per stage
   // bn: token-tile height actually used (<= BN, multiple of 16); BN sizes the smem ring
   using CF = Cfg<BN>;
   constexpr int STAGES = CF::STAGES;
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm_w);
+    if (w_tiled == nullptr) tma_prefetch(&tm_w);
     tma_prefetch(&tm_x);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -170,6 +174,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (elect_one()) {
+      auto load_w = [&](uint8_t* dst, int k, int f0, uint64_t* bar) {
+        if (w_tiled != nullptr)
+          bulk_load(smem_u32(dst), w_tiled + ((int64_t)(f0 / BM) * sched.kb + k) * (BM * BK), CF::W_BYTES, bar);
+        else
+          tma_load_2d(dst, &tm_w, bar, k * BK, f0);
+      };
       // weights first: the ring's first slots fill before the dependency wait
       SegIter pre(sched);
       int tile, k0, k1, i = 0;
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int f0 = (tile / sched.tiles_m) * BM;
         for (int k = k0; k < k1 && i < STAGES; ++k, ++i) {
           mbar_expect_tx(&full[i], CF::W_BYTES + bn * BK * 2);
-          tma_load_2d(smem + i * CF::STAGE, &tm_w, &full[i], k * BK, f0);
+          load_w(smem + i * CF::STAGE, k, f0, &full[i]);
         }
       }
       const int prefetched = i;
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b = (lw ? CF::W_BYTES : 0) + (lx ? bn * BK * 2 : 0);
             if (b) {
               mbar_expect_tx(&full[s], b);
-              if (lw) tma_load_2d(sw, &tm_w, &full[s], k * BK, f0);
+              if (lw) load_w(sw, k, f0, &full[s]);
               if (lx) tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
             } else {
               mbar_arrive(&full[s]);
@@ -210,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           mbar_expect_tx(&full[s], CF::W_BYTES + bn * BK * 2);
-          tma_load_2d(sw, &tm_w, &full[s], k * BK, f0);
+          load_w(sw, k, f0, &full[s]);
           tma_load_2d(sw + CF::W_BYTES, &tm_x, &full[s], k * BK, t0);
         }
       }
@@ -530,7 +540,12 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
            int mode, int flags, cudaStream_t st) {
   using CF = Cfg<BN>;
   CUtensorMap tw, tx;
-  if (int rc = cached_map(&tw, W, N, K, ldw, BM)) return rc;
+  const bool tiled = (flags & STB_GEMM_W_TILED) != 0;
+  if (tiled) {
+    memset(&tw, 0, sizeof(tw));  // unused: the producer bulk-copies whole tiles
+  } else if (int rc = cached_map(&tw, W, N, K, ldw, BM)) {
+    return rc;
+  }
   const int sms = sm_count();
   const Plan pl = plan(M, N, sms);
   const int bn = pl.bn;
@@ -561,12 +576,59 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr_set = true;
   }
-  cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), CF::SMEM, st, tw, tx, C, ldc, M, N, s, bn);
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), CF::SMEM, st, tw, tx, C, ldc, M, N, s, bn,
+                           tiled ? (const __nv_bfloat16*)W : (const __nv_bfloat16*)nullptr);
   if (e != cudaSuccess) return fail(STB_ECUDA, "gemm_bf16 launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
 
 }  // namespace
+
+namespace {
+// one thread per 16-byte chunk of the tiled layout: gathers 8 bf16 of W (zero padding)
+__global__ void weight_tile_kernel(const __nv_bfloat16* __restrict__ W, int64_t ldw, int N, int K, int kbs,
+                                   int64_t chunks, uint4* __restrict__ out) {
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    const int pc = (int)(i & 7);              // physical chunk within the 128-byte row
+    const int r = (int)((i >> 3) & (BM - 1));  // row within the tile
+    const int64_t t = i >> 10;                // tile index = n_tile * kbs + k_tile
+    const int c = pc ^ (r & 7);               // logical chunk stored at pc
+    const int64_t row = (t / kbs) * BM + r;
+    const int64_t col = (t % kbs) * BK + c * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row < N) {
+      const __nv_bfloat16* src = W + row * ldw + col;
+      if (col + 8 <= K) {
+        v = *reinterpret_cast<const uint4*>(src);
+      } else if (col < K) {
+        __nv_bfloat16 e[8];
+        for (int j = 0; j < 8; ++j) e[j] = col + j < K ? src[j] : __float2bfloat16(0.f);
+        v = *reinterpret_cast<const uint4*>(e);
+      }
+    }
+    out[i] = v;
+  }
+}
+}  // namespace
+
+extern "C" int64_t stb_weight_tiled_elems(int N, int K) {
+  if (N <= 0 || K <= 0) return 0;
+  return (int64_t)((N + BM - 1) / BM) * ((K + BK - 1) / BK) * BM * BK;
+}
+
+extern "C" int stb_weight_tile(const void* W, int64_t ldw, int N, int K, void* out, void* stream) {
+  if (N <= 0 || K <= 0) return STB_OK;
+  if (ldw < K || ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(out)) & 15) || ldw % 8)
+    return fail(STB_EINVAL, "weight_tile: W must be 16-byte aligned with ldw >= K, ldw %% 8 == 0");
+  const int64_t chunks = stb_weight_tiled_elems(N, K) / 8;
+  const int kbs = (K + BK - 1) / BK;
+  const int grid = (int)std::min<int64_t>((chunks + 255) / 256, 148 * 16);
+  launch_k(weight_tile_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)W, ldw, N, K,
+           kbs, chunks, (uint4*)out);
+  STB_CHECK_LAUNCH("weight_tile");
+  return STB_OK;
+}
 
 // 1 when stb_gemm_bf16(split_k = 0) would run this shape stream-K (reductions into C)
 extern "C" int stb_gemm_is_stream(int M, int N, int K) {
@@ -593,7 +655,8 @@ extern "C" int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t 
                              int N, int K, int split_k, int flags, void* stream) {
   if (M <= 0 || N <= 0) return STB_OK;
   if (K <= 0 || K % 8 != 0) return fail(STB_EINVAL, "gemm_bf16: K must be a positive multiple of 8");
-  if (lda % 8 != 0 || ldw % 8 != 0) return fail(STB_EINVAL, "gemm_bf16: row strides must be multiples of 8");
+  if (lda % 8 != 0 || (ldw % 8 != 0 && !(flags & STB_GEMM_W_TILED)))
+    return fail(STB_EINVAL, "gemm_bf16: row strides must be multiples of 8");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
     return fail(STB_EINVAL, "gemm_bf16: operands must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;

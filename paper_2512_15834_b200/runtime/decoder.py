@@ -49,7 +49,27 @@ def interleave_gate_up(w: torch.Tensor, d_ff: int) -> None:
         return
     w.copy_(w.view(2, d_ff, -1).transpose(0, 1).reshape(2 * d_ff, -1))
     w._stb_gate_up_interleaved = True   # include/stb200.h STB_GEMM_C_ZEROED
+GEMM_W_TILED = 4    # include/stb200.h STB_GEMM_W_TILED
 CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
+PROJECTIONS = ("wqkv", "wo", "w_gate_up", "w_down")
+
+
+class TiledWeight:
+    """A projection weight re-laid out once by stb_weight_tile: each 128 x 64 tile one
+    contiguous, pre-swizzled 16 KiB block, so every GEMM pipeline stage is a single
+    linear bulk copy of whole DRAM pages (STB_GEMM_W_TILED)."""
+
+    __slots__ = ("t", "N", "K")
+
+    def __init__(self, w: torch.Tensor):
+        self.N, self.K = int(w.shape[0]), int(w.shape[1])
+        self.t = torch.empty(lib.load().stb_weight_tiled_elems(self.N, self.K), dtype=torch.bfloat16,
+                             device=w.device)
+        lib.call("stb_weight_tile", C.c_void_p(w.data_ptr()), w.stride(0), self.N, self.K,
+                 C.c_void_p(self.t.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+    def data_ptr(self) -> int:
+        return self.t.data_ptr()
 
 
 class KVPool:
@@ -147,8 +167,15 @@ class Decoder:
                  use_graphs: bool = True):
         self.shape = shape
         self.w = weights
-        for i in range(shape.layers):  # (gate, up) pairs in adjacent rows: fused SiLU epilogue
-            interleave_gate_up(weights[f"l{i}.w_gate_up"], shape.d_ff)
+        for i in range(shape.layers):
+            gu = weights[f"l{i}.w_gate_up"]
+            if not isinstance(gu, TiledWeight):  # (gate, up) pairs in adjacent rows: fused SiLU epilogue
+                interleave_gate_up(gu, shape.d_ff)
+            del gu
+        # projections in the tiled HBM layout (once; a shared dict is converted in place)
+        for name in [f"l{i}.{p}" for i in range(shape.layers) for p in PROJECTIONS] + ["lm_head"]:
+            if not isinstance(weights[name], TiledWeight):
+                weights[name] = TiledWeight(weights[name])
         self.pool = pool
         self.device = device
         self.scale = 1.0 / math.sqrt(shape.d_head)
@@ -156,7 +183,9 @@ class Decoder:
         self.keep_logits = False
         self.use_graphs = use_graphs
         self.graphs: dict[tuple, tuple] = {}
+        self.graph_sizes: dict[tuple, int] = {}  # kernels captured per graph
         self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
+        self._pre_flops = 0
         self._pending: list | None = []             # (name, ev0, ev1, work) awaiting a sync
         self._graph_timed = False
         self.last_logits: torch.Tensor | None = None
@@ -169,6 +198,7 @@ class Decoder:
         self.meta_dev = torch.empty(self.META_CAP, dtype=torch.int32, device=device)
         self.h2d_bytes = 0
         self.graph_replays = 0
+        self.graph_kernels = 0   # kernels launched by graph replays (captured launches x replays)
         self._timed_parity = 0
         self.step_events: list | None = None  # (ev0, ev1, graphed, T) bracketing each step's kernels
         # leading rows of each GEMM output that may be non-zero (rows at and past it are zero)
@@ -252,6 +282,10 @@ class Decoder:
             e0.record()
         if not graphable:
             max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
+            if S:  # K2 algorithmic flops per layer: 4 H_q d (n ctx_prev + n(n+1)/2) per run
+                n = np.diff(b.pre_qstart).astype(np.float64)
+                prev = b.pre_ctx.astype(np.float64) - n
+                self._pre_flops = int(4 * self.shape.q_dim * float(np.sum(n * prev + n * (n + 1) / 2)))
             self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
         else:
             # decode graphs assume (and leave) zeroed every GEMM output they accumulate into
@@ -277,6 +311,7 @@ class Decoder:
             graph, events = self.graphs[key]
             graph.replay()
             self.graph_replays += 1
+            self.graph_kernels += self.graph_sizes.get(key, 0)
             if timed:
                 for name, a0, a1, work in events:
                     self._pending.append((name, a0, a1, dec_bytes if name == "attn_decode" else work))
@@ -302,8 +337,10 @@ class Decoder:
         events: list = []
         self._pending = events
         self._graph_timed = timed
+        n0 = lib.load().stb_launch_count()
         with torch.cuda.graph(graph):
             self._launch(m, B, B, B, 0, 0, 0, 0)
+        self.graph_sizes[key] = int(lib.load().stb_launch_count() - n0)
         self._pending, self.timers = saved, saved_timers
         self._graph_timed = False
         self.graphs[key] = (graph, events)
@@ -336,9 +373,11 @@ class Decoder:
                      _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
                 self._tock("attn_decode", ev, dec_bytes)
             if S:
+                ev = self._tick()
                 call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                      _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                      st)
+                self._tock("attn_prefill", ev, self._pre_flops)
             self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
             self._cleared("proj", clr)
@@ -405,7 +444,7 @@ class Decoder:
              fuse_silu: bool = False) -> bool:
         """Launch K5; returns True when the SiLU-gate epilogue was fused (output in self.act)."""
         M, K = a.shape
-        N = wt.shape[0]
+        N = wt.N
         key = (M, N, K)
         stream = self._stream_cache.get(key)
         if stream is None:
@@ -419,8 +458,8 @@ class Decoder:
         if "stb_gemm_bf16" in _SKIP or f"gemm:{tag}" in _SKIP:
             return fused
         ev = self._tick()
-        lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), wt.stride(0), _p(out), out.stride(0), M, N, K, 0,
-                 flags, st)
+        lib.call("stb_gemm_bf16", _p(a), a.stride(0), _p(wt), 0, _p(out), out.stride(0), M, N, K, 0,
+                 flags | GEMM_W_TILED, st)
         if not fused:
             self._dirty[out_name] = max(self._dirty[out_name], M)
         if M <= 128:  # decode-shaped: HBM-bound on the weights; work = algorithmic bytes

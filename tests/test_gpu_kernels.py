@@ -95,6 +95,47 @@ def test_gemm_explicit_split(lib):
         assert rel(c, ref) < 2e-5, split
 
 
+def _tiled(lib, w):
+    N, K = w.shape
+    t = torch.full((lib.load().stb_weight_tiled_elems(N, K),), float("nan"), device="cuda").to(torch.bfloat16)
+    lib.call("stb_weight_tile", P(w), w.stride(0), N, K, P(t), stream())
+    return t
+
+
+def test_weight_tile_layout(lib):
+    """stb_weight_tile: tile (n, k) contiguous, rows of 64, 16-byte chunk c of row r at c ^ (r & 7),
+    zero padding past N and K (restated here in torch)."""
+    N, K = 200, 72
+    w = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    t = _tiled(lib, w)
+    pad = torch.zeros(256, 128, device="cuda", dtype=torch.bfloat16)
+    pad[:N, :K] = w
+    ref = pad.view(2, 128, 2, 8, 8).permute(0, 2, 1, 3, 4).clone()  # [nt][kt][r][c][e]
+    r = torch.arange(128, device="cuda").view(128, 1)
+    perm = torch.arange(8, device="cuda").view(1, 8) ^ (r & 7)          # physical chunk -> logical
+    ref = torch.gather(ref, 3, perm.view(1, 1, 128, 8, 1).expand(2, 2, 128, 8, 8))
+    assert torch.equal(t, ref.reshape(-1))
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 256), (32, 6144, 4096), (32, 4096, 14336), (17, 130, 200),
+                                   (300, 640, 1024), (608, 28672, 4096)])
+def test_gemm_w_tiled(lib, M, N, K):
+    """STB_GEMM_W_TILED: the same products from the tiled weight layout (both schedules)."""
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (0.05 * torch.randn(N, K, device="cuda")).to(torch.bfloat16)
+    t = _tiled(lib, w)
+    ref = a.float() @ w.float().T
+    for split in (0, 1, 7):
+        c = torch.full((M, N), float("nan"), device="cuda")
+        lib.call("stb_gemm_bf16", P(a), K, P(t), 0, P(c), N, M, N, K, split, 4, stream())
+        assert rel(c, ref) < 2e-5, split
+    if N % 2 == 0:  # fused SiLU epilogue from tiled weights
+        act = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        lib.call("stb_gemm_bf16", P(a), K, P(t), 0, P(act), N // 2, M, N, K, 1, 2 | 4, stream())
+        want = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+        assert rel(act, want) < 1e-2
+
+
 def _pool(lib, shape, nb=256, slots=64, bps=512):
     from paper_2512_15834_b200.runtime.decoder import KVPool
 
@@ -247,6 +288,47 @@ def test_attn_prefill(lib, shape, runs, amp):
         qpos = torch.arange(c - n, c, device="cuda")
         ref = _ref_attn(q[qs[s]:qs[s + 1]], k, v, qpos, scale)
         assert rel(out[qs[s]:qs[s + 1]], ref) < 1e-2, s
+
+
+def _ref_attn_chunked(q, k, v, qpos, scale):
+    """_ref_attn one kv head (and its query-head group) at a time: bounds the fp32 score
+    tensor at 32k contexts."""
+    rep = q.shape[1] // k.shape[1]
+    return torch.cat([_ref_attn(q[:, g * rep:(g + 1) * rep], k[:, g:g + 1], v[:, g:g + 1], qpos, scale)
+                      for g in range(k.shape[1])], dim=1)
+
+
+@pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[2]], ids=lambda s: s.name)
+def test_attn_long_context_c5(lib, shape):
+    """Config C5 (KV pressure): a 2048-token tool output appended in place after a 32,768-token
+    resident context (K2), then decode over 32k+ contexts of several sequences (K3)."""
+    ctxs = [32768 + 2048, 32768 + 7, 33000]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(ctxs), bps=2304)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=5)
+    scale = 1 / math.sqrt(shape.d_head)
+    # K2: the ingest run of sequence 0
+    n = 2048
+    q = torch.randn(n, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out = torch.full_like(q, float("nan"))
+    slot0 = torch.zeros(1, dtype=torch.int32, device="cuda")  # kept alive: the launch reads them
+    qstart = torch.tensor([0, n], dtype=torch.int32, device="cuda")
+    ctx0 = torch.tensor([ctxs[0]], dtype=torch.int32, device="cuda")
+    lib.call("stb_attn_prefill", pool.h, 0, P(q), P(out), P(slot0), P(qstart), P(ctx0), 1, n, shape.n_q, scale, n,
+             stream())
+    k0, v0 = dense[0]
+    ref = _ref_attn_chunked(q, k0, v0, torch.arange(ctxs[0] - n, ctxs[0], device="cuda"), scale)
+    assert rel(out, ref) < 1e-2
+    # K3: one decode query per sequence at its full context
+    B = len(ctxs)
+    qd = torch.randn(B, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    od = torch.empty_like(qd)
+    ws = torch.empty(lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.d_head) // 4, device="cuda")
+    slots = torch.arange(B, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    lib.call("stb_attn_decode", pool.h, 0, P(qd), P(od), P(slots), P(ctx), B, shape.n_q, scale, 0, P(ws), stream())
+    for b, (k, v) in enumerate(dense):
+        r = _ref_attn(qd[b:b + 1], k, v, torch.tensor([ctxs[b] - 1], device="cuda"), scale)
+        assert rel(od[b:b + 1], r) < 1e-2, b
 
 
 @pytest.mark.parametrize("qk_norm", [False, True], ids=["llama", "qwen3-qknorm"])

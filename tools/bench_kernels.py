@@ -51,7 +51,7 @@ def time_it(fn, iters=40, warm=3):
     return e0.elapsed_time(e1) / iters * 1e3  # us
 
 
-def bench_gemm(shape, M, split=0):
+def bench_gemm(shape, M, split=0, layout="tiled"):
     s = shape
     gemms = {"qkv": (s.q_dim + 2 * s.kv_dim, s.d_model), "o": (s.d_model, s.q_dim),
              "gate_up": (2 * s.d_ff, s.d_model), "down": (s.d_model, s.d_ff), "lm_head": (s.vocab, s.d_model)}
@@ -62,14 +62,26 @@ def bench_gemm(shape, M, split=0):
         a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
         c = torch.empty(M, N, device="cuda")
         flags = 1 if lib.load().stb_gemm_is_stream(M, N, K) else 0  # as the decoder runs it
-        us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(ws[i % copies]), K, P(c), N, M, N, K, split,
-                                        flags, st()))
         byts = N * K * 2 + M * K * 2 + M * N * 4
         fl = 2 * M * N * K
-        out[name] = (us, byts / us / 1e3, fl / us / 1e6)
-        print(f"  M={M:5d} {name:8s} N={N:6d} K={K:5d}: {us:8.1f} us  {byts / us / 1e3:7.0f} GB/s "
-              f"({byts / us / 1e3 / PEAK['hbm_gbs']:.2f})  {fl / us / 1e6:7.1f} TF/s "
-              f"({fl / us / 1e6 / PEAK['bf16_tflops']:.2f})")
+        if layout in ("rowmajor", "both"):
+            us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(ws[i % copies]), K, P(c), N, M, N, K, split,
+                                            flags, st()))
+            out[name] = (us, byts / us / 1e3, fl / us / 1e6)
+            print(f"  M={M:5d} {name:8s} N={N:6d} K={K:5d}: {us:8.1f} us  {byts / us / 1e3:7.0f} GB/s "
+                  f"({byts / us / 1e3 / PEAK['hbm_gbs']:.2f})  {fl / us / 1e6:7.1f} TF/s "
+                  f"({fl / us / 1e6 / PEAK['bf16_tflops']:.2f})  row-major W")
+        if layout in ("tiled", "both"):
+            from paper_2512_15834_b200.runtime.decoder import TiledWeight
+
+            tw = [TiledWeight(w) for w in ws]
+            us = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(tw[i % copies]), 0, P(c), N, M, N, K, split,
+                                            flags | 4, st()))
+            out[name] = (us, byts / us / 1e3, fl / us / 1e6)
+            print(f"  M={M:5d} {name:8s} N={N:6d} K={K:5d}: {us:8.1f} us  {byts / us / 1e3:7.0f} GB/s "
+                  f"({byts / us / 1e3 / PEAK['hbm_gbs']:.2f})  {fl / us / 1e6:7.1f} TF/s "
+                  f"({fl / us / 1e6 / PEAK['bf16_tflops']:.2f})  tiled W")
+            del tw
         del ws
     tot = sum(v[0] for v in out.values())
     print(f"  M={M}: sum {tot:.1f} us")
@@ -199,6 +211,7 @@ def main():
     ap.add_argument("--what", default="gemm,attn,prefill")
     ap.add_argument("--M", default="32,2080")
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--layout", default="tiled", choices=["tiled", "rowmajor", "both"])
     ap.add_argument("--prefill-cases", default="4x2048x2048,1x2048x34816,8x512x4096,32x33x4096",
                     help="SxNxCTX list for --what prefill")
     args = ap.parse_args()
@@ -206,7 +219,7 @@ def main():
     shape = SHAPES[args.shape]
     if "gemm" in args.what:
         for M in [int(x) for x in args.M.split(",")]:
-            bench_gemm(shape, M, args.split)
+            bench_gemm(shape, M, args.split, args.layout)
     if "sweep" in args.what:
         bench_gemm_sweep()
     if "pdl" in args.what:

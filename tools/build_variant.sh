@@ -5,7 +5,7 @@
 set -e
 NAME=$1; shift
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
-C=$ROOT/paper_2512_15834_b200/csrc
+C=${SRC:-$ROOT/paper_2512_15834_b200/csrc}
 OUT=$ROOT/paper_2512_15834_b200/lib/variants/$NAME
 mkdir -p $OUT/obj
 for f in kv attention attn_prefill_tc gemm ops; do

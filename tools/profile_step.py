@@ -95,7 +95,7 @@ def main():
         print(f"  (event-pair overhead {ov * 1e3:.2f} us per launch subtracted)")
         for name, (t, work, n) in rt.dec.timers.items():
             t = max(t - n * ov, 1e-3 * t)
-            if name == "gemm_prefill":
+            if name in ("gemm_prefill", "attn_prefill"):
                 print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e12:8.1f} TFLOP/s")
             else:
                 print(f"  {name:12s} {t / n * 1e3:8.2f} us avg x{n}  {work / (t / 1e3) / 1e9:8.1f} GB/s algorithmic")
