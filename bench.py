@@ -101,6 +101,19 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def traffic(kernel: str, alg_bytes_per_launch: float) -> tuple:
+    """roofline.traffic: DRAM bytes per launch of the kernel class, from the committed ncu
+    --set full capture (profiles/traffic_*.json: measured dram bytes / algorithmic bytes of
+    the same launches) applied to this run's algorithmic bytes per launch; None if absent."""
+    files = sorted((ROOT / "profiles").glob("traffic_*.json"))
+    if not files:
+        return None, None, None
+    d = json.loads(files[-1].read_text()).get(kernel)
+    if not d or d.get("ratio") is None or kernel in ("gemm_prefill", "attn_prefill"):
+        return None, None, None
+    return int(d["ratio"] * alg_bytes_per_launch), d["ratio"], f"profiles/{files[-1].name}"
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -315,8 +328,10 @@ def run_b200(args, world, rank, local):
     if dominant:
         t, w, n = kern[dominant]
         bound, ach, peak, unit = rate(dominant)
+        tr, tr_ratio, tr_src = traffic(dominant, w / n)
         roof = {"kernel": dominant, "bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
-                "frac": round(ach / peak, 4), "traffic": None, "peak_source": src, "launches": n,
+                "frac": round(ach / peak, 4), "traffic": tr, "traffic_over_algorithmic": tr_ratio,
+                "traffic_source": tr_src, "peak_source": src, "launches": n,
                 "avg_us": round(t / n * 1e6, 2), "share_of_device_time": round(t / dev_s * TIMER_STRIDE, 4),
                 "sampling": f"CUDA events on 1 step in {TIMER_STRIDE} of the timed region, "
                             f"event-pair overhead {ov * 1e3:.2f} us subtracted per launch"}
