@@ -137,6 +137,54 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
  * 128-byte-swizzled order the tensor core reads, so each pipeline stage is one
  * linear bulk copy (whole DRAM pages) instead of 128 strided 128-byte rows */
 #define STB_GEMM_W_TILED 4
+/* ---- K5 with fused epilogues (the row ops that used to follow each GEMM) ----
+ * C = A * W^T is accumulated in `work` (fp32 [M][N], row stride ldwork), which
+ * must be zero on entry and is left zero on exit: stream-K partial tiles are
+ * reduced into it with fp32 red.add, the last CTA of each tile (ticket counter)
+ * reads the finished tile back and runs the epilogue, then clears it. Whole
+ * tiles run the epilogue straight from TMEM. `ss_in` (optional) applies the
+ * RMSNorm of the GEMM's input row after the reduction (the norm weight is
+ * folded into W): v *= rsqrt(sum_p ss_in[t][p] * inv_dim + eps).
+ *   STB_EPI_SILU   out bf16 [M][N/2] (ldo) = silu(gate) * up (W rows interleaved
+ *                  as for STB_GEMM_SILU_MUL)
+ *   STB_EPI_RESID  x[t][f] += v (fp32, ldx); out bf16 [M][N] (ldo) = x;
+ *                  ss_out[t][f / 128] = sum of x^2 over the tile's 128 features
+ *                  (the next norm's statistics, written
+ *                  with plain stores — deterministic, no atomics)
+ *   STB_EPI_QKV    [qk-norm] + RoPE on the q and k heads, q -> out bf16
+ *                  [M][n_q*d_head] (ldo), k and v committed into the pool pages
+ *                  of `layer` at (slot_of[t], pos_of[t]) — stb_qkv_norm_rope_commit
+ *                  fused into the QKV projection (engine.py:251,270,296,358)   */
+#define STB_EPI_SILU 1
+#define STB_EPI_QKV 2
+#define STB_EPI_RESID 3
+typedef struct stb_gemm_epi {
+  int kind;
+  const float* ss_in;   /* [M][ss_parts] partial sums of squares (summed here) */
+  int ss_parts;         /* row stride of ss_in / ss_out: >= ceil(d/128), a multiple of 4,
+                           unused slots zero (stb_embed_prep zeroes them) */
+  float inv_dim, eps;
+  void* out;
+  int64_t ldo;
+  float* x;
+  int64_t ldx;
+  float* ss_out;
+  stb_kv_pool* pool;
+  int layer, n_q;
+  const int32_t* slot_of;
+  const int32_t* pos_of;
+  float rope_theta;
+  const void* q_norm;
+  const void* k_norm;
+  float qk_eps;
+} stb_gemm_epi;
+int stb_gemm_bf16_fused(const void* A, int64_t lda, const void* W, int64_t ldw, float* work, int64_t ldwork, int M,
+                        int N, int K, int flags, const stb_gemm_epi* epi, void* stream);
+/* x[t] = embed[ids[t]] (fp32), xb = bf16(x), ss[t][0] = sum x^2, ss[t][p] = 0 for
+ * 1 <= p < ss_parts: the first layer's fused-norm inputs */
+int stb_embed_prep(const int32_t* ids, const void* table, float* x, void* xb, float* ss, int ss_parts, int n, int d,
+                   void* stream);
+
 /* elements of the tiled copy of an N x K weight (N padded to 128, K to 64) */
 int64_t stb_weight_tiled_elems(int N, int K);
 /* out (bf16, stb_weight_tiled_elems(N, K)) = W[N][K] (row stride ldw) in the tiled

@@ -47,6 +47,7 @@
 
 #include "../../include/stb200.h"
 #include "common.cuh"
+#include "pool.cuh"
 
 using namespace stb;
 
@@ -55,6 +56,10 @@ namespace {
 constexpr int BM = 128;  // weight rows per tile (UMMA M)
 constexpr int BK = 64;   // K per stage: one 128-byte swizzle atom of bf16
 constexpr int kThreads = 192;
+constexpr int EPI_CH = 16;        // tokens per fused-epilogue chunk
+constexpr int EPI_LD = BM + 4;    // fp32 row stride of the QKV staging tile
+constexpr int EPI_SMEM = 256 * 4 * 7 + EPI_CH * EPI_LD * 4;  // sizeof(EpiSmem)
+constexpr int kMaxSsParts = 64;   // d_model <= 8192 (ss partials per row, a multiple of 4)
 
 template <int BN>
 struct Cfg {
@@ -64,7 +69,7 @@ struct Cfg {
   static constexpr int RING = 200 * 1024;  // measured best: bytes in flight beat SM co-residence
   static constexpr int STAGES = (RING / STAGE) > 12 ? 12 : (RING / STAGE);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;  // two accumulator buffers
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
 };
 
 struct Sched {
@@ -83,6 +88,31 @@ struct Sched {
   int load_debug;    // timing experiments (STB200_GEMM_LOAD_DEBUG): after the first ring fill
                      // 1 = skip X loads, 2 = skip W loads, 3 = skip both (results are garbage)
 };
+
+// Fused epilogue (stb_gemm_bf16_fused, include/stb200.h). kind 0 = the plain path above.
+struct Epi {
+  int kind;                       // 0 none, STB_EPI_SILU, STB_EPI_QKV, STB_EPI_RESID
+  const float* ss_in;             // optional per-row RMSNorm statistics of the GEMM input:
+  int ss_parts;                   //   ss_in[t][ss_parts] partial sums of squares (RESID: ss_out)
+  float inv_dim, eps;
+  __nv_bfloat16* out;             // SILU: act; RESID: bf16 copy of x; QKV: q
+  int64_t ldo;
+  float* x;                       // RESID: fp32 residual stream
+  int64_t ldx;
+  float* ss_out;                  // RESID: sum of squares of the new x rows (atomic)
+  __nv_bfloat16* kpages;          // QKV: this layer's K / V pages (pre-swizzled, pool.cuh)
+  __nv_bfloat16* vpages;
+  const int32_t* table;
+  int max_bps, n_kv, d_head, q_dim, kv_dim;
+  const int32_t* slot_of;
+  const int32_t* pos_of;
+  const float* inv_freq;
+  const __nv_bfloat16* q_norm;
+  const __nv_bfloat16* k_norm;
+  float qk_eps;
+  unsigned* cnt;                  // stream-K tile tickets (self-resetting)
+};
+
 
 // Debug timeline (stb_debug_gemm_trace): per CTA {tag, t_last_epilogue, sm, t_entry,
 // t_dep_wait, t_first_stage, t_last_mma_issue, t_exit} in %globaltimer ns. Off (null) in
@@ -132,11 +162,270 @@ struct SegIter {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
+// Number of CTAs whose stream-K unit range [U*c/G, U*(c+1)/G) intersects tile t.
+__device__ __forceinline__ int owner_of(int64_t u, int64_t U, int G) {
+  int c = (int)((u * G) / U);
+  while (c + 1 < G && (U * (c + 1)) / G <= u) ++c;
+  return c;
+}
+
+// Per-tile token metadata of the fused epilogue, staged once per tile (the chunk loop then
+// never waits on a global load): row scale, and for QKV the position and the pool block.
+struct EpiSmem {
+  float rs[256];
+  int pos[256];
+  int blk[256];
+  float ssw[4][256];           // RESID: per-warp partial sums of squares
+  float stage[EPI_CH][EPI_LD];  // QKV: the chunk, feature-major -> token-major
+};
+
+__device__ __forceinline__ void epi_tile_prologue(const Epi& ep, EpiSmem& sm, int t0, int ntok) {
+  epi_bar();  // every epilogue thread is done with the previous tile's metadata
+  const int i = threadIdx.x - 64;
+  for (int t = i; t < ntok; t += 128) {
+    float r = 1.f;
+    if (ep.ss_in != nullptr) {
+      // all partial loads issued before the first add (one L2 latency, not ss_parts of them)
+      const float4* p = reinterpret_cast<const float4*>(ep.ss_in + (int64_t)(t0 + t) * ep.ss_parts);
+      const int n4 = ep.ss_parts >> 2;
+      float4 w[kMaxSsParts / 4];
+#pragma unroll
+      for (int j = 0; j < kMaxSsParts / 4; ++j) w[j] = j < n4 ? __ldcg(p + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMaxSsParts / 4; ++j) acc += (w[j].x + w[j].y) + (w[j].z + w[j].w);
+      r = rsqrtf(acc * ep.inv_dim + ep.eps);
+    }
+    sm.rs[t] = r;
+    if (ep.kind == STB_EPI_QKV) {
+      const int pos = ep.pos_of[t0 + t];
+      sm.pos[t] = pos;
+      sm.blk[t] = ep.table[(int64_t)ep.slot_of[t0 + t] * ep.max_bps + (pos >> 4)];
+    }
+  }
+  epi_bar();
+}
+
+// RESID: the tile's per-token partial sums of squares -> ss_out[t][tile_n] (plain stores:
+// every (token, feature tile) slot is written exactly once per GEMM — no atomics)
+__device__ __forceinline__ void epi_tile_finish(const Epi& ep, EpiSmem& sm, int t0, int ntok, int tile_n) {
+  if (ep.kind != STB_EPI_RESID) return;
+  epi_bar();
+  const int i = threadIdx.x - 64;
+  for (int t = i; t < ntok; t += 128)
+    ep.ss_out[(int64_t)(t0 + t) * ep.ss_parts + tile_n] = (sm.ssw[0][t] + sm.ssw[1][t]) + (sm.ssw[2][t] + sm.ssw[3][t]);
+}
+
+// The fused epilogue for one chunk of EPI_CH tokens of a finished tile. Thread = weight row
+// (feature fl = quarter * 32 + lane of the tile); v[q] = C[t0 + c + q][f0 + fl] (fp32 sum);
+// xr[q] = x[t0 + c + q][f] for RESID (loaded a chunk ahead by the caller). All 128 epilogue
+// threads call it together (QKV synchronises through smem).
+__device__ __forceinline__ void epi_chunk(const Epi& ep, EpiSmem& sm, float* v, const float* xr, int f0, int fl,
+                                          int t0, int c, int ntile, int N, int quarter, int lane) {
+  const int ntok = min(EPI_CH, ntile - c);  // valid tokens of this chunk (>= 1)
+  const int f = f0 + fl;
+#pragma unroll
+  for (int q = 0; q < EPI_CH; ++q) v[q] *= sm.rs[c + q];  // (rs of invalid tokens: unused)
+  if (ep.kind == STB_EPI_SILU) {
+    // (gate, up) of output feature f/2 sit in lanes (2i, 2i+1); the even lane emits the
+    // first half of the chunk, the odd lane the second half
+    const bool odd = lane & 1;
+    __nv_bfloat16* __restrict__ out = ep.out;
+#pragma unroll
+    for (int q = 0; q < EPI_CH / 2; ++q) {
+      const float mine = odd ? v[EPI_CH / 2 + q] : v[q];
+      const float other = __shfl_xor_sync(0xffffffffu, odd ? v[q] : v[EPI_CH / 2 + q], 1);
+      const int tok = odd ? EPI_CH / 2 + q : q;
+      if (f < N && tok < ntok)
+        out[(int64_t)(t0 + c + tok) * ep.ldo + (f >> 1)] =
+            __float2bfloat16_rn(odd ? silu_gate(other, mine) : silu_gate(mine, other));
+    }
+  } else if (ep.kind == STB_EPI_RESID) {
+    float* __restrict__ x = ep.x;
+    __nv_bfloat16* __restrict__ out = ep.out;
+#pragma unroll
+    for (int q = 0; q < EPI_CH; ++q) {
+      const float xn = xr[q] + v[q];
+      float sq = 0.f;
+      if (q < ntok && f < N) {
+        const int64_t t = t0 + c + q;
+        x[t * ep.ldx + f] = xn;
+        out[t * ep.ldo + f] = __float2bfloat16_rn(xn);
+        sq = xn * xn;
+      }
+      sq = warp_sum(sq);
+      if (lane == 0) sm.ssw[quarter][c + q] = sq;
+    }
+  } else {  // STB_EPI_QKV: stage the chunk, then thread = (token, 8 rotation pairs)
+#pragma unroll
+    for (int q = 0; q < EPI_CH; ++q) sm.stage[q][fl] = v[q];
+    epi_bar();
+    const int i = threadIdx.x - 64;          // 0..127
+    const int tt = i >> 3, sub = i & 7;      // token in chunk, pair group (8 pairs)
+    const int d = ep.d_head, hp = d >> 1;    // rotation pairs per head
+    const int p0 = sub * 8;                  // first pair (of the tile's 64)
+    const int hl = p0 / hp, ip = p0 % hp;    // head in tile, pair index in head
+    const int fa = hl * d + ip;              // local feature of the first element
+    const int fh = f0 + hl * d;              // global first feature of the head
+    float a[8], b[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      a[j] = sm.stage[tt][fa + j];
+      b[j] = sm.stage[tt][fa + hp + j];
+    }
+    const int kind = fh < ep.q_dim ? 0 : (fh < ep.q_dim + ep.kv_dim ? 1 : 2);
+    const int gpl = hp / 8;                  // lanes sharing one head (8, 4 or 2)
+    if (kind < 2 && ep.q_norm != nullptr) {  // Qwen3 qk-norm over the head
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss = fmaf(a[j], a[j], fmaf(b[j], b[j], ss));
+      for (int o = 1; o < gpl; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float r = rsqrtf(ss / (float)d + ep.qk_eps);
+      const __nv_bfloat16* w = kind == 0 ? ep.q_norm : ep.k_norm;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a[j] *= r * __bfloat162float(w[ip + j]);
+        b[j] *= r * __bfloat162float(w[ip + hp + j]);
+      }
+    }
+    const bool valid = tt < ntok;
+    const int64_t t = t0 + c + tt;
+    const int pos = sm.pos[c + tt];
+    if (kind < 2) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float sn, cs;
+        sincosf((float)pos * ep.inv_freq[ip + j], &sn, &cs);
+        const float x1 = a[j], x2 = b[j];
+        a[j] = x1 * cs - x2 * sn;
+        b[j] = x2 * cs + x1 * sn;
+      }
+    }
+    const uint4 lo = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+    const uint4 hi = make_uint4(pack_bf16(b[0], b[1]), pack_bf16(b[2], b[3]), pack_bf16(b[4], b[5]), pack_bf16(b[6], b[7]));
+    if (valid) {
+      if (kind == 0) {
+        __nv_bfloat16* dst = ep.out + t * ep.ldo + fh + ip;
+        *reinterpret_cast<uint4*>(dst) = lo;
+        *reinterpret_cast<uint4*>(dst + hp) = hi;
+      } else {
+        const int kvh = (fh - ep.q_dim - (kind == 2 ? ep.kv_dim : 0)) / d;
+        const int blk = sm.blk[c + tt];
+        __nv_bfloat16* row = (kind == 1 ? ep.kpages : ep.vpages) + (((int64_t)blk * ep.n_kv + kvh) * 16 + (pos & 15)) * d;
+        *reinterpret_cast<uint4*>(row + kv_phys_chunk(pos & 15, ip >> 3) * 8) = lo;
+        *reinterpret_cast<uint4*>(row + kv_phys_chunk(pos & 15, (ip + hp) >> 3) * 8) = hi;
+      }
+    }
+    epi_bar();  // staging reused by the next chunk
+  }
+}
+
+// RESID: the residual values of chunk c (independent loads, issued a chunk ahead)
+__device__ __forceinline__ void load_x(const Epi& ep, float* xr, int t0, int c, int ntile, int f, int N) {
+#pragma unroll
+  for (int q = 0; q < EPI_CH; ++q)
+    xr[q] = (c + q < ntile && f < N) ? __ldcg(ep.x + (int64_t)(t0 + c + q) * ep.ldx + f) : 0.f;
+}
+
+// Epilogue warps of a fused-epilogue GEMM: whole tiles straight from TMEM; stream-K partial
+// tiles are red.added into the zeroed workspace C, and the CTA that completes a tile
+// (ticket) reads it back, runs the epilogue and clears it (C stays zero between calls).
+template <int BN>
+__device__ __forceinline__ void fused_epilogue(const Epi& ep, const Sched& sched, float* C, int64_t ldc, int M,
+                                               int N, int bn, uint32_t tmem, uint64_t* acc_full, uint64_t* acc_empty,
+                                               int* s_last, EpiSmem& sm, int quarter, int lane) {
+  SegIter it(sched);
+  int tile, k0, k1, j = 0;
+  const int fl = quarter * 32 + lane;
+  const bool resid = ep.kind == STB_EPI_RESID;
+  while (it.next(tile, k0, k1)) {
+    const int buf = j & 1;
+    mbar_wait(&acc_full[buf], (j >> 1) & 1);
+    tc_fence_after();
+    const int tile_n = tile / sched.tiles_m;
+    const int f0 = tile_n * BM;
+    const int t0 = (tile % sched.tiles_m) * bn;
+    const int f = f0 + fl;
+    const int ntile = min(bn, M - t0);  // valid tokens of the tile
+    const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
+    const bool whole = k0 == 0 && k1 == sched.kb;
+    if (whole) {
+      epi_tile_prologue(ep, sm, t0, ntile);
+      float xr[EPI_CH], xn[EPI_CH];
+      if (resid) load_x(ep, xr, t0, 0, ntile, f, N);
+      for (int c = 0; c < ntile; c += EPI_CH) {
+        if (resid) load_x(ep, xn, t0, c + EPI_CH, ntile, f, N);
+        uint32_t r[EPI_CH];
+        tmem_ld16(base + c, r);
+        tmem_ld_wait();
+        float v[EPI_CH];
+#pragma unroll
+        for (int q = 0; q < EPI_CH; ++q) v[q] = __uint_as_float(r[q]);
+        epi_chunk(ep, sm, v, xr, f0, fl, t0, c, ntile, N, quarter, lane);
+#pragma unroll
+        for (int q = 0; q < EPI_CH; ++q) xr[q] = xn[q];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      epi_tile_finish(ep, sm, t0, ntile, tile_n);
+    } else {
+      for (int c = 0; c < bn; c += EPI_CH) {
+        uint32_t r[EPI_CH];
+        tmem_ld16(base + c, r);
+        tmem_ld_wait();
+        if (f < N) {
+#pragma unroll
+          for (int q = 0; q < EPI_CH; ++q)
+            if (c + q < ntile) atomicAdd(C + (int64_t)(t0 + c + q) * ldc + f, __uint_as_float(r[q]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      __threadfence();
+      epi_bar();
+      if (threadIdx.x == 64) {
+        const int64_t kb = sched.kb, G = gridDim.x;
+        const int first = owner_of((int64_t)tile * kb, sched.units, (int)G);
+        const int last = owner_of((int64_t)(tile + 1) * kb - 1, sched.units, (int)G);
+        *s_last = atomicAdd(ep.cnt + tile, 1u) == (unsigned)(last - first);
+      }
+      epi_bar();
+      if (*s_last) {
+        __threadfence();
+        epi_tile_prologue(ep, sm, t0, ntile);
+        auto load_c = [&](float* v, int c) {
+#pragma unroll
+          for (int q = 0; q < EPI_CH; ++q)
+            v[q] = (f < N && c + q < ntile) ? __ldcg(C + (int64_t)(t0 + c + q) * ldc + f) : 0.f;
+        };
+        float v[EPI_CH], vn[EPI_CH], xr[EPI_CH], xn[EPI_CH];
+        load_c(v, 0);
+        if (resid) load_x(ep, xr, t0, 0, ntile, f, N);
+        for (int c = 0; c < ntile; c += EPI_CH) {
+          load_c(vn, c + EPI_CH);
+          if (resid) load_x(ep, xn, t0, c + EPI_CH, ntile, f, N);
+#pragma unroll
+          for (int q = 0; q < EPI_CH; ++q)  // leave the workspace zeroed
+            if (f < N && c + q < ntile) __stcg(C + (int64_t)(t0 + c + q) * ldc + f, 0.f);
+          epi_chunk(ep, sm, v, xr, f0, fl, t0, c, ntile, N, quarter, lane);
+#pragma unroll
+          for (int q = 0; q < EPI_CH; ++q) v[q] = vn[q], xr[q] = xn[q];
+        }
+        epi_tile_finish(ep, sm, t0, ntile, tile_n);
+        if (threadIdx.x == 64) ep.cnt[tile] = 0u;
+      }
+    }
+    ++j;
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_persistent(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                          float* __restrict__ C, int64_t ldc, int M, int N, Sched sched, int bn,
-                         const __nv_bfloat16* __restrict__ w_tiled) {
+                         const __nv_bfloat16* __restrict__ w_tiled, const Epi ep) {
   // w_tiled != nullptr: W in the stb_weight_tile layout, one 16 KiB bulk copy per stage
   // bn: token-tile height actually used (<= BN, multiple of 16); BN sizes the smem ring
   using CF = Cfg<BN>;
@@ -148,6 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + STAGES;   // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  EpiSmem& esm = *reinterpret_cast<EpiSmem*>(smem + STAGES * CF::STAGE + 256);
   __shared__ unsigned long long tt[5];
   const bool tracing = g_trace != nullptr;
   if (tracing && threadIdx.x == 0) tt[0] = gtime();
@@ -260,6 +551,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue warps 2..5 -> TMEM lane quarters 2,3,0,1
     pdl_wait();
     const int quarter = warp & 3;
+    if (ep.kind != 0) {
+      fused_epilogue<BN>(ep, sched, C, ldc, M, N, bn, tmem, acc_full, acc_empty, s_last, esm, quarter, lane);
+    } else {
     const bool atomic = sched.stream != 0;
     const bool zero_here = atomic && !sched.c_zeroed;
     unsigned gen = 0;
@@ -395,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (!passed && threadIdx.x == 64)  // no segment: still let the barrier complete before exiting
       while (*(volatile unsigned*)(sched.bar + 1) == gen) __nanosleep(64);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -495,6 +790,18 @@ unsigned* grid_barrier() {
   return bar;
 }
 
+// stream-K tile tickets of the fused-epilogue path: zeroed once, reset by each tile's finisher
+constexpr int kMaxTickets = 1 << 14;
+unsigned* tile_tickets() {
+  static unsigned* cnt = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cudaMalloc(&cnt, kMaxTickets * sizeof(unsigned)) == cudaSuccess)
+      cudaMemset(cnt, 0, kMaxTickets * sizeof(unsigned));
+  });
+  return cnt;
+}
+
 int bn_template(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
 
 // Token-tile height and schedule for an M x N product.
@@ -537,7 +844,7 @@ Plan plan(int M, int N, int sms) {
 
 template <int BN>
 int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
-           int mode, int flags, cudaStream_t st) {
+           int mode, int flags, cudaStream_t st, const Epi& ep) {
   using CF = Cfg<BN>;
   CUtensorMap tw, tx;
   const bool tiled = (flags & STB_GEMM_W_TILED) != 0;
@@ -576,10 +883,23 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr_set = true;
   }
+  if (ep.kind != 0 && s.stream && (C == nullptr || ep.cnt == nullptr))
+    return fail(STB_EINVAL, "gemm_bf16_fused: the stream-K schedule needs the zeroed fp32 workspace");
+  if (ep.kind != 0 && s.stream && s.tiles > kMaxTickets)
+    return fail(STB_EINVAL, "gemm_bf16_fused: %d stream-K tiles exceed the ticket array", s.tiles);
   cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), CF::SMEM, st, tw, tx, C, ldc, M, N, s, bn,
-                           tiled ? (const __nv_bfloat16*)W : (const __nv_bfloat16*)nullptr);
+                           tiled ? (const __nv_bfloat16*)W : (const __nv_bfloat16*)nullptr, ep);
   if (e != cudaSuccess) return fail(STB_ECUDA, "gemm_bf16 launch: %s", cudaGetErrorString(e));
   return STB_OK;
+}
+
+int dispatch(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
+             int split_k, int flags, cudaStream_t st, const Epi& ep) {
+  if (M <= 16) return launch<16>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, ep);
+  if (M <= 32) return launch<32>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, ep);
+  if (M <= 64) return launch<64>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, ep);
+  if (M <= 128) return launch<128>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, ep);
+  return launch<256>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, ep);
 }
 
 }  // namespace
@@ -660,9 +980,68 @@ extern "C" int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t 
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
     return fail(STB_EINVAL, "gemm_bf16: operands must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  if (M <= 16) return launch<16>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
-  if (M <= 32) return launch<32>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
-  if (M <= 64) return launch<64>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
-  if (M <= 128) return launch<128>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
-  return launch<256>(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st);
+  Epi none;
+  memset(&none, 0, sizeof(none));
+  return dispatch(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, none);
+}
+
+extern "C" int stb_gemm_bf16_fused(const void* A, int64_t lda, const void* W, int64_t ldw, float* work,
+                                   int64_t ldwork, int M, int N, int K, int flags, const stb_gemm_epi* e,
+                                   void* stream) {
+  if (M <= 0 || N <= 0) return STB_OK;
+  if (!e || e->kind < STB_EPI_SILU || e->kind > STB_EPI_RESID) return fail(STB_EINVAL, "gemm_bf16_fused: bad epilogue");
+  if (K <= 0 || K % 8 != 0) return fail(STB_EINVAL, "gemm_bf16: K must be a positive multiple of 8");
+  if (lda % 8 != 0 || (ldw % 8 != 0 && !(flags & STB_GEMM_W_TILED)))
+    return fail(STB_EINVAL, "gemm_bf16: row strides must be multiples of 8");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
+    return fail(STB_EINVAL, "gemm_bf16: operands must be 16-byte aligned");
+  Epi ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.kind = e->kind;
+  ep.ss_in = e->ss_in;
+  ep.ss_parts = e->ss_parts;
+  ep.inv_dim = e->inv_dim;
+  ep.eps = e->eps;
+  ep.out = (__nv_bfloat16*)e->out;
+  ep.ldo = e->ldo;
+  ep.cnt = tile_tickets();
+  if (!ep.cnt) return fail(STB_ENOMEM, "gemm_bf16_fused: tickets");
+  if (e->kind == STB_EPI_SILU && N % 2) return fail(STB_EINVAL, "gemm_bf16_fused: SiLU-gate needs even N");
+  if (e->ss_in && (e->ss_parts <= 0 || e->ss_parts % 4 || e->ss_parts > kMaxSsParts ||
+                   (reinterpret_cast<uintptr_t>(e->ss_in) & 15)))
+    return fail(STB_EINVAL, "gemm_bf16_fused: ss_in needs 16-byte rows of ss_parts (multiple of 4, <= %d)",
+                kMaxSsParts);
+  if (e->kind == STB_EPI_RESID) {
+    if (!e->x || !e->out || !e->ss_out) return fail(STB_EINVAL, "gemm_bf16_fused: RESID needs x, out, ss_out");
+    if (e->ss_parts < (N + BM - 1) / BM || e->ss_parts % 4)
+      return fail(STB_EINVAL, "gemm_bf16_fused: RESID needs ss_parts >= ceil(N/128), a multiple of 4");
+    ep.x = e->x;
+    ep.ldx = e->ldx;
+    ep.ss_out = e->ss_out;
+  }
+  if (e->kind == STB_EPI_QKV) {
+    stb_kv_pool* p = e->pool;
+    if (!p || e->layer < 0 || e->layer >= p->layers) return fail(STB_EINVAL, "gemm_bf16_fused: QKV needs a pool layer");
+    if ((e->q_norm == nullptr) != (e->k_norm == nullptr)) return fail(STB_EINVAL, "gemm_bf16_fused: q_norm/k_norm");
+    ep.d_head = p->d_head;
+    ep.n_kv = p->n_kv;
+    ep.q_dim = e->n_q * p->d_head;
+    ep.kv_dim = p->n_kv * p->d_head;
+    if (ep.d_head % 32 || ep.d_head > 128 || ep.q_dim % BM || ep.kv_dim % BM || N != ep.q_dim + 2 * ep.kv_dim)
+      return fail(STB_EINVAL, "gemm_bf16_fused: QKV needs d_head in {32,64,128} and 128-aligned q/kv widths");
+    void *kp, *vp;
+    stb_kv_layer_ptrs(p, e->layer, &kp, &vp);
+    ep.kpages = (__nv_bfloat16*)kp;
+    ep.vpages = (__nv_bfloat16*)vp;
+    ep.table = p->dev_table;
+    ep.max_bps = p->max_bps;
+    ep.slot_of = e->slot_of;
+    ep.pos_of = e->pos_of;
+    ep.inv_freq = stb_rope_inv_freq(e->rope_theta, p->d_head);
+    if (!ep.inv_freq) return fail(STB_ENOMEM, "gemm_bf16_fused: inv_freq");
+    ep.q_norm = (const __nv_bfloat16*)e->q_norm;
+    ep.k_norm = (const __nv_bfloat16*)e->k_norm;
+    ep.qk_eps = e->qk_eps;
+  }
+  return dispatch(A, lda, W, ldw, work, ldwork, M, N, K, 0, flags | STB_GEMM_C_ZEROED, (cudaStream_t)stream, ep);
 }

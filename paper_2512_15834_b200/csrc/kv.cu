@@ -192,6 +192,23 @@ __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* _
 }
 
 // ------------------------------------------------------------------- C ABI
+// inverse frequencies are a pure function of (theta, d_head): one cached device table per pair
+const float* stb_rope_inv_freq(float rope_theta, int d_head) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<float, int>, float*>> cache;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& e : cache)
+    if (e.first.first == rope_theta && e.first.second == d_head) return e.second;
+  const int half = d_head / 2;
+  std::vector<float> h(half);
+  for (int i = 0; i < half; ++i) h[i] = (float)(1.0 / pow((double)rope_theta, (2.0 * i) / d_head));
+  float* inv = nullptr;
+  if (cudaMalloc(&inv, half * sizeof(float)) != cudaSuccess) return nullptr;
+  cudaMemcpy(inv, h.data(), half * sizeof(float), cudaMemcpyHostToDevice);
+  cache.push_back({{rope_theta, d_head}, inv});
+  return inv;
+}
+
 extern "C" {
 
 const char* stb_last_error(void) { return g_err.c_str(); }
@@ -395,23 +412,8 @@ int stb_qkv_norm_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out,
   if ((q_norm == nullptr) != (k_norm == nullptr)) return fail(STB_EINVAL, "qkv_rope_commit: q_norm and k_norm go together");
   if (!p || layer < 0 || layer >= p->layers) return fail(STB_EINVAL, "qkv_rope_commit: bad layer");
   if (n <= 0) return STB_OK;
-  // inverse frequencies are a pure function of (theta, d_head): cache one device table per pair
-  static std::mutex mu;
-  static std::vector<std::pair<std::pair<float, int>, float*>> cache;
-  float* inv = nullptr;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    for (auto& e : cache)
-      if (e.first.first == rope_theta && e.first.second == p->d_head) inv = e.second;
-    if (!inv) {
-      int half = p->d_head / 2;
-      std::vector<float> h(half);
-      for (int i = 0; i < half; ++i) h[i] = (float)(1.0 / pow((double)rope_theta, (2.0 * i) / p->d_head));
-      if (cudaMalloc(&inv, half * sizeof(float)) != cudaSuccess) return fail(STB_ENOMEM, "qkv_rope_commit: inv_freq");
-      cudaMemcpy(inv, h.data(), half * sizeof(float), cudaMemcpyHostToDevice);
-      cache.push_back({{rope_theta, p->d_head}, inv});
-    }
-  }
+  const float* inv = stb_rope_inv_freq(rope_theta, p->d_head);
+  if (!inv) return fail(STB_ENOMEM, "qkv_rope_commit: inv_freq");
   void *kp, *vp;
   stb_kv_layer_ptrs(p, layer, &kp, &vp);
   if (p->d_head % 16 != 0) return fail(STB_EINVAL, "qkv_rope_commit: d_head must be a multiple of 16");

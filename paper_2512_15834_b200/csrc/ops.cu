@@ -45,6 +45,37 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
+// embed + the first layer's fused-norm inputs: x = embed row (fp32), xb = bf16(x),
+// ss[t][0] = sum x^2, ss[t][p] = 0 for the other partial slots
+__global__ void embed_prep_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
+                                  float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ss,
+                                  int parts, int d) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const __nv_bfloat16* row = table + (int64_t)ids[t] * d;
+  float acc = 0.f;
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + c);
+    *reinterpret_cast<uint4*>(xb + (int64_t)t * d + c) = v;  // bf16(x) == the embedding row
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float f[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 p = __bfloat1622float2(h[j]);
+      f[2 * j] = p.x;
+      f[2 * j + 1] = p.y;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = fmaf(f[j], f[j], acc);
+    *reinterpret_cast<float4*>(x + (int64_t)t * d + c) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(x + (int64_t)t * d + c + 4) = make_float4(f[4], f[5], f[6], f[7]);
+  }
+  acc = block_sum(acc, red);
+  for (int j = threadIdx.x; j < parts; j += blockDim.x) ss[(int64_t)t * parts + j] = j == 0 ? acc : 0.f;
+}
+
 // one CTA per row, the row held in registers (VPT float4 per thread, blockDim*4*VPT == d):
 // x (+)= delta; y = bf16(x * rsqrt(mean(x^2) + eps) * w). One global read of x (and
 // delta), one write of x and y, a single block reduction.
@@ -295,6 +326,17 @@ int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, voi
   if (d % 8) return fail(STB_EINVAL, "embed: d must be a multiple of 8");
   launch_k(embed_kernel, dim3(n), dim3(128), 0, (cudaStream_t)stream, ids, (const __nv_bfloat16*)table, x, n, d);
   STB_CHECK_LAUNCH("embed");
+  return STB_OK;
+}
+
+int stb_embed_prep(const int32_t* ids, const void* table, float* x, void* xb, float* ss, int ss_parts, int n, int d,
+                   void* stream) {
+  if (n <= 0) return STB_OK;
+  if (d % 8) return fail(STB_EINVAL, "embed_prep: d must be a multiple of 8");
+  if (ss_parts < 1) return fail(STB_EINVAL, "embed_prep: ss_parts >= 1");
+  launch_k(embed_prep_kernel, dim3(n), dim3(128), 0, (cudaStream_t)stream, ids, (const __nv_bfloat16*)table, x,
+           (__nv_bfloat16*)xb, ss, ss_parts, d);
+  STB_CHECK_LAUNCH("embed_prep");
   return STB_OK;
 }
 

@@ -33,6 +33,9 @@ struct stb_kv_pool {
 // swizzle) and consumed in place.
 __host__ __device__ __forceinline__ int kv_phys_chunk(int row, int c) { return (c & ~7) | ((c ^ row) & 7); }
 
+// RoPE inverse frequencies 1/theta^(2i/d_head) (fp32 from a float64 pow), one cached device
+// table per (theta, d_head) — shared by the rope/commit kernel and the fused QKV epilogue
+const float* stb_rope_inv_freq(float rope_theta, int d_head);
 extern "C" int stb_pool_geometry(const stb_kv_pool* p, int* n_kv, int* d_head);
 extern "C" int stb_kv_layer_ptrs(const stb_kv_pool* pool, int layer, void** k_pages, void** v_pages);
 // K2 tensor-core path (attn_prefill_tc.cu), dispatched from stb_attn_prefill

@@ -4,9 +4,16 @@ A step packs T tokens: first the B_dec decode sequences (one token each), then
 S append-prefill runs (prefill chunks, verify passes, tool-output ingests),
 each a contiguous token range. Per layer:
 
-  rmsnorm -> K5 QKV GEMM -> fused RoPE + K1 commit into the paged pool ->
+  rmsnorm -> K5 QKV GEMM -> fused (qk-norm +) RoPE + K1 commit into the paged pool ->
   K3 decode attention (rows [0, B_dec)) + K2 append-prefill (rows [B_dec, T)) ->
   K5 O GEMM -> residual + rmsnorm -> K5 gate-up GEMM -> SiLU*up -> K5 down GEMM
+
+(with STB200_FUSED=1: five launches per layer, every row op inside the GEMM that
+produces its input; the norm weights are folded into the QKV / gate-up weights once
+at load, and the 1/rms of each row — known only after the whole row is reduced —
+scales the GEMM's finished sums. Parity-green but measured slower than the default
+separate-kernel path: rmsnorm -> QKV -> RoPE+commit -> attention -> O -> add+rmsnorm
+-> gate-up [SiLU fused for whole-tile schedules] -> down -> add+rmsnorm.)
 
 then the final norm on the R sampled rows only, the K5 LM-head GEMM on those
 rows, and script-forced greedy sampling. Every launch goes through the C ABI
@@ -52,6 +59,31 @@ def interleave_gate_up(w: torch.Tensor, d_ff: int) -> None:
 GEMM_W_TILED = 4    # include/stb200.h STB_GEMM_W_TILED
 CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
 PROJECTIONS = ("wqkv", "wo", "w_gate_up", "w_down")
+
+
+class GemmEpi(C.Structure):
+    """include/stb200.h stb_gemm_epi."""
+
+    _fields_ = [("kind", C.c_int), ("ss_in", C.c_void_p), ("ss_parts", C.c_int), ("inv_dim", C.c_float),
+                ("eps", C.c_float),
+                ("out", C.c_void_p), ("ldo", C.c_int64), ("x", C.c_void_p), ("ldx", C.c_int64),
+                ("ss_out", C.c_void_p), ("pool", C.c_void_p), ("layer", C.c_int), ("n_q", C.c_int),
+                ("slot_of", C.c_void_p), ("pos_of", C.c_void_p), ("rope_theta", C.c_float),
+                ("q_norm", C.c_void_p), ("k_norm", C.c_void_p), ("qk_eps", C.c_float)]
+
+
+EPI_SILU, EPI_QKV, EPI_RESID = 1, 2, 3   # include/stb200.h STB_EPI_*
+
+
+def fusable(shape: ModelShape) -> bool:
+    """The fused QKV epilogue needs 128-aligned q / kv widths and d_head <= 128."""
+    return shape.d_head in (32, 64, 128) and shape.q_dim % 128 == 0 and shape.kv_dim % 128 == 0
+
+
+def fold_norm(w: torch.Tensor, g: torch.Tensor) -> None:
+    """In place: W[n][k] <- bf16(W[n][k] * g[k]) (fp32 product): the RMSNorm weight of the
+    GEMM's input folded into the GEMM (the fused epilogue applies only 1/rms)."""
+    w.copy_((w.float() * g.float()[None, :]).to(w.dtype))
 
 
 class TiledWeight:
@@ -172,7 +204,18 @@ class Decoder:
             if not isinstance(gu, TiledWeight):  # (gate, up) pairs in adjacent rows: fused SiLU epilogue
                 interleave_gate_up(gu, shape.d_ff)
             del gu
-        # projections in the tiled HBM layout (once; a shared dict is converted in place)
+        # fused epilogues: correct (tests/test_gpu_parity.py) but measured slower on B200 — the
+        # epilogue's global round trips sit on the GEMM's critical path; opt in
+        self.fused = os.environ.get("STB200_FUSED", "") == "1" and fusable(shape)
+        # projections in the tiled HBM layout (once; a shared dict is converted in place —
+        # the first Decoder over a dict decides whether the norm weights are folded in)
+        if "_stb_fused" not in weights:
+            weights["_stb_fused"] = self.fused
+            for i in range(shape.layers):
+                if self.fused:
+                    fold_norm(weights[f"l{i}.wqkv"], weights[f"l{i}.attn_norm"])
+                    fold_norm(weights[f"l{i}.w_gate_up"], weights[f"l{i}.mlp_norm"])
+        self.fused = bool(weights["_stb_fused"])
         for name in [f"l{i}.{p}" for i in range(shape.layers) for p in PROJECTIONS] + ["lm_head"]:
             if not isinstance(weights[name], TiledWeight):
                 weights[name] = TiledWeight(weights[name])
@@ -222,6 +265,9 @@ class Decoder:
             self.proj = torch.zeros(cap, s.d_model, dtype=f32, device=dev)
             self.gu = torch.zeros(cap, 2 * s.d_ff, dtype=f32, device=dev)
             self.act = torch.empty(cap, s.d_ff, dtype=bf, device=dev)
+            # fused path: per-row partial sums of squares (one per 128-feature tile of d) of
+            # every norm input (2 per layer + 1)
+            self.ss = torch.zeros(2 * s.layers + 1, cap, -(-s.d_model // 512) * 4, dtype=f32, device=dev)
             self._cap_t = cap
             self._dirty.update(qkv=0, proj=0, gu=0)
             self.graphs.clear()  # captured graphs point at the old buffers
@@ -347,6 +393,8 @@ class Decoder:
 
     def _launch(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
                 dec_bytes: int) -> None:
+        if self.fused:
+            return self._launch_fused(m, T, R, B, S, max_q, max_ctx, dec_bytes)
         s, w = self.shape, self.w
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         d = s.d_model
@@ -401,6 +449,75 @@ class Decoder:
              _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)
         if clear:
             self._cleared("logits", R)
+
+    def _attention(self, call, m, i: int, T: int, B: int, S: int, max_q: int, max_ctx: int, dec_bytes: int, st):
+        s = self.shape
+        if B:
+            ev = self._tick()
+            call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
+                 _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
+            self._tock("attn_decode", ev, dec_bytes)
+        if S:
+            ev = self._tick()
+            call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
+                 _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q, st)
+            self._tock("attn_prefill", ev, self._pre_flops)
+
+    def _launch_fused(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
+                      dec_bytes: int) -> None:
+        """Five launches per layer; row ops live in the GEMM epilogues (module docstring)."""
+        s, w = self.shape, self.w
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        d = s.d_model
+        x, xb, ss = self.x, self.h, self.ss
+        ld_ss = ss.stride(0)
+        call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
+        for _ in range(2):  # empty pairs: the timers' own overhead, subtracted by the reader
+            self._tock("event_overhead", self._tick(), 0)
+        parts = ss.shape[2]
+        call("stb_embed_prep", _p(m["ids"]), _p(w["embed"]), _p(x), _p(xb), _p(ss), parts, T, d, st)
+        inv_d = 1.0 / d
+        ss_at = lambda j: ss.data_ptr() + 4 * j * ld_ss  # noqa: E731
+        for i in range(s.layers):
+            e = GemmEpi(kind=EPI_QKV, ss_in=ss_at(2 * i), ss_parts=parts, inv_dim=inv_d, eps=s.rms_eps,
+                        out=self.q.data_ptr(), ldo=self.q.stride(0), pool=self.pool.h.value, layer=i, n_q=s.n_q, slot_of=m["slot_of"],
+                        pos_of=m["pos"], rope_theta=s.rope_theta,
+                        q_norm=w[f"l{i}.q_norm"].data_ptr() if s.qk_norm else None,
+                        k_norm=w[f"l{i}.k_norm"].data_ptr() if s.qk_norm else None, qk_eps=s.rms_eps)
+            self.gemm_fused(xb[:T], w[f"l{i}.wqkv"], self.qkv, e, st, "wqkv")
+            self._attention(call, m, i, T, B, S, max_q, max_ctx, dec_bytes, st)
+            e = GemmEpi(kind=EPI_RESID, out=xb.data_ptr(), ldo=xb.stride(0), x=x.data_ptr(), ldx=x.stride(0),
+                        ss_out=ss_at(2 * i + 1), ss_parts=parts)
+            self.gemm_fused(self.attn[:T], w[f"l{i}.wo"], self.proj, e, st, "wo")
+            e = GemmEpi(kind=EPI_SILU, ss_in=ss_at(2 * i + 1), ss_parts=parts, inv_dim=inv_d, eps=s.rms_eps,
+                        out=self.act.data_ptr(), ldo=self.act.stride(0))
+            self.gemm_fused(xb[:T], w[f"l{i}.w_gate_up"], self.gu, e, st, "w_gate_up")
+            e = GemmEpi(kind=EPI_RESID, out=xb.data_ptr(), ldo=xb.stride(0), x=x.data_ptr(), ldx=x.stride(0),
+                        ss_out=ss_at(2 * i + 2), ss_parts=parts)
+            self.gemm_fused(self.act[:T], w[f"l{i}.w_down"], self.proj, e, st, "w_down")
+        rows = self.rows[:R]
+        call("stb_gather_rmsnorm", _p(x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows), R, d, s.rms_eps, st)
+        self.gemm(rows, w["lm_head"], "logits", st, "lm_head")
+        clear = 0 if self.keep_logits or not self._stream_cache[(R, s.vocab, d)] else 1
+        call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
+             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)
+        if clear:
+            self._cleared("logits", R)
+
+    def gemm_fused(self, a: torch.Tensor, wt: "TiledWeight", work: torch.Tensor, epi: GemmEpi, st, tag: str):
+        """K5 with a fused epilogue; `work` is a zeroed fp32 accumulator the kernel leaves zeroed."""
+        M, K = a.shape
+        N = wt.N
+        if "stb_gemm_bf16_fused" in _SKIP or f"gemm:{tag}" in _SKIP:
+            return
+        ev = self._tick()
+        lib.call("stb_gemm_bf16_fused", _p(a), a.stride(0), _p(wt), 0, _p(work), work.stride(0), M, N, K,
+                 GEMM_W_TILED, C.byref(epi), st)
+        if ev is not None:
+            if M <= 128:
+                self._tock("gemm_decode", ev, N * K * 2 + M * K * 2 + M * N * 4)
+            else:
+                self._tock("gemm_prefill", ev, 2 * M * N * K)
 
     def _cleared(self, name: str, rows: int) -> None:
         if rows >= self._dirty[name]:

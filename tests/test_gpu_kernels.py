@@ -136,6 +136,132 @@ def test_gemm_w_tiled(lib, M, N, K):
         assert rel(act, want) < 1e-2
 
 
+def _epi(**kw):
+    from paper_2512_15834_b200.runtime.decoder import GemmEpi
+
+    return GemmEpi(**kw)
+
+
+@pytest.mark.parametrize("M", [1, 32, 100, 300])
+def test_gemm_fused_silu_resid(lib, M):
+    """STB_EPI_SILU with the input-row RMSNorm scale, and STB_EPI_RESID, vs torch fp32; the
+    workspace is left zeroed (stream-K fixups clear what they reduce)."""
+    from paper_2512_15834_b200.runtime.decoder import TiledWeight
+
+    K, F, D = 1024, 640, 512
+    g = torch.Generator(device="cuda").manual_seed(M)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    ss = (a.float() ** 2).sum(1) * torch.rand(M, device="cuda", generator=g) * 2
+    wgu = TiledWeight((0.05 * torch.randn(2 * F, K, device="cuda", generator=g)).to(torch.bfloat16))
+    work = torch.zeros(M, 2 * F, device="cuda")
+    act = torch.full((M, F), float("nan"), device="cuda").to(torch.bfloat16)
+    ss4 = torch.zeros(M, 4, device="cuda")  # partial sums of squares: the total in slot 0
+    ss4[:, 0] = ss
+    e = _epi(kind=1, ss_in=ss4.data_ptr(), ss_parts=4, inv_dim=1.0 / K, eps=1e-5, out=act.data_ptr(), ldo=F)
+    fn = lib.load().stb_gemm_bf16_fused
+    # M <= 128: stream-K (every tile split over ~16 CTAs: the ticket fixup); M = 300: whole tiles
+    rc = fn(P(a), K, P(wgu), 0, P(work), 2 * F, M, 2 * F, K, 4, C.byref(e), stream())
+    assert rc == 0, lib.load().stb_last_error()
+    full = a.float() @ TiledWeight_ref(wgu).T
+    full = full * torch.rsqrt(ss / K + 1e-5)[:, None]
+    want = torch.nn.functional.silu(full[:, 0::2]) * full[:, 1::2]
+    torch.cuda.synchronize()
+    assert rel(act, want) < 1e-2
+    assert not work.any()
+    # RESID
+    wo = (0.05 * torch.randn(D, K, device="cuda", generator=g)).to(torch.bfloat16)
+    two = TiledWeight(wo)
+    x = torch.randn(M, D, device="cuda", generator=g)
+    x0 = x.clone()
+    xb = torch.empty(M, D, device="cuda", dtype=torch.bfloat16)
+    sso = torch.full((M, D // 128), float("nan"), device="cuda")
+    workd = torch.zeros(M, D, device="cuda")
+    e = _epi(kind=3, out=xb.data_ptr(), ldo=D, x=x.data_ptr(), ldx=D, ss_out=sso.data_ptr(), ss_parts=D // 128)
+    rc = fn(P(a), K, P(two), 0, P(workd), D, M, D, K, 4, C.byref(e), stream())
+    assert rc == 0, lib.load().stb_last_error()
+    xr = x0 + a.float() @ wo.float().T
+    torch.cuda.synchronize()
+    assert rel(x, xr) < 1e-5
+    assert torch.equal(xb, x.to(torch.bfloat16))
+    assert torch.allclose(sso, (xr ** 2).view(M, D // 128, 128).sum(2), rtol=1e-4)  # per 128-feature tile
+    assert not workd.any()
+
+
+def TiledWeight_ref(tw):
+    """fp32 [N][K] from a TiledWeight (inverse of stb_weight_tile)."""
+    N, K = tw.N, tw.K
+    nt, kt = -(-N // 128), -(-K // 64)
+    t = tw.t.view(nt, kt, 128, 8, 8)
+    r = torch.arange(128, device="cuda").view(128, 1)
+    inv = torch.arange(8, device="cuda").view(1, 8) ^ (r & 7)   # logical chunk -> physical (an involution)
+    t = torch.gather(t, 3, inv.view(1, 1, 128, 8, 1).expand(nt, kt, 128, 8, 8))
+    return t.permute(0, 2, 1, 3, 4).reshape(nt * 128, kt * 64)[:N, :K].float()
+
+
+@pytest.mark.parametrize("qk_norm", [False, True])
+@pytest.mark.parametrize("d_head,n_q,n_kv", [(128, 8, 2), (64, 4, 2)])
+@pytest.mark.parametrize("M", [3, 32, 200])
+def test_gemm_fused_qkv(lib, qk_norm, d_head, n_q, n_kv, M):
+    """STB_EPI_QKV: input-row RMSNorm scale, (qk-norm,) RoPE, q out and K/V commit into the
+    pool — equal to the unfused GEMM + stb_qkv_norm_rope_commit."""
+    from paper_2512_15834_b200.runtime.decoder import TiledWeight
+
+    shape = ModelShape("t", 1, 512, n_q, n_kv, d_head, 64, 64, rope_theta=10000.0, rms_eps=1e-6, qk_norm=qk_norm)
+    K, N = 512, (n_q + 2 * n_kv) * d_head
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + d_head)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    ss = (a.float() ** 2).sum(1)
+    w = (0.05 * torch.randn(N, K, device="cuda", generator=g)).to(torch.bfloat16)
+    tw = TiledWeight(w)
+    qn = (1.0 + 0.1 * torch.randn(d_head, device="cuda", generator=g)).to(torch.bfloat16)
+    kn = (1.0 + 0.1 * torch.randn(d_head, device="cuda", generator=g)).to(torch.bfloat16)
+    ctx0 = 40
+    pos = torch.arange(ctx0, ctx0 + M, dtype=torch.int32, device="cuda")
+    slot_of = torch.zeros(M, dtype=torch.int32, device="cuda")
+    pools = []
+    for _ in range(2):
+        pool = _pool(lib, shape)
+        pool.reserve(0, ctx0 + M)
+        pool.sync(torch.cuda.current_stream().cuda_stream)
+        pools.append(pool)
+    # fused
+    q1 = torch.zeros(M, n_q * d_head, device="cuda", dtype=torch.bfloat16)
+    work = torch.zeros(M, N, device="cuda")
+    ss4 = torch.zeros(M, 4, device="cuda")
+    ss4[:, 1] = ss
+    e = _epi(kind=2, ss_in=ss4.data_ptr(), ss_parts=4, inv_dim=1.0 / K, eps=1e-6, out=q1.data_ptr(), ldo=n_q * d_head,
+             pool=pools[0].h.value, layer=0, n_q=n_q, slot_of=slot_of.data_ptr(), pos_of=pos.data_ptr(),
+             rope_theta=10000.0, q_norm=qn.data_ptr() if qk_norm else None, k_norm=kn.data_ptr() if qk_norm else None,
+             qk_eps=1e-6)
+    rc = lib.load().stb_gemm_bf16_fused(P(a), K, P(tw), 0, P(work), N, M, N, K, 4, C.byref(e), stream())
+    assert rc == 0, lib.load().stb_last_error()
+    # unfused reference: scaled fp32 GEMM -> stb_qkv_norm_rope_commit
+    qkv = (a.float() @ w.float().T) * torch.rsqrt(ss / K + 1e-6)[:, None]
+    q2 = torch.zeros_like(q1)
+    lib.call("stb_qkv_norm_rope_commit", pools[1].h, 0, P(qkv), P(q2), P(slot_of), P(pos), M, n_q, 10000.0,
+             P(qn) if qk_norm else None, P(kn) if qk_norm else None, 1e-6, 0, stream())
+    torch.cuda.synchronize()
+    assert not work.any()
+    assert rel(q1, q2) < 1e-2
+    k1, v1 = _dense_kv(pools[0], 0, 0, ctx0 + M, shape)
+    k2, v2 = _dense_kv(pools[1], 0, 0, ctx0 + M, shape)
+    assert rel(k1[ctx0:], k2[ctx0:]) < 1e-2 and rel(v1[ctx0:], v2[ctx0:]) < 1e-2
+
+
+def test_embed_prep(lib):
+    V, d, n, parts = 300, 512, 37, 4
+    table = torch.randn(V, d, device="cuda").to(torch.bfloat16)
+    ids = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32)
+    x = torch.empty(n, d, device="cuda")
+    xb = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    ss = torch.full((n + 3, parts), 7.0, device="cuda")
+    lib.call("stb_embed_prep", P(ids), P(table), P(x), P(xb), P(ss), parts, n, d, stream())
+    ref = table[ids.long()].float()
+    assert torch.equal(x, ref) and torch.equal(xb, table[ids.long()])
+    assert torch.allclose(ss[:n, 0], (ref ** 2).sum(1), rtol=1e-5)
+    assert not ss[:n, 1:].any() and (ss[n:] == 7.0).all()
+
+
 def _pool(lib, shape, nb=256, slots=64, bps=512):
     from paper_2512_15834_b200.runtime.decoder import KVPool
 

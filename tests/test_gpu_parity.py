@@ -121,6 +121,20 @@ def test_fleet_parity_qwen3_qknorm(golden):
     pair.check()
 
 
+@pytest.mark.parametrize("shape", [TINY, QWEN3_MINI], ids=lambda s: s.name)
+@pytest.mark.parametrize("case", ["full_hit", "two_turn_mixed"])
+def test_timeline_parity_fused_epilogues(golden, monkeypatch, shape, case):
+    """STB200_FUSED=1: every row op inside its GEMM (norm weights folded, 1/rms applied to
+    the reduced sums, RoPE + KV commit in the QKV epilogue) — same goldens and tolerances."""
+    monkeypatch.setenv("STB200_FUSED", "1")
+    pair = Pair(shape)
+    got, eng = S.run_timeline(API, case, pair.gpu)
+    ora, _ = S.run_timeline(API, case, pair.oracle)
+    assert eng.rt.dec.fused
+    assert got == golden["timelines"][case] and ora == golden["timelines"][case]
+    pair.check()
+
+
 def test_default_engine_is_native():
     """`EngineSim(sim, config)` builds the CUDA runtime; its kernels really ran."""
     from paper_2512_15834_b200 import EngineConfig, EngineSim, Simulator

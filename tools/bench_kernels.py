@@ -88,6 +88,58 @@ def bench_gemm(shape, M, split=0, layout="tiled"):
     return out
 
 
+def bench_fused(shape, M):
+    """Decode/prefill projections with their fused epilogues (stb_gemm_bf16_fused) vs the plain
+    GEMM on the same tiled weights."""
+    from paper_2512_15834_b200.runtime.decoder import GemmEpi, KVPool, TiledWeight
+
+    s = shape
+    d, F = s.d_model, s.d_ff
+    pool = KVPool(s.with_layers(1), M // 16 + 64, 4, M // 16 + 8)
+    pool.reserve(0, M + 16)
+    pool.sync(torch.cuda.current_stream().cuda_stream)
+    slot_of = torch.zeros(M, dtype=torch.int32, device="cuda")
+    pos = torch.arange(M, dtype=torch.int32, device="cuda")
+    parts = d // 128
+    ss = torch.rand(M, parts, device="cuda") * 128
+    sso = torch.empty(M, parts, device="cuda")
+    x = torch.randn(M, d, device="cuda")
+    xb = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
+    q = torch.empty(M, s.q_dim, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    cases = {
+        "qkv": (s.q_dim + 2 * s.kv_dim, d, GemmEpi(kind=2, ss_in=ss.data_ptr(), ss_parts=parts, inv_dim=1.0 / d,
+                                                   eps=1e-5,
+                                                   out=q.data_ptr(), ldo=s.q_dim, pool=pool.h.value, layer=0,
+                                                   n_q=s.n_q, slot_of=slot_of.data_ptr(), pos_of=pos.data_ptr(),
+                                                   rope_theta=s.rope_theta)),
+        "o": (d, s.q_dim, GemmEpi(kind=3, out=xb.data_ptr(), ldo=d, x=x.data_ptr(), ldx=d, ss_out=sso.data_ptr(),
+                                  ss_parts=parts)),
+        "gate_up": (2 * F, d, GemmEpi(kind=1, ss_in=ss.data_ptr(), ss_parts=parts, inv_dim=1.0 / d, eps=1e-5,
+                                      out=act.data_ptr(), ldo=F)),
+        "down": (d, F, GemmEpi(kind=3, out=xb.data_ptr(), ldo=d, x=x.data_ptr(), ldx=d, ss_out=sso.data_ptr(),
+                               ss_parts=parts)),
+    }
+    fn = lib.load().stb_gemm_bf16_fused
+    tot = [0.0, 0.0]
+    for name, (N, K, e) in cases.items():
+        copies = max(2, int(math.ceil(400e6 / (N * K * 2))))
+        # the model's value ranges (weights N(0, 0.02)): silu/rsqrt stay on their fast paths
+        tw = [TiledWeight((0.02 * torch.randn(N, K, device="cuda")).to(torch.bfloat16)) for _ in range(copies)]
+        a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+        work = torch.zeros(M, N, device="cuda")
+        us_f = time_it(lambda i: fn(P(a), K, P(tw[i % copies]), 0, P(work), N, M, N, K, 4, C.byref(e), st()))
+        flags = 1 if lib.load().stb_gemm_is_stream(M, N, K) else 0
+        us_p = time_it(lambda i: lib.call("stb_gemm_bf16", P(a), K, P(tw[i % copies]), 0, P(work), N, M, N, K, 0,
+                                          flags | 4, st()))
+        work.zero_()
+        tot[0] += us_f
+        tot[1] += us_p
+        print(f"  M={M:5d} {name:8s} N={N:6d} K={K:5d}: fused {us_f:8.1f} us   plain {us_p:8.1f} us")
+        del tw
+    print(f"  M={M}: fused sum {tot[0]:.1f} us, plain sum {tot[1]:.1f} us")
+
+
 def bench_attn(shape, B, ctx, reps=4):
     from paper_2512_15834_b200.runtime.decoder import KVPool
 
@@ -220,6 +272,9 @@ def main():
     if "gemm" in args.what:
         for M in [int(x) for x in args.M.split(",")]:
             bench_gemm(shape, M, args.split, args.layout)
+    if "fused" in args.what:
+        for M in [int(x) for x in args.M.split(",")]:
+            bench_fused(shape, M)
     if "sweep" in args.what:
         bench_gemm_sweep()
     if "pdl" in args.what:
