@@ -271,6 +271,17 @@ constexpr int kMaxB = 1024;
 constexpr int kChunkPages = 2;  // pages (16 keys each) per online-softmax update
 constexpr int kMinChunks = 4;   // fewest chunks a warp is given (bounds merge fan-in)
 
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_max_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __device__ __forceinline__ int warp_of(int64_t u, int64_t U, int W) {
   return (int)(((u + 1) * W + U - 1) / U) - 1;  // largest w with floor(U*w/W) <= u
 }
@@ -287,7 +298,8 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int prefix[kMaxB + 1];  // chunk units before sequence b (< 2^31: B * n_kv * ctx/32)
   __shared__ int s_ctx[kMaxB], s_slot[kMaxB];
-  __shared__ int s_wsum[4];
+  __shared__ int s_wbase[kMaxB + 1];  // pair-aligned partition: warps before sequence b
+  __shared__ int s_wsum[4], s_target;
   __shared__ __align__(8) uint64_t full_bars[4 * STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = n_kv * G;
@@ -332,10 +344,70 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
   __syncthreads();
   pdl_launch();
   const int64_t U = prefix[B];
-  const int W = (int)max((int64_t)1, min((int64_t)gridDim.x * 4, U / kMinChunks));
+  // Work partition. Pair-aligned when it fits: every (sequence, kv head) pair is cut into
+  // k_b = ceil(chunks_b / T) equal parts, one per warp, with the smallest chunk target T
+  // (>= kMinChunks) for which all parts fit in the grid's warps — so no warp ever switches
+  // pairs mid-stream (q reload, partial write, second merge) and merges are k_b-way. The
+  // kernel is HBM-bound, so the uneven part lengths (T/2..T chunks) cost nothing while
+  // enough pages are in flight. Otherwise (more pairs than warps): equal contiguous ranges
+  // of the unit space, segments crossing pair boundaries.
+  const int Wmax = gridDim.x * 4;
+  if (warp == 0) {  // one warp, shuffles only (no block barriers inside the search)
+    auto chunks = [&](int b) { return (s_ctx[b] + 16 * NP - 1) / (16 * NP); };
+    auto count = [&](int T) {  // warps the pair-aligned cut with target T needs
+      int c = 0;
+      for (int b = lane; b < B; b += 32) c += n_kv * ((chunks(b) + T - 1) / T);
+      return warp_sum_i(c);
+    };
+    int maxch = 0;
+    for (int b = lane; b < B; b += 32) maxch = max(maxch, chunks(b));
+    maxch = warp_max_i(maxch);
+    int lo = (int)max((int64_t)kMinChunks, (U + Wmax - 1) / Wmax), hi = max(lo, maxch);
+    const bool fits = count(hi) <= Wmax;
+    if (fits) {
+      while (lo < hi) {  // smallest T with count(T) <= Wmax (count is non-increasing in T)
+        const int mid = (lo + hi) >> 1;
+        if (count(mid) <= Wmax) hi = mid; else lo = mid + 1;
+      }
+      int run = 0;  // warps before sequence b, 32 sequences per pass
+      for (int b0 = 0; b0 < B; b0 += 32) {
+        const int b = b0 + lane;
+        const int k = b < B ? n_kv * ((chunks(b) + lo - 1) / lo) : 0;
+        int incl = k;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (b < B) s_wbase[b] = run + incl - k;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) s_wbase[B] = run;
+    }
+    if (lane == 0) s_target = fits ? lo : 0;
+  }
+  __syncthreads();
+  const int T_al = s_target;  // > 0: pair-aligned partition with chunk target T_al
+  const int W = T_al ? s_wbase[B] : (int)max((int64_t)1, min((int64_t)Wmax, U / kMinChunks));
   const int w = blockIdx.x * 4 + warp;
   if (w >= W) return;
-  const int64_t u0 = U * w / W, u1 = U * (w + 1) / W;
+  int64_t u0, u1;
+  if (T_al) {
+    int lo = 0, hi = B - 1;  // sequence of warp w
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_wbase[mid] <= w) lo = mid; else hi = mid - 1;
+    }
+    const int ch = (s_ctx[lo] + 16 * NP - 1) / (16 * NP);
+    const int k = (ch + T_al - 1) / T_al;
+    const int r = w - s_wbase[lo], kh = r / k, part = r % k;
+    const int64_t pbase = prefix[lo] + (int64_t)kh * ch;
+    u0 = pbase + (int64_t)ch * part / k;
+    u1 = pbase + (int64_t)ch * (part + 1) / k;
+  } else {
+    u0 = U * w / W;
+    u1 = U * (w + 1) / W;
+  }
   const int n = (int)(u1 - u0);
   if (n <= 0) return;
 
@@ -502,7 +574,15 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
         __threadfence();
         __syncwarp();
         const int64_t pstart = prefix[sb] + (int64_t)skh * cu.chunks;
-        const int wf = warp_of(pstart, U, W), wl = warp_of(pstart + cu.chunks - 1, U, W);
+        int wf, wl;
+        if (T_al) {  // the pair's k consecutive warps
+          const int k = (cu.chunks + T_al - 1) / T_al;
+          wf = s_wbase[sb] + skh * k;
+          wl = wf + k - 1;
+        } else {
+          wf = warp_of(pstart, U, W);
+          wl = warp_of(pstart + cu.chunks - 1, U, W);
+        }
         int last = 0;
         if (lane == 0) last = atomicAdd(&tickets[sb * n_kv + skh], 1) == wl - wf;
         last = __shfl_sync(0xffffffffu, last, 0);
@@ -512,7 +592,9 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
           // reductions, then every lane accumulates D/32 dims of all G rows with the
           // contributor loop unrolled so the partial loads overlap
           const int nc = wl - wf + 1;
-          auto part = [&](int c) { return c * 2 + ((c == wf && (U * c / W) < pstart) ? 1 : 0); };
+          auto part = [&](int c) {
+            return c * 2 + ((!T_al && c == wf && (U * c / W) < pstart) ? 1 : 0);
+          };
           float M[G], L[G], wt_l[G];
 #pragma unroll
           for (int r = 0; r < G; ++r) M[r] = -INFINITY, L[r] = 0.f, wt_l[r] = 0.f;
@@ -684,7 +766,7 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (2 * (4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 4 * (3 * kMaxB + 1)) <= 220 * 1024 ? 2 : 1) * sms;
+  const int grid = (2 * (4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 4 * (4 * kMaxB + 2)) <= 220 * 1024 ? 2 : 1) * sms;
   const int W = grid * 4;
   const size_t need = (size_t)W * 2 * G * (D + 1);
   const int pairs = B * n_kv;

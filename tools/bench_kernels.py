@@ -264,6 +264,7 @@ def main():
     ap.add_argument("--M", default="32,2080")
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--layout", default="tiled", choices=["tiled", "rowmajor", "both"])
+    ap.add_argument("--attn-cases", default="32x2048,32x4096,16x32768,1x4096,64x4096", help="BxCTX list")
     ap.add_argument("--prefill-cases", default="4x2048x2048,1x2048x34816,8x512x4096,32x33x4096",
                     help="SxNxCTX list for --what prefill")
     args = ap.parse_args()
@@ -286,7 +287,8 @@ def main():
     if "small" in args.what:
         bench_small(shape)
     if "attn" in args.what:
-        for B, ctx in [(32, 2048), (32, 4096), (16, 32768), (1, 4096), (64, 4096)]:
+        for case in args.attn_cases.split(","):
+            B, ctx = (int(x) for x in case.split("x"))
             bench_attn(shape, B, ctx)
 
 
