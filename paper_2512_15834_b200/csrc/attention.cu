@@ -268,8 +268,15 @@ __device__ __forceinline__ void load_q(uint32_t (*qf)[4], const __nv_bfloat16* r
 // from each contributor and the last one to finish (ticket) merges them, so no
 // separate merge launch and no wave tail, whatever the context lengths.
 constexpr int kMaxB = 1024;
-constexpr int kChunkPages = 2;  // pages (16 keys each) per online-softmax update
-constexpr int kMinChunks = 4;   // fewest chunks a warp is given (bounds merge fan-in)
+#ifndef STB_K3_PAGES
+#define STB_K3_PAGES 1
+#endif
+#ifndef STB_K3_WARPS
+#define STB_K3_WARPS 8
+#endif
+constexpr int kChunkPages = STB_K3_PAGES;  // pages (16 keys each) per online-softmax update
+constexpr int kDecWarps = STB_K3_WARPS;    // warps per CTA (one CTA per SM: smem-bound)
+constexpr int kMinChunks = 8 / STB_K3_PAGES;  // fewest chunks (128 keys) a warp is given: bounds merge fan-in
 
 __device__ __forceinline__ int warp_sum_i(int v) {
 #pragma unroll
@@ -287,7 +294,7 @@ __device__ __forceinline__ int warp_of(int64_t u, int64_t U, int W) {
 }
 
 template <int D, int G, int STAGES>
-__global__ void __launch_bounds__(128, 2) attn_decode_kernel(
+__global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
@@ -299,19 +306,19 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
   __shared__ int prefix[kMaxB + 1];  // chunk units before sequence b (< 2^31: B * n_kv * ctx/32)
   __shared__ int s_ctx[kMaxB], s_slot[kMaxB];
   __shared__ int s_wbase[kMaxB + 1];  // pair-aligned partition: warps before sequence b
-  __shared__ int s_wsum[4], s_target;
-  __shared__ __align__(8) uint64_t full_bars[4 * STAGES];
+  __shared__ int s_wsum[kDecWarps], s_target;
+  __shared__ __align__(8) uint64_t full_bars[kDecWarps * STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = n_kv * G;
   if (threadIdx.x == 0) {
-    for (int s2 = 0; s2 < 4 * STAGES; ++s2) mbar_init(&full_bars[s2], 1);
+    for (int s2 = 0; s2 < kDecWarps * STAGES; ++s2) mbar_init(&full_bars[s2], 1);
     fence_mbar_init();
   }
   {
     // step metadata (host-uploaded, not produced by the preceding kernel): all threads load
     // ctx / slot in parallel (a serial loop would chain B global-load latencies in front of
     // the first page copy), then a block scan gives the unit prefix
-    const int per = (B + 127) >> 7, b0 = threadIdx.x * per;
+    const int per = (B + 32 * kDecWarps - 1) / (32 * kDecWarps), b0 = threadIdx.x * per;
     int local = 0;
     for (int j = 0; j < per; ++j) {
       const int b = b0 + j;
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
         run += n_kv * ((s_ctx[b] + 16 * NP - 1) / (16 * NP));
       }
     }
-    if (threadIdx.x == 127) prefix[B] = run;
+    if (threadIdx.x == 32 * kDecWarps - 1) prefix[B] = run;
   }
   __syncthreads();
   pdl_launch();
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
   // kernel is HBM-bound, so the uneven part lengths (T/2..T chunks) cost nothing while
   // enough pages are in flight. Otherwise (more pairs than warps): equal contiguous ranges
   // of the unit space, segments crossing pair boundaries.
-  const int Wmax = gridDim.x * 4;
+  const int Wmax = gridDim.x * kDecWarps;
   if (warp == 0) {  // one warp, shuffles only (no block barriers inside the search)
     auto chunks = [&](int b) { return (s_ctx[b] + 16 * NP - 1) / (16 * NP); };
     auto count = [&](int T) {  // warps the pair-aligned cut with target T needs
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(128, 2) attn_decode_kernel(
   __syncthreads();
   const int T_al = s_target;  // > 0: pair-aligned partition with chunk target T_al
   const int W = T_al ? s_wbase[B] : (int)max((int64_t)1, min((int64_t)Wmax, U / kMinChunks));
-  const int w = blockIdx.x * 4 + warp;
+  const int w = blockIdx.x * kDecWarps + warp;
   if (w >= W) return;
   int64_t u0, u1;
   if (T_al) {
@@ -747,7 +754,10 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
   }
 }
 
-constexpr int kDecodeStages = 3;
+#ifndef STB_K3_STAGES
+#define STB_K3_STAGES 3
+#endif
+constexpr int kDecodeStages = STB_K3_STAGES;
 constexpr int kPrefillStages = 3;
 
 struct DecodeScratch {
@@ -766,8 +776,8 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (2 * (4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 4 * (4 * kMaxB + 2)) <= 220 * 1024 ? 2 : 1) * sms;
-  const int W = grid * 4;
+  const int grid = (2 * (kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 4 * (4 * kMaxB + 2)) <= 220 * 1024 ? 2 : 1) * sms;
+  const int W = grid * kDecWarps;
   const size_t need = (size_t)W * 2 * G * (D + 1);
   const int pairs = B * n_kv;
   if (need > sc.floats || pairs > sc.n_tickets) {
@@ -787,7 +797,7 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
       sc.n_tickets = nt;
     }
   }
-  constexpr size_t smem = (size_t)4 * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
+  constexpr size_t smem = (size_t)kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
   auto kern = attn_decode_kernel<D, G, kDecodeStages>;
   static bool attr = false;
   if (!attr) {
@@ -796,7 +806,7 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   }
   float* o_part = sc.part;
   float* lse_part = sc.part + (size_t)W * 2 * G * D;
-  cudaError_t e = launch_k(kern, dim3(grid), dim3(128), smem, st, q, out, kp, vp, table, max_bps, slots, ctx, B, n_kv,
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(32 * kDecWarps), smem, st, q, out, kp, vp, table, max_bps, slots, ctx, B, n_kv,
                            qscale, o_part, lse_part, sc.tickets);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_decode launch: %s", cudaGetErrorString(e));
   return STB_OK;
