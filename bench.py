@@ -281,6 +281,8 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     state["timed"] = {}
+    if args.k2_stats:
+        rt.dec.run_log = []
     events = rt.dec.step_events = []
     h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
     launches0 = lib.load().stb_launch_count() + rt.dec.graph_kernels
@@ -364,6 +366,20 @@ def run_b200(args, world, rank, local):
                      "wall_ms_per_step": round(wall_s / args.steps * 1e3, 3)},
     }
     print(json.dumps(line), flush=True)
+    if args.k2_stats and rt.dec.run_log is not None:  # K2 launch shapes of the timed mixed steps
+        import collections
+
+        steps = rt.dec.run_log
+        kinds = collections.Counter()
+        for runs in steps:
+            for n, c in runs:
+                kinds["n<=40" if n <= 40 else "n<=256" if n <= 256 else "n<=1100" if n <= 1100 else "n>1100"] += 1
+        nruns = collections.Counter(len(r) for r in steps)
+        print(f"K2 stats: {len(steps)} mixed steps, runs by size {dict(kinds)}, runs per step {dict(sorted(nruns.items()))}",
+              file=sys.stderr)
+        mixed_t = [(round(ms, 2), T) for ms, g, T in per if not g]
+        for runs, mt in list(zip(steps, mixed_t))[:16]:
+            print("  ", runs, "step ms, T =", mt, file=sys.stderr)
 
 
 def main():
@@ -381,6 +397,7 @@ def main():
     ap.add_argument("--max-step-tokens", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--k2-stats", action="store_true", help="diagnostics: K2 run shapes of the mixed steps")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     resolve(args, world)

@@ -58,6 +58,9 @@ def interleave_gate_up(w: torch.Tensor, d_ff: int) -> None:
     w._stb_gate_up_interleaved = True   # include/stb200.h STB_GEMM_C_ZEROED
 GEMM_W_TILED = 4    # include/stb200.h STB_GEMM_W_TILED
 CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
+GRAPH_MAX_T = 192   # mixed steps up to this many tokens ...
+GRAPH_MAX_RUNS = 2  # ... and append-prefill runs are replayed from CUDA graphs
+GRAPH_CACHE = 48    # captured graphs kept
 PROJECTIONS = ("wqkv", "wo", "w_gate_up", "w_down")
 
 
@@ -229,6 +232,7 @@ class Decoder:
         self.graph_sizes: dict[tuple, int] = {}  # kernels captured per graph
         self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
         self._pre_flops = 0
+        self.run_log: list | None = None
         self._pending: list | None = []             # (name, ev0, ev1, work) awaiting a sync
         self._graph_timed = False
         self.last_logits: torch.Tensor | None = None
@@ -322,24 +326,30 @@ class Decoder:
         self.pool.sync(stream)
         m = self._upload(b)
         dec_bytes = (int(b.dec_ctx.sum()) * 2 * self.shape.kv_dim * 2 + 2 * B * self.shape.q_dim * 2) if B else 0
-        graphable = self.use_graphs and S == 0 and B > 0 and not self.keep_logits
+        max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
+        if S:  # K2 algorithmic flops per layer: 4 H_q d (n ctx_prev + n(n+1)/2) per run
+            n = np.diff(b.pre_qstart).astype(np.float64)
+            prev = b.pre_ctx.astype(np.float64) - n
+            self._pre_flops = int(4 * self.shape.q_dim * float(np.sum(n * prev + n * (n + 1) / 2)))
+            if self.run_log is not None:  # (n, ctx) of every K2 run of the step (diagnostics)
+                self.run_log.append([(int(a), int(c)) for a, c in zip(n, b.pre_ctx)])
+        # CUDA graphs: decode-only steps (one per batch size) and small mixed steps (verify
+        # passes: the same (B, T, R, S, max_q) shape recurs every few steps), whose ~300
+        # eager launches would otherwise be paced by the host
+        graphable = (self.use_graphs and B > 0 and not self.keep_logits
+                     and (S == 0 or (T <= GRAPH_MAX_T and S <= GRAPH_MAX_RUNS)))
         if self.step_events is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
         if not graphable:
-            max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
-            if S:  # K2 algorithmic flops per layer: 4 H_q d (n ctx_prev + n(n+1)/2) per run
-                n = np.diff(b.pre_qstart).astype(np.float64)
-                prev = b.pre_ctx.astype(np.float64) - n
-                self._pre_flops = int(4 * self.shape.q_dim * float(np.sum(n * prev + n * (n + 1) / 2)))
             self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
         else:
             # decode graphs assume (and leave) zeroed every GEMM output they accumulate into
             # (stream-K); a whole-tile LM head overwrites the logits, so those stay as they are
             V, d = self.shape.vocab, self.shape.d_model
-            lm_stream = self._stream_cache.get((B, V, d))
+            lm_stream = self._stream_cache.get((R, V, d))
             if lm_stream is None:
-                lm_stream = self._stream_cache[(B, V, d)] = bool(lib.load().stb_gemm_is_stream(B, V, d))
+                lm_stream = self._stream_cache[(R, V, d)] = bool(lib.load().stb_gemm_is_stream(R, V, d))
             for name, rows in self._dirty.items():
                 if rows and (name != "logits" or lm_stream):
                     getattr(self, name)[:rows].zero_()
@@ -351,20 +361,25 @@ class Decoder:
             if timed:
                 par = self._timed_parity
                 self._timed_parity ^= 1
-            key = (B, timed, par)
+            key = (B, T, R, S, max_q, timed, par)
             if key not in self.graphs:
-                self._capture(key, m, B)
+                if len(self.graphs) >= GRAPH_CACHE:  # drop the oldest mixed-step graph
+                    old = next((k for k in self.graphs if k[3] > 0), None)
+                    if old is not None:
+                        del self.graphs[old]
+                self._capture(key, m, T, R, B, S, max_q, dec_bytes)
             graph, events = self.graphs[key]
             graph.replay()
             self.graph_replays += 1
             self.graph_kernels += self.graph_sizes.get(key, 0)
             if timed:
+                live = {"attn_decode": dec_bytes, "attn_prefill": self._pre_flops}
                 for name, a0, a1, work in events:
-                    self._pending.append((name, a0, a1, dec_bytes if name == "attn_decode" else work))
+                    self._pending.append((name, a0, a1, live.get(name, work)))
         if self.step_events is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
-            self.step_events.append((e0, e1, graphable, T))
+            self.step_events.append((e0, e1, S == 0, T))  # (.., decode-only step, tokens)
         if self.keep_logits:
             self.last_logits = self.logits[:R].clone()
             self.logits[:R].zero_()
@@ -372,12 +387,14 @@ class Decoder:
             self.last_raw_argmax = self.raw_arg[:R].clone()
         return self.sampled[:R]
 
-    def _capture(self, key, m: dict[str, int], B: int) -> None:
-        timed = key[1]
+    def _capture(self, key, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, dec_bytes: int) -> None:
+        timed = key[5]
         saved, saved_timers = self._pending, self.timers
-        # warm once eagerly (first-call allocations, tensor-map encodes, attributes); untimed
+        # warm once eagerly (first-call allocations, tensor-map encodes, attributes); untimed.
+        # It runs the step's kernels for real: KV commits are idempotent and the replay
+        # below overwrites every output
         self.timers, self._pending = None, []
-        self._launch(m, B, B, B, 0, 0, 0, 0)
+        self._launch(m, T, R, B, S, max_q, 0, dec_bytes)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         events: list = []
@@ -385,7 +402,7 @@ class Decoder:
         self._graph_timed = timed
         n0 = lib.load().stb_launch_count()
         with torch.cuda.graph(graph):
-            self._launch(m, B, B, B, 0, 0, 0, 0)
+            self._launch(m, T, R, B, S, max_q, 0, dec_bytes)
         self.graph_sizes[key] = int(lib.load().stb_launch_count() - n0)
         self._pending, self.timers = saved, saved_timers
         self._graph_timed = False
