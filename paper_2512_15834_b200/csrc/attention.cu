@@ -867,6 +867,12 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
 int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                      const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale, int max_q,
                      void* stream) {
+  return stb_attn_prefill_split(pool, layer, q, out, slots, q_start, ctx_lens, S, T, n_q, scale, max_q, 0, stream);
+}
+
+int stb_attn_prefill_split(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                           const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,
+                           int max_q, int active_units, void* stream) {
   void *kp, *vp;
   if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
   int32_t* table;
@@ -879,7 +885,9 @@ int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, con
     const char* e = getenv("STB200_PREFILL");
     use_mma = (e && e[0] == 'm') ? 1 : 0;
   }
-  if (!use_mma) return stb_attn_prefill_tc(pool, layer, q, out, slots, q_start, ctx_lens, S, T, n_q, scale, max_q, stream);
+  if (!use_mma)
+    return stb_attn_prefill_tc(pool, layer, q, out, slots, q_start, ctx_lens, S, T, n_q, scale, max_q, active_units,
+                               stream);
   int n_kv, d_head;
   stb_pool_geometry(pool, &n_kv, &d_head);
   if (n_q % n_kv) return fail(STB_EINVAL, "attn_prefill: n_q %% n_kv != 0");

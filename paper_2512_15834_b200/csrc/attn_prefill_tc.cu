@@ -29,6 +29,8 @@
 // TMEM (512 columns): S/P_A | S/P_B | O_A | O_B.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -45,6 +47,15 @@ constexpr int KT = 128;     // keys per KV tile (UMMA N of S, K of P V)
 constexpr int KV_STAGES = 2;
 constexpr int kThreads = 320;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMaxSplits = 8;      // KV splits per (query-tile pair, kv head, run) work unit
+constexpr int kMinSplitTiles = 2;  // fewest KV tiles a split CTA streams
+template <int D>
+constexpr int kPartFloats = 2 * ROWS * (D + 1);  // one split's partial rows: O/l of both tiles + lse
+
+// KV splits of a unit whose query tiles need n_tiles KV tiles (identical in K2 and the merge)
+__host__ __device__ __forceinline__ int unit_splits(int n_tiles, int max_splits) {
+  return max(1, min(max_splits, n_tiles / kMinSplitTiles));
+}
 
 template <int D>
 struct TcCfg {
@@ -121,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out,
                            const int32_t* __restrict__ table, int max_bps, const int32_t* __restrict__ slots,
                            const int32_t* __restrict__ q_start, const int32_t* __restrict__ ctx_lens, int n_kv,
-                           float qscale) {
+                           float qscale, int max_splits, float* __restrict__ part) {
   using CF = TcCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -143,7 +154,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nyz = gridDim.y * gridDim.z;
   const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   const int bx = gridDim.x - 1 - lin / nyz;
-  const int kh = (lin % nyz) % gridDim.y, s = (lin % nyz) / gridDim.y;
+  const int kh = (lin % nyz) % gridDim.y, zz = (lin % nyz) / gridDim.y;
+  const int s = zz / max_splits, sp = zz % max_splits;  // run, KV split
   constexpr int QPT = ROWS / G;  // queries per tile
   pdl_wait();
   pdl_launch();
@@ -154,7 +166,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ctx = ctx_lens[s];
   const int pos0 = ctx - n;  // absolute position of query 0
   const int q_last = min(n, qi0 + 2 * QPT) - 1;
-  const int n_tiles = (pos0 + q_last) / KT + 1;  // KV tiles the CTA needs (causal)
+  const int n_tiles = (pos0 + q_last) / KT + 1;  // KV tiles the query tiles need (causal)
+  // KV split (launches with few work units, e.g. one verify pass): this CTA streams tiles
+  // [j0, j0 + nt) and writes partial rows; attn_prefill_merge_kernel combines them
+  const int nsplit = unit_splits(n_tiles, max_splits);
+  if (sp >= nsplit) return;
+  const int j0 = n_tiles * sp / nsplit, nt = n_tiles * (sp + 1) / nsplit - j0;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -191,9 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int h = 0; h < CF::HALVES; ++h)
           tma_load_4d(sQ + t * CF::Q_BYTES + h * ROWS * 128, &tm_q, q_full, h * 64, 0, kh, t0 + qi0 + t * QPT);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % KV_STAGES;
-        mbar_wait(&kv_empty[st], ((j / KV_STAGES) & 1) ^ 1);
+      for (int jj = 0; jj < nt; ++jj) {
+        const int j = j0 + jj;
+        const int st = jj % KV_STAGES;
+        mbar_wait(&kv_empty[st], ((jj / KV_STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], CF::STAGE);
         uint8_t* sk = sKV + st * CF::STAGE;
         uint8_t* sv = sk + CF::KV_BYTES;
@@ -241,8 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       issue_s(0, 0);
       if (ntile_q > 1) issue_s(1, 0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const bool more = j + 1 < n_tiles;
+      for (int j = 0; j < nt; ++j) {  // local tile index: ring slots and barrier phases
+        const bool more = j + 1 < nt;
         mbar_wait(&p_full[0], j & 1);
         tc_fence_after();
         issue_pv(0, j);
@@ -275,8 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     float m = -INFINITY, l = 0.f;
     if (tile_live) {
-      for (int j = 0; j < n_tiles; ++j) {
-        mbar_wait(&s_full[t], j & 1);
+      for (int jj = 0; jj < nt; ++jj) {
+        const int j = j0 + jj;  // absolute KV tile (masking); jj: barrier phases
+        mbar_wait(&s_full[t], jj & 1);
         tc_fence_after();
         uint32_t v[KT];
 #pragma unroll
@@ -315,8 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < KT / 2; c += 32) tmem_st32(tS(t) + lane_base + c, pk + c);
         // rescale O (in TMEM) when this warp's running max moved and O holds earlier tiles
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare with the lazy reference
-          mbar_wait(&o_done[t], (j - 1) & 1);
+        if (jj > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare with the lazy reference
+          mbar_wait(&o_done[t], (jj - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D; c += 32) {
@@ -333,16 +352,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&p_full[t]);
       }
       // final: O / l
-      mbar_wait(&o_done[t], (n_tiles - 1) & 1);
+      mbar_wait(&o_done[t], (nt - 1) & 1);
       tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
       __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D;
+      float* prow = nullptr;  // split: this row's partial slot
+      if (nsplit > 1) {
+        float* po = part + ((((int64_t)s * n_kv + kh) * gridDim.x + bx) * max_splits + sp) * kPartFloats<D>;
+        prow = po + (t * ROWS + r) * D;
+        po[2 * ROWS * D + t * ROWS + r] = (live && l > 0.f) ? m + log2f(l) : -INFINITY;
+      }
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t o[32];
         tmem_ld32(tO(t) + lane_base + c, o);
         tmem_ld_wait();
-        if (live) {
+        if (prow != nullptr) {
+#pragma unroll
+          for (int q = 0; q < 32; q += 4)
+            __stcg(reinterpret_cast<float4*>(prow + c + q),
+                   make_float4(__uint_as_float(o[q]) * inv, __uint_as_float(o[q + 1]) * inv,
+                               __uint_as_float(o[q + 2]) * inv, __uint_as_float(o[q + 3]) * inv));
+        } else if (live) {
 #pragma unroll
           for (int q = 0; q < 32; q += 8)
             *reinterpret_cast<uint4*>(dst + c + q) = make_uint4(
@@ -357,6 +388,61 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_free(tmem, CF::TMEM_COLS);
+}
+
+// Combine the KV-split partial rows of K2: one warp per (tile, packed row) of a work unit,
+// lane = 4 of the D columns (one float4 per split: all split loads in flight at once);
+// out = sum_k 2^(lse_k - M) (O/l)_k / sum_k 2^(lse_k - M).
+template <int D, int G>
+__global__ void __launch_bounds__(256) attn_prefill_merge_kernel(__nv_bfloat16* __restrict__ out,
+                                                                 const float* __restrict__ part,
+                                                                 const int32_t* __restrict__ q_start,
+                                                                 const int32_t* __restrict__ ctx_lens, int n_kv,
+                                                                 int max_splits, int gx) {
+  pdl_wait();
+  pdl_launch();
+  constexpr int QPT = ROWS / G;
+  const int unit = blockIdx.x / (2 * ROWS / 8);              // 8 rows (warps) per block
+  const int row = (blockIdx.x % (2 * ROWS / 8)) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int bx = unit % gx, kh = blockIdx.y, s = blockIdx.z;
+  const int t0 = q_start[s], n = q_start[s + 1] - t0;
+  const int qi0 = bx * 2 * QPT;
+  if (qi0 >= n) return;
+  const int pos0 = ctx_lens[s] - n;
+  const int nsplit = unit_splits((pos0 + min(n, qi0 + 2 * QPT) - 1) / KT + 1, max_splits);
+  if (nsplit == 1) return;  // K2 wrote this unit's rows directly
+  const int t = row / ROWS, r = row % ROWS;
+  const int qi = qi0 + t * QPT + r / G, g = r % G;
+  if (qi >= n) return;
+  const float* base = part + (((int64_t)s * n_kv + kh) * gx + bx) * max_splits * kPartFloats<D>;
+  float w[kMaxSplits];
+  float4 v[kMaxSplits];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k) {
+    w[k] = -INFINITY;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < nsplit) {
+      const float* pk = base + k * kPartFloats<D>;
+      w[k] = __ldcg(pk + 2 * ROWS * D + t * ROWS + r);
+      if (lane < D / 4) v[k] = __ldcg(reinterpret_cast<const float4*>(pk + (t * ROWS + r) * D) + lane);
+    }
+    mx = fmaxf(mx, w[k]);
+  }
+  float wsum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < kMaxSplits; ++k) {
+    const float e = (k < nsplit && w[k] != -INFINITY) ? exp2f(w[k] - mx) : 0.f;
+    wsum += e;
+    acc.x += e * v[k].x, acc.y += e * v[k].y, acc.z += e * v[k].z, acc.w += e * v[k].w;
+  }
+  const float winv = wsum > 0.f ? 1.f / wsum : 0.f;
+  if (lane < D / 4) {
+    __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D + lane * 4;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(acc.x * winv, acc.y * winv), pack_bf16(acc.z * winv, acc.w * winv));
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
@@ -388,9 +474,15 @@ struct Maps {
   CUtensorMap q, k, v;
 };
 
+// split-K partials, grown outside graph capture only (no split while capturing a new size)
+struct SplitScratch {
+  float* part = nullptr;
+  size_t floats = 0;
+};
+
 template <int D, int G>
 int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots, const int32_t* q_start,
-              const int32_t* ctx, int S, int T, int n_kv, float qscale, int max_q, cudaStream_t st) {
+              const int32_t* ctx, int S, int T, int n_kv, float qscale, int max_q, int active_hint, cudaStream_t st) {
   using CF = TcCfg<D>;
   // tensor maps: Q over [T][n_kv][G][D] (box 64 x G x 1 x 128/G), K / V pages of the layer as
   // [num_blocks * n_kv * 16 rows][D] (box 64 x 16); cached per (q base, T, layer pointers)
@@ -426,10 +518,44 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr = true;
   }
-  dim3 grid((max_q + 2 * ROWS / G - 1) / (2 * ROWS / G), n_kv, S);
+  const int gx = (max_q + 2 * ROWS / G - 1) / (2 * ROWS / G);
+  // KV split only for launches far from filling the machine (a verify pass is 8 work units
+  // on 148 SMs); `active_hint` = units that hold queries (0: the full grid)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t units = (int64_t)gx * n_kv * S;
+  const int64_t active = active_hint > 0 ? active_hint : units;
+  static const int split_env = getenv("STB200_K2_SPLIT") ? atoi(getenv("STB200_K2_SPLIT")) : -1;  // A/B only
+  int splits = 1;
+  if (2 * active <= sms) splits = (int)std::min<int64_t>(kMaxSplits, sms / active);
+  if (split_env >= 1) splits = std::min(split_env, kMaxSplits);
+  static SplitScratch sc;
+  if (splits > 1) {
+    const size_t need = (size_t)units * splits * kPartFloats<D>;
+    if (need > sc.floats) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone) return fail(STB_EINVAL, "attn_prefill: split scratch growth in capture");
+      if (sc.part) cudaFree(sc.part);
+      sc.part = nullptr;
+      sc.floats = 0;
+      if (cudaMalloc(&sc.part, need * sizeof(float)) != cudaSuccess) return fail(STB_ENOMEM, "attn_prefill split");
+      sc.floats = need;
+    }
+  }
+  dim3 grid(gx, n_kv, S * splits);
   cudaError_t e = launch_k(kern, grid, dim3(kThreads), CF::SMEM, st, mp.q, mp.k, mp.v, (__nv_bfloat16*)out,
-                           pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale);
+                           pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale, splits, sc.part);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill_tc launch: %s", cudaGetErrorString(e));
+  if (splits > 1) {
+    e = launch_k(attn_prefill_merge_kernel<D, G>, dim3(gx * (2 * ROWS / 8), n_kv, S), dim3(256), 0, st,
+                 (__nv_bfloat16*)out, (const float*)sc.part, q_start, ctx, n_kv, splits, gx);
+    if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill merge launch: %s", cudaGetErrorString(e));
+  }
   return STB_OK;
 }
 
@@ -438,12 +564,12 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
 // internal entry used by stb_attn_prefill (attention.cu) for tensor-core-sized runs
 int stb_attn_prefill_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                         const int32_t* q_start, const int32_t* ctx, int S, int T, int n_q, float scale, int max_q,
-                        void* stream) {
+                        int active_hint, void* stream) {
   int n_kv = pool->n_kv, d = pool->d_head;
   int g = n_q / n_kv;
   float qs = scale * kLog2e;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS pool, layer, q, out, slots, q_start, ctx, S, T, n_kv, qs, max_q, st
+#define ARGS pool, layer, q, out, slots, q_start, ctx, S, T, n_kv, qs, max_q, active_hint, st
   if (d == 128 && g == 4) return launch_tc<128, 4>(ARGS);
   if (d == 128 && g == 8) return launch_tc<128, 8>(ARGS);
   if (d == 128 && g == 1) return launch_tc<128, 1>(ARGS);

@@ -39,6 +39,7 @@ const float* stb_rope_inv_freq(float rope_theta, int d_head);
 extern "C" int stb_pool_geometry(const stb_kv_pool* p, int* n_kv, int* d_head);
 extern "C" int stb_kv_layer_ptrs(const stb_kv_pool* pool, int layer, void** k_pages, void** v_pages);
 // K2 tensor-core path (attn_prefill_tc.cu), dispatched from stb_attn_prefill
+// active_hint: (query-tile pair, kv head, run) units that hold queries (0: assume the full grid)
 int stb_attn_prefill_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                         const int32_t* q_start, const int32_t* ctx, int S, int T, int n_q, float scale, int max_q,
-                        void* stream);
+                        int active_hint, void* stream);

@@ -232,6 +232,7 @@ class Decoder:
         self.graph_sizes: dict[tuple, int] = {}  # kernels captured per graph
         self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
         self._pre_flops = 0
+        self._pre_units = 0
         self.run_log: list | None = None
         self._pending: list | None = []             # (name, ev0, ev1, work) awaiting a sync
         self._graph_timed = False
@@ -331,6 +332,9 @@ class Decoder:
             n = np.diff(b.pre_qstart).astype(np.float64)
             prev = b.pre_ctx.astype(np.float64) - n
             self._pre_flops = int(4 * self.shape.q_dim * float(np.sum(n * prev + n * (n + 1) / 2)))
+            # K2 work units holding queries: (query-tile pair of 2*128/G tokens, kv head, run)
+            pair = 2 * 128 // (self.shape.n_q // self.shape.n_kv)
+            self._pre_units = int(np.sum(np.ceil(n / pair))) * self.shape.n_kv
             if self.run_log is not None:  # (n, ctx) of every K2 run of the step (diagnostics)
                 self.run_log.append([(int(a), int(c)) for a, c in zip(n, b.pre_ctx)])
         # CUDA graphs: decode-only steps (one per batch size) and small mixed steps (verify
@@ -439,9 +443,9 @@ class Decoder:
                 self._tock("attn_decode", ev, dec_bytes)
             if S:
                 ev = self._tick()
-                call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
-                     _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
-                     st)
+                call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()),
+                     _p(self.attn[B:].data_ptr()), _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S,
+                     T - B, s.n_q, self.scale, max_q, self._pre_units, st)
                 self._tock("attn_prefill", ev, self._pre_flops)
             self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
@@ -476,8 +480,9 @@ class Decoder:
             self._tock("attn_decode", ev, dec_bytes)
         if S:
             ev = self._tick()
-            call("stb_attn_prefill", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
-                 _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q, st)
+            call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
+                 _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
+                 self._pre_units, st)
             self._tock("attn_prefill", ev, self._pre_flops)
 
     def _launch_fused(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
