@@ -131,7 +131,8 @@ def reduce(values: list[float], op: str, world: int, device) -> list[float]:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor(values, dtype=torch.float64, device=device)
+    on_dev = dist.get_backend() == "nccl"  # gloo reduces host tensors
+    t = torch.tensor(values, dtype=torch.float64, device=device if on_dev else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return t.tolist()
 
@@ -244,8 +245,11 @@ def run_b200(args, world, rank, local):
     from paper_2512_15834_b200.runtime.fleet import Fleet, TraceSpec, engine_config
     from paper_2512_15834_b200.runtime.realtime import RealtimeLoop
 
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    # one GPU per rank; on a box with fewer GPUs than ranks (CI smoke of the multi-rank path,
+    # gloo backend) ranks share devices round-robin
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    device = torch.device("cuda", dev)
     shape = SHAPES[args.shape]
     if args.layers:
         shape = shape.with_layers(args.layers)
@@ -287,7 +291,7 @@ def run_b200(args, world, rank, local):
     h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
     launches0 = lib.load().stb_launch_count() + rt.dec.graph_kernels
     resume0 = len(engine.resume_latencies)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
         w0 = time.perf_counter()
         for _ in range(args.steps):
