@@ -535,7 +535,9 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
   if (split_env >= 1) splits = std::min(split_env, kMaxSplits);
   static SplitScratch sc;
   if (splits > 1) {
-    const size_t need = (size_t)units * splits * kPartFloats<D>;
+    // sized on first use for any split launch (<= sms/2 units x 8 splits) so it never grows
+    // (cudaMalloc would stall a step); larger ragged grids grow it once more
+    const size_t need = std::max((size_t)units * splits, (size_t)(sms / 2) * kMaxSplits) * kPartFloats<D>;
     if (need > sc.floats) {
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(st, &cs);

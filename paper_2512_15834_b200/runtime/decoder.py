@@ -230,6 +230,7 @@ class Decoder:
         self.use_graphs = use_graphs
         self.graphs: dict[tuple, tuple] = {}
         self.graph_sizes: dict[tuple, int] = {}  # kernels captured per graph
+        self._seen: set = set()                  # mixed-step shapes already run eagerly once
         self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
         self._pre_flops = 0
         self._pre_units = 0
@@ -342,10 +343,17 @@ class Decoder:
         # eager launches would otherwise be paced by the host
         graphable = (self.use_graphs and B > 0 and not self.keep_logits
                      and (S == 0 or (T <= GRAPH_MAX_T and S <= GRAPH_MAX_RUNS)))
-        if self.step_events is not None:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record()
+        e0 = torch.cuda.Event(enable_timing=True) if self.step_events is not None else None
+        shape_key = (B, T, R, S, max_q)
+        if graphable and S > 0 and shape_key not in self._seen:
+            # first occurrence of a mixed-step shape runs eagerly (it also initialises every
+            # launch's one-time state); the graph is captured, without a warm-up run, only
+            # when the shape recurs
+            self._seen.add(shape_key)
+            graphable = False
         if not graphable:
+            if e0 is not None:
+                e0.record()
             self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
         else:
             # decode graphs assume (and leave) zeroed every GEMM output they accumulate into
@@ -354,10 +362,6 @@ class Decoder:
             lm_stream = self._stream_cache.get((R, V, d))
             if lm_stream is None:
                 lm_stream = self._stream_cache[(R, V, d)] = bool(lib.load().stb_gemm_is_stream(R, V, d))
-            for name, rows in self._dirty.items():
-                if rows and (name != "logits" or lm_stream):
-                    getattr(self, name)[:rows].zero_()
-                    self._dirty[name] = 0
             timed = self.timers is not None
             # timed graphs carry their own event nodes: two copies alternate so a step's
             # events are not re-recorded while the runtime still has that step in flight
@@ -371,8 +375,14 @@ class Decoder:
                     old = next((k for k in self.graphs if k[3] > 0), None)
                     if old is not None:
                         del self.graphs[old]
-                self._capture(key, m, T, R, B, S, max_q, dec_bytes)
+                self._capture(key, m, T, R, B, S, max_q, dec_bytes, warm=S == 0)
             graph, events = self.graphs[key]
+            if e0 is not None:  # after any capture: host-side capture time is not device work
+                e0.record()
+            for name, rows in self._dirty.items():  # part of the step: inside the timed bracket
+                if rows and (name != "logits" or lm_stream):
+                    getattr(self, name)[:rows].zero_()
+                    self._dirty[name] = 0
             graph.replay()
             self.graph_replays += 1
             self.graph_kernels += self.graph_sizes.get(key, 0)
@@ -391,14 +401,16 @@ class Decoder:
             self.last_raw_argmax = self.raw_arg[:R].clone()
         return self.sampled[:R]
 
-    def _capture(self, key, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, dec_bytes: int) -> None:
+    def _capture(self, key, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, dec_bytes: int,
+                 warm: bool = True) -> None:
         timed = key[5]
         saved, saved_timers = self._pending, self.timers
-        # warm once eagerly (first-call allocations, tensor-map encodes, attributes); untimed.
-        # It runs the step's kernels for real: KV commits are idempotent and the replay
-        # below overwrites every output
         self.timers, self._pending = None, []
-        self._launch(m, T, R, B, S, max_q, 0, dec_bytes)
+        if warm:
+            # warm once eagerly (first-call allocations, tensor-map encodes, attributes); untimed.
+            # It runs the step's kernels for real: KV commits are idempotent and the replay
+            # overwrites every output
+            self._launch(m, T, R, B, S, max_q, 0, dec_bytes)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         events: list = []

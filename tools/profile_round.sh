@@ -18,5 +18,8 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm
   -o $OUT/full_gemm_prefill python tools/gemm_once.py --M 608 --N 28672 --K 4096 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:attn_prefill_tc -c 2 \
   -o $OUT/full_prefill python tools/bench_kernels.py --what prefill > /dev/null 2>&1
-timeout 300 python tools/bench_kernels.py > $OUT/kernels.txt 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:attn_prefill_tc -c 1 \
+  -o $OUT/full_prefill_c5 python tools/bench_kernels.py --what prefill --prefill-cases 1x2048x34816 > /dev/null 2>&1
+timeout 300 python tools/bench_kernels.py --what gemm,attn,prefill,small \
+  --prefill-cases 4x2048x2048,1x2048x34816,8x512x4096,32x33x4096,1x33x2150,1x600x2700 > $OUT/kernels.txt 2>&1
 ls -la $OUT
