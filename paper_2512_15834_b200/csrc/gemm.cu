@@ -770,6 +770,32 @@ int cached_map(CUtensorMap* out, const void* base, int64_t rows, int64_t cols, i
   return STB_OK;
 }
 
+// [rows][64] bf16 with 128-byte rows, box [128][64], no swizzle: one pre-swizzled weight tile
+int cached_map_raw(CUtensorMap* out, const void* base, int64_t rows) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapHash> cache;
+  MapKey key{base, rows, -1, 64, BM};
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return STB_OK;
+  }
+  auto fn = encode_fn();
+  if (!fn) return fail(STB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(BK * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(STB_ECUDA, "cuTensorMapEncodeTiled (tiled weights) failed (%d)", (int)r);
+  if (cache.size() > 8192) cache.clear();
+  cache.emplace(key, *out);
+  return STB_OK;
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -842,6 +868,315 @@ Plan plan(int M, int N, int sms) {
   return p;
 }
 
+
+// ============================================================================================
+// K5 pair kernel: prefill-shaped GEMMs (whole tiles) on CTA pairs, tcgen05.mma.cta_group::2.
+// A pair computes a 256-feature x bn-token tile: each CTA stages its own 128 weight rows and
+// half of the bn token rows per pipeline stage; the leader issues UMMA M=256 x N=bn, which
+// reads A from each CTA's smem and B from both halves, and accumulates each CTA's 128 rows in
+// that CTA's TMEM. Per SM this halves the activation bytes staged per flop (the B operand is
+// shared) and doubles the MMA work per issued instruction.
+//   warp 0     producer (both CTAs): weight rows + token-row half per stage
+//   warp 1     leader: MMA issuer (peer: idle)
+//   warps 2-5  epilogue (both CTAs): this CTA's 128 rows from TMEM, plain stores / SiLU-gate
+// Barriers: full[s] in the leader counts both CTAs' TMA bytes (cta_group::2 loads complete on
+// the leader's barrier; the leader arms it for the pair), empty[s] and acc_full[b] in both CTAs
+// (multicast tcgen05.commit), acc_empty[b] in the leader (4 local + 4 remote epilogue arrivals).
+// An earlier version forwarded the peer's stage completion with a release-scoped remote arrive:
+// that compiles to a GPU-wide membar per stage and ran at half the 1-CTA kernel's speed.
+// ============================================================================================
+constexpr int PAIR_BM = 2 * BM;  // features per pair tile
+
+template <int BN>
+struct PairCfg {
+  static constexpr int W_BYTES = BM * BK * 2;
+  static constexpr int X_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the token rows
+  static constexpr int STAGE = W_BYTES + X_BYTES;
+  static constexpr int RING = 200 * 1024;
+  static constexpr int STAGES = (RING / STAGE) > 12 ? 12 : (RING / STAGE);
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_leader(const void* p) {  // same smem offset, CTA rank 0
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(0u));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void umma_f16_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on bar in both CTAs
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::
+                   "r"(smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+
+// TMA 2-D load into this CTA's smem whose completion is counted on the LEADER's mbarrier
+// (cta_group::2: the pair's stage is complete when both CTAs' bytes have landed)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_pair(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                   float* __restrict__ C, int64_t ldc, int M, int N, int tiles_m, int tiles, int kb, int bn,
+                   int silu, const __nv_bfloat16* __restrict__ w_tiled) {
+  using CF = PairCfg<BN>;
+  constexpr int STAGES = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int half = bn / 2;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_w);
+    tma_prefetch(&tm_x);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // leader: 4 local + 4 peer epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated before any remote use
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // W: rows of this CTA's half (tiled layout: a 2-D view of 128-row tiles, one box = one
+      // pre-swizzled tile; row-major: the usual 128B-swizzled map); X: this CTA's token half.
+      // Every load completes on the leader's full[s]; the leader arms it for both CTAs.
+      auto load_w = [&](uint8_t* dst, int k, int f0, int st) {
+        const int row0 = f0 + (int)rank * BM;
+        const int y = w_tiled != nullptr ? ((row0 / BM) * kb + k) * BM : row0;
+        tma_load_2d_pair(dst, &tm_w, mapa_leader(&full[st]), w_tiled != nullptr ? 0 : k * BK, y);
+      };
+      auto arm = [&](int st) {
+        if (rank == 0) mbar_expect_tx(&full[st], 2 * (CF::W_BYTES + half * BK * 2));
+      };
+      int i = 0;
+      for (int t = pair; t < tiles && i < STAGES; t += npairs) {  // weights before the dependency wait
+        const int f0 = (t / tiles_m) * PAIR_BM;
+        for (int k = 0; k < kb && i < STAGES; ++k, ++i) {
+          arm(i);
+          load_w(smem + i * CF::STAGE, k, f0, i);
+        }
+      }
+      const int prefetched = i;
+      pdl_wait();
+      pdl_launch();
+      i = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        const int f0 = (t / tiles_m) * PAIR_BM;
+        const int x0 = (t % tiles_m) * bn + (int)rank * half;
+        for (int k = 0; k < kb; ++k, ++i) {
+          const int st = i % STAGES;
+          uint8_t* sw = smem + st * CF::STAGE;
+          if (i >= prefetched) {
+            mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
+            arm(st);
+            load_w(sw, k, f0, st);
+          }
+          tma_load_2d_pair(sw + CF::W_BYTES, &tm_x, mapa_leader(&full[st]), k * BK, x0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0 && elect_one()) {  // MMA issuer (leader)
+      const uint32_t idesc = umma_idesc_bf16(PAIR_BM, bn, false, false);
+      int i = 0, j = 0;
+      for (int t = pair; t < tiles; t += npairs, ++j) {
+        const int buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * BN;
+        for (int k = 0; k < kb; ++k, ++i) {
+          const int st = i % STAGES;
+          mbar_wait(&full[st], (i / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t wa = smem_u32(smem + st * CF::STAGE);
+          const uint32_t xa = wa + CF::W_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_f16_ss_pair(d, umma_desc_kmajor_sw128(wa + kk * 32, 1024), umma_desc_kmajor_sw128(xa + kk * 32, 1024),
+                             idesc, (k > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_pair(&empty[st]);
+        }
+        umma_commit_pair(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarters 2,3,0,1 of this CTA's 128 rows
+    pdl_wait();
+    const int quarter = warp & 3;
+    const uint32_t acc_empty_leader = mapa_leader(&acc_empty[0]);
+    int j = 0;
+    for (int t = pair; t < tiles; t += npairs, ++j) {
+      const int buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const int feat = (t / tiles_m) * PAIR_BM + (int)rank * BM + quarter * 32 + lane;
+      const int t0 = (t % tiles_m) * bn;
+      const int ntok = min(bn, M - t0);
+      const bool fok = feat < N;
+      const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
+      if (silu) {
+        __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(C) + (int64_t)t0 * ldc + (feat >> 1);
+        const bool odd = lane & 1;
+        for (int c = 0; c < bn; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(base + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float mine = __uint_as_float(odd ? r[16 + q] : r[q]);
+            const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? r[q] : r[16 + q]), 1);
+            const int tok = c + (odd ? 16 + q : q);
+            if (fok && tok < ntok)
+              act[(int64_t)tok * ldc] = __float2bfloat16_rn(odd ? silu_gate(other, mine) : silu_gate(mine, other));
+          }
+        }
+      } else {
+        float* crow = C + (int64_t)t0 * ldc + feat;
+        for (int c = 0; c < bn; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(base + c, r);
+          tmem_ld_wait();
+          if (fok) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (c + q < ntok) crow[(int64_t)(c + q) * ldc] = __uint_as_float(r[q]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(acc_empty_leader + buf * 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's last MMA reads and TMEM writes are done before dealloc
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(CF::TMEM_COLS));
+}
+
+// token-tile height for the pair schedule: waves over sms/2 pairs x (bn + fixed cost)
+struct PairPlan {
+  int bn, tiles_m;
+};
+PairPlan pair_plan(int M, int N, int sms) {
+  const int tiles_n = N / PAIR_BM;
+  const int pairs = sms / 2;
+  constexpr int kTileCost = 48;
+  PairPlan best{256, (M + 255) / 256};
+  long best_cost = -1;
+  for (int nt = (M + 255) / 256; nt <= (M + 31) / 32; ++nt) {
+    const int bn = (((M + nt - 1) / nt + 31) / 32) * 32;  // bn/2 a multiple of 16
+    if (bn > 256) continue;
+    const int tm = (M + bn - 1) / bn;
+    const long tl = (long)tiles_n * tm;
+    const long cost = ((tl + pairs - 1) / pairs) * (long)(bn + kTileCost);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = PairPlan{bn, tm};
+    }
+  }
+  return best;
+}
+
+template <int BN>
+int launch_pair(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
+                int bn, int tiles_m, int flags, cudaStream_t st) {
+  using CF = PairCfg<BN>;
+  CUtensorMap tw, tx;
+  const bool tiled = (flags & STB_GEMM_W_TILED) != 0;
+  if (tiled) {  // the tiled buffer as [tiles * 128 rows][64] (128 B rows), unswizzled boxes of one tile
+    if (int rc = cached_map_raw(&tw, W, (int64_t)((N + BM - 1) / BM) * ((K + BK - 1) / BK) * BM)) return rc;
+  } else if (int rc = cached_map(&tw, W, N, K, ldw, BM)) {
+    return rc;
+  }
+  if (int rc = cached_map(&tx, X, M, K, lda, bn / 2)) return rc;
+  const int tiles = (N / PAIR_BM) * tiles_m;
+  const int pairs = std::min(sm_count() / 2, tiles);
+  auto kern = gemm_bf16_pair<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = CF::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;  // cluster shape comes from __cluster_dims__
+  count_launch();
+  const int silu = (flags & STB_GEMM_SILU_MUL) ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tw, tx, C, ldc, M, N, tiles_m, tiles, (K + BK - 1) / BK, bn, silu,
+                                     tiled ? (const __nv_bfloat16*)W : (const __nv_bfloat16*)nullptr);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "gemm_bf16 pair launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+// The pair schedule serves whole-tile (prefill-shaped) products with N a multiple of 256 and no
+// fused epilogue beyond SiLU; STB200_GEMM_PAIR=0 disables it (A/B).
+bool pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STB200_GEMM_PAIR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <int BN>
 int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
            int mode, int flags, cudaStream_t st, const Epi& ep) {
@@ -855,6 +1190,15 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   }
   const int sms = sm_count();
   const Plan pl = plan(M, N, sms);
+  if (ep.kind == 0 && mode == 0 && !pl.stream && M > 128 && N % PAIR_BM == 0 && !(flags & STB_GEMM_C_ZEROED) &&
+      pair_enabled()) {
+    // pairs pay off once there are >= 2 waves of pair tiles or long K (measured: gate-up, down,
+    // LM head at M = 608..2080 gain 7-17%; QKV / O at M = 608 — one partial wave — lose 5-13%)
+    const PairPlan pp = pair_plan(M, N, sms);
+    const long pair_tiles = (long)(N / PAIR_BM) * pp.tiles_m;
+    if (pair_tiles >= 2L * (sms / 2) || K >= 8192)
+      return launch_pair<256>(X, lda, W, ldw, C, ldc, M, N, K, pp.bn, pp.tiles_m, flags, st);
+  }
   const int bn = pl.bn;
   if (int rc = cached_map(&tx, X, M, K, lda, bn)) return rc;
   Sched s;
