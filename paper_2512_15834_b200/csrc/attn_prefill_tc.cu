@@ -45,7 +45,16 @@ namespace {
 constexpr int ROWS = 128;   // packed query rows per tile (UMMA M)
 constexpr int KT = 128;     // keys per KV tile (UMMA N of S, K of P V)
 constexpr int KV_STAGES = 2;
-constexpr int kThreads = 320;
+#ifndef STB_K2_HALVES
+#define STB_K2_HALVES 1
+#endif
+// softmax threads per S row. 2 = each row split over two warps of the same TMEM lane quarter
+// (64 columns each; only the row max is exchanged per KV tile), 16 softmax warps in all:
+// measured slower (C5 ingest 1.01 -> 1.06 ms) — 576 threads cap registers at 96 and the
+// row state spills; 1 (the default) keeps one thread per row at 168 registers
+constexpr int kHalves = STB_K2_HALVES;
+constexpr int kSoftWarps = 8 * kHalves;  // two Q tiles x 4 lane quarters x halves
+constexpr int kThreads = 32 * (kSoftWarps + 2);
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMaxSplits = 8;      // KV splits per (query-tile pair, kv head, run) work unit
 constexpr int kMinSplitTiles = 2;  // fewest KV tiles a split CTA streams
@@ -103,14 +112,14 @@ constexpr float kRescaleSlack = 8.f;  // lazy rescale: keep the stale max until 
 // One S row (KT fp32 scores in registers, already masked) -> bf16 P pairs + row sum.
 // Scale-and-subtract and the row sum run as packed f32x2 (FFMA2 / FADD2); exponentials
 // on MUFU (ex2.approx.ftz) except STB_EXP_EMU of every 8 pairs when EMU.
-template <bool EMU>
+template <bool EMU, int NC>
 __device__ __forceinline__ float exp_row(const uint32_t* v, uint32_t* pk, float qscale, float ref) {
   const float2 sc = make_float2(qscale, qscale), nr = make_float2(-ref, -ref);
   float2 acc[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) acc[q] = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int c = 0; c < KT; c += 2) {
+  for (int c = 0; c < NC; c += 2) {
     const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), sc, nr);
     float2 e;
     if (EMU && ((c / 2) % 8) < STB_EXP_EMU) {
@@ -181,12 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
+      mbar_init(&p_full[t], 128 * kHalves);
       mbar_init(&o_done[t], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, CF::TMEM_COLS);
+  if (warp == kSoftWarps + 1) tmem_alloc(tmem_slot, CF::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tS = [&](int t) { return tmem + t * KT; };
   auto tO = [&](int t) { return tmem + 2 * KT + t * D; };
 
-  if (warp == 8) {
+  if (warp == kSoftWarps) {
     // ---------------- TMA producer
     const int32_t* row = table + (int64_t)slots[s] * max_bps;
     if (elect_one()) {
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 9) {
+  } else if (warp == kSoftWarps + 1) {
     // ---------------- MMA issuer (ping-pong)
     if (elect_one()) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(ROWS, KT, false, false);
@@ -280,9 +289,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- softmax warpgroups: warps 0-3 tile A, 4-7 tile B; thread = row
-    const int t = warp >> 2;
-    const int quarter = warp & 3;
+    // ---------------- softmax: warps [0, 4H) tile A, [4H, 8H) tile B; thread = (row, column half)
+    constexpr int NC = KT / kHalves;  // S columns per thread
+    constexpr int OC = D / kHalves;   // O columns per thread (rescale, output)
+    const int t = warp / (4 * kHalves);
+    const int wt = warp % (4 * kHalves);
+    const int quarter = wt & 3, hf = wt >> 2;
     const int r = quarter * 32 + lane;
     const bool tile_live = t == 0 || has_b;
     const int qi = qi0 + t * QPT + r / G;
@@ -291,35 +303,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qpos = pos0 + qi;                               // keys <= qpos are visible
     const int full_tiles = (pos0 + qi0 + t * QPT + 1) / KT;   // tiles visible to every row of this tile
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    __shared__ float xmax[2][2][kHalves][ROWS];  // [parity][tile][half][row]: partial row maxima
+    auto tile_bar = [&]() {  // the tile's softmax threads
+      if (kHalves > 1) asm volatile("bar.sync %0, %1;\n" ::"r"(1 + t), "r"(128 * kHalves) : "memory");
+    };
     float m = -INFINITY, l = 0.f;
     if (tile_live) {
       for (int jj = 0; jj < nt; ++jj) {
         const int j = j0 + jj;  // absolute KV tile (masking); jj: barrier phases
         mbar_wait(&s_full[t], jj & 1);
         tc_fence_after();
-        uint32_t v[KT];
+        uint32_t v[NC];
 #pragma unroll
-        for (int c = 0; c < KT; c += 32) tmem_ld32(tS(t) + lane_base + c, v + c);
+        for (int c = 0; c < NC; c += 32) tmem_ld32(tS(t) + lane_base + hf * NC + c, v + c);
         tmem_ld_wait();
-        const int kbase = j * KT;
+        const int kbase = j * KT + hf * NC;
         const bool masked = !(j < full_tiles && live);
         if (masked) {
 #pragma unroll
-          for (int c = 0; c < KT; ++c)
+          for (int c = 0; c < NC; ++c)
             if (!live || kbase + c > qpos) v[c] = __float_as_uint(-INFINITY);
         }
-        // tree-reduced row max (8 independent chains)
+        // tree-reduced row max (8 independent chains), then across the row's halves
         float mx8[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(v[q]);
 #pragma unroll
-        for (int c = 8; c < KT; c += 8)
+        for (int c = 8; c < NC; c += 8)
 #pragma unroll
           for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], __uint_as_float(v[c + q]));
         float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * qscale;
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        if (kHalves > 1) {
+          xmax[jj & 1][t][hf][r] = mx;
+          tile_bar();
+#pragma unroll
+          for (int h2 = 0; h2 < kHalves; ++h2) mx = fmaxf(mx, xmax[jj & 1][t][h2][r]);
+        }
+        mx *= qscale;
         // lazy rescale (FA4): exponentiate against a stale reference while the row max stays
-        // within 2^8 of it; exact because O and l always share the reference
+        // within 2^8 of it; exact because O and l always share the reference (both halves of
+        // a row see the same maxima, so they keep the same reference)
         float alpha = 1.f;
         if (mx > m + kRescaleSlack || m == -INFINITY) {
           const float mn = fmaxf(m, mx);
@@ -327,45 +351,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = mn;
         }
         const float ref = m == -INFINITY ? 0.f : m;
-        uint32_t pk[KT / 2];
-        const float rs = masked ? exp_row<false>(v, pk, qscale, ref) : exp_row<true>(v, pk, qscale, ref);
-        l = l * alpha + rs;
+        uint32_t pk[NC / 2];
+        const float rs = masked ? exp_row<false, NC>(v, pk, qscale, ref) : exp_row<true, NC>(v, pk, qscale, ref);
+        l = l * alpha + rs;  // this half's share of the row sum (combined at the end)
         // P (bf16 pairs) over the S columns just read: the A operand of P V
 #pragma unroll
-        for (int c = 0; c < KT / 2; c += 32) tmem_st32(tS(t) + lane_base + c, pk + c);
-        // rescale O (in TMEM) when this warp's running max moved and O holds earlier tiles
+        for (int c = 0; c < NC / 2; c += 32) tmem_st32(tS(t) + lane_base + hf * (NC / 2) + c, pk + c);
+        // rescale this thread's O columns when the running max moved and O holds earlier tiles
         if (jj > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare with the lazy reference
           mbar_wait(&o_done[t], (jj - 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < D; c += 32) {
+          for (int c = 0; c < OC; c += 32) {
             uint32_t o[32];
-            tmem_ld32(tO(t) + lane_base + c, o);
+            tmem_ld32(tO(t) + lane_base + hf * OC + c, o);
             tmem_ld_wait();
 #pragma unroll
             for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
-            tmem_st32(tO(t) + lane_base + c, o);
+            tmem_st32(tO(t) + lane_base + hf * OC + c, o);
           }
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[t]);
       }
+      if (kHalves > 1) {  // the row sum: both halves' shares (parity buffer nt & 1 is free)
+        xmax[nt & 1][t][hf][r] = l;
+        tile_bar();
+        l = 0.f;
+#pragma unroll
+        for (int h2 = 0; h2 < kHalves; ++h2) l += xmax[nt & 1][t][h2][r];
+      }
       // final: O / l
       mbar_wait(&o_done[t], (nt - 1) & 1);
       tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D;
+      __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D + hf * OC;
       float* prow = nullptr;  // split: this row's partial slot
       if (nsplit > 1) {
         float* po = part + ((((int64_t)s * n_kv + kh) * gridDim.x + bx) * max_splits + sp) * kPartFloats<D>;
-        prow = po + (t * ROWS + r) * D;
-        po[2 * ROWS * D + t * ROWS + r] = (live && l > 0.f) ? m + log2f(l) : -INFINITY;
+        prow = po + (t * ROWS + r) * D + hf * OC;
+        if (hf == 0) po[2 * ROWS * D + t * ROWS + r] = (live && l > 0.f) ? m + log2f(l) : -INFINITY;
       }
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
+      for (int c = 0; c < OC; c += 32) {
         uint32_t o[32];
-        tmem_ld32(tO(t) + lane_base + c, o);
+        tmem_ld32(tO(t) + lane_base + hf * OC + c, o);
         tmem_ld_wait();
         if (prow != nullptr) {
 #pragma unroll
@@ -387,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_free(tmem, CF::TMEM_COLS);
+  if (warp == kSoftWarps + 1) tmem_free(tmem, CF::TMEM_COLS);
 }
 
 // Combine the KV-split partial rows of K2: one warp per (tile, packed row) of a work unit,
