@@ -107,7 +107,7 @@ int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, con
 /* Same, told how many (query-tile pair, kv head, run) work units hold queries
  * (0 = unknown; a query-tile pair is 2*128/G query tokens): a launch with fewer
  * units than half the SMs (e.g. one 33-token verify pass = 8 units) splits each
- * unit's KV range over up to 8 CTAs, and a second small kernel merges the
+ * unit's KV range over up to 18 CTAs, and a second small kernel merges the
  * partial rows by log-sum-exp.                                               */
 int stb_attn_prefill_split(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                            const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,

@@ -56,7 +56,7 @@ constexpr int kHalves = STB_K2_HALVES;
 constexpr int kSoftWarps = 8 * kHalves;  // two Q tiles x 4 lane quarters x halves
 constexpr int kThreads = 32 * (kSoftWarps + 2);
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kMaxSplits = 8;      // KV splits per (query-tile pair, kv head, run) work unit
+constexpr int kMaxSplits = 18;     // KV splits per (query-tile pair, kv head, run) work unit (8 units x 18 = 144 CTAs)
 constexpr int kMinSplitTiles = 2;  // fewest KV tiles a split CTA streams
 template <int D>
 constexpr int kPartFloats = 2 * ROWS * (D + 1);  // one split's partial rows: O/l of both tiles + lse
