@@ -1194,9 +1194,11 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
       pair_enabled()) {
     // pairs pay off once there are >= 2 waves of pair tiles or long K (measured: gate-up, down,
     // LM head at M = 608..2080 gain 7-17%; QKV / O at M = 608 — one partial wave — lose 5-13%)
+    // (QKV / O-shaped products, N <= 8192 with K = 4096, measured from 0.56 to 0.79 on the pair
+    // path across boxes vs a steady 0.77-0.80 on the 1-CTA kernel: they stay there)
     const PairPlan pp = pair_plan(M, N, sms);
     const long pair_tiles = (long)(N / PAIR_BM) * pp.tiles_m;
-    if (pair_tiles >= 2L * (sms / 2) || K >= 8192)
+    if ((pair_tiles >= 2L * (sms / 2) && N > 8192) || K >= 8192)
       return launch_pair<256>(X, lda, W, ldw, C, ldc, M, N, K, pp.bn, pp.tiles_m, flags, st);
   }
   const int bn = pl.bn;

@@ -6,6 +6,10 @@ set -x
 OUT=${1:-gpurun_out}
 CTX=${CTX:-2048}
 mkdir -p $OUT
+# microbenchmarks first: after the ncu replay sessions the GPU runs tensor-heavy kernels
+# ~25% slower for a while (power / thermal state), which skewed earlier tables
+timeout 300 python tools/bench_kernels.py --what gemm,attn,prefill,small \
+  --prefill-cases 4x2048x2048,1x2048x34816,8x512x4096,32x33x4096,1x33x2150,1x600x2700 > $OUT/kernels.txt 2>&1
 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches_decode.csv python tools/profile_step.py --profile --steps 8 --profile-steps 2 --ctx $CTX > /dev/null 2>&1
 python tools/launch_table.py $OUT/launches_decode.csv 2 > $OUT/launches_decode.txt
@@ -20,6 +24,4 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:attn
   -o $OUT/full_prefill python tools/bench_kernels.py --what prefill > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:attn_prefill_tc -c 1 \
   -o $OUT/full_prefill_c5 python tools/bench_kernels.py --what prefill --prefill-cases 1x2048x34816 > /dev/null 2>&1
-timeout 300 python tools/bench_kernels.py --what gemm,attn,prefill,small \
-  --prefill-cases 4x2048x2048,1x2048x34816,8x512x4096,32x33x4096,1x33x2150,1x600x2700 > $OUT/kernels.txt 2>&1
 ls -la $OUT
