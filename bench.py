@@ -229,6 +229,7 @@ def workload_config(args) -> dict:
     c = CONFIGS[args.config]
     prompt = args.trace.get("prompt_tokens", 2048)
     return {"workload": c["label"], "config_id": args.config, "shape": args.shape,
+            "engine_mode": getattr(args, "engine_mode", "tool_cache"),
             "agents_per_gpu": args.agents, "prompt_tokens": prompt, "draft_latency_s": 0.05, "accept_rate": 0.8,
             "layers": args.layers, "parallelism": f"replicas x{args.gpus}",
             "l2": "working set > L2 (weights + KV streamed every step)"}
@@ -261,7 +262,7 @@ def run_b200(args, world, rank, local):
                       max_ctx=args.max_ctx, max_step_tokens=args.max_step_tokens)
     rt.precapture(args.agents)
     loop = RealtimeLoop()
-    engine = B200Engine(loop, engine_config(args.agents), runtime=rt)
+    engine = B200Engine(loop, engine_config(args.agents, args.engine_mode), runtime=rt)
     fleet = Fleet(engine, loop, TraceSpec(seed=args.seed, **args.trace), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
@@ -401,6 +402,8 @@ def main():
     ap.add_argument("--max-step-tokens", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--engine-mode", default="tool_cache", choices=["tool_cache", "prefix", "vanilla"],
+                    help="tool_cache (the paper's engine-side path, default) or the evict + re-prefill baselines")
     ap.add_argument("--k2-stats", action="store_true", help="diagnostics: K2 run shapes of the mixed steps")
     args = ap.parse_args()
     world, rank, local = dist_setup()

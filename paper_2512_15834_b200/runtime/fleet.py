@@ -99,7 +99,15 @@ class Fleet:
             slot += 1
 
 
-def engine_config(agents: int) -> EngineConfig:
+ENGINE_MODES = {  # the paper's three engine variants (Eqs. 3-5; reference engine.py:245-255,374-387)
+    "tool_cache": (True, True),   # tool output ingested in place into the resident sequence
+    "prefix": (True, False),      # every tool call evicts down to the turn base, then re-prefills
+    "vanilla": (False, False),    # every tool call evicts everything, then re-prefills it all
+}
+
+
+def engine_config(agents: int, mode: str = "tool_cache") -> EngineConfig:
     # rates are virtual-time charges; the wall-clock engine ignores them
-    return EngineConfig(prefill_rate=0.0, decode_rate=0.0, batch_size=max(64, agents), prefix_cache=True,
-                        tool_cache=True)
+    prefix, tool = ENGINE_MODES[mode]
+    return EngineConfig(prefill_rate=0.0, decode_rate=0.0, batch_size=max(64, agents), prefix_cache=prefix,
+                        tool_cache=tool)
