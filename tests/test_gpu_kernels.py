@@ -136,6 +136,29 @@ def test_gemm_w_tiled(lib, M, N, K):
         assert rel(act, want) < 1e-2
 
 
+@pytest.mark.parametrize("M,N,K,tiled", [(608, 4096, 14336, True), (608, 4096, 14336, False), (608, 28672, 4096, True),
+                                         (2080, 9216, 4096, False), (700, 10240, 2048, True)])
+def test_gemm_pair_cta_group2(lib, M, N, K, tiled):
+    """K5 pair kernel (CTA pairs, tcgen05.mma.cta_group::2): prefill-shaped products with
+    N > 8192 or K >= 8192 take it; plain stores and the SiLU-gate epilogue, ragged M."""
+    from paper_2512_15834_b200.runtime.decoder import TiledWeight
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (0.05 * torch.randn(N, K, device="cuda", generator=g)).to(torch.bfloat16)
+    wt, ldw, fl = (TiledWeight(w), 0, 4) if tiled else (w, K, 0)
+    assert not lib.load().stb_gemm_is_stream(M, N, K)  # whole tiles: pair-eligible shapes
+    ref = a.float() @ w.float().T
+    c = torch.full((M, N), float("nan"), device="cuda")
+    lib.call("stb_gemm_bf16", P(a), K, P(wt), ldw, P(c), N, M, N, K, 0, fl, stream())
+    torch.cuda.synchronize()
+    assert rel(c, ref) < 2e-5
+    act = torch.full((M, N // 2), float("nan"), device="cuda").to(torch.bfloat16)
+    lib.call("stb_gemm_bf16", P(a), K, P(wt), ldw, P(act), N // 2, M, N, K, 0, fl | 2, stream())
+    want = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+    assert rel(act, want) < 1e-2
+
+
 def _epi(**kw):
     from paper_2512_15834_b200.runtime.decoder import GemmEpi
 
