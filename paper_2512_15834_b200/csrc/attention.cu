@@ -12,6 +12,7 @@
 // query heads that share a kv head are rows of one 16-row MMA tile, so each K/V
 // page is read from HBM exactly once per step for the whole group. Softmax is
 // online (exp2 domain) with quad shuffles; rows of one warp live in one quad.
+#include <algorithm>
 #include <cstdlib>
 
 #include "../../include/stb200.h"
@@ -267,7 +268,10 @@ __device__ __forceinline__ void load_q(uint32_t (*qf)[4], const __nv_bfloat16* r
 // written out directly; a pair split across warps gets a partial (o/l, lse)
 // from each contributor and the last one to finish (ticket) merges them, so no
 // separate merge launch and no wave tail, whatever the context lengths.
-constexpr int kMaxB = 1024;
+#ifndef STB_K3_MAXB
+#define STB_K3_MAXB 1024
+#endif
+constexpr int kMaxB = STB_K3_MAXB;  // sequences per decode launch (static smem: ~16 B each)
 #ifndef STB_K3_PAGES
 #define STB_K3_PAGES 1
 #endif
@@ -776,7 +780,18 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (2 * (kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2 + 4 * (4 * kMaxB + 2)) <= 220 * 1024 ? 2 : 1) * sms;
+  constexpr size_t smem = (size_t)kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
+  auto kern = attn_decode_kernel<D, G, kDecodeStages>;
+  static bool attr = false;
+  static int per_sm = 1;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kDecWarps, smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    per_sm = std::min(per_sm, 2);
+    attr = true;
+  }
+  const int grid = per_sm * sms;
   const int W = grid * kDecWarps;
   const size_t need = (size_t)W * 2 * G * (D + 1);
   const int pairs = B * n_kv;
@@ -796,13 +811,6 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
         return fail(STB_ENOMEM, "attn_decode tickets");
       sc.n_tickets = nt;
     }
-  }
-  constexpr size_t smem = (size_t)kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
-  auto kern = attn_decode_kernel<D, G, kDecodeStages>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
   }
   float* o_part = sc.part;
   float* lse_part = sc.part + (size_t)W * 2 * G * D;
