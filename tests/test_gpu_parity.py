@@ -135,6 +135,21 @@ def test_timeline_parity_fused_epilogues(golden, monkeypatch, shape, case):
     pair.check()
 
 
+@pytest.mark.parametrize("shape,prompt", [(TINY, 6000), (QWEN3_MINI, 2500)], ids=["tiny-6k", "qwen3mini-2.5k"])
+@pytest.mark.parametrize("case", ["full_hit", "partial_hit", "two_turn_mixed"])
+def test_long_context_parity(shape, prompt, case):
+    """Long resident contexts (config C5's regime, at oracle size): multi-thousand-token prompt
+    prefills (K2 causal, many KV tiles), verify passes and in-place ingests against a long
+    cached prefix (K2 KV split), decode over long pages (K3) — the GPU engine equals the oracle
+    engine event for event, ids and block tables bit-exact, logits within 2e-2."""
+    pair = Pair(shape)
+    got, _ = S.run_timeline(API, case, pair.gpu, prompt=prompt)
+    ora, _ = S.run_timeline(API, case, pair.oracle, prompt=prompt)
+    assert got == ora
+    assert any(f"prefill tokens={prompt}" in e for e in got["events"])
+    pair.check()
+
+
 def test_default_engine_is_native():
     """`EngineSim(sim, config)` builds the CUDA runtime; its kernels really ran."""
     from paper_2512_15834_b200 import EngineConfig, EngineSim, Simulator
