@@ -266,14 +266,16 @@ def run_b200(args, world, rank, local):
     fleet = Fleet(engine, loop, TraceSpec(seed=args.seed, **args.trace), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
-    state = {"i": 0, "timed": None}
+    state = {"i": 0, "timed": None, "idle_s": 0.0}
 
     def one_step():
         while True:
             loop._fire_due()
             if rt.busy():
                 break
+            t_idle = time.perf_counter()
             time.sleep(0.0005)
+            state["idle_s"] += time.perf_counter() - t_idle  # nothing runnable: agents wait on tools
         # kernel roofline timers ride on 1 step in TIMER_STRIDE (their graph event nodes
         # cost ~9 us each; every-step timing would distort the measured step)
         if state["timed"] is not None:
@@ -286,19 +288,33 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     state["timed"] = {}
+    state["idle_s"] = 0.0
     if args.k2_stats:
         rt.dec.run_log = []
     events = rt.dec.step_events = []
     h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
     launches0 = lib.load().stb_launch_count() + rt.dec.graph_kernels
     resume0 = len(engine.resume_latencies)
+    prof = None
+    if os.environ.get("BENCH_HOST_PROFILE"):  # diagnostics: host-side profile of the timed loop
+        import cProfile
+
+        prof = cProfile.Profile()
     with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
         w0 = time.perf_counter()
+        if prof is not None:
+            prof.enable()
         for _ in range(args.steps):
             one_step()
+        if prof is not None:
+            prof.disable()
         torch.cuda.synchronize()
         w1 = time.perf_counter()
+    if prof is not None:
+        import pstats
+
+        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(25)
     barrier(world)
     emitted = rt.emitted - em0
     rt.drain()
@@ -368,7 +384,8 @@ def run_b200(args, world, rank, local):
         "step_mix": {"decode_steps": len(graphed), "decode_ms_avg": round(sum(graphed) / max(1, len(graphed)), 3),
                      "mixed_steps": len(mixed), "mixed_ms_avg": round(sum(m for m, _ in mixed) / max(1, len(mixed)), 3),
                      "mixed_tokens_avg": round(sum(t for _, t in mixed) / max(1, len(mixed)), 1),
-                     "wall_ms_per_step": round(wall_s / args.steps * 1e3, 3)},
+                     "wall_ms_per_step": round(wall_s / args.steps * 1e3, 3),
+                     "host_idle_ms_per_step": round(state["idle_s"] / args.steps * 1e3, 3)},
     }
     print(json.dumps(line), flush=True)
     if args.k2_stats and rt.dec.run_log is not None:  # K2 launch shapes of the timed mixed steps
