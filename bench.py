@@ -207,7 +207,7 @@ CONFIGS = {
     "c3": {"shape": "qwen3-32b", "agents": 64, "per_gpu": False, "max_ctx": 16384, "trace": {},
            "label": "C3 qwen3-32b-shaped (qk-norm) random-init bf16, 64 agents sharded over the replicas, "
                     "tool-call trace as C2"},
-    "c5": {"shape": "llama3-8b", "agents": 16, "per_gpu": True, "max_ctx": 49152,
+    "c5": {"shape": "llama3-8b", "agents": 16, "per_gpu": True, "max_ctx": 49152, "max_step_tokens": 36864,
            "trace": {"prompt_tokens": 32768, "output": (2048, 2048)},
            "label": "C5 KV-pressure: llama3-8b-shaped random-init bf16, 16 agents/GPU, 32k-token resident "
                     "contexts, 2k-token tool outputs"},
@@ -223,6 +223,8 @@ def resolve(args, world: int) -> None:
     args.scaling = "weak" if c["per_gpu"] else "strong"
     args.trace = dict(c["trace"])
     args.max_ctx = c["max_ctx"]
+    if not args.max_step_tokens:  # a 32k-token prompt is one packed run: size the step for it
+        args.max_step_tokens = c.get("max_step_tokens", 8192)
 
 
 def workload_config(args) -> dict:
@@ -321,6 +323,8 @@ def run_b200(args, world, rank, local):
     rt.dec.timers = state["timed"]
     rt.dec.step_events = None
     per = [(a.elapsed_time(b), g, T) for a, b, g, T in events]
+    # device idle between consecutive steps (end of step k -> start of step k+1)
+    gaps = [events[k][1].elapsed_time(events[k + 1][0]) for k in range(len(events) - 1)]
     dev_s = sum(ms for ms, _, _ in per) / 1e3
     graphed = [ms for ms, g, _ in per if g]
     mixed = [(ms, T) for ms, g, T in per if not g]
@@ -385,7 +389,11 @@ def run_b200(args, world, rank, local):
                      "mixed_steps": len(mixed), "mixed_ms_avg": round(sum(m for m, _ in mixed) / max(1, len(mixed)), 3),
                      "mixed_tokens_avg": round(sum(t for _, t in mixed) / max(1, len(mixed)), 1),
                      "wall_ms_per_step": round(wall_s / args.steps * 1e3, 3),
-                     "host_idle_ms_per_step": round(state["idle_s"] / args.steps * 1e3, 3)},
+                     "host_idle_ms_per_step": round(state["idle_s"] / args.steps * 1e3, 3),
+                     "device_gap_ms_per_step": round(sum(gaps) / max(1, len(gaps)), 3),
+                     "device_gap_max_ms": round(max(gaps), 3) if gaps else 0.0,
+                     "device_gap_ms_over_1ms": round(sum(g for g in gaps if g > 1.0), 3),
+                     "device_gap_p50_ms": round(sorted(gaps)[len(gaps) // 2], 3) if gaps else 0.0},
     }
     print(json.dumps(line), flush=True)
     if args.k2_stats and rt.dec.run_log is not None:  # K2 launch shapes of the timed mixed steps
@@ -416,7 +424,7 @@ def main():
     ap.add_argument("--shape", default="", help="override the config's model shape")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--max-step-tokens", type=int, default=8192)
+    ap.add_argument("--max-step-tokens", type=int, default=0, help="default: 8192 (c5: 36864)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine-mode", default="tool_cache", choices=["tool_cache", "prefix", "vanilla"],

@@ -58,8 +58,13 @@ def interleave_gate_up(w: torch.Tensor, d_ff: int) -> None:
     w._stb_gate_up_interleaved = True   # include/stb200.h STB_GEMM_C_ZEROED
 GEMM_W_TILED = 4    # include/stb200.h STB_GEMM_W_TILED
 CLEAR_MAX = 256     # consumers clear up to this many rows they read (decode-sized steps)
-GRAPH_MAX_T = 192   # mixed steps up to this many tokens ...
-GRAPH_MAX_RUNS = 2  # ... and append-prefill runs are replayed from CUDA graphs
+# Mixed steps (verify passes, small ingests) can be replayed from CUDA graphs too, but their
+# shapes keep changing with the batch (B, T, R, max_q), so captures — each a ~10 ms host stall
+# the GPU idles through — outnumber the replays that pay them back; measured on C2: no gain
+# in the verify steps (their host launch is hidden behind the previous step), 0.25 ms/step of
+# device idle from captures. Off by default (STB200_GRAPH_MIXED=1 enables).
+GRAPH_MAX_T = 192 if os.environ.get("STB200_GRAPH_MIXED") == "1" else 0
+GRAPH_MAX_RUNS = 2
 GRAPH_CACHE = 48    # captured graphs kept
 PROJECTIONS = ("wqkv", "wo", "w_gate_up", "w_down")
 

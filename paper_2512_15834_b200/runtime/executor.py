@@ -169,6 +169,10 @@ class Runtime:
     def precapture(self, max_batch: int) -> None:
         """Capture the decode-step CUDA graphs for B = 1..max_batch up front (timed and
         untimed variants) against a scratch slot, so no capture lands in a timed run."""
+        # size the step buffers for the largest packed step up front: growing them later would
+        # drop every captured graph (they point at the buffers) and recapture them mid-run
+        cap_t = getattr(self, "max_step_tokens", 0) + max_batch + 64
+        self.dec._ensure(cap_t, min(cap_t, 512), max(max_batch, 64))
         scratch = self._free_slots.pop(0)  # highest slot id: the last one handed out
         self.pool.reserve(scratch, 16)
         z = np.zeros
