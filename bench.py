@@ -38,7 +38,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-TIMER_STRIDE = 16
+TIMER_STRIDE = 32  # 1 step in 32 carries the kernel timers (their event nodes cost ~9 us each)
 METRIC = "agent tokens/sec (whole box) at N concurrent agents; tool-resume latency ms"
 REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
            "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
