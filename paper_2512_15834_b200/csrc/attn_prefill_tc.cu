@@ -57,7 +57,10 @@ constexpr int kSoftWarps = 8 * kHalves;  // two Q tiles x 4 lane quarters x halv
 constexpr int kThreads = 32 * (kSoftWarps + 2);
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMaxSplits = 18;     // KV splits per (query-tile pair, kv head, run) work unit (8 units x 18 = 144 CTAs)
-constexpr int kMinSplitTiles = 2;  // fewest KV tiles a split CTA streams
+#ifndef STB_K2_MIN_SPLIT_TILES
+#define STB_K2_MIN_SPLIT_TILES 1
+#endif
+constexpr int kMinSplitTiles = STB_K2_MIN_SPLIT_TILES;  // fewest KV tiles a split CTA streams
 template <int D>
 constexpr int kPartFloats = 2 * ROWS * (D + 1);  // one split's partial rows: O/l of both tiles + lse
 
