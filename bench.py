@@ -393,7 +393,10 @@ def run_b200(args, world, rank, local):
                      "device_gap_ms_per_step": round(sum(gaps) / max(1, len(gaps)), 3),
                      "device_gap_max_ms": round(max(gaps), 3) if gaps else 0.0,
                      "device_gap_ms_over_1ms": round(sum(g for g in gaps if g > 1.0), 3),
-                     "device_gap_p50_ms": round(sorted(gaps)[len(gaps) // 2], 3) if gaps else 0.0},
+                     "device_gap_p50_ms": round(sorted(gaps)[len(gaps) // 2], 3) if gaps else 0.0,
+                     "decode_ms_p50_p90_max": [round(sorted(graphed)[len(graphed) // 2], 3),
+                                               round(sorted(graphed)[int(len(graphed) * 0.9)], 3),
+                                               round(max(graphed), 3)] if graphed else None},
     }
     print(json.dumps(line), flush=True)
     if args.k2_stats and rt.dec.run_log is not None:  # K2 launch shapes of the timed mixed steps
