@@ -150,6 +150,35 @@ def test_long_context_parity(shape, prompt, case):
     pair.check()
 
 
+@pytest.mark.parametrize("when,fate", [(3.0, "full_hit"), (9.0, "miss")])
+def test_wire_submission_gpu(when, fate):
+    """a tool output POSTed to /cache-tool-output of the live engine's store
+    (wire bytes -> CacheEntry -> interned draft ids) validates on the GPU (K4 against the verify
+    pass's forced samples) and ingests in place exactly as the oracle engine does."""
+    import json
+
+    from fastapi.testclient import TestClient
+
+    from paper_2512_15834_b200.engine import EngineConfig
+    from paper_2512_15834_b200.service import create_app
+    from paper_2512_15834_b200.sim import Simulator
+
+    pair = Pair()
+    runs = []
+    for factory in (pair.gpu, pair.oracle):
+        sim = Simulator()
+        engine = factory(sim, EngineConfig(prefill_rate=0.25, decode_rate=0.5, tool_cache=True))
+        client = TestClient(create_app(engine.store))
+        engine.submit_request("resp-1", S._script(API, [4], ['{"q": 1}']), 10, S.StubClient(sim, engine))
+        body = json.dumps([{"name": "lookup", "params": {"q": 1}, "output": "x" * 40}])
+        sim.schedule(when, lambda c=client, b=body: c.post("/cache-tool-output/resp-1", content=b))
+        sim.run_until_idle()
+        runs.append((list(engine.events), engine.sequences["resp-1"].fates, engine.evictions))
+    assert runs[0] == runs[1]
+    assert runs[0][1] == [fate]
+    pair.check()
+
+
 def test_default_engine_is_native():
     """`EngineSim(sim, config)` builds the CUDA runtime; its kernels really ran."""
     from paper_2512_15834_b200 import EngineConfig, EngineSim, Simulator
