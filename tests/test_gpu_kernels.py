@@ -601,3 +601,28 @@ def test_spec_validate(lib):
         assert acc[s].item() == a
         assert con[s].item() == (spans[s] if a >= spans[s] else a + 1)
         assert nl[s].item() == 100 * s + a + s % 2
+
+
+def test_error_paths(lib):
+    """C-ABI error convention: negative STB_E* codes with a message, mapped to the reference's
+    exception types (capacity -> KVCapacityError, the rest -> KernelError); nothing launches."""
+    from paper_2512_15834_b200.errors import KernelError, KVCapacityError, SpectoolError
+
+    a = torch.zeros(8, 100, device="cuda", dtype=torch.bfloat16)
+    w = torch.zeros(64, 100, device="cuda", dtype=torch.bfloat16)
+    c = torch.zeros(8, 64, device="cuda")
+    with pytest.raises(KernelError, match="multiple of 8"):  # K % 8 != 0
+        lib.call("stb_gemm_bf16", P(a), 100, P(w), 100, P(c), 64, 8, 64, 100 - 4 + 2, 0, 0, stream())
+    shape = ModelShape("t", 1, 256, 6, 2, 64, 64, 64)  # group 3: no decode kernel instance
+    pool = _pool(lib, shape, nb=8, slots=2, bps=4)
+    with pytest.raises(KVCapacityError):  # 8 blocks of 16 rows cannot hold 200 rows
+        pool.reserve(0, 200)
+    with pytest.raises(KernelError, match="unsupported"):
+        q = torch.zeros(1, 6, 64, device="cuda", dtype=torch.bfloat16)
+        pool.reserve(1, 16)
+        pool.sync(torch.cuda.current_stream().cuda_stream)
+        slots = torch.tensor([1], dtype=torch.int32, device="cuda")
+        ctx = torch.tensor([16], dtype=torch.int32, device="cuda")
+        ws = torch.empty(lib.load().stb_attn_decode_workspace(1, 6, 64) // 4, device="cuda")
+        lib.call("stb_attn_decode", pool.h, 0, P(q), P(q), P(slots), P(ctx), 1, 6, 0.125, 0, P(ws), stream())
+    assert issubclass(KernelError, SpectoolError) and issubclass(KVCapacityError, SpectoolError)
