@@ -66,7 +66,12 @@ struct Cfg {
   static constexpr int W_BYTES = BM * BK * 2;
   static constexpr int X_BYTES = BN * BK * 2;
   static constexpr int STAGE = W_BYTES + X_BYTES;
-  static constexpr int RING = 200 * 1024;  // measured best: bytes in flight beat SM co-residence
+#ifndef STB_GEMM_DECODE_RING_KB
+#define STB_GEMM_DECODE_RING_KB 200
+#endif
+  // decode-shaped tiles (BN <= 64) may use a smaller ring so that the next GEMM's CTAs can be
+  // resident next to this one's (STB_GEMM_DECODE_RING_KB, tuning); prefill tiles keep 200 KiB
+  static constexpr int RING = (BN <= 64 ? STB_GEMM_DECODE_RING_KB : 200) * 1024;
   static constexpr int STAGES = (RING / STAGE) > 12 ? 12 : (RING / STAGE);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
