@@ -179,6 +179,24 @@ def test_wire_submission_gpu(when, fate):
     pair.check()
 
 
+@pytest.mark.parametrize("base", ["llama3-8b", "qwen3-32b"])
+def test_full_width_parity(base):
+    """The BASELINE model widths (C2 Llama-3-8B: d 4096, ffn 14336, GQA 4; C3 Qwen3-32B: d 5120,
+    ffn 25600, GQA 8, qk-norm) at one layer and a 32k vocabulary (oracle-sized): a 300-token
+    prompt prefill (K2 on tcgen05, whole-tile and CTA-pair GEMMs), decode (stream-K GEMMs, K3),
+    draft validation and an in-place ingest, ids bit-exact and logits within 2e-2."""
+    import dataclasses
+
+    from paper_2512_15834_b200.modelcfg import SHAPES
+
+    shape = dataclasses.replace(SHAPES[base], name=f"{base}[L=1,V=32k]", layers=1, vocab=32768)
+    pair = Pair(shape)
+    got, _ = S.run_timeline(API, "full_hit", pair.gpu, prompt=300)
+    ora, _ = S.run_timeline(API, "full_hit", pair.oracle, prompt=300)
+    assert got == ora
+    pair.check()
+
+
 def test_default_engine_is_native():
     """`EngineSim(sim, config)` builds the CUDA runtime; its kernels really ran."""
     from paper_2512_15834_b200 import EngineConfig, EngineSim, Simulator
