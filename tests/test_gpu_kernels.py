@@ -626,3 +626,48 @@ def test_error_paths(lib):
         ws = torch.empty(lib.load().stb_attn_decode_workspace(1, 6, 64) // 4, device="cuda")
         lib.call("stb_attn_decode", pool.h, 0, P(q), P(q), P(slots), P(ctx), 1, 6, 0.125, 0, P(ws), stream())
     assert issubclass(KernelError, SpectoolError) and issubclass(KVCapacityError, SpectoolError)
+
+
+@pytest.mark.parametrize("case", ["decode_c2", "decode_c5", "ingest_c5"])
+def test_attention_full_size_invariant(lib, case):
+    """Size-independent property at BASELINE sizes (no fp32 reference needed): with every V row
+    equal to the same vector u, each attention output row is u whatever the scores — the
+    softmax weights of every split, merge and masked tile must sum to one. C2: 32 sequences at
+    ctx 4096 (K3); C5: 16 sequences at ctx 33k (K3) and a 2048-token ingest at ctx 34816 (K2)."""
+    shape = SHAPES[0]  # Llama-3-8B attention geometry
+    ctxs = {"decode_c2": [4096] * 32, "decode_c5": [33000] * 16, "ingest_c5": [34816]}[case]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(ctxs), bps=2304)
+    for b, c in enumerate(ctxs):
+        pool.reserve(b, c)
+    pool.sync(torch.cuda.current_stream().cuda_stream)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    u = torch.randn(shape.n_kv, shape.d_head, device="cuda", generator=g).to(torch.bfloat16)
+    for b, c in enumerate(ctxs):
+        k = (3.0 * torch.randn(c, shape.kv_dim, device="cuda", generator=g)).to(torch.bfloat16)
+        v = u.reshape(1, -1).expand(c, -1).contiguous()
+        slot_of = torch.full((c,), b, dtype=torch.int32, device="cuda")
+        pos = torch.arange(c, dtype=torch.int32, device="cuda")
+        lib.call("stb_kv_commit", pool.h, 0, P(k), P(v), shape.kv_dim, P(slot_of), P(pos), c, stream())
+    scale = 1 / math.sqrt(shape.d_head)
+    want = u.float().repeat_interleave(shape.n_q // shape.n_kv, dim=0)  # [n_q, d]
+    if case == "ingest_c5":
+        n = 2048
+        q = torch.randn(n, shape.n_q, shape.d_head, device="cuda", generator=g).to(torch.bfloat16)
+        out = torch.full_like(q, float("nan"))
+        slot0 = torch.zeros(1, dtype=torch.int32, device="cuda")
+        qstart = torch.tensor([0, n], dtype=torch.int32, device="cuda")
+        ctx0 = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+        lib.call("stb_attn_prefill", pool.h, 0, P(q), P(out), P(slot0), P(qstart), P(ctx0), 1, n, shape.n_q, scale, n,
+                 stream())
+    else:
+        B = len(ctxs)
+        q = torch.randn(B, shape.n_q, shape.d_head, device="cuda", generator=g).to(torch.bfloat16)
+        out = torch.full_like(q, float("nan"))
+        slots = torch.arange(B, dtype=torch.int32, device="cuda")
+        ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+        ws = torch.empty(lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.d_head) // 4, device="cuda")
+        lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, 0, P(ws),
+                 stream())
+    torch.cuda.synchronize()
+    err = (out.float() - want).abs().max().item()
+    assert err <= 2e-2 * want.abs().max().item(), err
