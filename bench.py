@@ -337,6 +337,7 @@ def run_b200(args, world, rank, local):
     # subtracted from every kernel's bracketed time
     ov_ms, _, ov_n = timers.pop("event_overhead", (0.0, 0, 0))
     ov = ov_ms / ov_n if ov_n else 0.0
+    k2_launches = timers.pop("attn_prefill:launches", [])
     kern = {name: (max(ms - n * ov, 1e-3 * ms) / 1e3, work, n) for name, (ms, work, n) in timers.items()}
     tot_emit, = reduce([float(emitted)], "sum", world, device)
     dev_max, wall_max = reduce([dev_s, wall_s], "max", world, device)
@@ -369,6 +370,15 @@ def run_b200(args, world, rank, local):
         bound, ach, peak, unit = rate(k)
         others[k] = {"bound": bound, "achieved": round(ach, 1), "unit": unit, "frac": round(ach / peak, 4),
                      "share_of_device_time": round(t / dev_s * TIMER_STRIDE, 4), "launches": n}
+    if k2_launches:  # K2 mixes HBM-bound verify passes (33 queries) with tensor-bound ingests
+        roof_t = sum(max(f / (tf_sus * 1e12), by / (hbm * 1e9)) for _, f, by in k2_launches)
+        meas_t = sum(max(ms - ov, 1e-3 * ms) / 1e3 for ms, _, _ in k2_launches)
+        hbm_t = sum(by / (hbm * 1e9) for _, f, by in k2_launches if by / (hbm * 1e9) > f / (tf_sus * 1e12))
+        entry = roof if roof and roof["kernel"] == "attn_prefill" else others.get("attn_prefill")
+        if entry is not None:
+            entry["roofline_frac"] = round(roof_t / meas_t, 4)
+            entry["hbm_bound_share_of_roofline_time"] = round(hbm_t / roof_t, 4)
+            entry["roofline_note"] = "per launch max(flops / sustained tensor peak, KV+q+o bytes / HBM peak)"
     cpu = (cpu_sample(SHAPES[args.shape], seconds_budget=args.cpu_seconds, batch=args.agents,
                       ctx=args.trace.get("prompt_tokens", 2048)) if not args.no_cpu else None)
     rs = sorted(resume)
@@ -413,6 +423,15 @@ def run_b200(args, world, rank, local):
         mixed_t = [(round(ms, 2), T) for ms, g, T in per if not g]
         for runs, mt in list(zip(steps, mixed_t))[:16]:
             print("  ", runs, "step ms, T =", mt, file=sys.stderr)
+        qd = SHAPES[args.shape].q_dim
+        by_flops = {int(4 * qd * float(sum(n * (c - n) + n * (n + 1) / 2 for n, c in runs))): runs for runs in steps}
+        per_launch = collections.defaultdict(list)
+        for ms, f, _ in k2_launches:
+            per_launch[f].append(max(ms - ov, 1e-3 * ms))
+        print("K2 timed launches (us avg, TFLOP/s, runs (n, ctx)):", file=sys.stderr)
+        for f, ts in sorted(per_launch.items(), key=lambda kv: -sum(kv[1])):
+            t = sum(ts) / len(ts) / 1e3
+            print(f"   {t * 1e6:8.1f} us x{len(ts):3d} {f / t / 1e12:7.1f} TF/s  {by_flops.get(f, '?')}", file=sys.stderr)
 
 
 def main():

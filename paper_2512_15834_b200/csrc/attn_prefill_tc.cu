@@ -311,17 +311,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (kHalves > 1) asm volatile("bar.sync %0, %1;\n" ::"r"(1 + t), "r"(128 * kHalves) : "memory");
     };
     float m = -INFINITY, l = 0.f;
+    // the softmax variant depends on the KV tile only, never on the row: a run whose query
+    // count is not a multiple of 32 rows leaves a warp of the last tile partly live, and a
+    // per-row choice ran both exp variants back to back on every KV tile of the longest CTA
+    // (+80% at n=996). Dead rows of such a warp exponentiate finite scores (keys below the
+    // first row's position, Q rows of the next run or TMA zero fill) and are never stored;
+    // a split writes lse = -inf for them, so the merge weighs them 0. Warps with no live row
+    // write zero P and skip the exponentials
+    const bool warp_dead = !__any_sync(0xffffffffu, live);
     if (tile_live) {
       for (int jj = 0; jj < nt; ++jj) {
         const int j = j0 + jj;  // absolute KV tile (masking); jj: barrier phases
         mbar_wait(&s_full[t], jj & 1);
         tc_fence_after();
+        if (warp_dead) {
+          if (kHalves > 1) {
+            xmax[jj & 1][t][hf][r] = -INFINITY;
+            tile_bar();
+          }
+          uint32_t pk[NC / 2];
+#pragma unroll
+          for (int c = 0; c < NC / 2; ++c) pk[c] = 0u;
+#pragma unroll
+          for (int c = 0; c < NC / 2; c += 32) tmem_st32(tS(t) + lane_base + hf * (NC / 2) + c, pk + c);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&p_full[t]);
+          continue;
+        }
         uint32_t v[NC];
 #pragma unroll
         for (int c = 0; c < NC; c += 32) tmem_ld32(tS(t) + lane_base + hf * NC + c, v + c);
         tmem_ld_wait();
         const int kbase = j * KT + hf * NC;
-        const bool masked = !(j < full_tiles && live);
+        const bool masked = j >= full_tiles;
         if (masked) {
 #pragma unroll
           for (int c = 0; c < NC; ++c)
@@ -350,7 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         float alpha = 1.f;
         if (mx > m + kRescaleSlack || m == -INFINITY) {
           const float mn = fmaxf(m, mx);
-          alpha = (m == -INFINITY || mn == -INFINITY) ? (m == -INFINITY ? 0.f : 1.f) : exp2f(m - mn);
+          // a row that saw only masked keys has P = 0, so O = 0 and l = 0: no rescale (alpha 1
+          // keeps dead rows off the O rescale path below)
+          alpha = m == -INFINITY ? 1.f : exp2f(m - mn);
           m = mn;
         }
         const float ref = m == -INFINITY ? 0.f : m;

@@ -238,6 +238,7 @@ class Decoder:
         self._seen: set = set()                  # mixed-step shapes already run eagerly once
         self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
         self._pre_flops = 0
+        self._pre_work = (0, 0)  # (flops, bytes) of one K2 launch: verify runs are HBM-bound, ingests tensor-bound
         self._pre_units = 0
         self.run_log: list | None = None
         self._pending: list | None = []             # (name, ev0, ev1, work) awaiting a sync
@@ -338,6 +339,9 @@ class Decoder:
             n = np.diff(b.pre_qstart).astype(np.float64)
             prev = b.pre_ctx.astype(np.float64) - n
             self._pre_flops = int(4 * self.shape.q_dim * float(np.sum(n * prev + n * (n + 1) / 2)))
+            # algorithmic bytes: every run's K/V read once plus its q and o rows
+            pre_bytes = int(np.sum(b.pre_ctx)) * 2 * self.shape.kv_dim * 2 + int(np.sum(n)) * 2 * self.shape.q_dim * 2
+            self._pre_work = (self._pre_flops, pre_bytes)
             # K2 work units holding queries: (query-tile pair of 2*128/G tokens, kv head, run)
             pair = 2 * 128 // (self.shape.n_q // self.shape.n_kv)
             self._pre_units = int(np.sum(np.ceil(n / pair))) * self.shape.n_kv
@@ -392,7 +396,7 @@ class Decoder:
             self.graph_replays += 1
             self.graph_kernels += self.graph_sizes.get(key, 0)
             if timed:
-                live = {"attn_decode": dec_bytes, "attn_prefill": self._pre_flops}
+                live = {"attn_decode": dec_bytes, "attn_prefill": self._pre_work}
                 for name, a0, a1, work in events:
                     self._pending.append((name, a0, a1, live.get(name, work)))
         if self.step_events is not None:
@@ -463,7 +467,7 @@ class Decoder:
                 call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()),
                      _p(self.attn[B:].data_ptr()), _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S,
                      T - B, s.n_q, self.scale, max_q, self._pre_units, st)
-                self._tock("attn_prefill", ev, self._pre_flops)
+                self._tock("attn_prefill", ev, self._pre_work)
             self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
             self._cleared("proj", clr)
@@ -500,7 +504,7 @@ class Decoder:
             call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                  _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                  self._pre_units, st)
-            self._tock("attn_prefill", ev, self._pre_flops)
+            self._tock("attn_prefill", ev, self._pre_work)
 
     def _launch_fused(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
                       dec_bytes: int) -> None:
@@ -589,9 +593,14 @@ class Decoder:
         if sink is not None:
             for name, e0, e1, work in pending:
                 t = sink.setdefault(name, [0.0, 0, 0])
-                t[0] += e0.elapsed_time(e1)
-                t[1] += work
+                ms = e0.elapsed_time(e1)
+                t[0] += ms
                 t[2] += 1
+                if isinstance(work, tuple):  # (flops, bytes): per-launch list for a max(tensor, hbm) roofline
+                    t[1] += work[0]
+                    sink.setdefault(name + ":launches", []).append((ms, *work))
+                else:
+                    t[1] += work
 
     def collect(self) -> None:
         self.fold(self.take_pending())

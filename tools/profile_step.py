@@ -92,6 +92,7 @@ def main():
     if args.timers:
         ov_t, _, ov_n = rt.dec.timers.pop("event_overhead", (0.0, 0, 0))
         ov = ov_t / ov_n if ov_n else 0.0
+        rt.dec.timers.pop("attn_prefill:launches", None)
         print(f"  (event-pair overhead {ov * 1e3:.2f} us per launch subtracted)")
         for name, (t, work, n) in rt.dec.timers.items():
             t = max(t - n * ov, 1e-3 * t)
