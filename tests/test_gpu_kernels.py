@@ -412,7 +412,8 @@ def test_attn_decode(lib, shape, ctxs):
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
-@pytest.mark.parametrize("runs", [[(1, 1)], [(4, 10), (21, 33)], [(300, 300), (33, 1200), (7, 8)]])
+@pytest.mark.parametrize("runs", [[(1, 1)], [(4, 10), (21, 33)], [(300, 300), (33, 1200), (7, 8)],
+                                  [(996, 3044), (33, 2174)]])  # C2 trace: ragged ingest + verify
 @pytest.mark.parametrize("amp", [1.0, 40.0], ids=["unit", "spiky"])
 def test_attn_prefill(lib, shape, runs, amp):
     # amp scales q: "spiky" scores span hundreds of log2 units, exercising the lazy
