@@ -13,6 +13,9 @@ forward of the continuous-batching engine over every resident sequence
   e2e    the same tokens / wall time of the K steps through the public API:
          host scheduling, timers, per-step H2D metadata + D2H sampled ids
   roofline  live CUDA-event timing of the dominant kernel over the timed region
+  mean_agent_tokens_per_s  the reference's mean per-agent throughput
+         (workload.py:275-277), elapsed = the timed window; plus the window's
+         tool-call fates, evictions and tool-resume latency
 
 N > 1 (torchrun): sessions are independent, so every rank is a replica with
 its own agents (C2/C5: a fixed count per GPU, weak scaling; C3: the config's
@@ -297,6 +300,7 @@ def run_b200(args, world, rank, local):
     h2d0, d2h0, em0 = rt.h2d_bytes, rt.d2h_bytes, rt.emitted
     launches0 = lib.load().stb_launch_count() + rt.dec.graph_kernels
     resume0 = len(engine.resume_latencies)
+    fates0, evict0 = fate_counts(engine), engine.evictions
     prof = None
     if os.environ.get("BENCH_HOST_PROFILE"):  # diagnostics: host-side profile of the timed loop
         import cProfile
@@ -331,6 +335,8 @@ def run_b200(args, world, rank, local):
     wall_s = w1 - w0
     launches = lib.load().stb_launch_count() + rt.dec.graph_kernels - launches0  # eager + graph-replayed
     resume = engine.resume_latencies[resume0:]
+    fates = {k: v - fates0.get(k, 0) for k, v in fate_counts(engine).items() if v - fates0.get(k, 0)}
+    evictions = engine.evictions - evict0
     timers = state["timed"]
     rt.dec.timers = None
     # per-launch overhead of an event pair inside the step (measured on empty pairs) is
@@ -339,7 +345,7 @@ def run_b200(args, world, rank, local):
     ov = ov_ms / ov_n if ov_n else 0.0
     k2_launches = timers.pop("attn_prefill:launches", [])
     kern = {name: (max(ms - n * ov, 1e-3 * ms) / 1e3, work, n) for name, (ms, work, n) in timers.items()}
-    tot_emit, = reduce([float(emitted)], "sum", world, device)
+    tot_emit, tot_agents = reduce([float(emitted), float(args.agents)], "sum", world, device)
     dev_max, wall_max = reduce([dev_s, wall_s], "max", world, device)
     if rank != 0:
         return
@@ -390,6 +396,10 @@ def run_b200(args, world, rank, local):
         "e2e": {"value": round(tot_emit / wall_max, 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": int((rt.h2d_bytes - h2d0) / args.steps),
                 "d2h_bytes_per_step": int((rt.d2h_bytes - d2h0) / args.steps)},
+        # the reference's mean per-agent throughput (workload.py:275-277: tokens / elapsed per
+        # agent), elapsed = the timed window's wall time; fates / evictions of this replica
+        "mean_agent_tokens_per_s": round(tot_emit / wall_max / tot_agents, 2),
+        "fates": fates, "evictions": evictions,
         "tool_resume_ms": {"p50": round(rs[len(rs) // 2] * 1e3, 2) if rs else None,
                            "p90": round(rs[int(len(rs) * 0.9)] * 1e3, 2) if rs else None, "count": len(rs)},
         "roofline": roof, "kernels": others, "gpu_launches": int(launches), "clocks": clocks.summary(),
@@ -432,6 +442,16 @@ def run_b200(args, world, rank, local):
         for f, ts in sorted(per_launch.items(), key=lambda kv: -sum(kv[1])):
             t = sum(ts) / len(ts) / 1e3
             print(f"   {t * 1e6:8.1f} us x{len(ts):3d} {f / t / 1e12:7.1f} TF/s  {by_flops.get(f, '?')}", file=sys.stderr)
+
+
+def fate_counts(engine) -> dict:
+    """Tool-call fates (full_hit / late_hit / partial_hit / miss) over every sequence so far."""
+    import collections
+
+    c = collections.Counter()
+    for seq in list(engine.sequences.values()):
+        c.update(seq.fates)
+    return dict(c)
 
 
 def main():
