@@ -672,3 +672,68 @@ def test_attention_full_size_invariant(lib, case):
     torch.cuda.synchronize()
     err = (out.float() - want).abs().max().item()
     assert err <= 2e-2 * want.abs().max().item(), err
+
+
+def test_attn_decode_max_batch_and_empty(lib):
+    """K3 at its per-launch maximum (STB_K3_MAXB = 1024 sequences, ragged contexts 1..97, so
+    the partition cuts many tiny pairs), one past it (EINVAL, nothing launched), and B = 0
+    (a no-op that leaves the output untouched)."""
+    from paper_2512_15834_b200.errors import KernelError
+
+    shape = SHAPES[0]
+    B = 1024
+    rng = random.Random(11)
+    ctxs = [rng.randint(1, 97) for _ in range(B)]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=B + 1, bps=16)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=4)
+    q = torch.randn(B + 1, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out = torch.full_like(q, float("nan"))
+    slots = torch.arange(B + 1, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs + [1], dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.load().stb_attn_decode_workspace(B + 1, shape.n_q, shape.d_head) // 4, device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, 0, P(ws), stream())
+    worst = 0.0
+    for b, (k, v) in enumerate(dense):
+        ref = _ref_attn(q[b:b + 1], k, v, torch.tensor([ctxs[b] - 1], device="cuda"), scale)
+        worst = max(worst, rel(out[b:b + 1], ref))
+    assert worst < 1e-2
+    assert torch.isnan(out[B].float()).all()  # row B is not part of the launch
+    with pytest.raises(KernelError, match="at most 1024"):
+        lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B + 1, shape.n_q, scale, 0, P(ws),
+                 stream())
+    keep = out.clone()
+    lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), 0, shape.n_q, scale, 0, P(ws), stream())
+    torch.cuda.synchronize()
+    assert torch.equal(out[:B], keep[:B])
+
+
+def test_attn_prefill_empty_runs(lib):
+    """K2 with empty runs between non-empty ones (q_start repeats) and S = 0: empty runs
+    launch no work and write nothing, the others match the fp32 reference."""
+    shape = SHAPES[0]
+    runs = [(0, 40), (37, 300), (0, 5), (1, 129)]
+    ctxs = [c for _, c in runs]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(runs), bps=64)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=9)
+    T = sum(n for n, _ in runs)
+    q = torch.randn(T, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out = torch.full_like(q, float("nan"))
+    qs = [0]
+    for n, _ in runs:
+        qs.append(qs[-1] + n)
+    slots = torch.arange(len(runs), dtype=torch.int32, device="cuda")
+    qstart = torch.tensor(qs, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    lib.call("stb_attn_prefill", pool.h, 0, P(q), P(out), P(slots), P(qstart), P(ctx), len(runs), T, shape.n_q,
+             scale, max(n for n, _ in runs), stream())
+    for s, ((n, c), (k, v)) in enumerate(zip(runs, dense)):
+        if n:
+            ref = _ref_attn(q[qs[s]:qs[s + 1]], k, v, torch.arange(c - n, c, device="cuda"), scale)
+            assert rel(out[qs[s]:qs[s + 1]], ref) < 1e-2, s
+    keep = out.clone()
+    lib.call("stb_attn_prefill", pool.h, 0, P(q), P(out), P(slots), P(qstart), P(ctx), 0, T, shape.n_q, scale, 1,
+             stream())
+    torch.cuda.synchronize()
+    assert torch.equal(out, keep)
