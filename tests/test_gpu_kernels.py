@@ -118,7 +118,8 @@ def test_weight_tile_layout(lib):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 256, 256), (32, 6144, 4096), (32, 4096, 14336), (17, 130, 200),
-                                   (300, 640, 1024), (608, 28672, 4096)])
+                                   (300, 640, 1024), (608, 28672, 4096),
+                                   (32, 128256, 4096), (65, 28672, 4096)])  # C2 LM head, verify-step gate-up
 def test_gemm_w_tiled(lib, M, N, K):
     """STB_GEMM_W_TILED: the same products from the tiled weight layout (both schedules)."""
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
