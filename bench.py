@@ -438,6 +438,11 @@ def run_b200(args, world, rank, local):
         per_launch = collections.defaultdict(list)
         for ms, f, _ in k2_launches:
             per_launch[f].append(max(ms - ov, 1e-3 * ms))
+        slow = sorted(range(len(per)), key=lambda k: -per[k][0])[:10]
+        print("slowest steps (index, ms, decode-only, tokens, event-timed):", file=sys.stderr)
+        for k in slow:
+            print(f"   {k:4d} {per[k][0]:8.2f} {per[k][1]!s:5s} {per[k][2]:5d} {(args.warmup + k) % TIMER_STRIDE == 0}",
+                  file=sys.stderr)
         print("K2 timed launches (us avg, TFLOP/s, runs (n, ctx)):", file=sys.stderr)
         for f, ts in sorted(per_launch.items(), key=lambda kv: -sum(kv[1])):
             t = sum(ts) / len(ts) / 1e3
