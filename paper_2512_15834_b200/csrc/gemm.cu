@@ -854,7 +854,10 @@ Plan plan(int M, int N, int sms) {
     p.stream = tiles_n >= 4 * sms ? 0 : 1;
     return p;
   }
-  constexpr int kTileCost = 48;  // per-tile fill/epilogue + smaller-tile inefficiency, in token columns
+#ifndef STB_GEMM_TILE_COST
+#define STB_GEMM_TILE_COST 48
+#endif
+  constexpr int kTileCost = STB_GEMM_TILE_COST;  // per-tile fill/epilogue + smaller-tile inefficiency, in token columns
   long best = -1;
   for (int nt = (M + 255) / 256; nt <= (M + 63) / 64; ++nt) {
     const int bn = (((M + nt - 1) / nt + 15) / 16) * 16;
@@ -1117,7 +1120,10 @@ struct PairPlan {
 PairPlan pair_plan(int M, int N, int sms) {
   const int tiles_n = N / PAIR_BM;
   const int pairs = sms / 2;
-  constexpr int kTileCost = 48;
+#ifndef STB_PAIR_TILE_COST
+#define STB_PAIR_TILE_COST 48
+#endif
+  constexpr int kTileCost = STB_PAIR_TILE_COST;
   PairPlan best{256, (M + 255) / 256};
   long best_cost = -1;
   for (int nt = (M + 255) / 256; nt <= (M + 31) / 32; ++nt) {
