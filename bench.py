@@ -82,7 +82,14 @@ class ClockSampler:
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
-            self.proc.wait()
+            try:  # never block the bench on a sampler stuck in a driver call
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                try:
+                    self.proc.wait(timeout=5)
+                except subprocess.TimeoutExpired:
+                    pass
 
     def summary(self) -> dict:
         sm, mx, reasons = [], 0.0, set()
@@ -274,6 +281,7 @@ def run_b200(args, world, rank, local):
     state = {"i": 0, "timed": None, "idle_s": 0.0}
 
     def one_step():
+        t_wait = time.perf_counter()
         while True:
             loop._fire_due()
             if rt.busy():
@@ -281,6 +289,9 @@ def run_b200(args, world, rank, local):
             t_idle = time.perf_counter()
             time.sleep(0.0005)
             state["idle_s"] += time.perf_counter() - t_idle  # nothing runnable: agents wait on tools
+            if t_idle - t_wait > IDLE_LIMIT_S:  # tools take <= 2 s: the engine is stuck, say so
+                raise RuntimeError(f"bench: no runnable step for {IDLE_LIMIT_S} s "
+                                   f"(resident {len(engine.sequences)} sequences, step {state['i']})")
         # kernel roofline timers ride on 1 step in TIMER_STRIDE (their graph event nodes
         # cost ~9 us each; every-step timing would distort the measured step)
         if state["timed"] is not None:
@@ -459,6 +470,9 @@ def fate_counts(engine) -> dict:
     return dict(c)
 
 
+IDLE_LIMIT_S = 120.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -477,7 +491,13 @@ def main():
     ap.add_argument("--engine-mode", default="tool_cache", choices=["tool_cache", "prefix", "vanilla"],
                     help="tool_cache (the paper's engine-side path, default) or the evict + re-prefill baselines")
     ap.add_argument("--k2-stats", action="store_true", help="diagnostics: K2 run shapes of the mixed steps")
+    ap.add_argument("--watchdog-s", type=float, default=1800.0,
+                    help="dump every thread's stack and exit(1) if the run exceeds this (0: off)")
     args = ap.parse_args()
+    if args.watchdog_s > 0:  # a hung run ends with a diagnosable stack dump, not silence
+        import faulthandler
+
+        faulthandler.dump_traceback_later(args.watchdog_s, exit=True)
     world, rank, local = dist_setup()
     resolve(args, world)
     if args.impl == "reference":
