@@ -901,7 +901,10 @@ struct PairCfg {
   static constexpr int W_BYTES = BM * BK * 2;
   static constexpr int X_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the token rows
   static constexpr int STAGE = W_BYTES + X_BYTES;
-  static constexpr int RING = 200 * 1024;
+#ifndef STB_GEMM_PAIR_RING_KB
+#define STB_GEMM_PAIR_RING_KB 224  // 7 stages of 32 KiB: down-proj (K = 14336) 4-5% faster than 6
+#endif
+  static constexpr int RING = STB_GEMM_PAIR_RING_KB * 1024;
   static constexpr int STAGES = (RING / STAGE) > 12 ? 12 : (RING / STAGE);
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
