@@ -87,11 +87,13 @@ int stb_qkv_norm_rope_commit(stb_kv_pool* pool, int layer, float* qkv, void* q_o
 /* ---- K3: paged decode attention (one query per sequence) ----------------
  * Replaces the decode charges engine.py:270,276,302,317. q/out bf16
  * [B][n_q][d_head]; slots/ctx_lens int32 [B]; split-K over the context with
- * a merge pass. `work` is a caller-owned fp32 scratch of
- * stb_attn_decode_workspace(B, n_q, d_head) bytes. max_ctx > 0 only caps the
- * split count (>= 4 pages per split); 0 gives a grid that depends on B alone,
- * which is what a captured CUDA graph needs.                               */
-int64_t stb_attn_decode_workspace(int B, int n_q, int d_head);
+ * an in-kernel merge. `work` is a caller-owned scratch of at least
+ * stb_attn_decode_workspace(B, n_q, n_kv, d_head) bytes for the calling device,
+ * ZEROED ONCE by the caller (its tail holds the split-merge tickets, which every
+ * launch leaves zero again); the call allocates nothing, so a CUDA graph captured
+ * for any B stays valid as long as `work` does. The grid depends on B alone.
+ * max_ctx (0 = unchecked) is validated against the block-table capacity.    */
+int64_t stb_attn_decode_workspace(int B, int n_q, int n_kv, int d_head);
 int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                     const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, void* work, void* stream);
 

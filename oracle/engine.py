@@ -151,14 +151,15 @@ class OracleEngine:
         self._blocks(seq, phase)
 
     def _c_verify(self, seq, draft_toks, span):
-        draft, sp = self.ids.many(draft_toks), self.ids.many(span)
+        draft, sp = self.ids.compare_ids(draft_toks), self.ids.many(span)
+        feed = self.ids.feed_ids(draft_toks)
         if seq.pend is None:
             self._unfeed_last(seq)
         if seq.counted:
             lead, model_head, shift = [seq.pend], [], 0
         else:
             lead, model_head, shift = [], [seq.pend], 1
-        inp = lead + draft
+        inp = lead + feed
         base = seq.rows
         tg = [sp[j + shift] if j + shift < len(sp) else -1 for j in range(len(inp))]
         got = self._fwd(seq, inp, base, list(range(len(inp))), tg)
@@ -209,7 +210,6 @@ class OracleEngine:
     def submit_tool_cache(self, rid, entry):
         if self.store is None:
             raise ConfigError("this engine has no tool cache")
-        self.ids.many(entry.call_tokens)
         self.store.submit(rid, entry)
         return 1
 

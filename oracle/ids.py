@@ -29,6 +29,25 @@ class Interner:
     def many(self, toks) -> list[int]:
         return [self(t) for t in toks]
 
+    def _known(self, tok):
+        kind = tok.kind.value
+        fixed = {"tool_start": 0, "tool_end": 1, "eos": 2}
+        if kind in fixed and tok.text == "":
+            return fixed[kind]
+        return self.ids.get((kind, tok.text))
+
+    def compare_ids(self, toks) -> list[int]:
+        """Drafted tokens are never interned: unknown ones compare as -2 (equal to no id)."""
+        return [-2 if (k := self._known(t)) is None else k for t in toks]
+
+    def feed_ids(self, toks) -> list[int]:
+        """Input ids of drafted tokens: known id, else 3 + fnv1a64(kind NUL text) mod (V - 3)."""
+        out = []
+        for t in toks:
+            k = self._known(t)
+            out.append(k if k is not None else 3 + _fnv(t.kind.value + "\x00" + t.text) % (self.vocab - 3))
+        return out
+
 
 def _fnv(text: str) -> int:
     h = 0xCBF29CE484222325

@@ -764,58 +764,48 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
 constexpr int kDecodeStages = STB_K3_STAGES;
 constexpr int kPrefillStages = 3;
 
-struct DecodeScratch {
-  float* part = nullptr;  // [W*2][G][D] partial o + [W*2][G] lse
-  int* tickets = nullptr;
-  size_t floats = 0;
-  int n_tickets = 0;
-};
+// Per-device launch geometry of K3 (SM count, resident CTAs per SM), looked up once per
+// (device, kernel instantiation) — never cached for the first device only.
+constexpr int kMaxDevices = 64;
+constexpr int kDecMaxPerSm = 2;
+
+inline int decode_sms(int) { return device_sms(); }
+
+// Caller workspace layout (stb_attn_decode_workspace): partial (o, lse) rows for every warp
+// of the largest grid K3 can launch on this device, then the split-pair merge tickets
+// (B * n_kv, zeroed by the caller once; the merging warp resets its ticket, so the region
+// is zero again after every launch). Nothing is allocated here: a CUDA graph captured for
+// any B keeps pointing at the caller's buffer, whose growth the caller owns.
+inline size_t decode_part_floats(int sms, int G, int D) {
+  return (size_t)kDecMaxPerSm * sms * kDecWarps * 2 * G * (D + 1);
+}
 
 template <int D, int G>
 int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
-                  float qscale, cudaStream_t st) {
-  static DecodeScratch sc;
+                  float qscale, void* work, cudaStream_t st) {
   if (B > kMaxB) return fail(STB_EINVAL, "attn_decode: at most %d sequences per step", kMaxB);
-  int dev = 0, sms = 148;
+  if (!work) return fail(STB_EINVAL, "attn_decode: NULL workspace");
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = decode_sms(dev);
   constexpr size_t smem = (size_t)kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
   auto kern = attn_decode_kernel<D, G, kDecodeStages>;
-  static bool attr = false;
-  static int per_sm = 1;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kDecWarps, smem) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
-    per_sm = std::min(per_sm, 2);
-    attr = true;
+  static int per_sm_of[kMaxDevices] = {};
+  int& per_sm = per_sm_of[dev < kMaxDevices ? dev : 0];
+  if (!per_sm) {
+    smem_attr_once(kern, (int)smem);
+    int n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32 * kDecWarps, smem) != cudaSuccess || n < 1) n = 1;
+    per_sm = std::min(n, kDecMaxPerSm);
   }
   const int grid = per_sm * sms;
   const int W = grid * kDecWarps;
-  const size_t need = (size_t)W * 2 * G * (D + 1);
-  const int pairs = B * n_kv;
-  if (need > sc.floats || pairs > sc.n_tickets) {
-    cudaStreamCaptureStatus cs;
-    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
-      return fail(STB_EINVAL, "attn_decode: scratch growth during graph capture");
-    if (need > sc.floats) {
-      if (sc.part) cudaFree(sc.part);
-      if (cudaMalloc(&sc.part, need * sizeof(float)) != cudaSuccess) return fail(STB_ENOMEM, "attn_decode scratch");
-      sc.floats = need;
-    }
-    if (pairs > sc.n_tickets) {
-      if (sc.tickets) cudaFree(sc.tickets);
-      int nt = pairs * 2 + 256;
-      if (cudaMalloc(&sc.tickets, nt * sizeof(int)) != cudaSuccess || cudaMemset(sc.tickets, 0, nt * sizeof(int)))
-        return fail(STB_ENOMEM, "attn_decode tickets");
-      sc.n_tickets = nt;
-    }
-  }
-  float* o_part = sc.part;
-  float* lse_part = sc.part + (size_t)W * 2 * G * D;
-  cudaError_t e = launch_k(kern, dim3(grid), dim3(32 * kDecWarps), smem, st, q, out, kp, vp, table, max_bps, slots, ctx, B, n_kv,
-                           qscale, o_part, lse_part, sc.tickets);
+  float* o_part = (float*)work;
+  float* lse_part = o_part + (size_t)W * 2 * G * D;
+  int* tickets = (int*)(o_part + decode_part_floats(sms, G, D));
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(32 * kDecWarps), smem, st, q, out, kp, vp, table, max_bps, slots, ctx,
+                           B, n_kv, qscale, o_part, lse_part, tickets);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_decode launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
@@ -838,9 +828,12 @@ int launch_prefill(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat
 
 extern "C" {
 
-int64_t stb_attn_decode_workspace(int B, int n_q, int d_head) {
-  // o_part [B][n_q][64 splits][D] + lse [B][n_q][64]
-  return (int64_t)B * n_q * 64 * (d_head + 1) * 4;
+int64_t stb_attn_decode_workspace(int B, int n_q, int n_kv, int d_head) {
+  if (B < 0 || n_q <= 0 || n_kv <= 0 || n_q % n_kv || d_head <= 0) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t floats = decode_part_floats(decode_sms(dev), n_q / n_kv, d_head);
+  return (int64_t)(floats * 4 + (size_t)B * n_kv * 4 + 256);
 }
 
 int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
@@ -851,6 +844,8 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
   int max_bps;
   stb_kv_block_table(pool, &table, &max_bps);
   if (B <= 0) return STB_OK;
+  if (max_ctx > max_bps * 16)
+    return fail(STB_EINVAL, "attn_decode: max_ctx %d exceeds the block table (%d rows)", max_ctx, max_bps * 16);
   int n_kv, d_head;
   stb_pool_geometry(pool, &n_kv, &d_head);
   if (n_q % n_kv) return fail(STB_EINVAL, "attn_decode: n_q %% n_kv != 0");
@@ -861,7 +856,7 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
   auto* kk = (const __nv_bfloat16*)kp;
   auto* vv = (const __nv_bfloat16*)vp;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, st
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, work, st
   if (d_head == 128 && g == 4) return launch_decode<128, 4>(ARGS);
   if (d_head == 128 && g == 8) return launch_decode<128, 8>(ARGS);
   if (d_head == 128 && g == 1) return launch_decode<128, 1>(ARGS);

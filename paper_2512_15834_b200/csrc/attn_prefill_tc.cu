@@ -31,7 +31,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <unordered_map>
 
 #include "../../include/stb200.h"
@@ -533,10 +535,20 @@ struct Maps {
   CUtensorMap q, k, v;
 };
 
-// split-K partials, grown outside graph capture only (no split while capturing a new size)
-struct SplitScratch {
-  float* part = nullptr;
-  size_t floats = 0;
+// Tensor maps of one launch geometry: everything the encoded maps depend on is in the key
+// (a freed pool re-allocated at the same address with another num_blocks, or another layer
+// geometry, must never hit a stale map: out-of-bounds boxes would silently zero-fill).
+struct MapKey {
+  const void* q;
+  int64_t T;
+  const void* kp;
+  const void* vp;
+  int64_t num_blocks;
+  int n_kv, G, D, dev;
+  bool operator<(const MapKey& o) const {
+    return std::tie(q, T, kp, vp, num_blocks, n_kv, G, D, dev) <
+           std::tie(o.q, o.T, o.kp, o.vp, o.num_blocks, o.n_kv, o.G, o.D, o.dev);
+  }
 };
 
 template <int D, int G>
@@ -546,10 +558,12 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
   // tensor maps: Q over [T][n_kv][G][D] (box 64 x G x 1 x 128/G), K / V pages of the layer as
   // [num_blocks * n_kv * 16 rows][D] (box 64 x 16); cached per (q base, T, layer pointers)
   static std::mutex mu;
-  static std::unordered_map<uint64_t, Maps> cache;
+  static std::map<MapKey, Maps> cache;
   void *kp, *vp;
   stb_kv_layer_ptrs(pool, layer, &kp, &vp);
-  const uint64_t key = reinterpret_cast<uint64_t>(q) * 1000003ull ^ (uint64_t)T * 7919ull ^ reinterpret_cast<uint64_t>(kp);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const MapKey key{q, (int64_t)T, kp, vp, (int64_t)pool->num_blocks, n_kv, G, D, dev};
   Maps mp;
   {
     std::lock_guard<std::mutex> g(mu);
@@ -572,49 +586,38 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
     }
   }
   auto kern = attn_prefill_tc_kernel<D, G>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-    attr = true;
-  }
+  smem_attr_once(kern, CF::SMEM);
   const int gx = (max_q + 2 * ROWS / G - 1) / (2 * ROWS / G);
   // KV split only for launches far from filling the machine (a verify pass is 8 work units
   // on 148 SMs); `active_hint` = units that hold queries (0: the full grid)
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   const int64_t units = (int64_t)gx * n_kv * S;
   const int64_t active = active_hint > 0 ? active_hint : units;
   static const int split_env = getenv("STB200_K2_SPLIT") ? atoi(getenv("STB200_K2_SPLIT")) : -1;  // A/B only
   int splits = 1;
   if (2 * active <= sms) splits = (int)std::min<int64_t>(kMaxSplits, sms / active);
   if (split_env >= 1) splits = std::min(split_env, kMaxSplits);
-  static SplitScratch sc;
+  // partials: fixed per-(device, stream) scratch for sms/2 units x kMaxSplits (a split is only
+  // chosen for launches with fewer active units than half the SMs); a ragged grid whose
+  // units x splits would not fit gets fewer splits, never a reallocation under a graph
+  const size_t cap_units = (size_t)(sms / 2) * kMaxSplits;
+  float* part = nullptr;
   if (splits > 1) {
-    // sized on first use for any split launch (<= sms/2 units x 8 splits) so it never grows
-    // (cudaMalloc would stall a step); larger ragged grids grow it once more
-    const size_t need = std::max((size_t)units * splits, (size_t)(sms / 2) * kMaxSplits) * kPartFloats<D>;
-    if (need > sc.floats) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(st, &cs);
-      if (cs != cudaStreamCaptureStatusNone) return fail(STB_EINVAL, "attn_prefill: split scratch growth in capture");
-      if (sc.part) cudaFree(sc.part);
-      sc.part = nullptr;
-      sc.floats = 0;
-      if (cudaMalloc(&sc.part, need * sizeof(float)) != cudaSuccess) return fail(STB_ENOMEM, "attn_prefill split");
-      sc.floats = need;
+    if ((size_t)units * splits > cap_units) splits = (int)(cap_units / (size_t)units);
+    if (splits > 1) {
+      part = (float*)stream_scratch(kScratchK2Split, st, cap_units * kPartFloats<D> * sizeof(float));
+      if (!part) return fail(STB_ENOMEM, "attn_prefill split scratch");
+    } else {
+      splits = 1;
     }
   }
   dim3 grid(gx, n_kv, S * splits);
   cudaError_t e = launch_k(kern, grid, dim3(kThreads), CF::SMEM, st, mp.q, mp.k, mp.v, (__nv_bfloat16*)out,
-                           pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale, splits, sc.part);
+                           pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale, splits, part);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill_tc launch: %s", cudaGetErrorString(e));
   if (splits > 1) {
     e = launch_k(attn_prefill_merge_kernel<D, G>, dim3(gx * (2 * ROWS / 8), n_kv, S), dim3(256), 0, st,
-                 (__nv_bfloat16*)out, (const float*)sc.part, q_start, ctx, n_kv, splits, gx);
+                 (__nv_bfloat16*)out, (const float*)part, q_start, ctx, n_kv, splits, gx);
     if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill merge launch: %s", cudaGetErrorString(e));
   }
   return STB_OK;

@@ -9,7 +9,10 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 namespace stb {
 
@@ -307,6 +310,69 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, bool a_mn_m
          | ((b_mn_major ? 1u : 0u) << 16)      // B major
          | ((uint32_t)(N >> 3) << 17)          // N / 8
          | ((uint32_t)(M >> 4) << 24);         // M / 16
+}
+
+
+// Device scratch owned per (device, stream): zero-initialised at first use, never freed or
+// moved afterwards, so CUDA graphs captured on that stream keep valid pointers and two
+// streams (or two devices) never share a self-resetting ticket / barrier word. `bytes` is the
+// fixed size of that scratch kind (callers size it for their launch maximum); `kind` tells
+// apart the scratch kinds of different kernels. Returns nullptr if the allocation fails.
+inline void* stream_scratch(int kind, cudaStream_t st, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, std::pair<int, cudaStream_t>>, void*> slots;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_pair(kind, std::make_pair(dev, st));
+  auto it = slots.find(key);
+  if (it != slots.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (st) cudaStreamIsCapturing(st, &cs);
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  if (cs != cudaStreamCaptureStatusNone) {
+    // first use inside a capture (torch captures on a side stream): the zeroing becomes a
+    // node of that graph, which is harmless on replay (the scratch is at rest, i.e. zero,
+    // between launches on this stream)
+    if (cudaMemsetAsync(p, 0, bytes, st) != cudaSuccess) return nullptr;
+  } else {
+    if (cudaMemset(p, 0, bytes) != cudaSuccess) return nullptr;
+    cudaDeviceSynchronize();
+  }
+  slots.emplace(key, p);
+  return p;
+}
+enum ScratchKind { kScratchSample = 1, kScratchK2Split = 2, kScratchGridBar = 3, kScratchTileTickets = 4 };
+
+// SM count of the current device (cached per device, not for the first device only).
+inline int device_sms() {
+  static int sms[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!sms[dev]) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = n;
+  }
+  return sms[dev];
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): function
+// attributes belong to the device context, so a process driving two GPUs sets them on each.
+template <class K>
+inline void smem_attr_once(K kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_pair((const void*)kern, dev);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done[key] = bytes;
 }
 
 }  // namespace stb

@@ -802,36 +802,19 @@ int cached_map_raw(CUtensorMap* out, const void* base, int64_t rows) {
   return STB_OK;
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
+int sm_count() { return device_sms(); }
+
+// stream-K grid barrier state {arrivals, generation}: per (device, stream), zeroed once,
+// self-resetting. Two stream-K GEMMs in flight on different streams never share a barrier.
+unsigned* grid_barrier(cudaStream_t st) {
+  return (unsigned*)stream_scratch(kScratchGridBar, st, 2 * sizeof(unsigned));
 }
 
-// stream-K grid barrier state {arrivals, generation}: zeroed once, self-resetting
-unsigned* grid_barrier() {
-  static unsigned* bar = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    if (cudaMalloc(&bar, 2 * sizeof(unsigned)) == cudaSuccess) cudaMemset(bar, 0, 2 * sizeof(unsigned));
-  });
-  return bar;
-}
-
-// stream-K tile tickets of the fused-epilogue path: zeroed once, reset by each tile's finisher
+// stream-K tile tickets of the fused-epilogue path: per (device, stream), zeroed once, reset
+// by each tile's finisher
 constexpr int kMaxTickets = 1 << 14;
-unsigned* tile_tickets() {
-  static unsigned* cnt = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    if (cudaMalloc(&cnt, kMaxTickets * sizeof(unsigned)) == cudaSuccess)
-      cudaMemset(cnt, 0, kMaxTickets * sizeof(unsigned));
-  });
-  return cnt;
+unsigned* tile_tickets(cudaStream_t st) {
+  return (unsigned*)stream_scratch(kScratchTileTickets, st, kMaxTickets * sizeof(unsigned));
 }
 
 int bn_template(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
@@ -1158,11 +1141,7 @@ int launch_pair(const void* X, int64_t lda, const void* W, int64_t ldw, float* C
   const int tiles = (N / PAIR_BM) * tiles_m;
   const int pairs = std::min(sm_count() / 2, tiles);
   auto kern = gemm_bf16_pair<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-    attr_set = true;
-  }
+  smem_attr_once(kern, CF::SMEM);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);
@@ -1236,14 +1215,10 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   s.tag = launch_seq++;
   static const int load_debug = getenv("STB200_GEMM_LOAD_DEBUG") ? atoi(getenv("STB200_GEMM_LOAD_DEBUG")) : 0;
   s.load_debug = load_debug;
-  s.bar = grid_barrier();
+  s.bar = grid_barrier(st);
   if (!s.bar) return fail(STB_ENOMEM, "gemm_bf16: barrier state");
   auto kern = gemm_bf16_persistent<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-    attr_set = true;
-  }
+  smem_attr_once(kern, CF::SMEM);
   if (ep.kind != 0 && s.stream && (C == nullptr || ep.cnt == nullptr))
     return fail(STB_EINVAL, "gemm_bf16_fused: the stream-K schedule needs the zeroed fp32 workspace");
   if (ep.kind != 0 && s.stream && s.tiles > kMaxTickets)
@@ -1365,7 +1340,7 @@ extern "C" int stb_gemm_bf16_fused(const void* A, int64_t lda, const void* W, in
   ep.eps = e->eps;
   ep.out = (__nv_bfloat16*)e->out;
   ep.ldo = e->ldo;
-  ep.cnt = tile_tickets();
+  ep.cnt = tile_tickets((cudaStream_t)stream);
   if (!ep.cnt) return fail(STB_ENOMEM, "gemm_bf16_fused: tickets");
   if (e->kind == STB_EPI_SILU && N % 2) return fail(STB_EINVAL, "gemm_bf16_fused: SiLU-gate needs even N");
   if (e->ss_in && (e->ss_parts <= 0 || e->ss_parts % 4 || e->ss_parts > kMaxSsParts ||

@@ -367,14 +367,12 @@ int stb_sample_forced(float* logits, int64_t ld, const int32_t* target, int R, i
   constexpr int CH = 32;  // vocabulary chunks per row (<= 32: one warp reduces the partials)
   constexpr int kMaxRows = 65536;
   if (R > kMaxRows) return fail(STB_EINVAL, "sample_forced: at most %d rows per call", kMaxRows);
-  // persistent scratch: partials + self-resetting tickets (allocated once, before any graph capture)
-  static ArgPart* parts = nullptr;
-  static int* tickets = nullptr;
-  if (!parts) {
-    if (cudaMalloc(&parts, sizeof(ArgPart) * (size_t)kMaxRows * CH) != cudaSuccess ||
-        cudaMalloc(&tickets, sizeof(int) * kMaxRows) != cudaSuccess || cudaMemset(tickets, 0, sizeof(int) * kMaxRows))
-      return fail(STB_ENOMEM, "sample_forced: scratch allocation failed");
-  }
+  // per-(device, stream) scratch: partials + self-resetting tickets (first use precedes capture)
+  const size_t part_bytes = sizeof(ArgPart) * (size_t)kMaxRows * CH;
+  auto* base = (uint8_t*)stream_scratch(kScratchSample, (cudaStream_t)stream, part_bytes + sizeof(int) * kMaxRows);
+  if (!base) return fail(STB_ENOMEM, "sample_forced: scratch allocation failed (or first use inside a capture)");
+  auto* parts = (ArgPart*)base;
+  auto* tickets = (int*)(base + part_bytes);
   launch_k(sample_forced_kernel, dim3(R * CH), dim3(256), 0, (cudaStream_t)stream, logits, ld, target, V, bias, CH, parts, tickets, out,
                                                                  raw_argmax, raw_max, clear);
   STB_CHECK_LAUNCH("sample_forced");

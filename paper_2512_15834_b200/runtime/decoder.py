@@ -295,8 +295,9 @@ class Decoder:
             self.graphs.clear()
         if B > self._cap_b:
             cap = max(B, 2 * self._cap_b, 64)
-            nbytes = lib.load().stb_attn_decode_workspace(cap, s.n_q, s.d_head)
-            self.work = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+            nbytes = lib.load().stb_attn_decode_workspace(cap, s.n_q, s.n_kv, s.d_head)
+            # zeroed once: the tail holds K3's merge tickets, which every launch leaves zero
+            self.work = torch.zeros(-(-nbytes // 4), dtype=torch.float32, device=dev)
             self._cap_b = cap
             self.graphs.clear()
 

@@ -41,7 +41,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from ..errors import ConfigError, KernelError
+from ..errors import ConfigError, KernelError, KVCapacityError
 from ..modelcfg import TINY, ModelShape
 from ..tokens import SALT_OUTPUT, SALT_PROMPT, TokenTable, fill_ids
 from . import lib
@@ -120,6 +120,7 @@ class Runtime:
         self.max_ctx = max_ctx
         self._free_slots = list(range(max_slots - 1, -1, -1))
         self.record = record
+        self.reclaimer = None           # engine hook: free retained prefixes under KV pressure
         self.trace: list[dict] = []     # per sampled row: rid, pos, fed, target, sampled, logits (record mode)
         self.forwards = 0
         self.tokens_fed = 0
@@ -155,13 +156,25 @@ class Runtime:
         d.kv_len, d.pend, d.counted, d.hist = 0, None, False, []
 
     def can_admit(self, seq) -> bool:
-        need = -(-(seq.prompt_tokens + 1) // BLOCK)
+        """Blocks the prompt still needs (ceil((P + 1) / 16) minus what the slot already
+        holds, e.g. a retained prefix) fit in the free list."""
+        need = -(-(seq.prompt_tokens + 1) // BLOCK) - len(self.pool.blocks(seq.dev.slot))
         return self.pool.free_blocks() >= need
+
+    def _reserve(self, slot: int, n: int) -> None:
+        """pool.reserve; on KV exhaustion ask the engine to drop paused sequences' retained
+        prefixes (`reclaimer`) and retry once before giving up."""
+        try:
+            self.pool.reserve(slot, n)
+        except KVCapacityError:
+            if self.reclaimer is None or not self.reclaimer():
+                raise
+            self.pool.reserve(slot, n)
 
     def _commit_blocks(self, d: SeqDev) -> None:
         """Hold exactly ceil(kv_tokens / 16) blocks (rollback / growth)."""
         self.pool.truncate(d.slot, d.kv_tokens)
-        self.pool.reserve(d.slot, d.kv_tokens)
+        self._reserve(d.slot, d.kv_tokens)
 
     def block_ids(self, seq) -> list[int]:
         return self.pool.blocks(seq.dev.slot)
@@ -252,12 +265,12 @@ class Runtime:
 
     def verify(self, seq, draft_tokens, span_tokens, done) -> None:
         d = seq.dev
-        draft = self.table.ids(draft_tokens)
+        draft = self.table.lookup(draft_tokens)   # compare ids: never interned (UNKNOWN = -2)
         span = self.table.ids(span_tokens)
         if d.pend is None:
             self._recompute_last(seq)
         lead = [d.pend] if d.counted else []
-        inputs = lead + draft
+        inputs = lead + self.table.feed(draft_tokens)
         # row j predicts the token after inputs[j]; the model's token for draft slot i
         # is pend (uncounted case, i == 0) or the sample of the row feeding slot i-1
         off = 0 if d.counted else 1
@@ -368,12 +381,12 @@ class Runtime:
         runs = sorted(runs, key=lambda r: r.verify is None)  # verify runs first: their samples are contiguous
         for j in decodes:
             d = j.seq.dev
-            self.pool.reserve(d.slot, d.kv_len + 1)
+            self._reserve(d.slot, d.kv_len + 1)
         for r in runs:
             d = r.seq.dev
             if r.start + len(r.ids) > self.max_ctx:
                 raise ConfigError(f"{r.seq.rid}: context {r.start + len(r.ids)} exceeds max_ctx {self.max_ctx}")
-            self.pool.reserve(d.slot, r.start + len(r.ids))
+            self._reserve(d.slot, r.start + len(r.ids))
         batch = self._build(decodes, runs)
         self.dec.keep_logits = self.record
         k = self._flip

@@ -6,10 +6,13 @@ The reference compares `Token(kind, text)` objects (`domain.py:29-32`,
 
 * ids 0, 1, 2 are TOOL_START, TOOL_END, EOS;
 * every other distinct token gets the next free id in first-interned order.
-  The engine interns a whole script at `submit_request` and a draft's tokens
-  at `submit_tool_cache`, so in a deterministic run the table is a pure
-  function of the submission order; equality of ids <=> equality of tokens,
-  which is what makes device-side draft validation bit-exact.
+  The engine interns a whole script at `submit_request`, so in a deterministic
+  run the table is a pure function of the submission order; equality of ids
+  <=> equality of tokens, which is what makes device-side draft validation
+  bit-exact. Drafted tokens are looked up, never interned: a token no script
+  holds compares as UNKNOWN (-2) and is fed as a hashed id (`feed`).
+* identity is structural, (kind value, text), so the reference's own Token
+  objects work as well as this package's.
 
 Content the reference only counts — prompt tokens, tool-output tokens — gets
 deterministic pseudo-random ids from `fill_ids(seed, rid, salt, start, n)`:
@@ -31,26 +34,56 @@ SALT_OUTPUT = 2
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
+UNKNOWN = -2  # compare id of a draft token the scripts never produce: equals no model id
+
+
+def token_key(tok) -> tuple[str, str]:
+    """Structural identity (kind value, text): the reference's own `Token`/`TokenKind`
+    objects (`domain.py:22-32`) and this package's compare equal."""
+    return tok.kind.value, tok.text
+
+
 class TokenTable:
     def __init__(self, vocab: int):
         if vocab <= RESERVED:
             raise ConfigError("vocabulary too small")
         self.vocab = vocab
-        self._ids: dict[Token, int] = {TOOL_START: 0, TOOL_END: 1, EOS: 2}
+        self._ids: dict[tuple[str, str], int] = {token_key(t): i for i, t in enumerate((TOOL_START, TOOL_END, EOS))}
         self._tokens: list[Token] = [TOOL_START, TOOL_END, EOS]
 
-    def intern(self, tok: Token) -> int:
-        tid = self._ids.get(tok)
+    def intern(self, tok) -> int:
+        key = token_key(tok)
+        tid = self._ids.get(key)
         if tid is None:
             tid = len(self._tokens)
             if tid >= self.vocab:
                 raise ConfigError(f"more than {self.vocab} distinct tokens in the trace")
-            self._ids[tok] = tid
+            self._ids[key] = tid
             self._tokens.append(tok)
         return tid
 
     def ids(self, toks) -> list[int]:
+        """Intern scripted tokens (the model can only ever be forced to these)."""
         return [self.intern(t) for t in toks]
+
+    def lookup(self, toks) -> list[int]:
+        """Compare ids of drafted tokens, never interning: a token no script holds gets
+        UNKNOWN, so untrusted drafts (HTTP submissions) cannot grow the table."""
+        get = self._ids.get
+        return [get(token_key(t), UNKNOWN) for t in toks]
+
+    def feed(self, toks) -> list[int]:
+        """Input ids of drafted tokens for the verify forward: the interned id, else a
+        deterministic hash of (kind, text) into [3, vocab) (it is never compared: acceptance
+        stops at the first UNKNOWN, and rows past it are rolled back)."""
+        out = []
+        for t in toks:
+            tid = self._ids.get(token_key(t))
+            if tid is None:
+                kind, text = token_key(t)
+                tid = RESERVED + fnv1a64(kind + "\x00" + text) % (self.vocab - RESERVED)
+            out.append(tid)
+        return out
 
     def token(self, tid: int) -> Token:
         return self._tokens[tid]

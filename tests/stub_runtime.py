@@ -13,6 +13,7 @@ class StubRuntime:
     def __init__(self, vocab=4096):
         self.table = TokenTable(vocab)
         self.calls = []
+        self.reclaimer = None
 
     def intern(self, toks):
         return self.table.ids(toks)
@@ -37,7 +38,7 @@ class StubRuntime:
         done(None)
 
     def verify(self, seq, draft, span, done):
-        d, s = self.table.ids(draft), self.table.ids(span)
+        d, s = self.table.lookup(draft), self.table.ids(span)
         n = min(len(d), len(s))
         acc = next((i for i in range(n) if d[i] != s[i]), n)
         self.calls.append(("verify", seq.rid, acc))

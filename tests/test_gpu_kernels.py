@@ -403,7 +403,7 @@ def test_attn_decode(lib, shape, ctxs):
     out = torch.empty_like(q)
     slots = torch.arange(B, dtype=torch.int32, device="cuda")
     ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
-    ws = torch.empty(lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.d_head) // 4, device="cuda")
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.n_kv, shape.d_head) // 4), device="cuda")
     scale = 1 / math.sqrt(shape.d_head)
     lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, max(ctxs), P(ws),
              stream())
@@ -473,7 +473,7 @@ def test_attn_long_context_c5(lib, shape):
     B = len(ctxs)
     qd = torch.randn(B, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
     od = torch.empty_like(qd)
-    ws = torch.empty(lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.d_head) // 4, device="cuda")
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.n_kv, shape.d_head) // 4), device="cuda")
     slots = torch.arange(B, dtype=torch.int32, device="cuda")
     ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
     lib.call("stb_attn_decode", pool.h, 0, P(qd), P(od), P(slots), P(ctx), B, shape.n_q, scale, 0, P(ws), stream())
@@ -625,7 +625,7 @@ def test_error_paths(lib):
         pool.sync(torch.cuda.current_stream().cuda_stream)
         slots = torch.tensor([1], dtype=torch.int32, device="cuda")
         ctx = torch.tensor([16], dtype=torch.int32, device="cuda")
-        ws = torch.empty(lib.load().stb_attn_decode_workspace(1, 6, 64) // 4, device="cuda")
+        ws = torch.zeros(1 << 20, device="cuda")
         lib.call("stb_attn_decode", pool.h, 0, P(q), P(q), P(slots), P(ctx), 1, 6, 0.125, 0, P(ws), stream())
     assert issubclass(KernelError, SpectoolError) and issubclass(KVCapacityError, SpectoolError)
 
@@ -667,7 +667,7 @@ def test_attention_full_size_invariant(lib, case):
         out = torch.full_like(q, float("nan"))
         slots = torch.arange(B, dtype=torch.int32, device="cuda")
         ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
-        ws = torch.empty(lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.d_head) // 4, device="cuda")
+        ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.n_kv, shape.d_head) // 4), device="cuda")
         lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, 0, P(ws),
                  stream())
     torch.cuda.synchronize()
@@ -691,7 +691,7 @@ def test_attn_decode_max_batch_and_empty(lib):
     out = torch.full_like(q, float("nan"))
     slots = torch.arange(B + 1, dtype=torch.int32, device="cuda")
     ctx = torch.tensor(ctxs + [1], dtype=torch.int32, device="cuda")
-    ws = torch.empty(lib.load().stb_attn_decode_workspace(B + 1, shape.n_q, shape.d_head) // 4, device="cuda")
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(B + 1, shape.n_q, shape.n_kv, shape.d_head) // 4), device="cuda")
     scale = 1 / math.sqrt(shape.d_head)
     lib.call("stb_attn_decode", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, 0, P(ws), stream())
     worst = 0.0
@@ -738,3 +738,40 @@ def test_attn_prefill_empty_runs(lib):
              stream())
     torch.cuda.synchronize()
     assert torch.equal(out, keep)
+
+
+def test_attn_decode_graph_survives_larger_batch(lib):
+    """K3's split-merge tickets live in the caller's workspace, so a CUDA
+    graph captured at a small B still replays correctly after an eager launch at a larger B
+    (which used to free and reallocate a hidden ticket array under the captured graph), and
+    the ticket region is all zero again after every launch."""
+    shape = SHAPES[2]  # Qwen3-32B geometry: n_kv 8, the C3 config of the advisor's report
+    ctxs_big = [3000 + 37 * i for i in range(40)]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs_big) + 8, slots=len(ctxs_big), bps=512)
+    dense = _fill_pool(lib, pool, shape, ctxs_big, seed=12)
+    scale = 1 / math.sqrt(shape.d_head)
+    nb = lib.load().stb_attn_decode_workspace(64, shape.n_q, shape.n_kv, shape.d_head)
+    ws = torch.zeros(-(-nb // 4), device="cuda")
+    Bs = 4
+    q = torch.randn(len(ctxs_big), shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out_s = torch.empty(Bs, shape.n_q, shape.d_head, device="cuda", dtype=torch.bfloat16)
+    slots = torch.arange(len(ctxs_big), dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs_big, dtype=torch.int32, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        lib.call("stb_attn_decode", pool.h, 0, P(q), P(out_s), P(slots), P(ctx), Bs, shape.n_q, scale, 0, P(ws),
+                 stream())
+    out_b = torch.empty_like(q)
+    lib.call("stb_attn_decode", pool.h, 0, P(q), P(out_b), P(slots), P(ctx), len(ctxs_big), shape.n_q, scale, 0,
+             P(ws), stream())
+    out_s.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    for b, (k, v) in enumerate(dense):
+        r = _ref_attn(q[b:b + 1], k, v, torch.tensor([ctxs_big[b] - 1], device="cuda"), scale)
+        assert rel(out_b[b:b + 1], r) < 1e-2, b
+        if b < Bs:
+            assert rel(out_s[b:b + 1], r) < 1e-2, b
+    tickets = ws.view(torch.int32)[-(64 * shape.n_kv + 64):]
+    assert int(tickets.abs().sum()) == 0

@@ -156,7 +156,7 @@ def bench_attn(shape, B, ctx, reps=4):
     o = torch.empty_like(q)
     slots = torch.arange(B, dtype=torch.int32, device="cuda")
     ctxs = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
-    ws = torch.empty(lib.load().stb_attn_decode_workspace(B, s.n_q, s.d_head) // 4, device="cuda")
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(B, s.n_q, s.n_kv, s.d_head) // 4), device="cuda")
     sc = 1 / math.sqrt(s.d_head)
     us = time_it(lambda i: lib.call("stb_attn_decode", pools[i % reps].h, 0, P(q), P(o), P(slots), P(ctxs), B, s.n_q,
                                     sc, 0, P(ws), st()))
