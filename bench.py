@@ -31,6 +31,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -41,7 +42,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-TIMER_STRIDE = 32  # 1 step in 32 carries the kernel timers (their event nodes cost ~9 us each)
+TIMER_STRIDE = 32  # long runs: 1 step in 32 carries the kernel timers (event nodes cost ~9 us each)
+SHORT_TIMER_STRIDE = 10  # runs under 128 timed steps (the driver's 20): timed steps 0, 10, ...
 METRIC = "agent tokens/sec (whole box) at N concurrent agents; tool-resume latency ms"
 REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
            "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
@@ -155,41 +157,89 @@ def barrier(world: int):
 
 
 # ------------------------------------------------------------------ CPU arm
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+class CpuDecodeArm:
+    """The reference's CPU path for a decode step, restated by the oracle (fp32 CpuDecoder math:
+    RMSNorm, RoPE, GQA attention, SwiGLU, LM head), at FULL depth: every one of the shape's L
+    layers runs its GEMMs and its attention over the batch's `ctx`-token KV. To fit host memory
+    the L layers share one drawn weight set and one preallocated KV buffer per sequence (the
+    arithmetic and the bytes streamed per layer are those of the untied model; only the values
+    repeat). K/V rows are written in place (no per-step concatenation)."""
+
+    def __init__(self, shape, batch: int, ctx: int, threads: int):
+        import torch
+
+        from oracle.cpu_decoder import CpuDecoder
+
+        torch.set_num_threads(threads)
+        self.torch = torch
+        self.dec = CpuDecoder(shape, seed=0, layers=1)  # layer 0, reused for every layer
+        self.L, self.B, self.ctx = shape.layers, batch, ctx
+        g = torch.Generator().manual_seed(0)
+        cap = ctx + 4096
+        self.k = [torch.randn(cap, shape.n_kv, shape.d_head, generator=g) for _ in range(batch)]
+        self.v = [torch.randn(cap, shape.n_kv, shape.d_head, generator=g) for _ in range(batch)]
+        self.n = ctx
+
+    def step(self):
+        torch, dec, s = self.torch, self.dec, self.dec.s
+        H, G, D, B = s.n_q, s.n_kv, s.d_head, self.B
+        pos = torch.full((B,), self.n)
+        x = dec.embed[torch.full((B,), 5, dtype=torch.long)]
+        w = dec.layers[0]
+        for _ in range(self.L):
+            h = dec._norm(x, w["an"])
+            qkv = h @ w["qkv"].T
+            q, k = dec._qk(w, qkv[:, : H * D].view(B, H, D), qkv[:, H * D: (H + G) * D].view(B, G, D))
+            q, k = dec._rope(q, pos), dec._rope(k, pos)
+            v = qkv[:, (H + G) * D:].view(B, G, D)
+            outs = []
+            for b in range(B):
+                self.k[b][self.n] = k[b]
+                self.v[b][self.n] = v[b]
+                kk = self.k[b][: self.n + 1]  # [n, G, D]
+                vv = self.v[b][: self.n + 1]
+                qb = q[b].view(G, H // G, D)
+                p = torch.softmax(torch.einsum("grd,ngd->grn", qb, kk) / math.sqrt(D), dim=-1)
+                outs.append(torch.einsum("grn,ngd->grd", p, vv).reshape(H * D))
+            x = x + torch.stack(outs) @ w["o"].T
+            h = dec._norm(x, w["mn"])
+            gu = h @ w["gu"].T
+            x = x + (torch.nn.functional.silu(gu[:, : s.d_ff]) * gu[:, s.d_ff:]) @ w["dn"].T
+        logits = dec._norm(x, dec.fn) @ dec.head.T
+        self.n += 1
+        return logits
+
+    def describe(self) -> str:
+        return (f"oracle fp32 CpuDecoder math, {self.dec.s.name} at full depth ({self.L} layers, weights tied across "
+                f"layers to fit host memory): batched decode steps of {self.B} sequences at ctx {self.ctx}, KV written "
+                f"in place")
+
+
 def cpu_sample(shape, seconds_budget: float = 20.0, threads: int | None = None, batch: int = 32,
                ctx: int = 2048) -> dict:
-    """Oracle fp32 CPU decoder on a bounded sample of the workload.
-
-    Batched decode steps of `batch` sequences at a `ctx`-token context (the
-    trace's prompt length; caches pre-filled with random K/V, since only the
-    step time is sampled), GEMMs batched over the sequences as a CPU server
-    would run them. Timed on a 0-layer (embed + final norm + LM head) and a
-    2-layer slice of the shape, then scaled: t_step = t0 + (L/2) * (t2 - t0).
-    """
-    import torch
-
-    from oracle.cpu_decoder import CpuDecoder, decode_batch
-
+    """The CPU arm on a bounded sample: full-depth decode steps until `seconds_budget` (>= 2)."""
     threads = threads or os.cpu_count() or 1
-    torch.set_num_threads(threads)
-    g = torch.Generator().manual_seed(0)
-    res = {}
-    for L in (0, 2):
-        dec = CpuDecoder(shape, seed=0, layers=L)
-        caches = [[(torch.randn(ctx, shape.n_kv, shape.d_head, generator=g),
-                    torch.randn(ctx, shape.n_kv, shape.d_head, generator=g)) for _ in range(L)]
-                  for _ in range(batch)]
-        decode_batch(dec, caches, [5] * batch, [ctx] * batch)
-        n, t0 = 0, time.perf_counter()
-        while n < 2 or (time.perf_counter() - t0 < seconds_budget / 4 and n < 8):
-            decode_batch(dec, caches, [5] * batch, [ctx + 1 + n] * batch)
-            n += 1
-        res[L] = (time.perf_counter() - t0) / n
-        del dec, caches
-    t_step = res[0] + shape.layers / 2 * (res[2] - res[0])
-    return {"value": batch / t_step, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": (f"oracle fp32 CpuDecoder, {shape.name}: batched decode steps of {batch} sequences at ctx "
-                       f"{ctx}, timed on 0 and 2 layers ({res[0] * 1e3:.0f} / {res[2] * 1e3:.0f} ms/step) and "
-                       f"scaled to {shape.layers} layers")}
+    arm = CpuDecodeArm(shape, batch, ctx, threads)
+    arm.step()  # warm-up
+    n, t0 = 0, time.perf_counter()
+    while n < 2 or (time.perf_counter() - t0 < seconds_budget and n < 16):
+        arm.step()
+        n += 1
+    t_step = (time.perf_counter() - t0) / n
+    return {"value": batch / t_step, "unit": "tokens/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+            "ms_per_step": round(t_step * 1e3, 1), "steps_timed": n,
+            "sample": f"{arm.describe()}; {n} steps timed after 1 warm-up step"}
 
 
 def run_reference(args, world, rank):
@@ -198,13 +248,22 @@ def run_reference(args, world, rank):
     from paper_2512_15834_b200.modelcfg import SHAPES
 
     shape = SHAPES[args.shape]
-    base = cpu_sample(shape, seconds_budget=max(8.0, min(60.0, 2.0 * (args.steps + args.warmup))), batch=args.agents,
-                      ctx=args.trace.get("prompt_tokens", 2048))
-    line = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / base["value"],
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(args), "cpu_baseline": base,
-            "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    threads = os.cpu_count() or 1
+    arm = CpuDecodeArm(shape, args.agents, args.trace.get("prompt_tokens", 2048), threads)
+    for _ in range(args.warmup):
+        arm.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        arm.step()
+    dt = time.perf_counter() - t0
+    value = args.agents * args.steps / dt
+    base = {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"{arm.describe()}; {args.warmup} warm-up + {args.steps} timed steps, every step executed"}
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 1),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload_config(args), "cpu_baseline": base,
+            "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -237,13 +296,19 @@ def resolve(args, world: int) -> None:
         args.max_step_tokens = c.get("max_step_tokens", 8192)
 
 
+def shape_layers(name: str) -> int:
+    from paper_2512_15834_b200.modelcfg import SHAPES
+
+    return SHAPES[name].layers
+
+
 def workload_config(args) -> dict:
     c = CONFIGS[args.config]
     prompt = args.trace.get("prompt_tokens", 2048)
     return {"workload": c["label"], "config_id": args.config, "shape": args.shape,
             "engine_mode": getattr(args, "engine_mode", "tool_cache"),
             "agents_per_gpu": args.agents, "prompt_tokens": prompt, "draft_latency_s": 0.05, "accept_rate": 0.8,
-            "layers": args.layers, "parallelism": f"replicas x{args.gpus}",
+            "layers": args.layers or shape_layers(args.shape), "parallelism": f"replicas x{args.gpus}",
             "l2": "working set > L2 (weights + KV streamed every step)"}
 
 
@@ -273,12 +338,14 @@ def run_b200(args, world, rank, local):
     rt = BatchRuntime(shape, init_device="cuda", num_blocks=num_blocks, max_slots=max(256, 4 * args.agents),
                       max_ctx=args.max_ctx, max_step_tokens=args.max_step_tokens)
     rt.precapture(args.agents)
+    canary = run_canary(rt, shape) if not args.layers else {"status": "skipped (--layers override)"}
     loop = RealtimeLoop()
     engine = B200Engine(loop, engine_config(args.agents, args.engine_mode), runtime=rt)
     fleet = Fleet(engine, loop, TraceSpec(seed=args.seed, **args.trace), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
-    state = {"i": 0, "timed": None, "idle_s": 0.0}
+    state = {"i": 0, "timed": None, "idle_s": 0.0, "t0": 0}
+    stride = TIMER_STRIDE if args.steps >= 128 else SHORT_TIMER_STRIDE
 
     def one_step():
         t_wait = time.perf_counter()
@@ -292,18 +359,38 @@ def run_b200(args, world, rank, local):
             if t_idle - t_wait > IDLE_LIMIT_S:  # tools take <= 2 s: the engine is stuck, say so
                 raise RuntimeError(f"bench: no runnable step for {IDLE_LIMIT_S} s "
                                    f"(resident {len(engine.sequences)} sequences, step {state['i']})")
-        # kernel roofline timers ride on 1 step in TIMER_STRIDE (their graph event nodes
-        # cost ~9 us each; every-step timing would distort the measured step)
+        # kernel roofline timers ride on the first timed step and 1 in `stride` after it (their
+        # graph event nodes cost ~9 us each; every-step timing would distort the measured step)
         if state["timed"] is not None:
-            rt.dec.timers = state["timed"] if state["i"] % TIMER_STRIDE == 0 else None
+            rt.dec.timers = state["timed"] if (state["i"] - state["t0"]) % stride == 0 else None
         state["i"] += 1
         rt.step()
+
+    # pre-roll (not counted, before the W warm-up steps): run the fleet past the start-up
+    # transient — every agent's initial prompt prefill and the first resolved tool turns — so
+    # the timed window is the steady state the metric is quoted on
+    pre0 = time.perf_counter()
+    need_turns = args.agents if args.preroll else 0
+    while args.preroll and (sum(fate_counts(engine).values()) < need_turns
+                            or len(engine.resume_latencies) < need_turns // 2):
+        one_step()
+        if state["i"] >= args.preroll_max_steps or time.perf_counter() - pre0 > args.preroll_max_s:
+            break
+    torch.cuda.synchronize()
+    preroll = {"steps": state["i"], "seconds": round(time.perf_counter() - pre0, 2),
+               "tool_turns_resolved": sum(fate_counts(engine).values()),
+               "resumes": len(engine.resume_latencies),
+               "rule": f"steps until >= {need_turns} tool calls resolved and >= {need_turns // 2} tool resumes "
+                       f"(cap {args.preroll_max_steps} steps / {args.preroll_max_s:.0f} s), then W warm-up steps"}
+    steady_resume0 = len(engine.resume_latencies)
+    steady_fates0 = fate_counts(engine)
 
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
     barrier(world)
     state["timed"] = {}
+    state["t0"] = state["i"]
     state["idle_s"] = 0.0
     if args.k2_stats:
         rt.dec.run_log = []
@@ -338,6 +425,9 @@ def run_b200(args, world, rank, local):
     rt.dec.timers = state["timed"]
     rt.dec.step_events = None
     per = [(a.elapsed_time(b), g, T) for a, b, g, T in events]
+    timed_idx = [k for k in range(len(per)) if k % stride == 0]
+    n_timed_steps = len(timed_idx)
+    timed_dev_s = max(1e-9, sum(per[k][0] for k in timed_idx) / 1e3)
     # device idle between consecutive steps (end of step k -> start of step k+1)
     gaps = [events[k][1].elapsed_time(events[k + 1][0]) for k in range(len(events) - 1)]
     dev_s = sum(ms for ms, _, _ in per) / 1e3
@@ -346,6 +436,9 @@ def run_b200(args, world, rank, local):
     wall_s = w1 - w0
     launches = lib.load().stb_launch_count() + rt.dec.graph_kernels - launches0  # eager + graph-replayed
     resume = engine.resume_latencies[resume0:]
+    steady_resume = engine.resume_latencies[steady_resume0:]
+    steady_fates = {k: v - steady_fates0.get(k, 0) for k, v in fate_counts(engine).items()
+                    if v - steady_fates0.get(k, 0)}
     fates = {k: v - fates0.get(k, 0) for k, v in fate_counts(engine).items() if v - fates0.get(k, 0)}
     evictions = engine.evictions - evict0
     timers = state["timed"]
@@ -377,8 +470,9 @@ def run_b200(args, world, rank, local):
         roof = {"kernel": dominant, "bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
                 "frac": round(ach / peak, 4), "traffic": tr, "traffic_over_algorithmic": tr_ratio,
                 "traffic_source": tr_src, "peak_source": src, "launches": n,
-                "avg_us": round(t / n * 1e6, 2), "share_of_device_time": round(t / dev_s * TIMER_STRIDE, 4),
-                "sampling": f"CUDA events on 1 step in {TIMER_STRIDE} of the timed region, "
+                "avg_us": round(t / n * 1e6, 2), "share_of_device_time": round(t / timed_dev_s, 4),
+                "sampling": f"CUDA events on timed-region steps 0, {stride}, {2 * stride}, ... "
+                            f"({n_timed_steps} of {args.steps}); share = kernel time / those steps' device time; "
                             f"event-pair overhead {ov * 1e3:.2f} us subtracted per launch"}
     others = {}
     for k, (t, w, n) in kern.items():
@@ -386,7 +480,7 @@ def run_b200(args, world, rank, local):
             continue
         bound, ach, peak, unit = rate(k)
         others[k] = {"bound": bound, "achieved": round(ach, 1), "unit": unit, "frac": round(ach / peak, 4),
-                     "share_of_device_time": round(t / dev_s * TIMER_STRIDE, 4), "launches": n}
+                     "share_of_device_time": round(t / timed_dev_s, 4), "launches": n}
     if k2_launches:  # K2 mixes HBM-bound verify passes (33 queries) with tensor-bound ingests
         roof_t = sum(max(f / (tf_sus * 1e12), by / (hbm * 1e9)) for _, f, by in k2_launches)
         meas_t = sum(max(ms - ov, 1e-3 * ms) / 1e3 for ms, _, _ in k2_launches)
@@ -411,8 +505,10 @@ def run_b200(args, world, rank, local):
         # agent), elapsed = the timed window's wall time; fates / evictions of this replica
         "mean_agent_tokens_per_s": round(tot_emit / wall_max / tot_agents, 2),
         "fates": fates, "evictions": evictions,
-        "tool_resume_ms": {"p50": round(rs[len(rs) // 2] * 1e3, 2) if rs else None,
-                           "p90": round(rs[int(len(rs) * 0.9)] * 1e3, 2) if rs else None, "count": len(rs)},
+        "tool_resume_ms": pct_ms(steady_resume, f"steady state: the {args.warmup} warm-up + {args.steps} timed "
+                                                 f"steps after the pre-roll"),
+        "tool_resume_ms_timed_window": pct_ms(rs, f"the {args.steps} timed steps only"),
+        "fates_steady_state": steady_fates, "preroll": preroll, "canary": canary,
         "roofline": roof, "kernels": others, "gpu_launches": int(launches), "clocks": clocks.summary(),
         "cpu_baseline": cpu, "emitted_tokens": int(tot_emit), "tasks_completed": fleet.completed,
         "graph_replays": rt.dec.graph_replays,
@@ -452,12 +548,49 @@ def run_b200(args, world, rank, local):
         slow = sorted(range(len(per)), key=lambda k: -per[k][0])[:10]
         print("slowest steps (index, ms, decode-only, tokens, event-timed):", file=sys.stderr)
         for k in slow:
-            print(f"   {k:4d} {per[k][0]:8.2f} {per[k][1]!s:5s} {per[k][2]:5d} {(args.warmup + k) % TIMER_STRIDE == 0}",
+            print(f"   {k:4d} {per[k][0]:8.2f} {per[k][1]!s:5s} {per[k][2]:5d} {k % stride == 0}",
                   file=sys.stderr)
         print("K2 timed launches (us avg, TFLOP/s, runs (n, ctx)):", file=sys.stderr)
         for f, ts in sorted(per_launch.items(), key=lambda kv: -sum(kv[1])):
             t = sum(ts) / len(ts) / 1e3
             print(f"   {t * 1e6:8.1f} us x{len(ts):3d} {f / t / 1e12:7.1f} TF/s  {by_flops.get(f, '?')}", file=sys.stderr)
+
+
+def run_canary(rt, shape) -> dict:
+    """Non-vacuous numerics check of the benchmarked model: the engine's logits for a fixed
+    32-token canary sequence vs the fp32 CPU oracle's at the SAME full depth and width
+    (tests/golden/canary_<shape>.npz, written by oracle/gen_canary.py from the same GPU-drawn
+    weights). Relative L2 error <= 2e-2 (BASELINE north star), argmax within the oracle's top 5.
+    A failure raises: the bench never reports a number for a model that computes garbage."""
+    import numpy as np
+
+    from paper_2512_15834_b200.tokens import SALT_PROMPT, fill_ids
+
+    path = ROOT / "tests" / "golden" / f"canary_{shape.name}.npz"
+    if not path.exists():
+        return {"status": "no golden", "golden": str(path.relative_to(ROOT))}
+    g = np.load(path)
+    ids = fill_ids(0, "canary", SALT_PROMPT, 0, int(g["ids"].shape[0]), shape.vocab).tolist()
+    if ids != g["ids"].tolist():
+        raise RuntimeError("canary: token ids differ from the golden's (tokens.fill_ids vs oracle/ids.fill)")
+    got = rt.probe_logits(ids).numpy().astype(np.float64)
+    want = g["logits"].astype(np.float64)
+    err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+    top5 = np.argsort(-want)[:5].tolist()
+    res = {"status": "pass", "rel_l2_err": round(err, 5), "tolerance": 2e-2, "argmax": int(got.argmax()),
+           "oracle_top5": top5, "golden": str(path.relative_to(ROOT)),
+           "what": "32-token canary prefill through the benchmarked weights, last-row logits vs fp32 oracle"}
+    if err > 2e-2 or int(got.argmax()) not in top5:
+        res["status"] = "FAIL"
+        raise RuntimeError(f"canary failed: {res}")
+    return res
+
+
+def pct_ms(xs, window: str) -> dict:
+    xs = sorted(xs)
+    return {"p50": round(xs[len(xs) // 2] * 1e3, 2) if xs else None,
+            "p90": round(xs[int(len(xs) * 0.9)] * 1e3, 2) if xs else None,
+            "mean": round(sum(xs) / len(xs) * 1e3, 2) if xs else None, "count": len(xs), "window": window}
 
 
 def fate_counts(engine) -> dict:
@@ -491,6 +624,10 @@ def main():
     ap.add_argument("--engine-mode", default="tool_cache", choices=["tool_cache", "prefix", "vanilla"],
                     help="tool_cache (the paper's engine-side path, default) or the evict + re-prefill baselines")
     ap.add_argument("--k2-stats", action="store_true", help="diagnostics: K2 run shapes of the mixed steps")
+    ap.add_argument("--no-preroll", dest="preroll", action="store_false",
+                    help="start the warm-up at fleet start (the start-up transient lands in the window)")
+    ap.add_argument("--preroll-max-steps", type=int, default=4000)
+    ap.add_argument("--preroll-max-s", type=float, default=90.0)
     ap.add_argument("--watchdog-s", type=float, default=1800.0,
                     help="dump every thread's stack and exit(1) if the run exceeds this (0: off)")
     args = ap.parse_args()

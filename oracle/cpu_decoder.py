@@ -28,33 +28,51 @@ def draw(shape, seed: int, name: str, norm: bool) -> torch.Tensor:
 
 
 class CpuDecoder:
-    def __init__(self, shape, seed: int = 0, layers: int | None = None, threads: int | None = None):
+    """`source(name, shape, norm)` -> fp32 tensor supplies the weights (default: `draw` on the
+    CPU); `stream=True` keeps no layer resident: each forward rebuilds every layer from
+    `source` (full-size canaries of shapes whose fp32 weights exceed host memory)."""
+
+    def __init__(self, shape, seed: int = 0, layers: int | None = None, threads: int | None = None,
+                 source=None, stream: bool = False):
         self.s = shape
         self.L = shape.layers if layers is None else layers
         if threads:
             torch.set_num_threads(threads)
+        self.source = source or (lambda name, shp, norm: draw(shp, seed, name, norm))
+        self.stream = stream
         d, V = shape.d_model, shape.vocab
-        qd, kvd = shape.n_q * shape.d_head, shape.n_kv * shape.d_head
-        self.embed = draw((V, d), seed, "embed", False)
-        self.layers = []
-        for i in range(self.L):
-            self.layers.append({
-                "an": draw((d,), seed, f"l{i}.attn_norm", True),
-                "qkv": draw((qd + 2 * kvd, d), seed, f"l{i}.wqkv", False),
-                "o": draw((d, qd), seed, f"l{i}.wo", False),
-                "mn": draw((d,), seed, f"l{i}.mlp_norm", True),
-                "gu": draw((2 * shape.d_ff, d), seed, f"l{i}.w_gate_up", False),
-                "dn": draw((d, shape.d_ff), seed, f"l{i}.w_down", False),
-            })
-            if shape.qk_norm:  # Qwen3: per-head RMSNorm of q and k before RoPE
-                self.layers[-1]["qn"] = draw((shape.d_head,), seed, f"l{i}.q_norm", True)
-                self.layers[-1]["kn"] = draw((shape.d_head,), seed, f"l{i}.k_norm", True)
-        self.fn = draw((d,), seed, "final_norm", True)
-        self.head = draw((V, d), seed, "lm_head", False)
+        self.embed = self.source("embed", (V, d), False)
+        self.layers = [] if stream else [self.layer(i) for i in range(self.L)]
+        self.fn = self.source("final_norm", (d,), True)
+        self.head = self.source("lm_head", (V, d), False)
         half = shape.d_head // 2
         inv = np.array([1.0 / math.pow(shape.rope_theta, 2.0 * i / shape.d_head) for i in range(half)])
         self.inv_freq = torch.tensor(inv.astype(np.float32))
         self.cache: dict[str, list] = {}
+
+    def layer(self, i: int) -> dict:
+        s, src = self.s, self.source
+        d = s.d_model
+        qd, kvd = s.n_q * s.d_head, s.n_kv * s.d_head
+        w = {
+            "an": src(f"l{i}.attn_norm", (d,), True),
+            "qkv": src(f"l{i}.wqkv", (qd + 2 * kvd, d), False),
+            "o": src(f"l{i}.wo", (d, qd), False),
+            "mn": src(f"l{i}.mlp_norm", (d,), True),
+            "gu": src(f"l{i}.w_gate_up", (2 * s.d_ff, d), False),
+            "dn": src(f"l{i}.w_down", (d, s.d_ff), False),
+        }
+        if s.qk_norm:  # Qwen3: per-head RMSNorm of q and k before RoPE
+            w["qn"] = src(f"l{i}.q_norm", (s.d_head,), True)
+            w["kn"] = src(f"l{i}.k_norm", (s.d_head,), True)
+        return w
+
+    def iter_layers(self):
+        if not self.stream:
+            yield from enumerate(self.layers)
+        else:
+            for i in range(self.L):
+                yield i, self.layer(i)
 
     def _norm(self, x, w):
         return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps) * w
@@ -87,7 +105,7 @@ class CpuDecoder:
         cache = self.cache.setdefault(rid, [(torch.zeros(0, G, D), torch.zeros(0, G, D)) for _ in range(self.L)])
         pos = torch.arange(start, start + T)
         x = self.embed[torch.tensor(ids, dtype=torch.long)]
-        for i, w in enumerate(self.layers):
+        for i, w in self.iter_layers():
             h = self._norm(x, w["an"])
             qkv = h @ w["qkv"].T
             q = qkv[:, : H * D].view(T, H, D)

@@ -1,0 +1,61 @@
+"""ORACLE (test infrastructure). Full-size canary goldens: the fp32 CPU oracle decoder
+(`oracle/cpu_decoder.py`) at the BASELINE model's full depth and width, run over a fixed
+32-token canary sequence, logits of its last row saved to tests/golden/canary_<shape>.npz.
+
+The engine's weights for the large configs are drawn on the GPU (runtime/weights.py), so
+this script needs a CUDA device only to *draw the same inputs*: every tensor is drawn with
+the product's seeded generator on cuda, copied to the host, upcast to fp32, and the whole
+forward runs on the CPU, one layer at a time (`stream=True`: no layer stays resident, so
+Qwen3-32B fits host memory). Run on the GPU box; the .npz it writes is committed:
+
+    python -m oracle.gen_canary llama3-8b qwen3-32b
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from .cpu_decoder import CpuDecoder
+from .ids import SALT_PROMPT, fill
+
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+CANARY_LEN = 32
+
+
+def canary_ids(vocab: int) -> list[int]:
+    return fill(0, "canary", SALT_PROMPT, 0, CANARY_LEN, vocab)
+
+
+def gpu_drawn_source(seed: int = 0):
+    from paper_2512_15834_b200.runtime.weights import draw
+
+    def src(name, shp, norm):
+        return draw(shp, seed, name, device="cuda", norm=norm).float().cpu()
+
+    return src
+
+
+def main(names: list[str]) -> None:
+    from paper_2512_15834_b200.modelcfg import SHAPES
+
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    for name in names:
+        shape = SHAPES[name]
+        t0 = time.time()
+        dec = CpuDecoder(shape, source=gpu_drawn_source(0), stream=True)
+        ids = canary_ids(shape.vocab)
+        logits = dec.forward("canary", ids, 0, [len(ids) - 1])[0]
+        path = OUT / f"canary_{name}.npz"
+        np.savez_compressed(path, ids=np.asarray(ids, np.int32), logits=logits.numpy().astype(np.float16),
+                            norm=np.float64(logits.norm()), argmax=np.int64(logits.argmax()))
+        print(f"{name}: wrote {path} in {time.time() - t0:.0f} s (argmax {int(logits.argmax())}, "
+              f"norm {float(logits.norm()):.3f})", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["llama3-8b"])

@@ -330,7 +330,17 @@ inline void* stream_scratch(int kind, cudaStream_t st, size_t bytes) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (st) cudaStreamIsCapturing(st, &cs);
   void* p = nullptr;
-  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  if (cs != cudaStreamCaptureStatusNone) {
+    // cudaMalloc is a prohibited call under torch's global capture mode: allow it for this
+    // thread (relaxed), then restore the caller's mode
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (e != cudaSuccess) return nullptr;
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    return nullptr;
+  }
   if (cs != cudaStreamCaptureStatusNone) {
     // first use inside a capture (torch captures on a side stream): the zeroing becomes a
     // node of that graph, which is harmless on replay (the scratch is at rest, i.e. zero,

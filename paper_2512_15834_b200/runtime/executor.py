@@ -215,6 +215,31 @@ class Runtime:
         self.pool.release(scratch)
         self._free_slots.insert(0, scratch)
 
+    def probe_logits(self, ids: list[int]) -> torch.Tensor:
+        """Self-check (the bench's canary): prefill `ids` at positions 0.. on a scratch slot
+        and return the fp32 logits of the last row (host). Leaves no state behind."""
+        if self._host_ev[0] is not None or self._host_ev[1] is not None:
+            torch.cuda.synchronize()
+        slot = self._free_slots.pop(0)
+        n = len(ids)
+        try:
+            self.pool.reserve(slot, n)
+            z = np.zeros
+            batch = StepBatch(np.asarray(ids, np.int32), np.arange(n, dtype=np.int32), np.full(n, slot, np.int32),
+                              z(0, np.int32), z(0, np.int32), np.array([slot], np.int32), np.array([0, n], np.int32),
+                              np.array([n], np.int32), np.array([n - 1], np.int32), np.full(1, -1, np.int32))
+            keep = self.dec.keep_logits
+            self.dec.keep_logits = True
+            self.dec.forward(batch)
+            torch.cuda.synchronize()
+            out = self.dec.last_logits[0].float().cpu()
+            self.dec.keep_logits = keep
+            self.dec.collect()
+        finally:
+            self.pool.release(slot)
+            self._free_slots.insert(0, slot)
+        return out
+
     # -- phase entry points (called by B200Engine) ------------------------------
 
     def prefill(self, seq, cached: int, next_turn: int, done) -> None:

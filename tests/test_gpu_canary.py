@@ -1,0 +1,36 @@
+"""Full-size numerics parity (the benchmarked models at their full depth and width): the
+engine's logits for the fixed 32-token canary sequence vs the fp32 CPU oracle's
+(tests/golden/canary_<shape>.npz, oracle/gen_canary.py, same GPU-drawn weights), relative
+L2 error <= 2e-2 (BASELINE north star) and argmax within the oracle's top 5."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+SHAPES = sorted(p.stem[len("canary_"):] for p in GOLDEN.glob("canary_*.npz"))
+
+
+@pytest.mark.parametrize("name", SHAPES)
+def test_full_size_canary(name):
+    import torch
+
+    from oracle.ids import SALT_PROMPT, fill
+    from paper_2512_15834_b200.modelcfg import SHAPES as ALL
+    from paper_2512_15834_b200.runtime.executor import EagerRuntime
+
+    shape = ALL[name]
+    g = np.load(GOLDEN / f"canary_{name}.npz")
+    ids = fill(0, "canary", SALT_PROMPT, 0, int(g["ids"].shape[0]), shape.vocab)
+    assert ids == g["ids"].tolist()
+    rt = EagerRuntime(shape, init_device="cuda", num_blocks=256, max_slots=8, max_ctx=4096)
+    got = rt.probe_logits(ids).numpy().astype(np.float64)
+    want = g["logits"].astype(np.float64)
+    err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+    assert err <= 2e-2, err
+    assert int(got.argmax()) in np.argsort(-want)[:5].tolist()
+    del rt
+    torch.cuda.empty_cache()
