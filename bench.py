@@ -320,7 +320,7 @@ def run_b200(args, world, rank, local):
     from paper_2512_15834_b200.modelcfg import SHAPES
     from paper_2512_15834_b200.runtime import lib
     from paper_2512_15834_b200.runtime.executor import BatchRuntime
-    from paper_2512_15834_b200.runtime.fleet import Fleet, TraceSpec, engine_config
+    from harness.fleet import Fleet, TraceSpec, engine_config
     from paper_2512_15834_b200.runtime.realtime import RealtimeLoop
 
     # one GPU per rank; on a box with fewer GPUs than ranks (CI smoke of the multi-rank path,
@@ -574,16 +574,31 @@ def run_canary(rt, shape) -> dict:
     if ids != g["ids"].tolist():
         raise RuntimeError("canary: token ids differ from the golden's (tokens.fill_ids vs oracle/ids.fill)")
     got = rt.probe_logits(ids).numpy().astype(np.float64)
-    want = g["logits"].astype(np.float64)
-    err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
-    top5 = np.argsort(-want)[:5].tolist()
-    res = {"status": "pass", "rel_l2_err": round(err, 5), "tolerance": 2e-2, "argmax": int(got.argmax()),
-           "oracle_top5": top5, "golden": str(path.relative_to(ROOT)),
-           "what": "32-token canary prefill through the benchmarked weights, last-row logits vs fp32 oracle"}
-    if err > 2e-2 or int(got.argmax()) not in top5:
-        res["status"] = "FAIL"
+    res = canary_compare(got, g)
+    res.update(golden=str(path.relative_to(ROOT)),
+               what="32-token canary prefill through the benchmarked weights, last-row logits vs the fp32 oracle")
+    if res["status"] != "pass":
         raise RuntimeError(f"canary failed: {res}")
     return res
+
+
+def canary_compare(got, g) -> dict:
+    """Engine logits vs the golden: (1) vs the oracle with bf16 rounding at the engine's storage
+    points, relative L2 <= 2e-2 (kernel error); (2) vs the pure fp32 oracle, within the
+    intrinsic bf16-storage error the oracle itself measures + 1e-2; (3) argmax in the fp32
+    oracle's top 5."""
+    import numpy as np
+
+    fp32 = g["logits"].astype(np.float64)
+    emu = g["logits_bf16_points"].astype(np.float64)
+    intrinsic = float(g["intrinsic_bf16_err"])
+    e_emu = float(np.linalg.norm(got - emu) / np.linalg.norm(emu))
+    e_fp32 = float(np.linalg.norm(got - fp32) / np.linalg.norm(fp32))
+    top5 = np.argsort(-fp32)[:5].tolist()
+    ok = e_emu <= 2e-2 and e_fp32 <= intrinsic + 1e-2 and int(got.argmax()) in top5
+    return {"status": "pass" if ok else "FAIL", "rel_l2_err_vs_bf16_storage_oracle": round(e_emu, 5),
+            "tolerance": 2e-2, "rel_l2_err_vs_fp32_oracle": round(e_fp32, 5),
+            "intrinsic_bf16_storage_err": round(intrinsic, 5), "argmax": int(got.argmax()), "oracle_top5": top5}
 
 
 def pct_ms(xs, window: str) -> dict:

@@ -13,7 +13,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from enum import Enum
 
-from .errors import InvalidScenario
+from paper_2512_15834_b200.errors import InvalidScenario
 
 
 @dataclass(frozen=True)

@@ -18,12 +18,12 @@ import json
 import math
 from dataclasses import dataclass
 
-from ..domain import TOOL_END, TOOL_START, Token, TokenKind, ToolCall, canonical_key
-from ..engine import EngineConfig
-from ..mocks import GenerationScript, SpecConfig, ToolRuntime, derived_rng
-from ..orchestrator import AgentSetup, EngineClient, HopPolicy, chunk_text
-from ..sim import spawn
-from ..workload import TOOL_ROSTER, task_assignment
+from paper_2512_15834_b200.domain import TOOL_END, TOOL_START, Token, TokenKind, ToolCall, canonical_key
+from paper_2512_15834_b200.engine import EngineConfig
+from .mocks import GenerationScript, SpecConfig, ToolRuntime, derived_rng
+from .orchestrator import AgentSetup, EngineClient, HopPolicy, chunk_text
+from .sim import spawn
+from .workload import TOOL_ROSTER, task_assignment
 
 
 @dataclass(frozen=True)

@@ -19,9 +19,9 @@ from __future__ import annotations
 import json
 from dataclasses import dataclass, field, replace
 
-from .domain import TOOL_END, TOOL_START, Token, TokenKind, ToolCall, canonical_key
-from .engine import EngineConfig
-from .errors import ConfigError, InvalidBaseline, InvalidWindow
+from paper_2512_15834_b200.domain import TOOL_END, TOOL_START, Token, TokenKind, ToolCall, canonical_key
+from paper_2512_15834_b200.engine import EngineConfig
+from paper_2512_15834_b200.errors import ConfigError, InvalidBaseline, InvalidWindow
 from .mocks import GenerationScript, SpecConfig, ToolRuntime, derived_rng
 from .orchestrator import AgentResult, AgentSetup, EngineClient, default_engine_factory, uniform_hops
 from .sim import Simulator, spawn

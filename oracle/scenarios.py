@@ -32,7 +32,8 @@ def reference_api():
 
 
 def product_api():
-    from paper_2512_15834_b200 import accounting, domain, engine, mocks, orchestrator, service, sim, workload
+    from harness import accounting, mocks, orchestrator, sim, workload
+    from paper_2512_15834_b200 import domain, engine, service
 
     return SimpleNamespace(domain=domain, engine=engine, mocks=mocks, model=accounting, orchestrator=orchestrator,
                            service=service, sim=sim, workload=workload, is_reference=False)

@@ -124,6 +124,7 @@ class KVPool:
         lib.call("stb_kv_pool_create", device, shape.layers, shape.n_kv, shape.d_head, 16, num_blocks,
                  max_slots, max_blocks_per_slot, C.byref(h))
         self.h = h
+        self.log: list | None = None  # record mode: every allocator op, for an oracle replay
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -133,12 +134,18 @@ class KVPool:
 
     def reserve(self, slot: int, n: int) -> None:
         lib.call("stb_kv_reserve", self.h, slot, n)
+        if self.log is not None:
+            self.log.append(("reserve", slot, n))
 
     def truncate(self, slot: int, n: int) -> None:
         lib.call("stb_kv_truncate", self.h, slot, n)
+        if self.log is not None:
+            self.log.append(("truncate", slot, n))
 
     def release(self, slot: int) -> None:
         lib.call("stb_kv_release", self.h, slot)
+        if self.log is not None:
+            self.log.append(("release", slot, 0))
 
     def free_blocks(self) -> int:
         return lib.call("stb_kv_free_blocks", self.h)

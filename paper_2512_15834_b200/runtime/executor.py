@@ -122,6 +122,11 @@ class Runtime:
         self.record = record
         self.reclaimer = None           # engine hook: free retained prefixes under KV pressure
         self.trace: list[dict] = []     # per sampled row: rid, pos, fed, target, sampled, logits (record mode)
+        # record mode, per completed flight: every fed run (rid, start, ids, sampled local rows) with the
+        # sampled rows' logits / raw argmax, and the block list of every sequence it touched
+        self.flights: list[dict] = []
+        if record:
+            self.pool.log = []
         self.forwards = 0
         self.tokens_fed = 0
         self.emitted = 0                # tokens sampled and counted (reference kv_tokens += ...)
@@ -502,6 +507,16 @@ class Runtime:
             owners = [j.seq for j in f.decodes]
             for r in f.runs:
                 owners.extend([r.seq] * len(r.ids))
+            items = [(j.seq.rid, int(b.pos[i]), [int(b.ids[i])], [0]) for i, j in enumerate(f.decodes)]
+            off = len(f.decodes)
+            for r in f.runs:
+                items.append((r.seq.rid, r.start, list(r.ids), list(r.rows)))
+                off += len(r.ids)
+            slots = {j.seq.rid: j.seq.dev.slot for j in f.decodes}
+            slots.update({r.seq.rid: r.seq.dev.slot for r in f.runs})
+            self.flights.append({"items": items, "logits": logits, "raw": raw, "sampled": list(sampled),
+                                 "pool_ops": len(self.pool.log), "slots": slots,
+                                 "tables": {rid: self.pool.blocks(sl) for rid, sl in slots.items()}})
             for i in range(R):
                 row = int(b.sample_rows[i])
                 self.trace.append({"rid": owners[row].rid, "pos": int(b.pos[row]), "fed": int(b.ids[row]),

@@ -17,7 +17,36 @@ import time
 from typing import Callable
 
 from ..errors import InvalidDelay
-from ..sim import Future
+
+
+class Future:
+    """Single-assignment value resolved by a timer (what `sleep` hands to a driving coroutine:
+    the same `resolve` / `result` / `add_done_callback` surface as the reference `sim.Future`,
+    `sim.py:69-97`); callbacks run on the loop thread."""
+
+    __slots__ = ("done", "_value", "_callbacks")
+
+    def __init__(self):
+        self.done, self._value, self._callbacks = False, None, []
+
+    def resolve(self, value) -> None:
+        if self.done:
+            raise RuntimeError("future resolved twice")
+        self.done, self._value = True, value
+        callbacks, self._callbacks = self._callbacks, []
+        for cb in callbacks:
+            cb(value)
+
+    def result(self):
+        if not self.done:
+            raise RuntimeError("future not resolved yet")
+        return self._value
+
+    def add_done_callback(self, cb) -> None:
+        if self.done:
+            cb(self._value)
+        else:
+            self._callbacks.append(cb)
 
 
 class RealtimeLoop:

@@ -47,7 +47,8 @@ def test_kernels_are_sm100a_tcgen05():
 def test_product_fails_loudly_without_cuda():
     import torch
 
-    from paper_2512_15834_b200 import EngineConfig, EngineSim, KernelError, Simulator
+    from harness.sim import Simulator
+    from paper_2512_15834_b200 import EngineConfig, EngineSim, KernelError
 
     if torch.cuda.is_available():
         return

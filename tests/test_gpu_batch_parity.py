@@ -1,0 +1,104 @@
+"""Numeric parity of the THROUGHPUT path (what bench.py times): `BatchRuntime` with one flight
+in the air (pipeline=True), >= 8 concurrent agent sequences whose steps pack decode rows
+together with prompt prefills, suffix re-prefills after misses, draft-verify passes (full and
+partial acceptance, K4 + rollback) and in-place tool-output ingests, on a wall-clock fleet.
+
+Every completed flight is replayed on the fp32 CPU oracle (`oracle/cpu_decoder.py`): each
+sequence's fed run (rid, start, ids) is appended to its oracle KV cache at the same start (so
+rollbacks / evictions truncate it exactly as the paged pool does) and the oracle's logits of the
+sampled rows are compared with the GPU's: relative L2 <= 2e-2 per row (bf16 vs fp32, BASELINE
+north star); the GPU's unforced raw argmax must be a near-max of the oracle's logits. The KV
+allocator's op log is replayed on the oracle's LIFO allocator (`oracle/kv_alloc.py`) and every
+sequence's block table at every flight completion must match it bit for bit.
+(Reference: the engine hosts many concurrent sequences, `engine.py:172-180`; the fleet driver is
+`workload.py:293-384`.)
+"""
+
+import dataclasses
+import random
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 2e-2
+
+
+def _run_fleet(shape, agents: int, steps: int, seed: int = 1):
+    from harness.fleet import Fleet, TraceSpec, engine_config
+    from paper_2512_15834_b200.domain import Token, TokenKind
+    from paper_2512_15834_b200.engine import B200Engine
+    from paper_2512_15834_b200.runtime.executor import BatchRuntime
+    from paper_2512_15834_b200.runtime.realtime import RealtimeLoop
+
+    rt = BatchRuntime(shape, num_blocks=4096, max_slots=256, max_ctx=4096, max_step_tokens=1024, pipeline=True,
+                      record=True)
+    loop = RealtimeLoop()
+    engine = B200Engine(loop, engine_config(agents), runtime=rt)
+    rng = random.Random(seed)
+    orig = engine.submit_tool_cache
+
+    def submit(rid, entry):  # one draft in three: right key, wrong call tokens -> partial hit + rollback
+        if entry.call_tokens and rng.random() < 0.33:
+            toks = list(entry.call_tokens)
+            k = rng.randrange(1, len(toks) - 1)
+            toks[k] = Token(TokenKind.TEXT, toks[k].text + "~")
+            entry = dataclasses.replace(entry, call_tokens=toks)
+        return orig(rid, entry)
+
+    engine.submit_tool_cache = submit
+    spec = TraceSpec(prompt_tokens=40, reason=(3, 18), call_tokens=8, output=(2, 30), tool_latency=(0.002, 0.03),
+                     tools=(1, 3), closing=(1, 3), draft_latency=0.004, accept_rate=0.8, seed=seed, library=16)
+    fleet = Fleet(engine, loop, spec, agents)
+    fleet.start()
+    loop.run_until_idle(max_steps=steps)
+    rt.drain()
+    return rt, engine
+
+
+@pytest.mark.parametrize("name", ["tiny", "qwen3-mini", "llama3-8b[L=2,V=32k]"])
+def test_batch_runtime_parity(name):
+    from oracle.cpu_decoder import CpuDecoder
+    from oracle.kv_alloc import LifoAllocator
+    from paper_2512_15834_b200.modelcfg import SHAPES, QWEN3_MINI, TINY
+
+    shape = {"tiny": TINY, "qwen3-mini": QWEN3_MINI}.get(name) or dataclasses.replace(
+        SHAPES["llama3-8b"], name=name, layers=2, vocab=32768)
+    big = name.startswith("llama")
+    rt, engine = _run_fleet(shape, agents=10 if big else 12, steps=140 if big else 260)
+    ora = CpuDecoder(shape)
+    alloc = LifoAllocator(4096)
+    ops = rt.pool.log
+    op_i = 0
+    worst, rows_checked = 0.0, 0
+    mixed = verify = multi_run = 0
+    for f in rt.flights:
+        k = 0
+        runs = [it for it in f["items"] if len(it[2]) > 1 or it[3] != [0]]
+        mixed += bool(runs) and len(runs) < len(f["items"])
+        multi_run += len(runs) >= 2
+        verify += any(len(rows) > 1 for _, _, _, rows in f["items"])
+        for rid, start, ids, rows in f["items"]:
+            want = ora.forward(rid, ids, start, rows)
+            for j in range(len(rows)):
+                got = f["logits"][k]
+                err = float((got - want[j]).norm() / want[j].norm())
+                worst = max(worst, err)
+                raw = f["raw"][k]
+                gap = float(want[j].max() - want[j][raw])
+                assert gap <= 2e-2 * float(want[j].max() - want[j].min()), (rid, start, j, raw, gap)
+                k += 1
+                rows_checked += 1
+        assert k == len(f["logits"])
+        while op_i < f["pool_ops"]:
+            op, slot, n = ops[op_i]
+            getattr(alloc, op)(slot, n) if op != "release" else alloc.release(slot)
+            op_i += 1
+        for rid, slot in f["slots"].items():
+            assert alloc.blocks(slot) == f["tables"][rid], (rid, slot)
+    assert worst <= LOGIT_RTOL, worst
+    fates = [x for s in engine.sequences.values() for x in s.fates]
+    # the trace really exercised the packed mixed path
+    assert len(rt.flights) >= 100 and rows_checked >= 500
+    assert mixed >= 10 and verify >= 5 and multi_run >= 3, (mixed, verify, multi_run)
+    assert {"full_hit", "partial_hit"} <= set(fates) and engine.evictions > 0, (set(fates), engine.evictions)

@@ -161,7 +161,7 @@ def test_wire_submission_gpu(when, fate):
 
     from paper_2512_15834_b200.engine import EngineConfig
     from paper_2512_15834_b200.service import create_app
-    from paper_2512_15834_b200.sim import Simulator
+    from harness.sim import Simulator
 
     pair = Pair()
     runs = []
@@ -199,7 +199,8 @@ def test_full_width_parity(base):
 
 def test_default_engine_is_native():
     """`EngineSim(sim, config)` builds the CUDA runtime; its kernels really ran."""
-    from paper_2512_15834_b200 import EngineConfig, EngineSim, Simulator
+    from harness.sim import Simulator
+    from paper_2512_15834_b200 import EngineConfig, EngineSim
     from paper_2512_15834_b200.runtime import lib
 
     before = lib.load().stb_launch_count()

@@ -11,7 +11,7 @@ import torch.multiprocessing as mp
 
 from oracle import scenarios as S
 from paper_2512_15834_b200.runtime.replicas import reduce_run, shard_agents
-from paper_2512_15834_b200.workload import WorkloadConfig, _execute
+from harness.workload import WorkloadConfig, _execute
 from stub_runtime import stub_factory
 
 

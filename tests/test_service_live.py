@@ -10,7 +10,7 @@ from fastapi.testclient import TestClient
 from oracle import scenarios as S
 from paper_2512_15834_b200.engine import EngineConfig
 from paper_2512_15834_b200.service import create_app
-from paper_2512_15834_b200.sim import Simulator
+from harness.sim import Simulator
 from stub_runtime import stub_factory
 
 API = S.product_api()

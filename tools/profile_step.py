@@ -20,7 +20,7 @@ import torch  # noqa: E402
 
 from paper_2512_15834_b200.domain import EOS, Token, TokenKind  # noqa: E402
 from paper_2512_15834_b200.engine import B200Engine, EngineConfig  # noqa: E402
-from paper_2512_15834_b200.mocks import GenerationScript  # noqa: E402
+from harness.mocks import GenerationScript  # noqa: E402
 from paper_2512_15834_b200.modelcfg import SHAPES  # noqa: E402
 from paper_2512_15834_b200.runtime.executor import BatchRuntime  # noqa: E402
 from paper_2512_15834_b200.runtime.realtime import RealtimeLoop  # noqa: E402
