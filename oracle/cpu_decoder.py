@@ -99,6 +99,42 @@ class CpuDecoder:
     def drop(self, rid: str) -> None:
         self.cache.pop(rid, None)
 
+    def layer_forward(self, w: dict, x: torch.Tensor, pos: torch.Tensor, start: int, kv: tuple):
+        """One decoder layer: x [T, d] fp32 at absolute positions `pos` (= start..start+T-1), kv =
+        this layer's (K, V) cache rows; returns (new x, new kv). Also the per-layer teacher-forced
+        check of the full-size canary (tests/test_gpu_canary.py) feeds it the engine's own layer
+        inputs."""
+        s = self.s
+        T = x.shape[0]
+        r = (lambda t: t.to(torch.bfloat16).float()) if self.bf16_points else (lambda t: t)
+        H, G, D = s.n_q, s.n_kv, s.d_head
+        h = r(self._norm(x, w["an"]))
+        qkv = h @ w["qkv"].T
+        q = qkv[:, : H * D].view(T, H, D)
+        k = qkv[:, H * D: (H + G) * D].view(T, G, D)
+        v = qkv[:, (H + G) * D:].view(T, G, D)
+        q, k = self._qk(w, q, k)
+        q, k = self._rope(q, pos), self._rope(k, pos)
+        q, k, v = r(q), r(k), r(v)
+        kc, vc = kv
+        kc = torch.cat([kc[:start], k])
+        vc = torch.cat([vc[:start], v])
+        n = kc.shape[0]
+        rep = H // G
+        kk = kc.repeat_interleave(rep, dim=1)  # [n, H, D]
+        vv = vc.repeat_interleave(rep, dim=1)
+        scores = torch.einsum("thd,nhd->htn", q, kk) / math.sqrt(D)
+        mask = torch.arange(n)[None, :] > pos[:, None]
+        scores = scores.masked_fill(mask[None], float("-inf"))
+        p = torch.softmax(scores, dim=-1)
+        attn = r(torch.einsum("htn,nhd->thd", p, vv).reshape(T, H * D))
+        x = x + attn @ w["o"].T
+        h = r(self._norm(x, w["mn"]))
+        gu = h @ w["gu"].T
+        g, u = gu[:, : s.d_ff], gu[:, s.d_ff:]
+        x = x + r(torch.nn.functional.silu(g) * u) @ w["dn"].T
+        return x, (kc, vc)
+
     def forward(self, rid: str, ids: list[int], start: int, rows: list[int]) -> torch.Tensor:
         """fp32 forward; with `self.bf16_points` set, values are rounded to bf16 exactly where the
         B200 engine STORES bf16 (GEMM inputs, the rotated q and the K/V cache rows, the attention
@@ -113,32 +149,7 @@ class CpuDecoder:
         pos = torch.arange(start, start + T)
         x = self.embed[torch.tensor(ids, dtype=torch.long)]
         for i, w in self.iter_layers():
-            h = r(self._norm(x, w["an"]))
-            qkv = h @ w["qkv"].T
-            q = qkv[:, : H * D].view(T, H, D)
-            k = qkv[:, H * D: (H + G) * D].view(T, G, D)
-            v = qkv[:, (H + G) * D:].view(T, G, D)
-            q, k = self._qk(w, q, k)
-            q, k = self._rope(q, pos), self._rope(k, pos)
-            q, k, v = r(q), r(k), r(v)
-            kc, vc = cache[i]
-            kc = torch.cat([kc[:start], k])
-            vc = torch.cat([vc[:start], v])
-            cache[i] = (kc, vc)
-            n = kc.shape[0]
-            rep = H // G
-            kk = kc.repeat_interleave(rep, dim=1)  # [n, H, D]
-            vv = vc.repeat_interleave(rep, dim=1)
-            scores = torch.einsum("thd,nhd->htn", q, kk) / math.sqrt(D)
-            mask = torch.arange(n)[None, :] > pos[:, None]
-            scores = scores.masked_fill(mask[None], float("-inf"))
-            p = torch.softmax(scores, dim=-1)
-            attn = r(torch.einsum("htn,nhd->thd", p, vv).reshape(T, H * D))
-            x = x + attn @ w["o"].T
-            h = r(self._norm(x, w["mn"]))
-            gu = h @ w["gu"].T
-            g, u = gu[:, : s.d_ff], gu[:, s.d_ff:]
-            x = x + r(torch.nn.functional.silu(g) * u) @ w["dn"].T
+            x, cache[i] = self.layer_forward(w, x, pos, start, cache[i])
         sel = x[torch.tensor(rows, dtype=torch.long)]
         return r(self._norm(sel, self.fn)) @ self.head.T
 

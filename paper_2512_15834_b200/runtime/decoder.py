@@ -266,6 +266,7 @@ class Decoder:
         # leading rows of each GEMM output that may be non-zero (rows at and past it are zero)
         self._dirty = {"qkv": 0, "proj": 0, "gu": 0, "logits": 0}
         self._stream_cache: dict = {}
+        self.taps: list | None = None  # debug (canary): residual stream after the embedding and each layer
 
     # -- buffers ----------------------------------------------------------------
 
@@ -455,6 +456,8 @@ class Decoder:
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
         clr = T if T <= CLEAR_MAX else 0
+        if self.taps is not None:
+            self.taps.append(x[:T].clone())
         for i in range(s.layers):
             self.gemm(h[:T], w[f"l{i}.wqkv"], "qkv", st, "wqkv")
             if s.qk_norm:
@@ -489,6 +492,8 @@ class Decoder:
             else:  # residual add only; the final norm runs on the sampled rows
                 call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w["final_norm"]), None, T, d, s.rms_eps, clr, st)
             self._cleared("proj", clr)
+            if self.taps is not None:
+                self.taps.append(x[:T].clone())
         rows = self.rows[:R]
         call("stb_gather_rmsnorm", _p(x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows), R, d, s.rms_eps, st)
         self.gemm(rows, w["lm_head"], "logits", st, "lm_head")

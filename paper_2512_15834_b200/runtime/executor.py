@@ -220,9 +220,11 @@ class Runtime:
         self.pool.release(scratch)
         self._free_slots.insert(0, scratch)
 
-    def probe_logits(self, ids: list[int]) -> torch.Tensor:
+    def probe_logits(self, ids: list[int], taps: list | None = None) -> torch.Tensor:
         """Self-check (the bench's canary): prefill `ids` at positions 0.. on a scratch slot
-        and return the fp32 logits of the last row (host). Leaves no state behind."""
+        and return the fp32 logits of the last row (host). Leaves no state behind. `taps` (a
+        list) receives the residual stream [n, d] (fp32, host) after the embedding and after
+        every layer, for the per-layer teacher-forced check."""
         if self._host_ev[0] is not None or self._host_ev[1] is not None:
             torch.cuda.synchronize()
         slot = self._free_slots.pop(0)
@@ -235,8 +237,14 @@ class Runtime:
                               np.array([n], np.int32), np.array([n - 1], np.int32), np.full(1, -1, np.int32))
             keep = self.dec.keep_logits
             self.dec.keep_logits = True
-            self.dec.forward(batch)
-            torch.cuda.synchronize()
+            self.dec.taps = [] if taps is not None else None
+            try:
+                self.dec.forward(batch)
+                torch.cuda.synchronize()
+            finally:
+                if taps is not None:
+                    taps.extend(t.float().cpu() for t in self.dec.taps)
+                self.dec.taps = None
             out = self.dec.last_logits[0].float().cpu()
             self.dec.keep_logits = keep
             self.dec.collect()
