@@ -84,6 +84,14 @@ int stb_qkv_norm_rope_commit(stb_kv_pool* pool, int layer, float* qkv, void* q_o
                              const int32_t* pos_of, int n, int n_q, float rope_theta, const void* q_norm,
                              const void* k_norm, float eps, int clear_rows, void* stream);
 
+/* Same, gpt-oss attention inputs (config C4): `bias` (fp32 [(n_q + 2 n_kv) d_head], or NULL) is
+ * added to every q / k / v row before RoPE; `inv_freq` (device fp32 [d_head / 2], or NULL for
+ * theta^(-2i/d)) are the rotary frequencies — the YaRN table for gpt-oss — and `rope_scale`
+ * multiplies cos and sin (YaRN's attention factor; 1 = plain RoPE).                  */
+int stb_qkv_rope_commit_ex(stb_kv_pool* pool, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                           const int32_t* pos_of, int n, int n_q, float rope_theta, const float* inv_freq,
+                           float rope_scale, const float* bias, int clear_rows, void* stream);
+
 /* ---- K3: paged decode attention (one query per sequence) ----------------
  * Replaces the decode charges engine.py:270,276,302,317. q/out bf16
  * [B][n_q][d_head]; slots/ctx_lens int32 [B]; split-K over the context with
@@ -96,6 +104,13 @@ int stb_qkv_norm_rope_commit(stb_kv_pool* pool, int layer, float* qkv, void* q_o
 int64_t stb_attn_decode_workspace(int B, int n_q, int n_kv, int d_head);
 int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                     const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, void* work, void* stream);
+/* Same, gpt-oss attention (config C4): `window` > 0 restricts each query to its last `window`
+ * keys (sliding-window layers: key j is visible from query position p iff p - window < j <= p);
+ * `sinks` (device fp32 [n_q], or NULL) adds exp(sink_h) to head h's softmax denominator (a
+ * learned logit with no value row). window = 0 and sinks = NULL is stb_attn_decode.        */
+int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                       const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, int window,
+                       const float* sinks, void* work, void* stream);
 
 /* ---- K2: append-prefill attention (n new queries against resident pages)
  * Replaces prefill engine.py:251, verify engine.py:296 and ingest
@@ -114,6 +129,11 @@ int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, con
 int stb_attn_prefill_split(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                            const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,
                            int max_q, int active_units, void* stream);
+
+/* Same, with the sliding window and sinks of stb_attn_decode_ex (tensor-core path only). */
+int stb_attn_prefill_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                        const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,
+                        int max_q, int active_units, int window, const float* sinks, void* stream);
 
 /* ---- K4: speculation validation (greedy LCP, bit-exact int32) -----------
  * Replaces validate_draft (engine.py:96-111) + the consume rule (engine.py:291).
@@ -216,6 +236,10 @@ int stb_add_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d
 /* y bf16 [n][f] = silu(gate) * up with gu fp32 [n][2f] holding (gate_i, up_i) pairs
  * interleaved (gu[t][2i], gu[t][2i+1]); gu rows < clear_rows zeroed after reading */
 int stb_silu_mul(float* gu, void* y, int n, int f, int clear_rows, void* stream);
+/* stb_add_rmsnorm with a bias row (fp32 [d], or NULL) added to every delta row: the O
+ * projection's bias of the gpt-oss family (config C4) */
+int stb_add_bias_rmsnorm(float* x, float* delta, const float* bias, const void* w, void* y, int n, int d, float eps,
+                         int clear_rows, void* stream);
 /* rows[i] = x[idx[i]] as bf16 after rmsnorm: final norm fused with row gather */
 int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,
                        void* stream);
@@ -224,6 +248,35 @@ int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* 
  * clear != 0 zeroes the logits rows after reading */
 int stb_sample_forced(float* logits, int64_t ld, const int32_t* target, int R, int V, float bias, int32_t* out,
                       int32_t* raw_argmax, float* raw_max, int clear, void* stream);
+
+/* ---- MoE MLP of the gpt-oss family (config C4; moe.cu) --------------------
+ * Replaces the MLP share of the phase charges engine.py:251,270,296,358 for routed-expert
+ * models. Per layer: router logits [T][E] (K5, bf16) -> stb_moe_route -> stb_moe_gather ->
+ * stb_moe_gemm_mxfp4 (gate-up) -> stb_moe_gemm_mxfp4 (down) -> stb_moe_combine.
+ * route: + bias, top-k per token (ties -> lower id), softmax over the k logits; expert[t*k+r],
+ *   weight[t*k+r], rank[t*k+r] = arrival order within the expert (counts[E] must be zero on
+ *   entry and hold the per-expert totals on exit; stb_moe_combine zeroes them again).
+ * gather: offsets[E+1] = exclusive prefix of counts; perm[t*k+r] = offsets[e] + rank; xperm
+ *   fp16 [T*k][d] = the token rows, expert-contiguous.
+ * gemm: per expert e, out rows [offsets[e], offsets[e+1]) = xperm rows x W_e^T (+ bias[e]); W_e
+ *   MXFP4 tiles (runtime/weights.py pack_mxfp4_tiles: [E][ceil(N/128)][K/64][4352] bytes);
+ *   STB_MOE_GATE_UP: out fp16 [rows][N/2] (ldo) = (clamp(up,-l,l) + 1) * g * sigmoid(1.702 g),
+ *   g = min(gate, l), gate / up = even / odd rows of W_e; STB_MOE_DOWN: out fp32 [rows][N].
+ *   `rows` = T*k (the host's only view of the routing: it sizes the token tile); rows_cap =
+ *   rows allocated in xperm.
+ * combine: x[t] += sum_r weight[t*k+r] * y[perm[t*k+r]] (r ascending); h_out bf16 = RMSNorm(x) *
+ *   norm_w (skipped if h_out is NULL).                                                    */
+#define STB_MOE_GATE_UP 1
+#define STB_MOE_DOWN 2
+int stb_moe_route(const float* logits, int64_t ld, const float* bias, int T, int E, int k, int32_t* counts,
+                  int32_t* expert, int32_t* rank, float* weight, void* stream);
+int stb_moe_gather(const void* h, int64_t ldh, int T, int d, int k, int E, const int32_t* counts,
+                   const int32_t* expert, const int32_t* rank, int32_t* offsets, int32_t* perm, void* xperm,
+                   void* stream);
+int stb_moe_gemm_mxfp4(const void* xperm, int rows_cap, const void* wtiles, const float* bias, const int32_t* counts,
+                       int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows, void* stream);
+int stb_moe_combine(float* x, const float* y, int T, int d, int k, const int32_t* perm, const float* weight,
+                    const void* norm_w, void* h_out, float eps, int32_t* counts, int E, void* stream);
 
 #ifdef __cplusplus
 }

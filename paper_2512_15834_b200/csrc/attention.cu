@@ -149,7 +149,7 @@ __device__ __forceinline__ void page_step(const uint32_t (*qf)[4], uint32_t ks, 
 // keys of the chunk for the two rows this lane holds; full chunks skip masking.
 template <int D, int NP>
 __device__ __forceinline__ void chunk_step(const uint32_t (*qf)[4], uint32_t ks0, int lim0, int lim1, RowState<D>& st,
-                                           int lane) {
+                                           int lane, int lo = 0) {
   constexpr int PAGE = 16 * D * 2;
   // pages past both rows' limits were never loaded: no S, no P V for them
   const int lim = lim0 > lim1 ? lim0 : lim1;
@@ -172,14 +172,14 @@ __device__ __forceinline__ void chunk_step(const uint32_t (*qf)[4], uint32_t ks0
     }
   }
   const int kc = (lane & 3) * 2;
-  if (lim0 < 16 * NP || lim1 < 16 * NP) {
+  if (lim0 < 16 * NP || lim1 < 16 * NP || lo > 0) {  // lo: sliding-window start inside the chunk
 #pragma unroll
     for (int t = 0; t < 2 * NP; ++t)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int k = t * 8 + kc + j;
-        if (k >= lim0) s[t][j] = -INFINITY;
-        if (k >= lim1) s[t][2 + j] = -INFINITY;
+        if (k >= lim0 || k < lo) s[t][j] = -INFINITY;
+        if (k >= lim1 || k < lo) s[t][2 + j] = -INFINITY;
       }
   }
   float mx0 = -INFINITY, mx1 = -INFINITY;
@@ -302,9 +302,15 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
-    float* __restrict__ o_part, float* __restrict__ lse_part, int* __restrict__ tickets) {
+    float* __restrict__ o_part, float* __restrict__ lse_part, int* __restrict__ tickets, int window,
+    const float* __restrict__ sinks) {
   constexpr int PAGE = 16 * D * 2;
   constexpr int NP = kChunkPages;
+  // sliding window (gpt-oss, window > 0): a sequence's keys are [kst, ctx), kst = max(0, ctx -
+  // window); its chunks are counted from the chunk holding kst, so the partition, the page
+  // fetches and the merge fan-in only ever see the window
+  auto first_chunk = [&](int ctx) { return window > 0 ? max(0, ctx - window) / (16 * NP) : 0; };
+  auto nchunks = [&](int ctx) { return (ctx + 16 * NP - 1) / (16 * NP) - first_chunk(ctx); };
   constexpr int STAGE = NP * 2 * PAGE;  // K and V of NP pages
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int prefix[kMaxB + 1];  // chunk units before sequence b (< 2^31: B * n_kv * ctx/32)
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
         const int c = ctx_lens[b];
         s_ctx[b] = c;
         s_slot[b] = slots[b];
-        local += n_kv * ((c + 16 * NP - 1) / (16 * NP));
+        local += n_kv * nchunks(c);
       }
     }
     int incl = local;
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       const int b = b0 + j;
       if (b < B) {
         prefix[b] = run;
-        run += n_kv * ((s_ctx[b] + 16 * NP - 1) / (16 * NP));
+        run += n_kv * nchunks(s_ctx[b]);
       }
     }
     if (threadIdx.x == 32 * kDecWarps - 1) prefix[B] = run;
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   // of the unit space, segments crossing pair boundaries.
   const int Wmax = gridDim.x * kDecWarps;
   if (warp == 0) {  // one warp, shuffles only (no block barriers inside the search)
-    auto chunks = [&](int b) { return (s_ctx[b] + 16 * NP - 1) / (16 * NP); };
+    auto chunks = [&](int b) { return nchunks(s_ctx[b]); };
     auto count = [&](int T) {  // warps the pair-aligned cut with target T needs
       int c = 0;
       for (int b = lane; b < B; b += 32) c += n_kv * ((chunks(b) + T - 1) / T);
@@ -409,7 +415,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       const int mid = (lo + hi + 1) >> 1;
       if (s_wbase[mid] <= w) lo = mid; else hi = mid - 1;
     }
-    const int ch = (s_ctx[lo] + 16 * NP - 1) / (16 * NP);
+    const int ch = nchunks(s_ctx[lo]);
     const int k = (ch + T_al - 1) / T_al;
     const int r = w - s_wbase[lo], kh = r / k, part = r % k;
     const int64_t pbase = prefix[lo] + (int64_t)kh * ch;
@@ -425,12 +431,13 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   // cursor over (b, kh, chunk) — located once by binary search, then incremented;
   // the pair's block-table row and length are cached when the cursor enters it
   struct Cur {
-    int b, kh, c, chunks, ctx;
+    int b, kh, c, chunks, ctx, c0;  // c counts from the sequence's first chunk c0 (sliding window)
     const int32_t* row;
   };
   auto enter = [&](Cur& r) {
     r.ctx = s_ctx[r.b];
-    r.chunks = (r.ctx + 16 * NP - 1) / (16 * NP);
+    r.c0 = first_chunk(r.ctx);
+    r.chunks = nchunks(r.ctx);
     r.row = table + (int64_t)s_slot[r.b] * max_bps;
   };
   auto locate = [&](int64_t u) {
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     const int npages = (r.ctx + 15) >> 4;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const int page = r.c * NP + p;
+      const int page = (r.c0 + r.c) * NP + p;
       pid[p] = page < npages ? __ldg(r.row + page) : -1;
     }
   };
@@ -536,8 +543,10 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       st.init();
     }
     mbar_wait(full + (i % STAGES), (uint32_t)(i / STAGES) & 1u);
-    const int lim = seg_ctx - cu.c * 16 * NP;
-    chunk_step<D, NP>(qf, wbase + (i % STAGES) * STAGE, lim, lim, st, lane);
+    const int kbase = (cu.c0 + cu.c) * 16 * NP;
+    const int lim = seg_ctx - kbase;
+    const int lo = window > 0 ? max(0, seg_ctx - window) - kbase : 0;
+    chunk_step<D, NP>(qf, wbase + (i % STAGES) * STAGE, lim, lim, st, lane, lo);
     __syncwarp();  // every lane's ldmatrix reads of the slot refilled below are done
     if (lane == 0 && i + STAGES - 1 < n) {
       fence_proxy_async_smem();
@@ -553,10 +562,15 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
       l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
       l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-      const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
       const int r0 = lane >> 2, r1 = r0 + 8;
       const int sb = cu.b, skh = cu.kh;
-      if (seg_first == 0 && pair_end) {
+      const bool whole = seg_first == 0 && pair_end;
+      if (whole && sinks != nullptr) {  // the sink's exp(logit) joins the denominator (log2 domain)
+        if (r0 < G) l0 += fast_exp2(sinks[skh * G + r0] * kLog2e - st.m[0]);
+        if (r1 < G) l1 += fast_exp2(sinks[skh * G + r1] * kLog2e - st.m[1]);
+      }
+      const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+      if (whole) {
 #pragma unroll
         for (int nd = 0; nd < D / 8; ++nd) {
           const int c = nd * 8 + (lane & 3) * 2;
@@ -631,6 +645,10 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
           for (int r = 0; r < G; ++r)
 #pragma unroll
             for (int o = 16; o; o >>= 1) L[r] += __shfl_xor_sync(0xffffffffu, L[r], o);
+          if (sinks != nullptr) {
+#pragma unroll
+            for (int r = 0; r < G; ++r) L[r] += exp2f(sinks[skh * G + r] * kLog2e - M[r]);
+          }
           float acc[G][D / 32];
 #pragma unroll
           for (int r = 0; r < G; ++r)
@@ -783,7 +801,7 @@ inline size_t decode_part_floats(int sms, int G, int D) {
 template <int D, int G>
 int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
-                  float qscale, void* work, cudaStream_t st) {
+                  float qscale, int window, const float* sinks, void* work, cudaStream_t st) {
   if (B > kMaxB) return fail(STB_EINVAL, "attn_decode: at most %d sequences per step", kMaxB);
   if (!work) return fail(STB_EINVAL, "attn_decode: NULL workspace");
   int dev = 0;
@@ -805,7 +823,7 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   float* lse_part = o_part + (size_t)W * 2 * G * D;
   int* tickets = (int*)(o_part + decode_part_floats(sms, G, D));
   cudaError_t e = launch_k(kern, dim3(grid), dim3(32 * kDecWarps), smem, st, q, out, kp, vp, table, max_bps, slots, ctx,
-                           B, n_kv, qscale, o_part, lse_part, tickets);
+                           B, n_kv, qscale, o_part, lse_part, tickets, window, sinks);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_decode launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
@@ -838,6 +856,13 @@ int64_t stb_attn_decode_workspace(int B, int n_q, int n_kv, int d_head) {
 
 int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                     const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, void* work, void* stream) {
+  return stb_attn_decode_ex(pool, layer, q, out, slots, ctx_lens, B, n_q, scale, max_ctx, 0, nullptr, work, stream);
+}
+
+int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                       const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, int window,
+                       const float* sinks, void* work, void* stream) {
+  if (window < 0) return fail(STB_EINVAL, "attn_decode: window %d < 0", window);
   void *kp, *vp;
   if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
   int32_t* table;
@@ -856,7 +881,7 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
   auto* kk = (const __nv_bfloat16*)kp;
   auto* vv = (const __nv_bfloat16*)vp;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, work, st
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, window, sinks, work, st
   if (d_head == 128 && g == 4) return launch_decode<128, 4>(ARGS);
   if (d_head == 128 && g == 8) return launch_decode<128, 8>(ARGS);
   if (d_head == 128 && g == 1) return launch_decode<128, 1>(ARGS);
@@ -876,6 +901,14 @@ int stb_attn_prefill(stb_kv_pool* pool, int layer, const void* q, void* out, con
 int stb_attn_prefill_split(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                            const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,
                            int max_q, int active_units, void* stream) {
+  return stb_attn_prefill_ex(pool, layer, q, out, slots, q_start, ctx_lens, S, T, n_q, scale, max_q, active_units, 0,
+                             nullptr, stream);
+}
+
+int stb_attn_prefill_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                        const int32_t* q_start, const int32_t* ctx_lens, int S, int T, int n_q, float scale,
+                        int max_q, int active_units, int window, const float* sinks, void* stream) {
+  if (window < 0) return fail(STB_EINVAL, "attn_prefill: window %d < 0", window);
   void *kp, *vp;
   if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
   int32_t* table;
@@ -890,7 +923,9 @@ int stb_attn_prefill_split(stb_kv_pool* pool, int layer, const void* q, void* ou
   }
   if (!use_mma)
     return stb_attn_prefill_tc(pool, layer, q, out, slots, q_start, ctx_lens, S, T, n_q, scale, max_q, active_units,
-                               stream);
+                               window, sinks, stream);
+  if (window > 0 || sinks != nullptr)
+    return fail(STB_EINVAL, "attn_prefill: the mma.sync A/B kernel has no sliding window / sinks (unset STB200_PREFILL)");
   int n_kv, d_head;
   stb_pool_geometry(pool, &n_kv, &d_head);
   if (n_q % n_kv) return fail(STB_EINVAL, "attn_prefill: n_q %% n_kv != 0");

@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                            const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out,
                            const int32_t* __restrict__ table, int max_bps, const int32_t* __restrict__ slots,
                            const int32_t* __restrict__ q_start, const int32_t* __restrict__ ctx_lens, int n_kv,
-                           float qscale, int max_splits, float* __restrict__ part) {
+                           float qscale, int max_splits, float* __restrict__ part, int window,
+                           const float* __restrict__ sinks) {
   using CF = TcCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -181,11 +182,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pos0 = ctx - n;  // absolute position of query 0
   const int q_last = min(n, qi0 + 2 * QPT) - 1;
   const int n_tiles = (pos0 + q_last) / KT + 1;  // KV tiles the query tiles need (causal)
+  // sliding window (gpt-oss): the first query's window starts in tile j_lo; earlier tiles are
+  // never loaded
+  const int j_lo = window > 0 ? max(0, pos0 + qi0 - window + 1) / KT : 0;
   // KV split (launches with few work units, e.g. one verify pass): this CTA streams tiles
   // [j0, j0 + nt) and writes partial rows; attn_prefill_merge_kernel combines them
-  const int nsplit = unit_splits(n_tiles, max_splits);
+  const int nsplit = unit_splits(n_tiles - j_lo, max_splits);
   if (sp >= nsplit) return;
-  const int j0 = n_tiles * sp / nsplit, nt = n_tiles * (sp + 1) / nsplit - j0;
+  const int j0 = j_lo + (n_tiles - j_lo) * sp / nsplit, nt = j_lo + (n_tiles - j_lo) * (sp + 1) / nsplit - j0;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -346,11 +350,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NC; c += 32) tmem_ld32(tS(t) + lane_base + hf * NC + c, v + c);
         tmem_ld_wait();
         const int kbase = j * KT + hf * NC;
-        const bool masked = j >= full_tiles;
+        const bool masked = j >= full_tiles || window > 0;
         if (masked) {
+          const int klo = window > 0 ? qpos - window : -1;  // keys <= klo are outside the window
 #pragma unroll
           for (int c = 0; c < NC; ++c)
-            if (!live || kbase + c > qpos) v[c] = __float_as_uint(-INFINITY);
+            if (!live || kbase + c > qpos || kbase + c <= klo) v[c] = __float_as_uint(-INFINITY);
         }
         // tree-reduced row max (8 independent chains), then across the row's halves
         float mx8[8];
@@ -415,6 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // final: O / l
       mbar_wait(&o_done[t], (nt - 1) & 1);
       tc_fence_after();
+      if (sinks != nullptr && nsplit == 1 && m != -INFINITY)  // sink logit joins the denominator
+        l += fast_exp2(sinks[kh * G + g] * kLog2e - m);
       const float inv = l > 0.f ? 1.f / l : 0.f;
       __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D + hf * OC;
       float* prow = nullptr;  // split: this row's partial slot
@@ -459,7 +466,8 @@ __global__ void __launch_bounds__(256) attn_prefill_merge_kernel(__nv_bfloat16* 
                                                                  const float* __restrict__ part,
                                                                  const int32_t* __restrict__ q_start,
                                                                  const int32_t* __restrict__ ctx_lens, int n_kv,
-                                                                 int max_splits, int gx) {
+                                                                 int max_splits, int gx, int window,
+                                                                 const float* __restrict__ sinks) {
   pdl_wait();
   pdl_launch();
   constexpr int QPT = ROWS / G;
@@ -471,7 +479,8 @@ __global__ void __launch_bounds__(256) attn_prefill_merge_kernel(__nv_bfloat16* 
   const int qi0 = bx * 2 * QPT;
   if (qi0 >= n) return;
   const int pos0 = ctx_lens[s] - n;
-  const int nsplit = unit_splits((pos0 + min(n, qi0 + 2 * QPT) - 1) / KT + 1, max_splits);
+  const int j_lo = window > 0 ? max(0, pos0 + qi0 - window + 1) / KT : 0;
+  const int nsplit = unit_splits((pos0 + min(n, qi0 + 2 * QPT) - 1) / KT + 1 - j_lo, max_splits);
   if (nsplit == 1) return;  // K2 wrote this unit's rows directly
   const int t = row / ROWS, r = row % ROWS;
   const int qi = qi0 + t * QPT + r / G, g = r % G;
@@ -499,6 +508,7 @@ __global__ void __launch_bounds__(256) attn_prefill_merge_kernel(__nv_bfloat16* 
     wsum += e;
     acc.x += e * v[k].x, acc.y += e * v[k].y, acc.z += e * v[k].z, acc.w += e * v[k].w;
   }
+  if (sinks != nullptr && mx != -INFINITY) wsum += exp2f(sinks[kh * G + g] * kLog2e - mx);
   const float winv = wsum > 0.f ? 1.f / wsum : 0.f;
   if (lane < D / 4) {
     __nv_bfloat16* dst = out + ((int64_t)(t0 + qi) * (n_kv * G) + kh * G + g) * D + lane * 4;
@@ -553,7 +563,8 @@ struct MapKey {
 
 template <int D, int G>
 int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots, const int32_t* q_start,
-              const int32_t* ctx, int S, int T, int n_kv, float qscale, int max_q, int active_hint, cudaStream_t st) {
+              const int32_t* ctx, int S, int T, int n_kv, float qscale, int max_q, int active_hint, int window,
+              const float* sinks, cudaStream_t st) {
   using CF = TcCfg<D>;
   // tensor maps: Q over [T][n_kv][G][D] (box 64 x G x 1 x 128/G), K / V pages of the layer as
   // [num_blocks * n_kv * 16 rows][D] (box 64 x 16); cached per (q base, T, layer pointers)
@@ -613,11 +624,12 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
   }
   dim3 grid(gx, n_kv, S * splits);
   cudaError_t e = launch_k(kern, grid, dim3(kThreads), CF::SMEM, st, mp.q, mp.k, mp.v, (__nv_bfloat16*)out,
-                           pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale, splits, part);
+                           pool->dev_table, pool->max_bps, slots, q_start, ctx, n_kv, qscale, splits, part, window,
+                           sinks);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill_tc launch: %s", cudaGetErrorString(e));
   if (splits > 1) {
     e = launch_k(attn_prefill_merge_kernel<D, G>, dim3(gx * (2 * ROWS / 8), n_kv, S), dim3(256), 0, st,
-                 (__nv_bfloat16*)out, (const float*)part, q_start, ctx, n_kv, splits, gx);
+                 (__nv_bfloat16*)out, (const float*)part, q_start, ctx, n_kv, splits, gx, window, sinks);
     if (e != cudaSuccess) return fail(STB_ECUDA, "attn_prefill merge launch: %s", cudaGetErrorString(e));
   }
   return STB_OK;
@@ -628,12 +640,12 @@ int launch_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, cons
 // internal entry used by stb_attn_prefill (attention.cu) for tensor-core-sized runs
 int stb_attn_prefill_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                         const int32_t* q_start, const int32_t* ctx, int S, int T, int n_q, float scale, int max_q,
-                        int active_hint, void* stream) {
+                        int active_hint, int window, const float* sinks, void* stream) {
   int n_kv = pool->n_kv, d = pool->d_head;
   int g = n_q / n_kv;
   float qs = scale * kLog2e;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS pool, layer, q, out, slots, q_start, ctx, S, T, n_kv, qs, max_q, active_hint, st
+#define ARGS pool, layer, q, out, slots, q_start, ctx, S, T, n_kv, qs, max_q, active_hint, window, sinks, st
   if (d == 128 && g == 4) return launch_tc<128, 4>(ARGS);
   if (d == 128 && g == 8) return launch_tc<128, 8>(ARGS);
   if (d == 128 && g == 1) return launch_tc<128, 1>(ARGS);

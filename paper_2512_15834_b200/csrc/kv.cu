@@ -112,7 +112,8 @@ __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* _
                                        const int32_t* __restrict__ table, int max_bps,
                                        __nv_bfloat16* __restrict__ kpages, __nv_bfloat16* __restrict__ vpages,
                                        int clear_rows, const __nv_bfloat16* __restrict__ q_norm,
-                                       const __nv_bfloat16* __restrict__ k_norm, float eps) {
+                                       const __nv_bfloat16* __restrict__ k_norm, float eps,
+                                       const float* __restrict__ bias, float rope_scale) {
   pdl_wait();
   pdl_launch();
   const int half = d_head / 2;
@@ -132,6 +133,14 @@ __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* _
     const float4 b1 = *reinterpret_cast<const float4*>(row + half + g * 8 + 4);
     x1[0] = a0.x, x1[1] = a0.y, x1[2] = a0.z, x1[3] = a0.w, x1[4] = a1.x, x1[5] = a1.y, x1[6] = a1.z, x1[7] = a1.w;
     x2[0] = b0.x, x2[1] = b0.y, x2[2] = b0.z, x2[3] = b0.w, x2[4] = b1.x, x2[5] = b1.y, x2[6] = b1.z, x2[7] = b1.w;
+    if (bias != nullptr) {  // gpt-oss QKV bias (added before RoPE)
+      const float* br = bias + h * d_head;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x1[j] += br[g * 8 + j];
+        x2[j] += br[half + g * 8 + j];
+      }
+    }
     if (t < clear_rows) {  // leave the GEMM accumulator zeroed for the next stream-K product
       const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       *reinterpret_cast<float4*>(row + g * 8) = z;
@@ -166,6 +175,8 @@ __global__ void qkv_rope_commit_kernel(float* __restrict__ qkv, __nv_bfloat16* _
     for (int j = 0; j < 8; ++j) {
       float s, c;
       sincosf((float)pos * inv_freq[g * 8 + j], &s, &c);
+      s *= rope_scale;  // YaRN attention factor (1 for plain RoPE)
+      c *= rope_scale;
       y1[j] = x1[j] * c - x2[j] * s;
       y2[j] = x2[j] * c + x1[j] * s;
     }
@@ -406,13 +417,14 @@ int stb_kv_copy_blocks(stb_kv_pool* p, const int32_t* src, const int32_t* dst, i
   return STB_OK;
 }
 
-int stb_qkv_norm_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
-                             const int32_t* pos_of, int n, int n_q, float rope_theta, const void* q_norm,
-                             const void* k_norm, float eps, int clear_rows, void* stream) {
+static int rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                       const int32_t* pos_of, int n, int n_q, float rope_theta, const void* q_norm, const void* k_norm,
+                       float eps, int clear_rows, const float* inv_freq, float rope_scale, const float* bias,
+                       void* stream) {
   if ((q_norm == nullptr) != (k_norm == nullptr)) return fail(STB_EINVAL, "qkv_rope_commit: q_norm and k_norm go together");
   if (!p || layer < 0 || layer >= p->layers) return fail(STB_EINVAL, "qkv_rope_commit: bad layer");
   if (n <= 0) return STB_OK;
-  const float* inv = stb_rope_inv_freq(rope_theta, p->d_head);
+  const float* inv = inv_freq ? inv_freq : stb_rope_inv_freq(rope_theta, p->d_head);
   if (!inv) return fail(STB_ENOMEM, "qkv_rope_commit: inv_freq");
   void *kp, *vp;
   stb_kv_layer_ptrs(p, layer, &kp, &vp);
@@ -422,9 +434,23 @@ int stb_qkv_norm_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out,
   launch_k(qkv_rope_commit_kernel, dim3((unsigned)((total + threads - 1) / threads)), dim3(threads), 0, (cudaStream_t)stream, 
       qkv, (__nv_bfloat16*)q_out, slot_of, pos_of, n, n_q, p->n_kv, p->d_head, inv, p->dev_table, p->max_bps,
       (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, clear_rows, (const __nv_bfloat16*)q_norm,
-      (const __nv_bfloat16*)k_norm, eps);
+      (const __nv_bfloat16*)k_norm, eps, bias, rope_scale);
   STB_CHECK_LAUNCH("qkv_rope_commit");
   return STB_OK;
+}
+
+int stb_qkv_norm_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                             const int32_t* pos_of, int n, int n_q, float rope_theta, const void* q_norm,
+                             const void* k_norm, float eps, int clear_rows, void* stream) {
+  return rope_commit(p, layer, qkv, q_out, slot_of, pos_of, n, n_q, rope_theta, q_norm, k_norm, eps, clear_rows,
+                     nullptr, 1.f, nullptr, stream);
+}
+
+int stb_qkv_rope_commit_ex(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,
+                           const int32_t* pos_of, int n, int n_q, float rope_theta, const float* inv_freq,
+                           float rope_scale, const float* bias, int clear_rows, void* stream) {
+  return rope_commit(p, layer, qkv, q_out, slot_of, pos_of, n, n_q, rope_theta, nullptr, nullptr, 0.f, clear_rows,
+                     inv_freq, rope_scale, bias, stream);
 }
 
 int stb_qkv_rope_commit(stb_kv_pool* p, int layer, float* qkv, void* q_out, const int32_t* slot_of,

@@ -1,0 +1,595 @@
+// gpt-oss mixture-of-experts MLP (config C4): routing, token permutation, the MXFP4 grouped
+// GEMM on the 5th-gen tensor cores, and the weighted combine fused with the next RMSNorm.
+//
+// Replaces, for the MoE model family, the MLP part of every `rate x tokens` charge of the
+// reference engine (`engine.py:251,270,296,358`); the reference itself has no model
+// (SPEC.md:17). Expert weights are MXFP4 — e2m1 values with one ue8m0 scale per 32 along K, the
+// released gpt-oss checkpoint's format — which is what lets a 120B replica (65.6 GB) live on one
+// B200. Activations stay 16-bit: the tensor core runs kind::f16 (fp16 x fp16 -> fp32)
+// on weights dequantised on chip, so the only quantisation is the checkpoint's own.
+//
+// Per layer (one stream, programmatic dependent launch throughout):
+//   K5 router GEMM (bf16, gemm.cu) -> logits [T][E]
+//   moe_route_kernel      warp per token: + bias, top-k (ties -> lower expert id), softmax over
+//                         the k selected logits; claims a rank in its expert (atomic count)
+//   moe_gather_kernel     expert offsets (prefix of the counts), the permutation, and the
+//                         token rows copied expert-contiguous as fp16 (the GEMM's B operand)
+//   moe_gemm_mxfp4_kernel gate-up (clamped SwiGLU epilogue -> fp16 act) and down (+bias -> fp32)
+//   moe_combine_kernel    x += sum_k w_k * y[perm(t, k)] (fixed k order: deterministic), then
+//                         RMSNorm of the new residual row (the next layer's input); zeroes the
+//                         counts for the next layer
+//
+// Grouped GEMM, weight-stationary like K5: UMMA M = 128 expert weight rows, N = BN tokens of
+// that expert. Persistent, one CTA per SM; the work list (expert, 128-row tile, token tile) is
+// derived on the device from the counts, so the launch (and a CUDA graph of it) does not depend
+// on the routing. Per K block of 64 the weight tile is 4352 contiguous bytes (4096 B of codes +
+// 256 B of scales, runtime/weights.py pack_mxfp4_tiles): one bulk copy. Dequantisation never
+// touches shared memory on the way out: converter thread r (= TMEM lane r = weight row r) reads
+// its 32 code bytes, F2FP.F16.E2M1 unpacks two values per instruction, HMUL2 applies the 2^e
+// scale (exact), and tcgen05.st writes the 32 fp16x2 columns straight into a TMEM A-operand
+// ring; the MMA reads A from TMEM and the fp16 token rows (B) from smem. So shared memory
+// carries 4.25 KB of weight bytes per stage instead of 16 KB of dequantised tiles written and
+// read again — the MoE is HBM-bound on the weights at every batch the engine runs.
+//   warp 0      producer: weight tile + token tile per stage (bulk copy + TMA), STAGES ring
+//   warp 1      MMA issuer (one thread): 4 x tcgen05.mma kind::f16 per stage, A from TMEM
+//   warp 2      TMEM allocator
+//   warps 4-7   converters: smem codes -> fp16 -> TMEM A ring (lane quarter = warp & 3)
+//   warps 8-11  epilogue: TMEM accumulator (double-buffered) -> SwiGLU / bias -> global
+#include <cudaTypedefs.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/stb200.h"
+#include "common.cuh"
+
+using namespace stb;
+
+namespace {
+
+constexpr int kMaxE = 256;
+constexpr int kMaxK = 8;
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int RAW = 4352;  // one MXFP4 tile: 128 rows x 32 code bytes + 128 rows x 2 scale bytes
+constexpr int kThreads = 384;
+constexpr int A_COL0 = 128;  // TMEM: accumulators in [0, 2 BN), the A ring from column 128
+constexpr int A_STAGES = 8;  // 8 x 32 columns of fp16x2 (64 K values x 128 rows each)
+
+template <int BN>
+struct MCfg {
+  static constexpr int X_BYTES = BN * BK * 2;  // fp16 token rows of one K block, SW128 K-major
+#ifndef STB_MOE_RING_KB
+#define STB_MOE_RING_KB 196
+#endif
+  static constexpr int STAGES = std::min(24, (STB_MOE_RING_KB * 1024) / (RAW + X_BYTES));
+  static constexpr int SMEM = 1024 + STAGES * (X_BYTES + RAW) + 1024;
+};
+
+__device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// two e2m1 codes (low byte of x) -> fp16x2 (low nibble -> low half)
+__device__ __forceinline__ uint32_t e2m1x2_to_f16x2(uint32_t x) {
+  uint32_t d;
+  asm("{\n.reg .b8 b;\nmov.b32 {b, _, _, _}, %1;\ncvt.rn.f16x2.e2m1x2 %0, b;\n}" : "=r"(d) : "r"(x));
+  return d;
+}
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// ---------------------------------------------------------------- routing
+template <int EPL>
+__global__ void __launch_bounds__(256) moe_route_kernel(const float* __restrict__ logits, int64_t ld,
+                                                        const float* __restrict__ bias, int T, int E, int k,
+                                                        int* __restrict__ counts, int* __restrict__ expert,
+                                                        int* __restrict__ rank, float* __restrict__ wt) {
+  pdl_wait();
+  pdl_launch();
+  const int t = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (t >= T) return;
+  float v[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    const int e = j * 32 + lane;
+    v[j] = e < E ? logits[(int64_t)t * ld + e] + (bias ? bias[e] : 0.f) : -INFINITY;
+  }
+  float sv[kMaxK];
+  int se[kMaxK];
+#pragma unroll
+  for (int r = 0; r < kMaxK; ++r) {
+    if (r >= k) break;
+    float bv = -INFINITY;
+    int be = 1 << 30;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      const int e = j * 32 + lane;
+      if (e < E && (v[j] > bv || (v[j] == bv && e < be))) bv = v[j], be = e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (ov > bv || (ov == bv && oe < be)) bv = ov, be = oe;
+    }
+    sv[r] = bv;
+    se[r] = be;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+      if (j * 32 + lane == be) v[j] = -INFINITY;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int r = 0; r < kMaxK; ++r)
+    if (r < k) s += expf(sv[r] - sv[0]);
+#pragma unroll
+  for (int r = 0; r < kMaxK; ++r) {
+    if (r < k && lane == r) {
+      const int64_t p = (int64_t)t * k + r;
+      expert[p] = se[r];
+      rank[p] = atomicAdd(counts + se[r], 1);
+      wt[p] = expf(sv[r] - sv[0]) / s;
+    }
+  }
+}
+
+// exclusive prefix of counts[0..E) into off[0..E] (shared), whole block
+__device__ __forceinline__ void block_prefix(const int* __restrict__ counts, int E, int* off) {
+  __shared__ int part[kMaxE / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid < kMaxE) {
+    const int c = tid < E ? counts[tid] : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) part[w] = incl;
+    off[tid + 1] = incl;  // provisional (warp-local)
+  }
+  __syncthreads();
+  if (tid < kMaxE) {
+    int base = 0;
+    for (int j = 0; j < w; ++j) base += part[j];
+    off[tid + 1] += base;
+  }
+  if (tid == 0) off[0] = 0;
+  __syncthreads();
+}
+
+// expert-contiguous fp16 copy of the token rows; perm[t*k + r] = destination row
+__global__ void __launch_bounds__(256) moe_gather_kernel(const __nv_bfloat16* __restrict__ h, int64_t ldh, int T,
+                                                         int d, int k, int E, const int* __restrict__ counts,
+                                                         const int* __restrict__ expert, const int* __restrict__ rank,
+                                                         int* __restrict__ offsets, int* __restrict__ perm,
+                                                         __half* __restrict__ xperm) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ int off[kMaxE + 1];
+  block_prefix(counts, E, off);
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) offsets[e] = off[e];
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < T * k; p += nw) {
+    const int t = p / k;
+    const int row = off[expert[p]] + rank[p];
+    if (lane == 0) perm[p] = row;
+    const __nv_bfloat16* src = h + (int64_t)t * ldh;
+    __half* dst = xperm + (int64_t)row * d;
+    for (int c = lane * 8; c < d; c += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(src + c);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+      uint4 o;
+      __half2* oh = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) oh[q] = __float22half2_rn(__bfloat1622float2(b[q]));
+      *reinterpret_cast<uint4*>(dst + c) = o;
+    }
+  }
+}
+
+// x[t] += sum_r wt[t,r] * y[perm[t,r]] (+ the fixed r order), then RMSNorm(x[t]) * w -> hn (bf16)
+__global__ void __launch_bounds__(256) moe_combine_kernel(float* __restrict__ x, const float* __restrict__ y, int d,
+                                                          int k, const int* __restrict__ perm,
+                                                          const float* __restrict__ wt,
+                                                          const __nv_bfloat16* __restrict__ w,
+                                                          __nv_bfloat16* __restrict__ hn, float eps,
+                                                          int* __restrict__ counts, int E) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  if (t == 0)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) counts[e] = 0;  // the next layer's route starts clean
+  int rows[kMaxK];
+  float ws[kMaxK];
+#pragma unroll
+  for (int r = 0; r < kMaxK; ++r) {
+    rows[r] = r < k ? perm[(int64_t)t * k + r] : 0;
+    ws[r] = r < k ? wt[(int64_t)t * k + r] : 0.f;
+  }
+  float* xr = x + (int64_t)t * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(xr + c);
+#pragma unroll
+    for (int r = 0; r < kMaxK; ++r) {
+      if (r < k) {
+        const float4 yv = __ldcg(reinterpret_cast<const float4*>(y + (int64_t)rows[r] * d + c));
+        v.x += ws[r] * yv.x, v.y += ws[r] * yv.y, v.z += ws[r] * yv.z, v.w += ws[r] * yv.w;
+      }
+    }
+    *reinterpret_cast<float4*>(xr + c) = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (hn == nullptr) return;
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    s = warp_sum(s);
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / d + eps);
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c));
+    const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c + 2));
+    *reinterpret_cast<uint2*>(hn + (int64_t)t * d + c) =
+        make_uint2(pack_bf16(v.x * inv * w01.x, v.y * inv * w01.y), pack_bf16(v.z * inv * w23.x, v.w * inv * w23.y));
+  }
+}
+
+// ---------------------------------------------------------------- grouped MXFP4 GEMM
+struct MoeArgs {
+  const uint8_t* w;     // [E][NT][KB][RAW]
+  const float* bias;    // [E][N]
+  const int* counts;    // [E]
+  void* out;            // kind 1: fp16 act [rows][N/2]; kind 2: fp32 y [rows][N]
+  int64_t ldo;
+  int E, N, K, kind;
+  float limit;          // SwiGLU clamp (kind 1)
+};
+
+constexpr float kSwigluAlpha = 1.702f;
+
+__device__ __forceinline__ float gpt_oss_glu(float g, float u, float limit) {
+  g = fminf(g, limit);
+  u = fminf(fmaxf(u, -limit), limit);
+  return (u + 1.f) * (g / (1.f + __expf(-kSwigluAlpha * g)));
+}
+
+__device__ __forceinline__ void tmem_st32_wait_fence(uint32_t taddr, const uint32_t* r) {
+  tmem_st32(taddr, r);
+  tmem_st_wait();
+  tc_fence_before();
+}
+
+// instruction descriptor: fp16 x fp16 -> fp32, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __grid_constant__ CUtensorMap tm_x,
+                                                                     const MoeArgs a) {
+  using CF = MCfg<BN>;
+  constexpr int STAGES = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sx = smem;                              // [STAGES][X_BYTES], 1024-aligned (SW128)
+  uint8_t* sw = sx + STAGES * CF::X_BYTES;         // [STAGES][RAW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sw + STAGES * RAW);
+  uint64_t* empty = full + STAGES;
+  uint64_t* a_full = empty + STAGES;               // [A_STAGES]
+  uint64_t* a_empty = a_full + A_STAGES;           // [A_STAGES]
+  uint64_t* acc_full = a_empty + A_STAGES;         // [2]
+  uint64_t* acc_empty = acc_full + 2;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  __shared__ int s_off[kMaxE + 1];                 // token-row offset of each expert
+  __shared__ int s_item[kMaxE + 1];                // work-item prefix
+  __shared__ int s_cnt[kMaxE];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = a.E, NT = ceil_div(a.N, BM), KB = a.K / BK;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_x);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < A_STAGES; ++s) {
+      mbar_init(&a_full[s], 4);  // one arrive per converter warp
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  pdl_wait();  // counts (route) and token rows (gather) come from the preceding kernels
+  // work list: items of expert e = ceil(count_e / BN) token tiles x NT weight tiles
+  block_prefix(a.counts, E, s_off);
+  if (threadIdx.x < kMaxE) s_cnt[threadIdx.x] = threadIdx.x < E ? s_off[threadIdx.x + 1] - s_off[threadIdx.x] : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int e = 0; e < E; ++e) {
+      s_item[e] = run;
+      run += ceil_div(s_cnt[e], BN) * NT;
+    }
+    s_item[E] = run;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_launch();
+  const uint32_t tmem = *tmem_slot;
+  const int total = s_item[E];
+  auto decode = [&](int it, int& e, int& nt, int& m) {
+    int lo = 0, hi = E - 1;  // last e with s_item[e] <= it (experts with no items are skipped)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_item[mid] <= it) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    const int mt = ceil_div(s_cnt[e], BN);
+    const int local = it - s_item[e];
+    nt = local / mt;
+    m = local - nt * mt;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int i = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x) {
+        int e, nt, m;
+        decode(it, e, nt, m);
+        const uint8_t* wt = a.w + ((int64_t)e * NT + nt) * KB * RAW;
+        const int xrow = s_off[e] + m * BN;
+        for (int kb = 0; kb < KB; ++kb, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], RAW + CF::X_BYTES);
+          bulk_load(smem_u32(sw + s * RAW), wt + (int64_t)kb * RAW, RAW, &full[s]);
+          tma_load_2d(sx + s * CF::X_BYTES, &tm_x, &full[s], kb * BK, xrow);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_f16(BM, BN);
+      int i = 0, j = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
+        const int buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * BN;
+        for (int kb = 0; kb < KB; ++kb, ++i) {
+          const int s = i % STAGES, as = i % A_STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);        // token rows landed (TMA)
+          mbar_wait(&a_full[as], (i / A_STAGES) & 1);   // weights dequantised into TMEM
+          tc_fence_after();
+          const uint32_t xa = smem_u32(sx + s * CF::X_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_f16_ts(d, tmem + A_COL0 + as * 32 + kk * 8, umma_desc_kmajor_sw128(xa + kk * 32, 1024), idesc,
+                        (kb > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+          umma_commit(&a_empty[as]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 8) {
+    // converters: thread = weight row r of the tile = TMEM lane r
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int i = 0;
+    for (int it = blockIdx.x; it < total; it += gridDim.x) {
+      for (int kb = 0; kb < KB; ++kb, ++i) {
+        const int s = i % STAGES, as = i % A_STAGES;
+        mbar_wait(&full[s], (i / STAGES) & 1);
+        const uint8_t* raw = sw + s * RAW;
+        const uint4 c0 = *reinterpret_cast<const uint4*>(raw + r * 32);
+        const uint4 c1 = *reinterpret_cast<const uint4*>(raw + r * 32 + 16);
+        const uint32_t sc = *reinterpret_cast<const uint16_t*>(raw + 4096 + r * 2);
+        // 2^(e) as fp16: exponent field e + 15 = byte - 127 + 15 (byte in [114, 139] by construction)
+        const uint32_t h0 = ((sc & 0xFFu) - 112u) << 10, h1 = ((sc >> 8) - 112u) << 10;
+        const uint32_t s0 = h0 | (h0 << 16), s1 = h1 | (h1 << 16);
+        const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        uint32_t out[32];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const uint32_t scl = w < 4 ? s0 : s1;  // bytes 0-15: values 0-31 (scale 0), 16-31: scale 1
+#pragma unroll
+          for (int b = 0; b < 4; ++b) out[w * 4 + b] = hmul2(e2m1x2_to_f16x2(wv[w] >> (8 * b)), scl);
+        }
+        mbar_wait(&a_empty[as], ((i / A_STAGES) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st32_wait_fence(tmem + lane_addr + A_COL0 + as * 32, out);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[as]);
+      }
+    }
+  } else if (warp >= 8) {
+    // epilogue: thread = weight row (feature) of the tile; columns = tokens
+    const int q = warp & 3;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int j = 0;
+    for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
+      int e, nt, m;
+      decode(it, e, nt, m);
+      const int buf = j & 1;
+      const int f = nt * BM + q * 32 + lane;
+      const int row0 = s_off[e] + m * BN;
+      const int nv = min(BN, s_cnt[e] - m * BN);
+      const float b = f < a.N ? __ldg(a.bias + (int64_t)e * a.N + f) : 0.f;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t rr[16];
+        tmem_ld16(tmem + lane_addr + buf * BN + c, rr);
+        tmem_ld_wait();
+        if (a.kind == 2) {
+          float* y = reinterpret_cast<float*>(a.out);
+          if (f < a.N) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+              if (c + t < nv) y[(int64_t)(row0 + c + t) * a.ldo + f] = __uint_as_float(rr[t]) + b;
+          }
+        } else {
+          // (gate, up) of output feature f/2 in lanes (2i, 2i+1): the even lane emits tokens
+          // c..c+7 of the chunk, the odd lane c+8..c+15
+          __half* act = reinterpret_cast<__half*>(a.out);
+          const bool odd = lane & 1;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const float mine = __uint_as_float(odd ? rr[8 + t] : rr[t]) + b;
+            const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? rr[t] : rr[8 + t]) + b, 1);
+            // other holds the partner's value for MY token set: partner bias already added by it
+            const int tok = c + (odd ? 8 : 0) + t;
+            const float g = odd ? other : mine, u = odd ? mine : other;
+            if (f < a.N && tok < nv) act[(int64_t)(row0 + tok) * a.ldo + (f >> 1)] = __float2half_rn(gpt_oss_glu(g, u, a.limit));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_free(tmem, 512);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// fp16 [rows][K] token rows, box [BN rows][64], 128B swizzle; cached per (base, rows, K, BN, device)
+int x_map(CUtensorMap* out, const void* base, int64_t rows, int K, int bn) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int, int, int>, CUtensorMap> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(base, rows, K, bn, dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return STB_OK;
+  }
+  auto fn = encode_fn();
+  if (!fn) return fail(STB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)bn};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(STB_ECUDA, "moe: tensor map encode failed (%d)", (int)r);
+  if (cache.size() > 1024) cache.clear();
+  cache.emplace(key, *out);
+  return STB_OK;
+}
+
+template <int BN>
+int launch_moe_gemm(const void* xperm, int rows_cap, const MoeArgs& a, cudaStream_t st) {
+  CUtensorMap tm;
+  if (int rc = x_map(&tm, xperm, rows_cap, a.K, BN)) return rc;
+  auto kern = moe_gemm_mxfp4_kernel<BN>;
+  smem_attr_once(kern, MCfg<BN>::SMEM);
+  cudaError_t e = launch_k(kern, dim3(device_sms()), dim3(kThreads), MCfg<BN>::SMEM, st, tm, a);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_gemm launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stb_moe_route(const float* logits, int64_t ld, const float* bias, int T, int E, int k, int32_t* counts,
+                  int32_t* expert, int32_t* rank, float* weight, void* stream) {
+  if (T <= 0) return STB_OK;
+  if (E <= 0 || E > kMaxE || k <= 0 || k > kMaxK || k > E) return fail(STB_EINVAL, "moe_route: E=%d k=%d", E, k);
+  const int blocks = (T + 7) / 8;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (E <= 32)
+    e = launch_k(moe_route_kernel<1>, dim3(blocks), dim3(256), 0, st, logits, ld, bias, T, E, k, counts, expert, rank, weight);
+  else if (E <= 64)
+    e = launch_k(moe_route_kernel<2>, dim3(blocks), dim3(256), 0, st, logits, ld, bias, T, E, k, counts, expert, rank, weight);
+  else if (E <= 128)
+    e = launch_k(moe_route_kernel<4>, dim3(blocks), dim3(256), 0, st, logits, ld, bias, T, E, k, counts, expert, rank, weight);
+  else
+    e = launch_k(moe_route_kernel<8>, dim3(blocks), dim3(256), 0, st, logits, ld, bias, T, E, k, counts, expert, rank, weight);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_route launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+int stb_moe_gather(const void* h, int64_t ldh, int T, int d, int k, int E, const int32_t* counts,
+                   const int32_t* expert, const int32_t* rank, int32_t* offsets, int32_t* perm, void* xperm,
+                   void* stream) {
+  if (T <= 0) return STB_OK;
+  if (E <= 0 || E > kMaxE || d % 8 || ldh % 8) return fail(STB_EINVAL, "moe_gather: E=%d d=%d", E, d);
+  const int blocks = std::min(std::max(1, (T * k + 7) / 8), 4 * device_sms());
+  cudaError_t e = launch_k(moe_gather_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream,
+                           (const __nv_bfloat16*)h, ldh, T, d, k, E, counts, expert, rank, offsets, perm,
+                           (__half*)xperm);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_gather launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+int stb_moe_gemm_mxfp4(const void* xperm, int rows_cap, const void* wtiles, const float* bias, const int32_t* counts,
+                       int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows, void* stream) {
+  if (rows <= 0) return STB_OK;
+  if (E <= 0 || E > kMaxE || K % BK || N <= 0 || (kind != STB_MOE_GATE_UP && kind != STB_MOE_DOWN) ||
+      (kind == STB_MOE_GATE_UP && N % 2))
+    return fail(STB_EINVAL, "moe_gemm: E=%d N=%d K=%d kind=%d", E, N, K, kind);
+  MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit};
+  // token tile from the mean rows per expert: decode steps put ~T k / E <= a few rows on an
+  // expert (BN 16); larger tiles only once experts hold tens of rows
+  const int avg = (rows + E - 1) / E;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (avg <= 16) return launch_moe_gemm<16>(xperm, rows_cap, a, st);
+  if (avg <= 32) return launch_moe_gemm<32>(xperm, rows_cap, a, st);
+  return launch_moe_gemm<64>(xperm, rows_cap, a, st);
+}
+
+int stb_moe_combine(float* x, const float* y, int T, int d, int k, const int32_t* perm, const float* weight,
+                    const void* norm_w, void* h_out, float eps, int32_t* counts, int E, void* stream) {
+  if (T <= 0) return STB_OK;
+  if (d % 4 || k > kMaxK) return fail(STB_EINVAL, "moe_combine: d=%d k=%d", d, k);
+  cudaError_t e = launch_k(moe_combine_kernel, dim3(T), dim3(256), 0, (cudaStream_t)stream, x, y, d, k, perm, weight,
+                           (const __nv_bfloat16*)norm_w, (__nv_bfloat16*)h_out, eps, counts, E);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_combine launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+}  // extern "C"

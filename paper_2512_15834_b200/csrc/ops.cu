@@ -82,7 +82,8 @@ __global__ void embed_prep_kernel(const int32_t* __restrict__ ids, const __nv_bf
 template <int VPT>
 __global__ void add_rmsnorm_kernel(float* __restrict__ x, float* __restrict__ delta,
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y, int d,
-                                   float eps, const int32_t* __restrict__ gather, int clear_rows) {
+                                   float eps, const int32_t* __restrict__ gather, int clear_rows,
+                                   const float* __restrict__ bias) {
   pdl_wait();
   pdl_launch();
   __shared__ float red[32];
@@ -94,11 +95,19 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, float* __restrict__ de
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
+    if (c >= d) {  // d not a multiple of 4 x threads (gpt-oss d = 2880)
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
     v[i] = *reinterpret_cast<const float4*>(xr + c);
     if (delta) {
       float4* dp = reinterpret_cast<float4*>(delta + (int64_t)t * d + c);
-      const float4 e = *dp;
+      float4 e = *dp;
       if (t < clear_rows) *dp = make_float4(0.f, 0.f, 0.f, 0.f);  // GEMM accumulator back to zero
+      if (bias) {
+        const float4 b = *reinterpret_cast<const float4*>(bias + c);
+        e.x += b.x, e.y += b.y, e.z += b.z, e.w += b.w;
+      }
       v[i].x += e.x;
       v[i].y += e.y;
       v[i].z += e.z;
@@ -113,6 +122,7 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, float* __restrict__ de
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
+    if (c >= d) continue;
     const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c));
     const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + c + 2));
     *reinterpret_cast<uint2*>(yr + c) = make_uint2(pack_bf16(v[i].x * inv * w01.x, v[i].y * inv * w01.y),
@@ -122,21 +132,21 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, float* __restrict__ de
 
 // d = threads * 4 * VPT with threads a multiple of 32 and <= 1024
 int launch_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d, float eps,
-                   const int32_t* gather, int clear_rows, cudaStream_t st) {
-  if (d % 128) return fail(STB_EINVAL, "rmsnorm: d must be a multiple of 128");
+                   const int32_t* gather, int clear_rows, cudaStream_t st, const float* bias = nullptr) {
+  if (d % 4) return fail(STB_EINVAL, "rmsnorm: d must be a multiple of 4");
   const int v4 = d / 4;
   int vpt = 1;
-  while (v4 / vpt > 1024 || (v4 % vpt)) vpt *= 2;
+  while ((v4 + vpt - 1) / vpt > 1024) vpt *= 2;
   if (vpt > 8) return fail(STB_EINVAL, "rmsnorm: d too large");
-  const int threads = v4 / vpt;
+  const int threads = (((v4 + vpt - 1) / vpt) + 31) / 32 * 32;  // whole warps (block_sum); tail lanes idle
   const auto* wb = (const __nv_bfloat16*)w;
   auto* yb = (__nv_bfloat16*)y;
   cudaError_t e;
   switch (vpt) {
-    case 1: e = launch_k(add_rmsnorm_kernel<1>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
-    case 2: e = launch_k(add_rmsnorm_kernel<2>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
-    case 4: e = launch_k(add_rmsnorm_kernel<4>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
-    default: e = launch_k(add_rmsnorm_kernel<8>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows); break;
+    case 1: e = launch_k(add_rmsnorm_kernel<1>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows, bias); break;
+    case 2: e = launch_k(add_rmsnorm_kernel<2>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows, bias); break;
+    case 4: e = launch_k(add_rmsnorm_kernel<4>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows, bias); break;
+    default: e = launch_k(add_rmsnorm_kernel<8>, dim3(n), dim3(threads), 0, st, x, delta, wb, yb, d, eps, gather, clear_rows, bias); break;
   }
   if (e != cudaSuccess) return fail(STB_ECUDA, "rmsnorm launch: %s", cudaGetErrorString(e));
   return STB_OK;
@@ -344,6 +354,12 @@ int stb_add_rmsnorm(float* x, float* delta, const void* w, void* y, int n, int d
                     void* stream) {
   if (n <= 0) return STB_OK;
   return launch_rmsnorm(x, delta, w, y, n, d, eps, nullptr, clear_rows, (cudaStream_t)stream);
+}
+
+int stb_add_bias_rmsnorm(float* x, float* delta, const float* bias, const void* w, void* y, int n, int d, float eps,
+                         int clear_rows, void* stream) {
+  if (n <= 0) return STB_OK;
+  return launch_rmsnorm(x, delta, w, y, n, d, eps, nullptr, clear_rows, (cudaStream_t)stream, bias);
 }
 
 int stb_gather_rmsnorm(const float* x, const int32_t* idx, const void* w, void* y, int n, int d, float eps,

@@ -42,4 +42,4 @@ extern "C" int stb_kv_layer_ptrs(const stb_kv_pool* pool, int layer, void** k_pa
 // active_hint: (query-tile pair, kv head, run) units that hold queries (0: assume the full grid)
 int stb_attn_prefill_tc(const stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                         const int32_t* q_start, const int32_t* ctx, int S, int T, int n_q, float scale, int max_q,
-                        int active_hint, void* stream);
+                        int active_hint, int window, const float* sinks, void* stream);

@@ -67,6 +67,27 @@ GRAPH_MAX_T = 192 if os.environ.get("STB200_GRAPH_MIXED") == "1" else 0
 GRAPH_MAX_RUNS = 2
 GRAPH_CACHE = 48    # captured graphs kept
 PROJECTIONS = ("wqkv", "wo", "w_gate_up", "w_down")
+MOE_PROJECTIONS = ("wqkv", "wo", "router")   # gpt-oss: the experts are MXFP4 tiles (weights.MoELayer)
+MOE_GATE_UP, MOE_DOWN = 1, 2                 # include/stb200.h STB_MOE_*
+MOE_TILE_BYTES = 4352                        # one 128 x 64 MXFP4 tile (weights.TILE_BYTES)
+
+
+class _MoeWork:
+    """Algorithmic HBM bytes of one grouped-GEMM launch, known only after the step ran: the
+    touched experts' MXFP4 tiles (every weight byte once) + the token rows in + the rows out.
+    Evaluated by Decoder.fold from the per-layer expert offsets the step copied to pinned memory."""
+
+    __slots__ = ("host", "layer", "N", "K", "rows", "in_b", "out_b")
+
+    def __init__(self, host, layer, N, K, rows, in_b, out_b):
+        self.host, self.layer, self.N, self.K, self.rows, self.in_b, self.out_b = host, layer, N, K, rows, in_b, out_b
+
+    def __call__(self) -> int:
+        offs = self.host[self.layer].numpy()
+        touched = int(np.count_nonzero(np.diff(offs)))
+        w = touched * (-(-self.N // 128)) * (self.K // 64) * MOE_TILE_BYTES
+        n_out = self.N // 2 if self.out_b == 2 else self.N   # gate-up emits N/2 fp16 activations
+        return w + self.rows * self.K * self.in_b + self.rows * n_out * self.out_b
 
 
 class GemmEpi(C.Structure):
@@ -214,14 +235,14 @@ class Decoder:
                  use_graphs: bool = True):
         self.shape = shape
         self.w = weights
-        for i in range(shape.layers):
+        for i in range(shape.layers if not shape.moe else 0):
             gu = weights[f"l{i}.w_gate_up"]
             if not isinstance(gu, TiledWeight):  # (gate, up) pairs in adjacent rows: fused SiLU epilogue
                 interleave_gate_up(gu, shape.d_ff)
             del gu
         # fused epilogues: correct (tests/test_gpu_parity.py) but measured slower on B200 — the
         # epilogue's global round trips sit on the GEMM's critical path; opt in
-        self.fused = os.environ.get("STB200_FUSED", "") == "1" and fusable(shape)
+        self.fused = os.environ.get("STB200_FUSED", "") == "1" and fusable(shape) and not shape.moe
         # projections in the tiled HBM layout (once; a shared dict is converted in place —
         # the first Decoder over a dict decides whether the norm weights are folded in)
         if "_stb_fused" not in weights:
@@ -231,9 +252,15 @@ class Decoder:
                     fold_norm(weights[f"l{i}.wqkv"], weights[f"l{i}.attn_norm"])
                     fold_norm(weights[f"l{i}.w_gate_up"], weights[f"l{i}.mlp_norm"])
         self.fused = bool(weights["_stb_fused"])
-        for name in [f"l{i}.{p}" for i in range(shape.layers) for p in PROJECTIONS] + ["lm_head"]:
+        projections = MOE_PROJECTIONS if shape.moe else PROJECTIONS
+        for name in [f"l{i}.{p}" for i in range(shape.layers) for p in projections] + ["lm_head"]:
             if not isinstance(weights[name], TiledWeight):
                 weights[name] = TiledWeight(weights[name])
+        # rotary table (YaRN for gpt-oss: frequencies + cos/sin scale, modelcfg.rope_table)
+        self.rope_inv, self.rope_scale = None, 1.0
+        if shape.yarn:
+            inv, self.rope_scale = shape.rope_table()
+            self.rope_inv = torch.tensor(inv, dtype=torch.float32, device=device)
         self.pool = pool
         self.device = device
         self.scale = 1.0 / math.sqrt(shape.d_head)
@@ -267,6 +294,11 @@ class Decoder:
         self._dirty = {"qkv": 0, "proj": 0, "gu": 0, "logits": 0}
         self._stream_cache: dict = {}
         self.taps: list | None = None  # debug (canary): residual stream after the embedding and each layer
+        # MoE routing statistics for the grouped GEMM's algorithmic bytes: each timed step copies the
+        # per-layer expert offsets to pinned memory (4 buffers: eager / graph x 2 flight parities)
+        self._moe_host = None
+        self._moe_flip = 0
+        self._moe_buf = 0
 
     # -- buffers ----------------------------------------------------------------
 
@@ -288,6 +320,20 @@ class Decoder:
             # fused path: per-row partial sums of squares (one per 128-feature tile of d) of
             # every norm input (2 per layer + 1)
             self.ss = torch.zeros(2 * s.layers + 1, cap, -(-s.d_model // 512) * 4, dtype=f32, device=dev)
+            if s.moe:  # routed rows: T * top_k, plus one token tile of TMA overhang
+                rows = cap * s.top_k + 64
+                i32 = torch.int32
+                self.rlog = torch.zeros(cap, s.n_experts, dtype=f32, device=dev)
+                self.m_counts = torch.zeros(s.n_experts, dtype=i32, device=dev)   # zero at rest
+                self.m_expert = torch.empty(cap * s.top_k, dtype=i32, device=dev)
+                self.m_rank = torch.empty(cap * s.top_k, dtype=i32, device=dev)
+                self.m_wt = torch.empty(cap * s.top_k, dtype=f32, device=dev)
+                self.m_perm = torch.empty(cap * s.top_k, dtype=i32, device=dev)
+                self.m_offs = torch.zeros(s.layers, s.n_experts + 1, dtype=i32, device=dev)
+                self.m_x = torch.zeros(rows, s.d_model, dtype=torch.float16, device=dev)
+                self.m_act = torch.zeros(rows, s.d_ff, dtype=torch.float16, device=dev)
+                self.m_y = torch.empty(rows, s.d_model, dtype=f32, device=dev)
+                self._moe_rows = rows
             self._cap_t = cap
             self._dirty.update(qkv=0, proj=0, gu=0)
             self.graphs.clear()  # captured graphs point at the old buffers
@@ -444,6 +490,8 @@ class Decoder:
 
     def _launch(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
                 dec_bytes: int) -> None:
+        if self.shape.moe:
+            return self._launch_moe(m, T, R, B, S, max_q, max_ctx, dec_bytes)
         if self.fused:
             return self._launch_fused(m, T, R, B, S, max_q, max_ctx, dec_bytes)
         s, w = self.shape, self.w
@@ -499,6 +547,99 @@ class Decoder:
         self.gemm(rows, w["lm_head"], "logits", st, "lm_head")
         # the sampler re-zeroes the logits only when the LM head accumulated them (stream-K);
         # whole-tile LM heads (any decode batch) overwrite them with plain stores
+        clear = 0 if self.keep_logits or not self._stream_cache[(R, s.vocab, d)] else 1
+        call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
+             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)
+        if clear:
+            self._cleared("logits", R)
+
+    def _launch_moe(self, m: dict[str, int], T: int, R: int, B: int, S: int, max_q: int, max_ctx: int,
+                    dec_bytes: int) -> None:
+        """gpt-oss family (config C4), per layer: rmsnorm -> QKV GEMM -> bias + YaRN RoPE + K1
+        commit -> K3 / K2 with the layer's sliding window and sinks -> O GEMM -> + bias, residual,
+        rmsnorm -> router GEMM -> route -> gather -> MXFP4 gate-up (clamped SwiGLU) -> MXFP4 down
+        -> weighted combine + residual + the next rmsnorm (moe.cu)."""
+        s, w = self.shape, self.w
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        d, E, k = s.d_model, s.n_experts, s.top_k
+        x, h = self.x, self.h
+        call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
+        for _ in range(2):
+            self._tock("event_overhead", self._tick(), 0)
+        call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
+        call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
+        clr = T if T <= CLEAR_MAX else 0
+        if self.taps is not None:
+            self.taps.append(x[:T].clone())
+        rows = T * k
+        timed = self.timers is not None or self._graph_timed
+        offs_host = None
+        if timed:
+            if self._moe_host is None:
+                self._moe_host = [torch.empty(s.layers, E + 1, dtype=torch.int32, pin_memory=True) for _ in range(4)]
+            if self._graph_timed:
+                slot = self._timed_parity  # graphs: the capture's parity (key[6])
+            else:
+                self._moe_flip ^= 1
+                slot = 2 + self._moe_flip
+            offs_host = self._moe_host[slot]
+        inv = _p(self.rope_inv) if self.rope_inv is not None else None
+        for i in range(s.layers):
+            self.gemm(h[:T], w[f"l{i}.wqkv"], "qkv", st, "wqkv")
+            call("stb_qkv_rope_commit_ex", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]), _p(m["pos"]),
+                 T, s.n_q, s.rope_theta, inv, C.c_float(self.rope_scale),
+                 _p(w.get(f"l{i}.bqkv")), clr, st)
+            self._cleared("qkv", clr)
+            win, sinks = s.window(i), _p(w.get(f"l{i}.sinks"))
+            if B:
+                ev = self._tick()
+                call("stb_attn_decode_ex", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
+                     _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, win, sinks, _p(self.work), st)
+                self._tock("attn_decode", ev, dec_bytes)
+            if S:
+                ev = self._tick()
+                call("stb_attn_prefill_ex", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
+                     _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
+                     self._pre_units, win, sinks, st)
+                self._tock("attn_prefill", ev, self._pre_work)
+            self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
+            call("stb_add_bias_rmsnorm", _p(x), _p(self.proj), _p(w.get(f"l{i}.bo")), _p(w[f"l{i}.mlp_norm"]), _p(h),
+                 T, d, s.rms_eps, clr, st)
+            self._cleared("proj", clr)
+            # router: fp32 logits, zeroed by the GEMM itself (flags 0)
+            rt_w = w[f"l{i}.router"]
+            ev = self._tick()
+            if "stb_gemm_bf16" not in _SKIP:
+                lib.call("stb_gemm_bf16", _p(h), h.stride(0), _p(rt_w), 0, _p(self.rlog), self.rlog.stride(0), T, E, d,
+                         0, GEMM_W_TILED, st)
+            self._tock("gemm_decode" if T <= 128 else "gemm_prefill", ev,
+                       E * d * 2 + T * d * 2 + T * E * 4 if T <= 128 else 2 * T * E * d)
+            call("stb_moe_route", _p(self.rlog), self.rlog.stride(0), _p(w[f"l{i}.router_b"]), T, E, k,
+                 _p(self.m_counts), _p(self.m_expert), _p(self.m_rank), _p(self.m_wt), st)
+            offs = self.m_offs[i]
+            call("stb_moe_gather", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
+                 _p(self.m_rank), _p(offs), _p(self.m_perm), _p(self.m_x), st)
+            ex = w[f"l{i}.experts"]
+            ev = self._tick()
+            call("stb_moe_gemm_mxfp4", _p(self.m_x), self._moe_rows, _p(ex.gate_up), _p(ex.b_gate_up),
+                 _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),
+                 self.m_act.stride(0), rows, st)
+            self._tock("moe_gemm", ev, _MoeWork(offs_host, i, 2 * s.d_ff, d, rows, 2, 2) if timed else 0)
+            ev = self._tick()
+            call("stb_moe_gemm_mxfp4", _p(self.m_act), self._moe_rows, _p(ex.down), _p(ex.b_down),
+                 _p(self.m_counts), E, d, s.d_ff, MOE_DOWN, C.c_float(0.0), _p(self.m_y), self.m_y.stride(0), rows, st)
+            self._tock("moe_gemm", ev, _MoeWork(offs_host, i, d, s.d_ff, rows, 2, 4) if timed else 0)
+            last = i + 1 == s.layers
+            call("stb_moe_combine", _p(x), _p(self.m_y), T, d, k, _p(self.m_perm), _p(self.m_wt),
+                 None if last else _p(w[f"l{i + 1}.attn_norm"]), None if last else _p(h), s.rms_eps,
+                 _p(self.m_counts), E, st)
+            if self.taps is not None:
+                self.taps.append(x[:T].clone())
+        if offs_host is not None:
+            offs_host.copy_(self.m_offs, non_blocking=True)
+        rows_b = self.rows[:R]
+        call("stb_gather_rmsnorm", _p(x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows_b), R, d, s.rms_eps, st)
+        self.gemm(rows_b, w["lm_head"], "logits", st, "lm_head")
         clear = 0 if self.keep_logits or not self._stream_cache[(R, s.vocab, d)] else 1
         call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
              _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)
@@ -605,6 +746,8 @@ class Decoder:
         sink = self.timers if sink is None else sink
         if sink is not None:
             for name, e0, e1, work in pending:
+                if callable(work):  # known after the step (MoE: the touched experts)
+                    work = work()
                 t = sink.setdefault(name, [0.0, 0, 0])
                 ms = e0.elapsed_time(e1)
                 t[0] += ms

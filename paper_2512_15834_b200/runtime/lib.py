@@ -57,6 +57,15 @@ SIGNATURES: dict[str, tuple] = {
     "stb_silu_mul": (I32, [P, P, I32, I32, I32, P]),
     "stb_gather_rmsnorm": (I32, [P, P, P, P, I32, I32, F32, P]),
     "stb_sample_forced": (I32, [P, I64, P, I32, I32, F32, P, P, P, I32, P]),
+    # gpt-oss family (config C4)
+    "stb_qkv_rope_commit_ex": (I32, [P, I32, P, P, P, P, I32, I32, F32, P, F32, P, I32, P]),
+    "stb_attn_decode_ex": (I32, [P, I32, P, P, P, P, I32, I32, F32, I32, I32, P, P, P]),
+    "stb_attn_prefill_ex": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, I32, I32, P, P]),
+    "stb_add_bias_rmsnorm": (I32, [P, P, P, P, P, I32, I32, F32, I32, P]),
+    "stb_moe_route": (I32, [P, I64, P, I32, I32, I32, P, P, P, P, P]),
+    "stb_moe_gather": (I32, [P, I64, I32, I32, I32, I32, P, P, P, P, P, P, P]),
+    "stb_moe_gemm_mxfp4": (I32, [P, I32, P, P, P, I32, I32, I32, I32, F32, P, I64, I32, P]),
+    "stb_moe_combine": (I32, [P, P, I32, I32, I32, P, P, P, P, F32, P, I32, P]),
 }
 
 STATUS_CAPACITY = -4

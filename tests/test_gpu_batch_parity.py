@@ -56,17 +56,18 @@ def _run_fleet(shape, agents: int, steps: int, seed: int = 1):
     return rt, engine
 
 
-@pytest.mark.parametrize("name", ["tiny", "qwen3-mini", "llama3-8b[L=2,V=32k]"])
+@pytest.mark.parametrize("name", ["tiny", "qwen3-mini", "llama3-8b[L=2,V=32k]", "gpt-oss-mini"])
 def test_batch_runtime_parity(name):
     from oracle.cpu_decoder import CpuDecoder
     from oracle.kv_alloc import LifoAllocator
-    from paper_2512_15834_b200.modelcfg import SHAPES, QWEN3_MINI, TINY
+    from paper_2512_15834_b200.modelcfg import GPT_OSS_MINI, SHAPES, QWEN3_MINI, TINY
 
-    shape = {"tiny": TINY, "qwen3-mini": QWEN3_MINI}.get(name) or dataclasses.replace(
+    shape = {"tiny": TINY, "qwen3-mini": QWEN3_MINI, "gpt-oss-mini": GPT_OSS_MINI}.get(name) or dataclasses.replace(
         SHAPES["llama3-8b"], name=name, layers=2, vocab=32768)
     big = name.startswith("llama")
     rt, engine = _run_fleet(shape, agents=10 if big else 12, steps=140 if big else 260)
     ora = CpuDecoder(shape)
+    ora.bf16_points = shape.moe  # MoE: storage rounding as on the engine (router near-ties)
     alloc = LifoAllocator(4096)
     ops = rt.pool.log
     op_i = 0

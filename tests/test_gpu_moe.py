@@ -1,0 +1,272 @@
+"""gpt-oss family (config C4) kernels on the B200, each through the C ABI against a plain PyTorch
+fp32 restatement (integer routing outputs bit-exact): routing, permutation, the MXFP4 grouped GEMM
+(gate-up with the clamped SwiGLU epilogue, down with bias), the weighted combine + RMSNorm, paged
+attention with sliding windows and sinks (K3 decode, K2 append-prefill incl. its KV-split path),
+the biased YaRN RoPE commit and the biased residual RMSNorm at d = 2880."""
+
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2512_15834_b200.modelcfg import GPT_OSS_120B, ModelShape  # noqa: E402
+from paper_2512_15834_b200.runtime import weights as W  # noqa: E402
+from test_gpu_kernels import P, _dense_kv, _fill_pool, _pool, rel, stream  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_15834_b200.runtime import lib as L
+
+    L.load()
+    return L
+
+
+def _route(lib, logits, bias, k):
+    T, E = logits.shape
+    counts = torch.zeros(E, dtype=torch.int32, device="cuda")
+    ex = torch.empty(T * k, dtype=torch.int32, device="cuda")
+    rk = torch.empty_like(ex)
+    wt = torch.empty(T * k, device="cuda")
+    lib.call("stb_moe_route", P(logits), E, P(bias), T, E, k, P(counts), P(ex), P(rk), P(wt), stream())
+    torch.cuda.synchronize()
+    return counts, ex, rk, wt
+
+
+@pytest.mark.parametrize("T,E,k", [(1, 128, 4), (37, 128, 4), (300, 16, 4), (64, 32, 2), (5, 256, 8)])
+def test_moe_route(lib, T, E, k):
+    g = torch.Generator(device="cuda").manual_seed(T * E + k)
+    logits = torch.randn(T, E, device="cuda", generator=g)
+    logits[0, 3] = logits[0, 5] = 9.0  # a tie: the lower expert id ranks first
+    bias = 0.1 * torch.randn(E, device="cuda", generator=g)
+    counts, ex, rk, wt = _route(lib, logits, bias, k)
+    z = (logits + bias).cpu().numpy()
+    order = np.argsort(-z, axis=1, kind="stable")[:, :k]
+    assert np.array_equal(ex.view(T, k).cpu().numpy(), order)
+    top = np.take_along_axis(z, order, 1)
+    ref = np.exp(top - top[:, :1])
+    ref /= ref.sum(1, keepdims=True)
+    assert np.allclose(wt.view(T, k).cpu().numpy(), ref, rtol=1e-5, atol=1e-6)
+    assert np.array_equal(counts.cpu().numpy(), np.bincount(order.ravel(), minlength=E))
+    for e in range(E):  # ranks: a permutation of 0..count-1 within every expert
+        r = sorted(rk.cpu().numpy()[ex.cpu().numpy() == e].tolist())
+        assert r == list(range(len(r)))
+
+
+def _gather(lib, h, counts, ex, rk, E, k):
+    T, d = h.shape
+    offs = torch.empty(E + 1, dtype=torch.int32, device="cuda")
+    perm = torch.empty(T * k, dtype=torch.int32, device="cuda")
+    xp = torch.full((T * k + 64, d), float("nan"), device="cuda").to(torch.float16)
+    lib.call("stb_moe_gather", P(h), d, T, d, k, E, P(counts), P(ex), P(rk), P(offs), P(perm), P(xp), stream())
+    torch.cuda.synchronize()
+    return offs, perm, xp
+
+
+def test_moe_gather(lib):
+    T, E, k, d = 50, 16, 4, 2880
+    logits = torch.randn(T, E, device="cuda")
+    counts, ex, rk, wt = _route(lib, logits, torch.zeros(E, device="cuda"), k)
+    h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    offs, perm, xp = _gather(lib, h, counts, ex, rk, E, k)
+    c = counts.cpu().numpy()
+    assert offs.cpu().tolist() == [0] + np.cumsum(c).tolist()
+    pm = perm.cpu().numpy()
+    assert sorted(pm.tolist()) == list(range(T * k))
+    exn = ex.cpu().numpy()
+    o = offs.cpu().numpy()
+    assert np.all((pm >= o[exn]) & (pm < o[exn + 1]))  # every row inside its expert's range
+    for p in range(T * k):
+        assert torch.equal(xp[pm[p]], h[p // k].to(torch.float16))
+
+
+def _experts(E, N, K, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    tiles, deq = [], []
+    for _ in range(E):
+        w = (0.02 * torch.randn(N, K, device="cuda", generator=g)).to(torch.bfloat16)
+        c, e = W.quantize_mxfp4(w)
+        tiles.append(W.pack_mxfp4_tiles(c, e))
+        deq.append(W.dequantize_mxfp4(c, e))
+    bias = 0.02 * torch.randn(E, N, device="cuda", generator=g)
+    return torch.stack(tiles).contiguous(), torch.stack(deq), bias
+
+
+def glu_ref(gu, limit=7.0):
+    g, u = gu[:, 0::2].clamp(max=limit), gu[:, 1::2].clamp(-limit, limit)
+    return (u + 1) * (g * torch.sigmoid(1.702 * g))
+
+
+@pytest.mark.parametrize("T,E,k,d,ff", [(1, 16, 4, 512, 256), (32, 128, 4, 2880, 2880), (300, 16, 4, 512, 256),
+                                        (700, 32, 4, 1024, 512), (64, 8, 2, 256, 384)])
+def test_moe_gemm_mxfp4(lib, T, E, k, d, ff):
+    """Grouped MXFP4 GEMM, both kinds, vs fp32 math on the dequantised weights and the same fp16
+    inputs; token tiles 16 / 32 / 64 (decode, mixed, ingest-sized), experts with 0..many rows."""
+    gu_t, gu_w, gu_b = _experts(E, 2 * ff, d, 1)
+    dn_t, dn_w, dn_b = _experts(E, d, ff, 2)
+    logits = torch.randn(T, E, device="cuda")
+    counts, ex, rk, wt = _route(lib, logits, torch.zeros(E, device="cuda"), k)
+    h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    offs, perm, xp = _gather(lib, h, counts, ex, rk, E, k)
+    rows = T * k
+    cap = xp.shape[0]
+    act = torch.full((cap, ff), float("nan"), device="cuda").to(torch.float16)
+    y = torch.full((cap, d), float("nan"), device="cuda")
+    lib.call("stb_moe_gemm_mxfp4", P(xp), cap, P(gu_t), P(gu_b), P(counts), E, 2 * ff, d, 1, C.c_float(7.0), P(act),
+             ff, rows, stream())
+    lib.call("stb_moe_gemm_mxfp4", P(act), cap, P(dn_t), P(dn_b), P(counts), E, d, ff, 2, C.c_float(0.0), P(y), d,
+             rows, stream())
+    torch.cuda.synchronize()
+    o = offs.cpu().tolist()
+    for e in range(E):
+        a, b = o[e], o[e + 1]
+        if a == b:
+            continue
+        ref_act = glu_ref(xp[a:b].float() @ gu_w[e].T + gu_b[e])
+        assert rel(act[a:b], ref_act) < 2e-3, ("gate_up", e)
+        ref_y = act[a:b].float() @ dn_w[e].T + dn_b[e]
+        assert rel(y[a:b], ref_y) < 1e-4, ("down", e)
+    assert not torch.isnan(act[:rows]).any() and not torch.isnan(y[:rows]).any()
+
+
+def test_moe_combine(lib):
+    T, E, k, d = 9, 16, 4, 2880
+    counts, ex, rk, wt = _route(lib, torch.randn(T, E, device="cuda"), torch.zeros(E, device="cuda"), k)
+    h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    offs, perm, xp = _gather(lib, h, counts, ex, rk, E, k)
+    y = torch.randn(T * k, d, device="cuda")
+    x = torch.randn(T, d, device="cuda")
+    nw = (1 + 0.1 * torch.randn(d, device="cuda")).to(torch.bfloat16)
+    hn = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    x0 = x.clone()
+    lib.call("stb_moe_combine", P(x), P(y), T, d, k, P(perm), P(wt), P(nw), P(hn), C.c_float(1e-5), P(counts), E,
+             stream())
+    torch.cuda.synchronize()
+    ref = x0.clone()
+    pm = perm.long().view(T, k)
+    for r in range(k):
+        ref = ref + wt.view(T, k)[:, r:r + 1] * y[pm[:, r]]
+    assert rel(x, ref) < 1e-6
+    refn = ref * torch.rsqrt((ref * ref).mean(-1, keepdim=True) + 1e-5) * nw.float()
+    assert rel(hn, refn) < 5e-3
+    assert not counts.any()  # zeroed for the next layer's route
+
+
+def _ref_attn_ws(q, k, v, qpos, scale, window=0, sinks=None):
+    H, G = q.shape[1], k.shape[1]
+    kk = k.float().repeat_interleave(H // G, dim=1)
+    vv = v.float().repeat_interleave(H // G, dim=1)
+    s = torch.einsum("nhd,chd->hnc", q.float(), kk) * scale
+    keys = torch.arange(k.shape[0], device=q.device)[None, :]
+    mask = keys > qpos[:, None]
+    if window:
+        mask = mask | (keys <= qpos[:, None] - window)
+    s = s.masked_fill(mask[None], float("-inf"))
+    if sinks is not None:
+        sk = sinks.float()[:, None, None].expand(H, s.shape[1], 1)
+        p = torch.softmax(torch.cat([s, sk], -1), -1)[..., :-1]
+    else:
+        p = torch.softmax(s, -1)
+    return torch.einsum("hnc,chd->nhd", p, vv)
+
+
+OSS = ModelShape("oss-attn", 1, 2880, 64, 8, 64, 64, 64)
+
+
+@pytest.mark.parametrize("window", [0, 128, 16])
+@pytest.mark.parametrize("ctxs", [[1], [5, 127, 128, 129, 200], [4096] * 4 + [100, 2500], [700] * 32])
+def test_attn_decode_window_sinks(lib, window, ctxs):
+    shape = OSS
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(ctxs), bps=512)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=len(ctxs) + window)
+    B = len(ctxs)
+    q = torch.randn(B, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    sinks = 1.0 + torch.randn(shape.n_q, device="cuda")
+    out = torch.empty_like(q)
+    slots = torch.arange(B, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(B, shape.n_q, shape.n_kv, shape.d_head) // 4), device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    lib.call("stb_attn_decode_ex", pool.h, 0, P(q), P(out), P(slots), P(ctx), B, shape.n_q, scale, max(ctxs), window,
+             P(sinks), P(ws), stream())
+    for b, (k, v) in enumerate(dense):
+        ref = _ref_attn_ws(q[b:b + 1], k, v, torch.tensor([ctxs[b] - 1], device="cuda"), scale, window, sinks)
+        assert rel(out[b:b + 1], ref) < 1e-2, b
+
+
+@pytest.mark.parametrize("window", [0, 128, 32])
+@pytest.mark.parametrize("runs", [[(1, 1)], [(4, 10), (21, 33)], [(300, 300), (33, 1200), (7, 8)],
+                                  [(33, 2174)], [(996, 3044), (129, 4000)]])
+def test_attn_prefill_window_sinks(lib, window, runs):
+    shape = OSS
+    ctxs = [c for _, c in runs]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(runs), bps=512)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=11 + window)
+    T = sum(n for n, _ in runs)
+    q = torch.randn(T, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    sinks = 1.0 + torch.randn(shape.n_q, device="cuda")
+    out = torch.full_like(q, float("nan"))
+    qs = [0]
+    for n, _ in runs:
+        qs.append(qs[-1] + n)
+    slots = torch.arange(len(runs), dtype=torch.int32, device="cuda")
+    qstart = torch.tensor(qs, dtype=torch.int32, device="cuda")
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    G = shape.n_q // shape.n_kv
+    units = sum(-(-n // (256 // G)) for n, _ in runs) * shape.n_kv  # lone verify pass -> KV split path
+    lib.call("stb_attn_prefill_ex", pool.h, 0, P(q), P(out), P(slots), P(qstart), P(ctx), len(runs), T, shape.n_q,
+             scale, max(n for n, _ in runs), units, window, P(sinks), stream())
+    for s, ((n, c), (k, v)) in enumerate(zip(runs, dense)):
+        ref = _ref_attn_ws(q[qs[s]:qs[s + 1]], k, v, torch.arange(c - n, c, device="cuda"), scale, window, sinks)
+        assert rel(out[qs[s]:qs[s + 1]], ref) < 1e-2, s
+
+
+def test_rope_commit_ex_yarn_bias(lib):
+    shape = ModelShape("t", 1, 2880, 64, 8, 64, 64, 64, rope_theta=150000.0, yarn=GPT_OSS_120B.yarn)
+    pool = _pool(lib, shape, nb=300)
+    n = 37
+    pool.reserve(0, 4200)
+    pool.sync(torch.cuda.current_stream().cuda_stream)
+    width = (shape.n_q + 2 * shape.n_kv) * shape.d_head
+    qkv = torch.randn(n, width, device="cuda") * 3.0
+    bias = torch.randn(width, device="cuda")
+    pos = torch.arange(4100, 4100 + n, dtype=torch.int32, device="cuda")
+    slot_of = torch.zeros(n, dtype=torch.int32, device="cuda")
+    q = torch.empty(n, shape.q_dim, dtype=torch.bfloat16, device="cuda")
+    inv_l, sc = shape.rope_table()
+    inv = torch.tensor(inv_l, device="cuda")
+    qkv0 = qkv.clone()
+    lib.call("stb_qkv_rope_commit_ex", pool.h, 0, P(qkv), P(q), P(slot_of), P(pos), n, shape.n_q, C.c_float(150000.0),
+             P(inv), C.c_float(sc), P(bias), 0, stream())
+    from oracle.cpu_decoder import CpuDecoder, yarn_inv_freq
+
+    dec = CpuDecoder.__new__(CpuDecoder)
+    dec.s = shape
+    dec.inv_freq, dec.rope_scale = yarn_inv_freq(64, 150000.0, shape.yarn)
+    x = (qkv0 + bias).cpu().view(n, -1, shape.d_head)
+    rq = dec._rope(x[:, :shape.n_q], pos.cpu())
+    rk = dec._rope(x[:, shape.n_q:shape.n_q + shape.n_kv], pos.cpu())
+    assert rel(q.view(n, shape.n_q, -1).cpu(), rq) < 5e-3
+    kd, vd = _dense_kv(pool, 0, 0, 4100 + n, shape)
+    assert rel(kd[4100:].cpu(), rk) < 5e-3
+    assert rel(vd[4100:].cpu(), x[:, shape.n_q + shape.n_kv:]) < 5e-3
+
+
+@pytest.mark.parametrize("d", [2880, 512, 4096])
+def test_add_bias_rmsnorm(lib, d):
+    n = 11
+    x = torch.randn(n, d, device="cuda")
+    delta = torch.randn(n, d, device="cuda")
+    bias = torch.randn(d, device="cuda")
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).to(torch.bfloat16)
+    y = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    ref = x + delta + bias
+    lib.call("stb_add_bias_rmsnorm", P(x), P(delta), P(bias), P(w), P(y), n, d, C.c_float(1e-5), n, stream())
+    torch.cuda.synchronize()
+    assert rel(x, ref) < 1e-6 and not delta.any()
+    assert rel(y, ref * torch.rsqrt((ref * ref).mean(-1, keepdim=True) + 1e-5) * w.float()) < 5e-3

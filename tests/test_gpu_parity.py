@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 from oracle import scenarios as S  # noqa: E402
 from oracle.cpu_decoder import CpuDecoder  # noqa: E402
 from oracle.engine import OracleEngine  # noqa: E402
-from paper_2512_15834_b200.modelcfg import QWEN3_MINI, TINY  # noqa: E402
+from paper_2512_15834_b200.modelcfg import GPT_OSS_MINI, QWEN3_MINI, TINY  # noqa: E402
 
 API = S.product_api()
 LOGIT_RTOL = 2e-2
@@ -42,7 +42,11 @@ class Pair:
         return eng
 
     def oracle(self, sim, config):
-        eng = OracleEngine(sim, config, model=CpuDecoder(self.shape), num_blocks=4096)
+        model = CpuDecoder(self.shape)
+        # MoE: the oracle rounds to bf16 / fp16 exactly where the engine stores (all arithmetic
+        # fp32), so a router near-tie is never decided by storage rounding alone
+        model.bf16_points = self.shape.moe
+        eng = OracleEngine(sim, config, model=model, num_blocks=4096)
         eng.observers.append(lambda t, rid, ph, n: self.ora_tables.append(
             (rid, ph, eng.alloc.blocks(eng.sequences[rid].slot))))
         self.ora_engines.append(eng)
@@ -208,3 +212,25 @@ def test_default_engine_is_native():
     assert lib.load().stb_launch_count() > before
     assert eng.rt.forwards > 0
     del EngineConfig, Simulator
+    pair.check()
+
+
+@pytest.mark.parametrize("case", ["full_hit", "partial_hit", "two_turn_mixed", "prefix"])
+def test_timeline_parity_gpt_oss(golden, case):
+    """Config C4's model family at oracle size (gpt-oss: d_head 64, GQA 8, sinks, QKV/O biases,
+    YaRN, sliding window 32 on layer 0, 16 MXFP4 experts top-4 with the clamped SwiGLU): the
+    reference timelines, ids bit-exact, logits within 2e-2 of the oracle."""
+    pair = Pair(GPT_OSS_MINI)
+    got, _ = S.run_timeline(API, case, pair.gpu)
+    ora, _ = S.run_timeline(API, case, pair.oracle)
+    assert got == golden["timelines"][case] and ora == golden["timelines"][case]
+    pair.check()
+
+
+def test_fleet_parity_gpt_oss(golden):
+    """C1's fleet (256-token prompts: well past the 32-token window) on the gpt-oss family."""
+    pair = Pair(GPT_OSS_MINI)
+    got, _ = S.run_fleet(API, "c1", pair.gpu)
+    ora, _ = S.run_fleet(API, "c1", pair.oracle)
+    assert got == golden["fleets"]["c1"] and ora == golden["fleets"]["c1"]
+    pair.check()
