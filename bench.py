@@ -197,25 +197,39 @@ class CpuDecodeArm:
         pos = torch.full((B,), self.n)
         x = dec.embed[torch.full((B,), 5, dtype=torch.long)]
         w = dec.layers[0]
-        for _ in range(self.L):
+        for li in range(self.L):
             h = dec._norm(x, w["an"])
             qkv = h @ w["qkv"].T
+            if "bqkv" in w:
+                qkv = qkv + w["bqkv"]
             q, k = dec._qk(w, qkv[:, : H * D].view(B, H, D), qkv[:, H * D: (H + G) * D].view(B, G, D))
             q, k = dec._rope(q, pos), dec._rope(k, pos)
             v = qkv[:, (H + G) * D:].view(B, G, D)
+            win = s.window(li)
             outs = []
             for b in range(B):
                 self.k[b][self.n] = k[b]
                 self.v[b][self.n] = v[b]
-                kk = self.k[b][: self.n + 1]  # [n, G, D]
-                vv = self.v[b][: self.n + 1]
+                lo = max(0, self.n + 1 - win) if win else 0  # sliding-window layers read the window only
+                kk = self.k[b][lo: self.n + 1]  # [n, G, D]
+                vv = self.v[b][lo: self.n + 1]
                 qb = q[b].view(G, H // G, D)
-                p = torch.softmax(torch.einsum("grd,ngd->grn", qb, kk) / math.sqrt(D), dim=-1)
+                sc = torch.einsum("grd,ngd->grn", qb, kk) / math.sqrt(D)
+                if "sinks" in w:
+                    sk = w["sinks"].view(G, H // G, 1)
+                    p = torch.softmax(torch.cat([sc, sk], -1), dim=-1)[..., :-1]
+                else:
+                    p = torch.softmax(sc, dim=-1)
                 outs.append(torch.einsum("grn,ngd->grd", p, vv).reshape(H * D))
             x = x + torch.stack(outs) @ w["o"].T
+            if "bo" in w:
+                x = x + w["bo"]
             h = dec._norm(x, w["mn"])
-            gu = h @ w["gu"].T
-            x = x + (torch.nn.functional.silu(gu[:, : s.d_ff]) * gu[:, s.d_ff:]) @ w["dn"].T
+            if "router" in w:
+                x = x + dec._moe(w, h)
+            else:
+                gu = h @ w["gu"].T
+                x = x + (torch.nn.functional.silu(gu[:, : s.d_ff]) * gu[:, s.d_ff:]) @ w["dn"].T
         logits = dec._norm(x, dec.fn) @ dec.head.T
         self.n += 1
         return logits
@@ -267,8 +281,9 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-# BASELINE.json configs this bench can run on one node (C1 is the CPU parity config, C4 needs
-# TP/EP — out of scope). agents: per GPU (weak scaling) or whole box (strong).
+# BASELINE.json configs this bench can run on one node (C1 is the CPU parity config; C4's experts
+# are MXFP4, so a gpt-oss-120b replica fits one B200). agents: per GPU (weak
+# scaling) or whole box (strong).
 CONFIGS = {
     "c2": {"shape": "llama3-8b", "agents": 32, "per_gpu": True, "max_ctx": 16384, "trace": {},
            "label": "C2 llama3-8b-shaped random-init bf16, 32 agents/GPU, tool-call trace (prompt 2048, reason "
@@ -276,6 +291,9 @@ CONFIGS = {
     "c3": {"shape": "qwen3-32b", "agents": 64, "per_gpu": False, "max_ctx": 16384, "trace": {},
            "label": "C3 qwen3-32b-shaped (qk-norm) random-init bf16, 64 agents sharded over the replicas, "
                     "tool-call trace as C2"},
+    "c4": {"shape": "gpt-oss-120b", "agents": 32, "per_gpu": False, "max_ctx": 16384, "trace": {},
+           "label": "C4 gpt-oss-120b-shaped random-init (bf16 attention, MXFP4 experts: 128 top-4), 32 agents "
+                    "sharded over the replicas, tool-call trace as C2"},
     "c5": {"shape": "llama3-8b", "agents": 16, "per_gpu": True, "max_ctx": 49152, "max_step_tokens": 36864,
            "trace": {"prompt_tokens": 32768, "output": (2048, 2048)},
            "label": "C5 KV-pressure: llama3-8b-shaped random-init bf16, 16 agents/GPU, 32k-token resident "
@@ -632,7 +650,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=40)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
-                    help="BASELINE config: c2 (default, the metric's config), c3, c5")
+                    help="BASELINE config: c2 (default, the metric's config), c3, c4, c5")
     ap.add_argument("--agents", type=int, default=0, help="override the config's agent count (per GPU)")
     ap.add_argument("--shape", default="", help="override the config's model shape")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")

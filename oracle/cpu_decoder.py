@@ -36,6 +36,32 @@ def draw(shape, seed: int, name: str, norm: bool) -> torch.Tensor:
     return t.to(torch.bfloat16).to(torch.float32)
 
 
+ROUTE_TIE = 1e-2  # near-tie band of the router arbitration, as a fraction of the token's logit range
+
+
+class RouteHints:
+    """The engine's per-forward expert choices keyed by (rid, start, ids), FIFO per key, built from
+    record-mode flights (`Runtime.flights[i]["items"]` / `["routes"]`)."""
+
+    def __init__(self):
+        self.q: dict = {}
+
+    def add_flights(self, flights) -> "RouteHints":
+        for f in flights:
+            if not f.get("routes"):
+                continue
+            off = 0
+            for rid, start, ids, _rows in f["items"]:
+                n = len(ids)
+                self.q.setdefault((rid, start, tuple(ids)), []).append([r[off:off + n] for r in f["routes"]])
+                off += n
+        return self
+
+    def take(self, rid, start, ids):
+        lst = self.q.get((rid, start, tuple(ids)))
+        return lst.pop(0) if lst else None
+
+
 E2M1 = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0], dtype=np.float32)
 
 
@@ -120,6 +146,15 @@ class CpuDecoder:
             self.inv_freq, self.rope_scale = yarn_inv_freq(shape.d_head, shape.rope_theta, shape.yarn)
         self.cache: dict[str, list] = {}
         self.routes: list | None = None  # debug: per MoE layer call, the (experts, weights) chosen
+        # near-tie arbitration (parity tests): `route_hints.take(rid, start, ids)` -> per layer the
+        # engine's expert ids [n, k]; the oracle adopts the engine's experts for a token only where
+        # they differ from its own top-k by a near-tie (`ROUTE_TIE` of the token's logit range) and
+        # raises otherwise. Storage rounding upstream of the router (the bf16 attention output, the
+        # bf16 norm output) moves router logits by ~1e-3; a tie closer than that is decided by
+        # rounding on either side, and following the engine there keeps the comparison meaningful.
+        self.route_hints = None
+        self.arbitrated = 0       # token-layers where the engine's near-tie choice was adopted
+        self.routed = 0           # token-layers routed
 
     def layer(self, i: int) -> dict:
         s, src = self.s, self.source
@@ -189,7 +224,7 @@ class CpuDecoder:
     def drop(self, rid: str) -> None:
         self.cache.pop(rid, None)
 
-    def layer_forward(self, w: dict, x: torch.Tensor, pos: torch.Tensor, start: int, kv: tuple):
+    def layer_forward(self, w: dict, x: torch.Tensor, pos: torch.Tensor, start: int, kv: tuple, hint=None):
         """One decoder layer: x [T, d] fp32 at absolute positions `pos` (= start..start+T-1), kv =
         this layer's (K, V) cache rows; returns (new x, new kv). Also the per-layer teacher-forced
         check of the full-size canary (tests/test_gpu_canary.py) feeds it the engine's own layer
@@ -232,20 +267,36 @@ class CpuDecoder:
             x = x + w["bo"]
         h = r(self._norm(x, w["mn"]))
         if "router" in w:
-            x = x + self._moe(w, h)
+            x = x + self._moe(w, h, hint)
         else:
             gu = h @ w["gu"].T
             g, u = gu[:, : s.d_ff], gu[:, s.d_ff:]
             x = x + r(torch.nn.functional.silu(g) * u) @ w["dn"].T
         return x, (kc, vc)
 
-    def _moe(self, w: dict, h: torch.Tensor) -> torch.Tensor:
+    def _moe(self, w: dict, h: torch.Tensor, hint=None) -> torch.Tensor:
         """Routed experts (gpt-oss): top-k of router logits + bias (ties -> lower id, a stable
         sort), softmax over the k, clamped SwiGLU experts with biases, weighted sum in rank order."""
         s = self.s
         T, k, lim = h.shape[0], s.top_k, s.swiglu_limit
         logits = (h @ w["router"].T + w["router_b"]).numpy()
         order = np.argsort(-logits, axis=1, kind="stable")[:, :k]
+        self.routed += T
+        if hint is not None:
+            for t in range(T):
+                mine, theirs = set(order[t].tolist()), set(hint[t].tolist())
+                if mine == theirs:
+                    continue
+                kth = float(np.sort(logits[t])[::-1][k - 1])
+                tie = ROUTE_TIE * float(logits[t].max() - logits[t].min())
+                for e in theirs ^ mine:
+                    if abs(float(logits[t, e]) - kth) > tie:
+                        raise AssertionError(f"router: engine chose {sorted(theirs)}, oracle {sorted(mine)}; "
+                                             f"expert {e} is {float(logits[t, e]) - kth:+.4f} from the k-th logit "
+                                             f"(tie band {tie:.4f})")
+                chosen = np.array(sorted(theirs, key=lambda e: (-logits[t, e], e)))
+                order[t] = chosen
+                self.arbitrated += 1
         top = np.take_along_axis(logits, order, axis=1)
         ex = np.exp(top - top[:, :1])
         wts = ex / ex.sum(1, keepdims=True)
@@ -280,8 +331,9 @@ class CpuDecoder:
         cache = self.cache.setdefault(rid, [(torch.zeros(0, G, D), torch.zeros(0, G, D)) for _ in range(self.L)])
         pos = torch.arange(start, start + T)
         x = self.embed[torch.tensor(ids, dtype=torch.long)]
+        hints = self.route_hints.take(rid, start, ids) if self.route_hints is not None else None
         for i, w in self.iter_layers():
-            x, cache[i] = self.layer_forward(w, x, pos, start, cache[i])
+            x, cache[i] = self.layer_forward(w, x, pos, start, cache[i], hints[i] if hints else None)
         sel = x[torch.tensor(rows, dtype=torch.long)]
         return r(self._norm(sel, self.fn)) @ self.head.T
 

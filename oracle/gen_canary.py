@@ -12,7 +12,7 @@ the product's seeded generator on cuda, copied to the host, upcast to fp32, and 
 forward runs on the CPU, one layer at a time (`stream=True`: no layer stays resident, so
 Qwen3-32B fits host memory). Run on the GPU box; the .npz it writes is committed:
 
-    python -m oracle.gen_canary llama3-8b qwen3-32b
+    python -m oracle.gen_canary llama3-8b qwen3-32b gpt-oss-120b
 """
 
 from __future__ import annotations
@@ -44,6 +44,27 @@ def gpu_drawn_source(seed: int = 0):
     return src
 
 
+def gpu_expert_source(shape, seed: int = 0):
+    """MoE experts drawn like the engine's (product generator on cuda, bf16), put through the
+    oracle's own MXFP4 restatement (cpu_decoder.mxfp4_roundtrip, on the device for speed), fp32
+    on the host."""
+    from paper_2512_15834_b200.runtime.weights import draw
+
+    from .cpu_decoder import mxfp4_roundtrip
+
+    d, f = shape.d_model, shape.d_ff
+
+    def src(layer, e):
+        p = f"l{layer}.e{e}."
+        wg = mxfp4_roundtrip(draw((2 * f, d), seed, p + "w_gate_up", device="cuda").float()).cpu()
+        wd = mxfp4_roundtrip(draw((d, f), seed, p + "w_down", device="cuda").float()).cpu()
+        bg = draw((2 * f,), seed, p + "b_gate_up", device="cuda").float().cpu()
+        bd = draw((d,), seed, p + "b_down", device="cuda").float().cpu()
+        return wg, bg, wd, bd
+
+    return src
+
+
 def main(names: list[str]) -> None:
     from paper_2512_15834_b200.modelcfg import SHAPES
 
@@ -51,7 +72,8 @@ def main(names: list[str]) -> None:
     for name in names:
         shape = SHAPES[name]
         t0 = time.time()
-        dec = CpuDecoder(shape, source=gpu_drawn_source(0), stream=True)
+        dec = CpuDecoder(shape, source=gpu_drawn_source(0), stream=True,
+                         expert_source=gpu_expert_source(shape) if shape.moe else None)
         ids = canary_ids(shape.vocab)
         logits = dec.forward("canary", ids, 0, [len(ids) - 1])[0]
         dec.bf16_points = True  # same fp32 arithmetic, bf16 rounding where the engine stores bf16

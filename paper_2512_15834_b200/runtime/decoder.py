@@ -298,7 +298,7 @@ class Decoder:
         # per-layer expert offsets to pinned memory (4 buffers: eager / graph x 2 flight parities)
         self._moe_host = None
         self._moe_flip = 0
-        self._moe_buf = 0
+        self.route_log: list | None = None  # debug / parity: per layer, the step's expert ids [T*k] (device)
 
     # -- buffers ----------------------------------------------------------------
 
@@ -616,6 +616,8 @@ class Decoder:
                        E * d * 2 + T * d * 2 + T * E * 4 if T <= 128 else 2 * T * E * d)
             call("stb_moe_route", _p(self.rlog), self.rlog.stride(0), _p(w[f"l{i}.router_b"]), T, E, k,
                  _p(self.m_counts), _p(self.m_expert), _p(self.m_rank), _p(self.m_wt), st)
+            if self.route_log is not None:
+                self.route_log.append(self.m_expert[:rows].clone())
             offs = self.m_offs[i]
             call("stb_moe_gather", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
                  _p(self.m_rank), _p(offs), _p(self.m_perm), _p(self.m_x), st)

@@ -101,7 +101,7 @@ class Decode:
 
 class Flight:
     __slots__ = ("batch", "decodes", "runs", "event", "host", "n_sampled", "n_verify", "logits", "raw", "finished",
-                 "timers")
+                 "timers", "routes")
 
 
 class Runtime:
@@ -220,7 +220,7 @@ class Runtime:
         self.pool.release(scratch)
         self._free_slots.insert(0, scratch)
 
-    def probe_logits(self, ids: list[int], taps: list | None = None) -> torch.Tensor:
+    def probe_logits(self, ids: list[int], taps: list | None = None, routes: list | None = None) -> torch.Tensor:
         """Self-check (the bench's canary): prefill `ids` at positions 0.. on a scratch slot
         and return the fp32 logits of the last row (host). Leaves no state behind. `taps` (a
         list) receives the residual stream [n, d] (fp32, host) after the embedding and after
@@ -238,13 +238,16 @@ class Runtime:
             keep = self.dec.keep_logits
             self.dec.keep_logits = True
             self.dec.taps = [] if taps is not None else None
+            self.dec.route_log = [] if routes is not None else None
             try:
                 self.dec.forward(batch)
                 torch.cuda.synchronize()
             finally:
                 if taps is not None:
                     taps.extend(t.float().cpu() for t in self.dec.taps)
-                self.dec.taps = None
+                if routes is not None and self.dec.route_log:
+                    routes.extend(r.view(n, -1).cpu().numpy() for r in self.dec.route_log)
+                self.dec.taps = self.dec.route_log = None
             out = self.dec.last_logits[0].float().cpu()
             self.dec.keep_logits = keep
             self.dec.collect()
@@ -427,6 +430,7 @@ class Runtime:
             self._reserve(d.slot, r.start + len(r.ids))
         batch = self._build(decodes, runs)
         self.dec.keep_logits = self.record
+        self.dec.route_log = [] if (self.record and self.shape.moe) else None
         k = self._flip
         self._flip ^= 1
         if self._host_ev[k] is not None:  # the pinned buffers of two flights ago are free again
@@ -447,6 +451,7 @@ class Runtime:
         f.timers = (self.dec.take_pending(), self.dec.timers)
         f.logits = self.dec.last_logits if self.record else None
         f.raw = self.dec.last_raw_argmax if self.record else None
+        f.routes, self.dec.route_log = self.dec.route_log, None
         self.h2d_bytes += self.dec.h2d_bytes
         self.d2h_bytes += 4 * (R + 3 * nv)
         self.forwards += 1
@@ -522,8 +527,10 @@ class Runtime:
                 off += len(r.ids)
             slots = {j.seq.rid: j.seq.dev.slot for j in f.decodes}
             slots.update({r.seq.rid: r.seq.dev.slot for r in f.runs})
+            # MoE: each layer's expert ids [T, k] of the step (row order = the items' order)
+            routes = [r.view(b.T, -1).cpu().numpy() for r in f.routes] if f.routes else None
             self.flights.append({"items": items, "logits": logits, "raw": raw, "sampled": list(sampled),
-                                 "pool_ops": len(self.pool.log), "slots": slots,
+                                 "pool_ops": len(self.pool.log), "slots": slots, "routes": routes,
                                  "tables": {rid: self.pool.blocks(sl) for rid, sl in slots.items()}})
             for i in range(R):
                 row = int(b.sample_rows[i])

@@ -67,7 +67,11 @@ def test_batch_runtime_parity(name):
     big = name.startswith("llama")
     rt, engine = _run_fleet(shape, agents=10 if big else 12, steps=140 if big else 260)
     ora = CpuDecoder(shape)
-    ora.bf16_points = shape.moe  # MoE: storage rounding as on the engine (router near-ties)
+    if shape.moe:  # storage rounding as on the engine; the engine's choice on router near-ties only
+        from oracle.cpu_decoder import RouteHints
+
+        ora.bf16_points = True
+        ora.route_hints = RouteHints().add_flights(rt.flights)
     alloc = LifoAllocator(4096)
     ops = rt.pool.log
     op_i = 0
@@ -98,6 +102,7 @@ def test_batch_runtime_parity(name):
         for rid, slot in f["slots"].items():
             assert alloc.blocks(slot) == f["tables"][rid], (rid, slot)
     assert worst <= LOGIT_RTOL, worst
+    assert ora.arbitrated <= max(2, 0.03 * ora.routed), (ora.arbitrated, ora.routed)
     fates = [x for s in engine.sequences.values() for x in s.fates]
     # the trace really exercised the packed mixed path
     assert len(rt.flights) >= 100 and rows_checked >= 500

@@ -25,7 +25,7 @@ def test_full_size_canary(name):
     import torch
 
     from oracle.cpu_decoder import CpuDecoder
-    from oracle.gen_canary import gpu_drawn_source
+    from oracle.gen_canary import gpu_drawn_source, gpu_expert_source
     from oracle.ids import SALT_PROMPT, fill
     from paper_2512_15834_b200.modelcfg import SHAPES as ALL
     from paper_2512_15834_b200.runtime.executor import EagerRuntime
@@ -36,7 +36,8 @@ def test_full_size_canary(name):
     assert ids == g["ids"].tolist()
     rt = EagerRuntime(shape, init_device="cuda", num_blocks=256, max_slots=8, max_ctx=4096)
     taps: list = []
-    got = rt.probe_logits(ids, taps=taps).numpy().astype(np.float64)
+    routes: list = []
+    got = rt.probe_logits(ids, taps=taps, routes=routes).numpy().astype(np.float64)
     del rt
     torch.cuda.empty_cache()
     from bench import canary_compare
@@ -45,13 +46,16 @@ def test_full_size_canary(name):
     assert res["status"] == "pass", res
 
     assert len(taps) == shape.layers + 1
-    dec = CpuDecoder(shape, source=gpu_drawn_source(0), stream=True)
+    dec = CpuDecoder(shape, source=gpu_drawn_source(0), stream=True,
+                     expert_source=gpu_expert_source(shape) if shape.moe else None)
+    dec.bf16_points = shape.moe  # MoE: bf16 storage rounding as on the engine (router near-ties)
     pos = torch.arange(len(ids))
     G, D = shape.n_kv, shape.d_head
     errs = []
     for i, w in dec.iter_layers():
         x_in = taps[i]
-        ref, _ = dec.layer_forward(w, x_in, pos, 0, (torch.zeros(0, G, D), torch.zeros(0, G, D)))
+        ref, _ = dec.layer_forward(w, x_in, pos, 0, (torch.zeros(0, G, D), torch.zeros(0, G, D)),
+                                   hint=routes[i] if routes else None)
         d_ref, d_got = ref - x_in, taps[i + 1] - x_in
         errs.append(float((d_got - d_ref).norm() / d_ref.norm()))
     head = (dec._norm(taps[-1][-1:], dec.fn) @ dec.head.T)[0].double().numpy()
