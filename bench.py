@@ -131,10 +131,33 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if os.environ.get("BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+        if os.environ.get("BENCH_BACKEND", "nccl") == "nccl":
+            # communicator init lines in the log (one per rank), each rank bound to its own GPU
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch the N replica processes ourselves (one per GPU,
+    torch.distributed.run on 127.0.0.1) and return their exit code; rank 0 prints the line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    print(f"bench: launching {args.gpus} replica ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 def reduce(values: list[float], op: str, world: int, device) -> list[float]:
@@ -672,7 +695,13 @@ def main():
         import faulthandler
 
         faulthandler.dump_traceback_later(args.watchdog_s, exit=True)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world, rank, local = dist_setup()
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but {world} ranks were launched; refusing to report n_gpus wrongly",
+              file=sys.stderr)
+        sys.exit(2)
     resolve(args, world)
     if args.impl == "reference":
         run_reference(args, world, rank)

@@ -40,6 +40,7 @@ import torch
 from ..modelcfg import ModelShape
 from . import lib
 
+_NVTX = os.environ.get("STB200_NVTX", "1") != "0"  # one NVTX range per packed step (the phase marks: engine._log)
 FORCE_BIAS = 1.0e4  # >> any logit spread of the random-init models (|logit| < 10)
 # timing experiments only: comma-separated C-ABI entry points the step does not launch
 # (outputs are garbage; tools/profile_step.py uses it to attribute in-step time under PDL)
@@ -383,6 +384,15 @@ class Decoder:
 
     def forward(self, b: StepBatch) -> torch.Tensor:
         """Run one packed step; returns the sampled ids [R] (device int32)."""
+        if _NVTX:
+            torch.cuda.nvtx.range_push(f"step T={b.T} decode={b.B_dec} runs={b.S}")
+        try:
+            return self._forward(b)
+        finally:
+            if _NVTX:
+                torch.cuda.nvtx.range_pop()
+
+    def _forward(self, b: StepBatch) -> torch.Tensor:
         T, R, B, S = b.T, b.R, b.B_dec, b.S
         self._ensure(T, R, B)
         stream = torch.cuda.current_stream().cuda_stream
