@@ -22,7 +22,7 @@ from __future__ import annotations
 from paper_2512_15834_b200.domain import TokenKind, canonical_key, extract_tool_call
 from paper_2512_15834_b200.errors import ConfigError, InvalidScenario
 
-from .ids import SALT_OUTPUT, SALT_PROMPT, Interner, fill
+from .ids import SALT_OUTPUT, SALT_PROMPT, Interner, fill, text_ids
 from .kv_alloc import LifoAllocator
 
 
@@ -180,11 +180,11 @@ class OracleEngine:
         self._blocks(seq, "validate")
         return acc, consume
 
-    def _c_ingest(self, seq, n_out, nxt):
+    def _c_ingest(self, seq, n_out, nxt, text=None):
         if seq.pend is None and n_out == 0:
             self._unfeed_last(seq)
         lead = [seq.pend] if seq.pend is not None else []
-        out = fill(self.seed, seq.rid, SALT_OUTPUT, seq.rows + len(lead), n_out, self.vocab)
+        out = text_ids(self.seed, seq.rid, text, seq.rows + len(lead), n_out, self.vocab)
         inp = lead + out
         (tok,) = self._fwd(seq, inp, seq.rows, [len(inp) - 1], [self._first(seq, nxt)])
         seq.pend, seq.counted = tok, False
@@ -307,7 +307,7 @@ class OracleEngine:
             seq.fates.append("full_hit")
         else:
             seq.fates.append("partial_hit")
-        self._c_ingest(seq, hit.output_tokens, seq.turn + 1)
+        self._c_ingest(seq, hit.output_tokens, seq.turn + 1, hit.output)
 
         def ingested():
             self._log(seq, "ingest", hit.output_tokens)

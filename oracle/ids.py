@@ -1,13 +1,15 @@
 """ORACLE (test infrastructure). Token-id rules, restated independently of
 paper_2512_15834_b200/tokens.py: ids 0/1/2 = TOOL_START/TOOL_END/EOS, other
 tokens numbered in first-interned order; uncounted content (prompt / tool
-output) ids = 3 + splitmix64(seed, fnv1a64(rid), salt, position) mod (V - 3).
+output) ids = 3 + splitmix64(seed, fnv1a64(rid), salt, position) mod (V - 3); an
+in-place-ingested tool output with text: token i = 3 + splitmix64(fnv1a64(bytes 4i..4i+3) ^
+seed << 32 ^ 3) mod (V - 3) for the ceil(bytes / 4) chunks, the fill rule past them.
 """
 
 from __future__ import annotations
 
 MASK = (1 << 64) - 1
-SALT_PROMPT, SALT_OUTPUT = 1, 2
+SALT_PROMPT, SALT_OUTPUT, SALT_TEXT = 1, 2, 3
 
 
 class Interner:
@@ -66,3 +68,16 @@ def _mix(x: int) -> int:
 def fill(seed: int, rid: str, salt: int, start: int, n: int, vocab: int) -> list[int]:
     base = _fnv(rid) ^ ((seed & 0xFFFFFFFF) << 32) ^ salt
     return [3 + _mix(base ^ ((p * 0x2545F4914F6CDD1D) & MASK)) % (vocab - 3) for p in range(start, start + n)]
+
+
+def text_ids(seed: int, rid: str, text, start: int, n: int, vocab: int) -> list[int]:
+    out = fill(seed, rid, SALT_OUTPUT, start, n, vocab)
+    if not text:
+        return out
+    raw = text.encode("utf-8")
+    for i in range(min(n, (len(raw) + 3) // 4)):
+        h = 0xCBF29CE484222325
+        for b in raw[4 * i:4 * i + 4]:
+            h = ((h ^ b) * 0x100000001B3) & MASK
+        out[i] = 3 + _mix(h ^ ((seed & 0xFFFFFFFF) << 32) ^ SALT_TEXT) % (vocab - 3)
+    return out

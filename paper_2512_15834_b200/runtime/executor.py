@@ -43,7 +43,7 @@ import torch
 
 from ..errors import ConfigError, KernelError, KVCapacityError
 from ..modelcfg import TINY, ModelShape
-from ..tokens import SALT_OUTPUT, SALT_PROMPT, TokenTable, fill_ids
+from ..tokens import SALT_OUTPUT, SALT_PROMPT, TokenTable, fill_ids, output_ids
 from . import lib
 from . import weights as W
 from .decoder import Decoder, KVPool, StepBatch
@@ -337,14 +337,15 @@ class Runtime:
         self._submit_run(Run(seq, inputs, start, list(range(len(inputs))), targets, finish,
                              verify=(draft, len(span), len(lead), first)))
 
-    def ingest(self, seq, n_out: int, next_turn: int, done) -> None:
+    def ingest(self, seq, n_out: int, next_turn: int, done, output: str | None = None) -> None:
         d = seq.dev
         if d.pend is not None and not d.counted:
             raise KernelError(f"{seq.rid}: ingest with an unemitted sampled token")
         if d.pend is None and n_out == 0:
             self._recompute_last(seq)
         lead = [d.pend] if d.pend is not None else []
-        out = fill_ids(self.seed, seq.rid, SALT_OUTPUT, d.kv_len + len(lead), n_out, self.shape.vocab).tolist()
+        # the output's own text becomes its token ids (tokens.output_ids)
+        out = output_ids(self.seed, seq.rid, output, d.kv_len + len(lead), n_out, self.shape.vocab).tolist()
         inputs = lead + out
         target = _turn_first(seq, next_turn, self.table)
 

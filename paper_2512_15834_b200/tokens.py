@@ -17,6 +17,10 @@ The reference compares `Token(kind, text)` objects (`domain.py:29-32`,
 Content the reference only counts — prompt tokens, tool-output tokens — gets
 deterministic pseudo-random ids from `fill_ids(seed, rid, salt, start, n)`:
 splitmix64 over (seed, fnv1a(rid), salt, position), mapped into [3, vocab).
+A cached / speculated tool output that is ingested in place carries its text
+(`CacheEntry.output`): its ids come from the text itself (`output_ids`: one
+token per 4 UTF-8 bytes, the reference's `token_estimate`, domain.py:245-247),
+so different outputs put different rows into the KV cache.
 The oracle restates both rules independently (`oracle/ids.py`).
 """
 
@@ -30,6 +34,7 @@ from .errors import ConfigError
 RESERVED = 3
 SALT_PROMPT = 1
 SALT_OUTPUT = 2
+SALT_TEXT = 3
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -116,3 +121,28 @@ def fill_ids(seed: int, rid: str, salt: int, start: int, n: int, vocab: int) -> 
         pos = np.arange(start, start + n, dtype=np.uint64)
         h = _splitmix(base ^ (pos * np.uint64(0x2545F4914F6CDD1D)) & _M64)
     return (np.uint64(RESERVED) + h % np.uint64(vocab - RESERVED)).astype(np.int32)
+
+
+def output_ids(seed: int, rid: str, text: str | None, start: int, n: int, vocab: int) -> np.ndarray:
+    """Ids of an ingested tool output of n tokens at positions [start, start+n): token i is the
+    i-th 4-byte chunk of the output's UTF-8 bytes (ceil(bytes / 4) tokens, the reference's
+    `token_estimate`, domain.py:245-247), id = 3 + splitmix64(fnv1a64(chunk) ^ seed << 32 ^
+    SALT_TEXT) mod (V - 3): a text-only function, like a tokenizer. Tokens past the text (an
+    entry whose output_tokens exceeds its text, or no text) are `fill_ids(..., SALT_OUTPUT)`."""
+    out = fill_ids(seed, rid, SALT_OUTPUT, start, n, vocab)
+    if not text or n <= 0:
+        return out
+    raw = text.encode("utf-8")
+    m = min(n, -(-len(raw) // 4))
+    with np.errstate(over="ignore"):
+        h = np.array([fnv1a64_bytes(raw[4 * i:4 * i + 4]) for i in range(m)], dtype=np.uint64)
+        h = _splitmix(h ^ (np.uint64(seed & 0xFFFFFFFF) << np.uint64(32)) ^ np.uint64(SALT_TEXT))
+    out[:m] = (np.uint64(RESERVED) + h % np.uint64(vocab - RESERVED)).astype(np.int32)
+    return out
+
+
+def fnv1a64_bytes(data: bytes) -> int:
+    h = 0xCBF29CE484222325
+    for b in data:
+        h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h

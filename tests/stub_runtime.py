@@ -44,7 +44,7 @@ class StubRuntime:
         self.calls.append(("verify", seq.rid, acc))
         done((acc, len(s) if acc >= len(s) else acc + 1))
 
-    def ingest(self, seq, n_out, next_turn, done):
+    def ingest(self, seq, n_out, next_turn, done, output=None):
         self.calls.append(("ingest", seq.rid, n_out))
         done(None)
 
