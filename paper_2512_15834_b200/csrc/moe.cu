@@ -33,8 +33,11 @@
 //   warp 0      producer: weight tile + token tile per stage (bulk copy + TMA), STAGES ring
 //   warp 1      MMA issuer (one thread): 4 x tcgen05.mma kind::f16 per stage, A from TMEM
 //   warp 2      TMEM allocator
-//   warps 4-7   converters: smem codes -> fp16 -> TMEM A ring (lane quarter = warp & 3)
-//   warps 8-11  epilogue: TMEM accumulator (double-buffered) -> SwiGLU / bias -> global
+//   warps 4-11  converters: smem codes -> fp16 -> TMEM A ring (lane quarter = warp & 3); two
+//               warps per quarter take alternate stages, so a stage's unpack, TMEM store and
+//               store wait overlap the next stage's (one warp per quarter paced the kernel at
+//               0.38 of HBM on the C4 decode step)
+//   warps 12-15 epilogue: TMEM accumulator (double-buffered) -> SwiGLU / bias -> global
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
@@ -55,7 +58,8 @@ constexpr int kMaxK = 8;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int RAW = 4352;  // one MXFP4 tile: 128 rows x 32 code bytes + 128 rows x 2 scale bytes
-constexpr int kThreads = 384;
+constexpr int kConvWarps = 8;  // two converter warps per TMEM lane quarter, on alternating stages
+constexpr int kThreads = 32 * (4 + kConvWarps + 4);
 constexpr int A_COL0 = 128;  // TMEM: accumulators in [0, 2 BN), the A ring from column 128
 constexpr int A_STAGES = 8;  // 8 x 32 columns of fp16x2 (64 K values x 128 rows each)
 
@@ -394,13 +398,15 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
       }
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 8) {
-    // converters: thread = weight row r of the tile = TMEM lane r
-    const int q = warp & 3, r = q * 32 + lane;
+  } else if (warp >= 4 && warp < 4 + kConvWarps) {
+    // converters: thread = weight row r of the tile = TMEM lane r; this warp takes the stages
+    // i with i % 2 == par
+    const int q = warp & 3, r = q * 32 + lane, par = (warp - 4) >> 2;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int i = 0;
     for (int it = blockIdx.x; it < total; it += gridDim.x) {
       for (int kb = 0; kb < KB; ++kb, ++i) {
+        if ((i & 1) != par) continue;
         const int s = i % STAGES, as = i % A_STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
         const uint8_t* raw = sw + s * RAW;
@@ -425,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
         if (lane == 0) mbar_arrive(&a_full[as]);
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4 + kConvWarps) {
     // epilogue: thread = weight row (feature) of the tile; columns = tokens
     const int q = warp & 3;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
