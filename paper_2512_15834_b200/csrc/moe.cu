@@ -30,18 +30,24 @@
 // ring; the MMA reads A from TMEM and the fp16 token rows (B) from smem. So shared memory
 // carries 4.25 KB of weight bytes per stage instead of 16 KB of dequantised tiles written and
 // read again — the MoE is HBM-bound on the weights at every batch the engine runs.
-//   warp 0      producer: weight tile + token tile per stage (bulk copy + TMA), STAGES ring
+//   warp 0      weight producer: per stage the item's two 128-row tiles of one K block (a
+//               work item is 256 weight rows sharing one token tile: twice the bytes per
+//               pipeline stage, half the token-tile loads), into a ring the converters free
+//               as soon as the tiles are in their registers
+//   warp 3      token producer: the expert's fp16 token rows per stage (TMA, L2-resident), a
+//               ring the MMA frees
 //   warp 1      MMA issuer (one thread): 4 x tcgen05.mma kind::f16 per stage, A from TMEM
 //   warp 2      TMEM allocator
-//   warps 4-11  converters: smem codes -> fp16 -> TMEM A ring (lane quarter = warp & 3); two
-//               warps per quarter take alternate stages, so a stage's unpack, TMEM store and
-//               store wait overlap the next stage's (one warp per quarter paced the kernel at
-//               0.38 of HBM on the C4 decode step)
+//   warps 4-11  converters: smem codes -> fp16 -> TMEM A ring, one warp per (tile, lane
+//               quarter = warp & 3); per-stage fixed latencies (smem loads, the TMEM store wait,
+//               barrier hand-offs) are what paced the single-tile version (0.51 of HBM at the
+//               C4 decode shape), so each stage now carries two tiles' worth of bytes
 //   warps 12-15 epilogue: TMEM accumulator (double-buffered) -> SwiGLU / bias -> global
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -58,20 +64,61 @@ constexpr int kMaxK = 8;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int RAW = 4352;  // one MXFP4 tile: 128 rows x 32 code bytes + 128 rows x 2 scale bytes
-constexpr int kConvWarps = 8;  // two converter warps per TMEM lane quarter, on alternating stages
+#ifndef STB_MOE_NTP
+#define STB_MOE_NTP 2
+#endif
+constexpr int NTP = STB_MOE_NTP;  // weight tiles (of 128 rows) per work item: a 256-row item shares
+                                  // one token tile and doubles the bytes every pipeline stage carries
+#ifndef STB_MOE_CONV_PAR
+#define STB_MOE_CONV_PAR 2
+#endif
+constexpr int CPAR = STB_MOE_CONV_PAR;  // converter warps per (tile, lane quarter), on alternating stages
+constexpr int kConvWarps = 4 * NTP * CPAR;
 constexpr int kThreads = 32 * (4 + kConvWarps + 4);
-constexpr int A_COL0 = 128;  // TMEM: accumulators in [0, 2 BN), the A ring from column 128
-constexpr int A_STAGES = 8;  // 8 x 32 columns of fp16x2 (64 K values x 128 rows each)
+// TMEM: accumulators [buffer][tile][BN] in [0, 2 NTP BN), then the A ring: stages of NTP x 32
+// columns of fp16x2 (64 K values x 128 rows per tile), as many as fit (at most 8)
+template <int BN>
+constexpr int a_col0() { return 2 * NTP * BN; }
+template <int BN>
+constexpr int a_stages() { return std::min(8, (512 - a_col0<BN>()) / (32 * NTP)); }
 
 template <int BN>
 struct MCfg {
   static constexpr int X_BYTES = BN * BK * 2;  // fp16 token rows of one K block, SW128 K-major
+  static constexpr int XS = 8;                 // token-tile ring (L2-resident rows, freed by the MMA)
 #ifndef STB_MOE_RING_KB
 #define STB_MOE_RING_KB 196
 #endif
-  static constexpr int STAGES = std::min(24, (STB_MOE_RING_KB * 1024) / (RAW + X_BYTES));
-  static constexpr int SMEM = 1024 + STAGES * (X_BYTES + RAW) + 1024;
+  // weight-tile ring: freed by the converters as soon as they have read a tile, so the bytes in
+  // flight from HBM never wait behind the dequantise -> MMA pipeline
+  static constexpr int WS = std::min(24, (STB_MOE_RING_KB * 1024 - XS * X_BYTES) / (NTP * RAW));
+  static constexpr int SMEM = 1024 + XS * X_BYTES + WS * NTP * RAW + 1024;
 };
+
+// mbarrier wait that lets the hardware suspend the thread until the phase completes (long waits:
+// the epilogue warps, whose spinning otherwise steals issue slots from the converters)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -287,16 +334,20 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __grid_constant__ CUtensorMap tm_x,
                                                                      const MoeArgs a) {
   using CF = MCfg<BN>;
-  constexpr int STAGES = CF::STAGES;
+  constexpr int XS = CF::XS, WS = CF::WS;
+  constexpr int WSTAGE = NTP * RAW;
+  constexpr int A_COL0 = a_col0<BN>(), A_STAGES = a_stages<BN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sx = smem;                              // [STAGES][X_BYTES], 1024-aligned (SW128)
-  uint8_t* sw = sx + STAGES * CF::X_BYTES;         // [STAGES][RAW]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sw + STAGES * RAW);
-  uint64_t* empty = full + STAGES;
-  uint64_t* a_full = empty + STAGES;               // [A_STAGES]
-  uint64_t* a_empty = a_full + A_STAGES;           // [A_STAGES]
-  uint64_t* acc_full = a_empty + A_STAGES;         // [2]
+  uint8_t* sx = smem;                              // [XS][X_BYTES], 1024-aligned (SW128)
+  uint8_t* sw = sx + XS * CF::X_BYTES;             // [WS][NTP][RAW]
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(sw + WS * WSTAGE);
+  uint64_t* w_empty = w_full + WS;                 // converters -> weight producer
+  uint64_t* x_full = w_empty + WS;
+  uint64_t* x_empty = x_full + XS;                 // MMA -> token producer
+  uint64_t* a_full = x_empty + XS;                 // [A_STAGES] converters -> MMA
+  uint64_t* a_empty = a_full + 8;                  // [A_STAGES] MMA -> converters
+  uint64_t* acc_full = a_empty + 8;                // [2]
   uint64_t* acc_empty = acc_full + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   __shared__ int s_off[kMaxE + 1];                 // token-row offset of each expert
@@ -304,15 +355,19 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
   __shared__ int s_cnt[kMaxE];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int E = a.E, NT = ceil_div(a.N, BM), KB = a.K / BK;
+  const int E = a.E, NT = ceil_div(a.N, BM), NP = ceil_div(NT, NTP), KB = a.K / BK;
   if (threadIdx.x == 0) {
     tma_prefetch(&tm_x);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < WS; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 4 * NTP);  // the stage's converter warps (one per tile x quarter)
+    }
+    for (int s = 0; s < XS; ++s) {
+      mbar_init(&x_full[s], 1);
+      mbar_init(&x_empty[s], 1);
     }
     for (int s = 0; s < A_STAGES; ++s) {
-      mbar_init(&a_full[s], 4);  // one arrive per converter warp
+      mbar_init(&a_full[s], 4 * NTP);
       mbar_init(&a_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -323,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   pdl_wait();  // counts (route) and token rows (gather) come from the preceding kernels
-  // work list: items of expert e = ceil(count_e / BN) token tiles x NT weight tiles
+  // work list: items of expert e = ceil(count_e / BN) token tiles x NP pairs of weight tiles
   block_prefix(a.counts, E, s_off);
   if (threadIdx.x < kMaxE) s_cnt[threadIdx.x] = threadIdx.x < E ? s_off[threadIdx.x + 1] - s_off[threadIdx.x] : 0;
   __syncthreads();
@@ -331,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
     int run = 0;
     for (int e = 0; e < E; ++e) {
       s_item[e] = run;
-      run += ceil_div(s_cnt[e], BN) * NT;
+      run += ceil_div(s_cnt[e], BN) * NP;
     }
     s_item[E] = run;
   }
@@ -341,7 +396,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
   pdl_launch();
   const uint32_t tmem = *tmem_slot;
   const int total = s_item[E];
-  auto decode = [&](int it, int& e, int& nt, int& m) {
+  // item -> (expert, first weight tile, token tile); m fastest: the token tiles that share a
+  // weight slice run on neighbouring CTAs at the same time (the slice is read from HBM once)
+  auto decode = [&](int it, int& e, int& nt0, int& m) {
     int lo = 0, hi = E - 1;  // last e with s_item[e] <= it (experts with no items are skipped)
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -350,24 +407,43 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
     e = lo;
     const int mt = ceil_div(s_cnt[e], BN);
     const int local = it - s_item[e];
-    nt = local / mt;
-    m = local - nt * mt;
+    const int p = local / mt;
+    m = local - p * mt;
+    nt0 = p * NTP;
   };
 
   if (warp == 0) {
+    // weight producer: the item's NTP tiles of one K block per stage (one bulk copy each)
     if (elect_one()) {
       int i = 0;
       for (int it = blockIdx.x; it < total; it += gridDim.x) {
-        int e, nt, m;
-        decode(it, e, nt, m);
-        const uint8_t* wt = a.w + ((int64_t)e * NT + nt) * KB * RAW;
+        int e, nt0, m;
+        decode(it, e, nt0, m);
+        const int nt_n = min(NTP, NT - nt0);
+        const uint8_t* wt = a.w + ((int64_t)e * NT + nt0) * KB * RAW;
+        for (int kb = 0; kb < KB; ++kb, ++i) {
+          const int s = i % WS;
+          mbar_wait(&w_empty[s], ((i / WS) & 1) ^ 1);
+          mbar_expect_tx(&w_full[s], nt_n * RAW);
+          for (int t = 0; t < nt_n; ++t)
+            bulk_load(smem_u32(sw + s * WSTAGE + t * RAW), wt + ((int64_t)t * KB + kb) * RAW, RAW, &w_full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // token producer: the expert's BN fp16 rows of each K block (TMA, L2-resident)
+    if (elect_one()) {
+      int i = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x) {
+        int e, nt0, m;
+        decode(it, e, nt0, m);
         const int xrow = s_off[e] + m * BN;
         for (int kb = 0; kb < KB; ++kb, ++i) {
-          const int s = i % STAGES;
-          mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-          mbar_expect_tx(&full[s], RAW + CF::X_BYTES);
-          bulk_load(smem_u32(sw + s * RAW), wt + (int64_t)kb * RAW, RAW, &full[s]);
-          tma_load_2d(sx + s * CF::X_BYTES, &tm_x, &full[s], kb * BK, xrow);
+          const int s = i % XS;
+          mbar_wait(&x_empty[s], ((i / XS) & 1) ^ 1);
+          mbar_expect_tx(&x_full[s], CF::X_BYTES);
+          tma_load_2d(sx + s * CF::X_BYTES, &tm_x, &x_full[s], kb * BK, xrow);
         }
       }
     }
@@ -375,23 +451,31 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_f16(BM, BN);
+#ifndef STB_MOE_MMA_PER_STAGE
+#define STB_MOE_MMA_PER_STAGE (BK / 16)  // < 4: timing experiments only (results are wrong)
+#endif
       int i = 0, j = 0;
       for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
+        int e, nt0, m;
+        decode(it, e, nt0, m);
+        const int nt_n = min(NTP, NT - nt0);
         const int buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + buf * BN;
         for (int kb = 0; kb < KB; ++kb, ++i) {
-          const int s = i % STAGES, as = i % A_STAGES;
-          mbar_wait(&full[s], (i / STAGES) & 1);        // token rows landed (TMA)
-          mbar_wait(&a_full[as], (i / A_STAGES) & 1);   // weights dequantised into TMEM
+          const int xs = i % XS, as = i % A_STAGES;
+          mbar_wait(&x_full[xs], (i / XS) & 1);        // token rows landed (TMA)
+          mbar_wait(&a_full[as], (i / A_STAGES) & 1);  // weights dequantised into TMEM
           tc_fence_after();
-          const uint32_t xa = smem_u32(sx + s * CF::X_BYTES);
+          const uint64_t bdesc = umma_desc_kmajor_sw128(smem_u32(sx + xs * CF::X_BYTES), 1024);
+          for (int t = 0; t < nt_n; ++t) {
+            const uint32_t d = tmem + (buf * NTP + t) * BN;
+            const uint32_t acol = tmem + A_COL0 + (as * NTP + t) * 32;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            umma_f16_ts(d, tmem + A_COL0 + as * 32 + kk * 8, umma_desc_kmajor_sw128(xa + kk * 32, 1024), idesc,
-                        (kb > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&empty[s]);
+            for (int kk = 0; kk < STB_MOE_MMA_PER_STAGE; ++kk)  // +32 B along K = +2 in the descriptor
+              umma_f16_ts(d, acol + kk * 8, bdesc + 2 * kk, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&x_empty[xs]);
           umma_commit(&a_empty[as]);
         }
         umma_commit(&acc_full[buf]);
@@ -399,78 +483,99 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
     }
     __syncwarp();
   } else if (warp >= 4 && warp < 4 + kConvWarps) {
-    // converters: thread = weight row r of the tile = TMEM lane r; this warp takes the stages
-    // i with i % 2 == par
-    const int q = warp & 3, r = q * 32 + lane, par = (warp - 4) >> 2;
+    // converters: warp = (parity p, tile t, lane quarter q); thread = weight row r of tile t = TMEM
+    // lane r; the warp takes the stages i with i % CPAR == p
+    const int q = warp & 3, t = ((warp - 4) >> 2) % NTP, par = (warp - 4) / (4 * NTP), r = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t sw_u32 = smem_u32(sw);
     int i = 0;
     for (int it = blockIdx.x; it < total; it += gridDim.x) {
+      int e, nt0, m;
+      decode(it, e, nt0, m);
+      const bool live = nt0 + t < NT;  // the last pair of an odd tile count has one tile
       for (int kb = 0; kb < KB; ++kb, ++i) {
-        if ((i & 1) != par) continue;
-        const int s = i % STAGES, as = i % A_STAGES;
-        mbar_wait(&full[s], (i / STAGES) & 1);
-        const uint8_t* raw = sw + s * RAW;
-        const uint4 c0 = *reinterpret_cast<const uint4*>(raw + r * 32);
-        const uint4 c1 = *reinterpret_cast<const uint4*>(raw + r * 32 + 16);
-        const uint32_t sc = *reinterpret_cast<const uint16_t*>(raw + 4096 + r * 2);
-        // 2^(e) as fp16: exponent field e + 15 = byte - 127 + 15 (byte in [114, 139] by construction)
-        const uint32_t h0 = ((sc & 0xFFu) - 112u) << 10, h1 = ((sc >> 8) - 112u) << 10;
-        const uint32_t s0 = h0 | (h0 << 16), s1 = h1 | (h1 << 16);
-        const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        if (i % CPAR != par) continue;
+        const int s = i % WS, as = i % A_STAGES;
+        mbar_wait(&w_full[s], (i / WS) & 1);
         uint32_t out[32];
+#ifdef STB_MOE_SKIP_CONVERT  // timing experiments only: stream the weights, convert nothing
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&w_empty[s]);
+        mbar_wait(&a_empty[as], ((i / A_STAGES) & 1) ^ 1);
+        if (lane == 0) mbar_arrive(&a_full[as]);
+        continue;
+#endif
+        if (live) {
+          const uint32_t raw = sw_u32 + s * WSTAGE + t * RAW;
+          const uint4 c0 = lds128(raw + r * 32);
+          const uint4 c1 = lds128(raw + r * 32 + 16);
+          const uint32_t sc = lds16(raw + 4096 + r * 2);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&w_empty[s]);  // the tile is in registers: its slot may refill
+          // 2^(e) as fp16: exponent field e + 15 = byte - 127 + 15 (byte in [114, 139] by construction)
+          const uint32_t h0 = ((sc & 0xFFu) - 112u) << 10, h1 = ((sc >> 8) - 112u) << 10;
+          const uint32_t s0 = h0 | (h0 << 16), s1 = h1 | (h1 << 16);
+          const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const uint32_t scl = w < 4 ? s0 : s1;  // bytes 0-15: values 0-31 (scale 0), 16-31: scale 1
+          for (int w = 0; w < 8; ++w) {
+            const uint32_t scl = w < 4 ? s0 : s1;  // bytes 0-15: values 0-31 (scale 0), 16-31: scale 1
 #pragma unroll
-          for (int b = 0; b < 4; ++b) out[w * 4 + b] = hmul2(e2m1x2_to_f16x2(wv[w] >> (8 * b)), scl);
+            for (int b = 0; b < 4; ++b) out[w * 4 + b] = hmul2(e2m1x2_to_f16x2(wv[w] >> (8 * b)), scl);
+          }
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&w_empty[s]);
         }
         mbar_wait(&a_empty[as], ((i / A_STAGES) & 1) ^ 1);
         tc_fence_after();
-        tmem_st32_wait_fence(tmem + lane_addr + A_COL0 + as * 32, out);
+        if (live) tmem_st32_wait_fence(tmem + lane_addr + A_COL0 + (as * NTP + t) * 32, out);
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[as]);
       }
     }
   } else if (warp >= 4 + kConvWarps) {
-    // epilogue: thread = weight row (feature) of the tile; columns = tokens
+    // epilogue: thread = weight row (feature) of each of the item's tiles; columns = tokens
     const int q = warp & 3;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int j = 0;
     for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
-      int e, nt, m;
-      decode(it, e, nt, m);
+      int e, nt0, m;
+      decode(it, e, nt0, m);
+      const int nt_n = min(NTP, NT - nt0);
       const int buf = j & 1;
-      const int f = nt * BM + q * 32 + lane;
       const int row0 = s_off[e] + m * BN;
       const int nv = min(BN, s_cnt[e] - m * BN);
-      const float b = f < a.N ? __ldg(a.bias + (int64_t)e * a.N + f) : 0.f;
-      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
+      for (int t = 0; t < nt_n; ++t) {
+        const int f = (nt0 + t) * BM + q * 32 + lane;
+        const float b = f < a.N ? __ldg(a.bias + (int64_t)e * a.N + f) : 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t rr[16];
-        tmem_ld16(tmem + lane_addr + buf * BN + c, rr);
-        tmem_ld_wait();
-        if (a.kind == 2) {
-          float* y = reinterpret_cast<float*>(a.out);
-          if (f < a.N) {
+        for (int c = 0; c < BN; c += 16) {
+          uint32_t rr[16];
+          tmem_ld16(tmem + lane_addr + (buf * NTP + t) * BN + c, rr);
+          tmem_ld_wait();
+          if (a.kind == 2) {
+            float* y = reinterpret_cast<float*>(a.out);
+            if (f < a.N) {
 #pragma unroll
-            for (int t = 0; t < 16; ++t)
-              if (c + t < nv) y[(int64_t)(row0 + c + t) * a.ldo + f] = __uint_as_float(rr[t]) + b;
-          }
-        } else {
-          // (gate, up) of output feature f/2 in lanes (2i, 2i+1): the even lane emits tokens
-          // c..c+7 of the chunk, the odd lane c+8..c+15
-          __half* act = reinterpret_cast<__half*>(a.out);
-          const bool odd = lane & 1;
+              for (int u = 0; u < 16; ++u)
+                if (c + u < nv) y[(int64_t)(row0 + c + u) * a.ldo + f] = __uint_as_float(rr[u]) + b;
+            }
+          } else {
+            // (gate, up) of output feature f/2 in lanes (2i, 2i+1): the even lane emits tokens
+            // c..c+7 of the chunk, the odd lane c+8..c+15
+            __half* act = reinterpret_cast<__half*>(a.out);
+            const bool odd = lane & 1;
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float mine = __uint_as_float(odd ? rr[8 + t] : rr[t]) + b;
-            const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? rr[t] : rr[8 + t]) + b, 1);
-            // other holds the partner's value for MY token set: partner bias already added by it
-            const int tok = c + (odd ? 8 : 0) + t;
-            const float g = odd ? other : mine, u = odd ? mine : other;
-            if (f < a.N && tok < nv) act[(int64_t)(row0 + tok) * a.ldo + (f >> 1)] = __float2half_rn(gpt_oss_glu(g, u, a.limit));
+            for (int u = 0; u < 8; ++u) {
+              const float mine = __uint_as_float(odd ? rr[8 + u] : rr[u]) + b;
+              const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? rr[u] : rr[8 + u]) + b, 1);
+              const int tok = c + (odd ? 8 : 0) + u;
+              const float g = odd ? other : mine, up = odd ? mine : other;
+              if (f < a.N && tok < nv)
+                act[(int64_t)(row0 + tok) * a.ldo + (f >> 1)] = __float2half_rn(gpt_oss_glu(g, up, a.limit));
+            }
           }
         }
       }
@@ -581,10 +686,13 @@ int stb_moe_gemm_mxfp4(const void* xperm, int rows_cap, const void* wtiles, cons
   MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit};
   // token tile from the mean rows per expert: decode steps put ~T k / E <= a few rows on an
   // expert (BN 16); larger tiles only once experts hold tens of rows
-  const int avg = (rows + E - 1) / E;
+  // (a busy expert holds ~mean + 2 sqrt(mean) rows: one token tile should cover it, or its
+  // weights are streamed once per tile)
+  const double avg = (double)rows / E;
+  const double busy = avg + 2.0 * std::sqrt(avg);
   cudaStream_t st = (cudaStream_t)stream;
-  if (avg <= 16) return launch_moe_gemm<16>(xperm, rows_cap, a, st);
-  if (avg <= 32) return launch_moe_gemm<32>(xperm, rows_cap, a, st);
+  if (busy <= 16.0) return launch_moe_gemm<16>(xperm, rows_cap, a, st);
+  if (busy <= 32.0) return launch_moe_gemm<32>(xperm, rows_cap, a, st);
   return launch_moe_gemm<64>(xperm, rows_cap, a, st);
 }
 

@@ -60,6 +60,7 @@ class SeqDev:
     hist: list[int] = field(default_factory=list)  # id fed at each physical row
     replay: list[int] = field(default_factory=list)
     busy: bool = False                              # a run of this sequence is in flight
+    spilled: int = 0                                # rows dropped by a KV preemption (recomputed on restore)
 
     @property
     def kv_tokens(self) -> int:
@@ -593,6 +594,12 @@ class BatchRuntime(Runtime):
         self.runs: deque = deque()
         self.decodes: list[Decode] = []
         self.flight: Flight | None = None
+        # KV preemption (the pool is finite, the reference's is not: SPEC.md:521): decode jobs
+        # whose sequence was spilled to free blocks, restored FIFO by recomputing its rows
+        self.spilled: deque = deque()
+        self._in_step: set = set()  # slots of the step being packed (never preempted mid-launch)
+        self.spills = 0        # sequences preempted
+        self.deferred = 0      # steps that held a prefill / ingest run back for lack of blocks
 
     def _submit_run(self, run: Run) -> None:
         self.runs.append(run)
@@ -601,9 +608,10 @@ class BatchRuntime(Runtime):
         self.decodes.append(job)
 
     def busy(self) -> bool:
-        return bool(self.runs or self.decodes or self.flight is not None)
+        return bool(self.runs or self.decodes or self.spilled or self.flight is not None)
 
     def _pack(self):
+        self._restore()
         decodes = [j for j in self.decodes if not j.seq.dev.busy]
         budget = self.max_step_tokens - len(decodes)
         runs = []
@@ -611,7 +619,97 @@ class BatchRuntime(Runtime):
             r = self.runs.popleft()
             budget -= len(r.ids)
             runs.append(r)
+        free = self.pool.free_blocks()
+        if free < 2 * (len(decodes) + sum(-(-len(r.ids) // BLOCK) + 1 for r in runs)):  # cheap guard
+            decodes, runs = self._fit(decodes, runs, free)
         return decodes, runs
+
+    # -- KV pressure -------------------------------------------------------------
+
+    def _need(self, decodes, runs) -> int:
+        """Blocks the step adds: decode rows (+ the pending token the reference counts, H4) and
+        every run's rows, beyond what each slot already holds."""
+        need = 0
+        for j in decodes:
+            d = j.seq.dev
+            need += max(0, -(-(d.kv_len + 2) // BLOCK) - len(self.pool.blocks(d.slot)))
+        for r in runs:
+            d = r.seq.dev
+            need += max(0, -(-(r.start + len(r.ids) + 1) // BLOCK) - len(self.pool.blocks(d.slot)))
+        return need
+
+    def _fit(self, decodes, runs, free):
+        """Make the step fit the free blocks: drop retained prefixes (engine reclaimer), hold
+        prefill / ingest runs back (they wait in the queue), then preempt decoding sequences —
+        largest context first — whose rows are recomputed when blocks return (`_restore`)."""
+        need = self._need(decodes, runs)
+        if need <= free:
+            return decodes, runs
+        if self.reclaimer is not None and self.reclaimer():
+            free = self.pool.free_blocks()
+        while need > free and runs and (decodes or len(runs) > 1):
+            self.runs.appendleft(runs.pop())
+            self.deferred += 1
+            need = self._need(decodes, runs)
+        while need > free and len(decodes) + len(runs) > 1 and decodes:
+            victim = max(decodes, key=lambda j: j.seq.dev.kv_len)
+            decodes.remove(victim)
+            self._spill(victim)
+            free = self.pool.free_blocks()
+            need = self._need(decodes, runs)
+        if need > free:
+            raise KVCapacityError(f"KV pool exhausted: the step needs {need} blocks, {free} free, nothing left to "
+                                  "preempt")
+        return decodes, runs
+
+    def _reserve(self, slot: int, n: int) -> None:
+        """pool.reserve; under KV pressure drop retained prefixes, then preempt decoding sequences
+        outside the step being packed (largest context first) until the reservation fits."""
+        try:
+            self.pool.reserve(slot, n)
+            return
+        except KVCapacityError:
+            if self.reclaimer is not None and self.reclaimer():
+                try:
+                    self.pool.reserve(slot, n)
+                    return
+                except KVCapacityError:
+                    pass
+        while True:
+            cand = [j for j in self.decodes if j.seq.dev.slot != slot and j.seq.dev.slot not in self._in_step
+                    and not j.seq.dev.busy]
+            if not cand:
+                raise KVCapacityError(f"KV pool exhausted reserving {n} rows for slot {slot}; nothing to preempt")
+            self._spill(max(cand, key=lambda j: j.seq.dev.kv_len))
+            try:
+                self.pool.reserve(slot, n)
+                return
+            except KVCapacityError:
+                continue
+
+    def _spill(self, job: Decode) -> None:
+        d = job.seq.dev
+        d.spilled = d.kv_len
+        d.kv_len = 0
+        self.pool.release(d.slot)
+        self.decodes.remove(job)
+        self.spilled.append(job)
+        self.spills += 1
+
+    def _restore(self) -> None:
+        """Bring back the oldest preempted sequence once its rows (and some headroom for the
+        running batch) fit: one run recomputes its context, then its decode job resumes."""
+        if not self.spilled:
+            return
+        job = self.spilled[0]
+        d = job.seq.dev
+        need = -(-(d.spilled + 2) // BLOCK) + len(self.decodes) + 2
+        if self.pool.free_blocks() < need and (self.decodes or self.runs or self.flight is not None):
+            return
+        self.spilled.popleft()
+        ids = d.hist[:d.spilled]
+        d.spilled = 0
+        self.runs.appendleft(Run(job.seq, ids, 0, [len(ids) - 1], [-1], lambda _s, job=job: self.decodes.append(job)))
 
     def step(self) -> int:
         """Launch the next packed forward (if any work), then complete the previous one."""
@@ -619,10 +717,12 @@ class BatchRuntime(Runtime):
         decodes, runs = self._pack()
         emitted = 0
         if decodes or runs:
+            self._in_step = {j.seq.dev.slot for j in decodes} | {r.seq.dev.slot for r in runs}
             f = self._launch(runs, decodes)
             emitted = len(decodes)
             for j in decodes:
                 self._commit_blocks(j.seq.dev)
+            self._in_step = set()
             f.finished = [j for j in decodes if j.k >= len(j.targets)]
             self.decodes = [j for j in self.decodes if j.k < len(j.targets)]
             if self.pipeline:

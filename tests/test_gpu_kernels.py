@@ -775,3 +775,26 @@ def test_attn_decode_graph_survives_larger_batch(lib):
             assert rel(out_s[b:b + 1], r) < 1e-2, b
     tickets = ws.view(torch.int32)[-(64 * shape.n_kv + 64):]
     assert int(tickets.abs().sum()) == 0
+
+
+def test_kv_copy_blocks(lib):
+    """K1 fork / copy-on-write: stb_kv_copy_blocks duplicates whole blocks (every layer, K and V);
+    the copy's dense view equals the source's, and the source is untouched."""
+    shape = ModelShape("t", 3, 256, 4, 2, 64, 64, 64)
+    pool = _pool(lib, shape, nb=64, slots=4)
+    dense = _fill_pool(lib, pool, shape, [37], seed=3)
+    n = 37
+    pool.reserve(1, n)  # destination slot: its own 3 blocks
+    pool.sync(torch.cuda.current_stream().cuda_stream)
+    src = torch.tensor(pool.blocks(0), dtype=torch.int32, device="cuda")
+    dst = torch.tensor(pool.blocks(1), dtype=torch.int32, device="cuda")
+    assert set(src.tolist()).isdisjoint(dst.tolist())
+    lib.call("stb_kv_copy_blocks", pool.h, P(src), P(dst), len(src), stream())
+    torch.cuda.synchronize()
+    k0, v0 = dense[0]
+    for layer in range(shape.layers):
+        ks, vs = _dense_kv(pool, layer, 0, n, shape)
+        kd, vd = _dense_kv(pool, layer, 1, n, shape)
+        assert torch.equal(ks, k0) and torch.equal(vs, v0)
+        assert torch.equal(kd, k0) and torch.equal(vd, v0)
+    lib.call("stb_kv_copy_blocks", pool.h, P(src), P(dst), 0, stream())  # empty call: no-op

@@ -102,7 +102,7 @@ def glu_ref(gu, limit=7.0):
 
 
 @pytest.mark.parametrize("T,E,k,d,ff", [(1, 16, 4, 512, 256), (32, 128, 4, 2880, 2880), (300, 16, 4, 512, 256),
-                                        (700, 32, 4, 1024, 512), (64, 8, 2, 256, 384)])
+                                        (700, 32, 4, 1024, 512), (64, 8, 2, 256, 384), (16, 8, 2, 64, 128)])
 def test_moe_gemm_mxfp4(lib, T, E, k, d, ff):
     """Grouped MXFP4 GEMM, both kinds, vs fp32 math on the dequantised weights and the same fp16
     inputs; token tiles 16 / 32 / 64 (decode, mixed, ingest-sized), experts with 0..many rows."""

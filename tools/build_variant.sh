@@ -8,7 +8,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 C=${SRC:-$ROOT/paper_2512_15834_b200/csrc}
 OUT=$ROOT/paper_2512_15834_b200/lib/variants/$NAME
 mkdir -p $OUT/obj
-for f in kv attention attn_prefill_tc gemm ops; do
+for f in kv attention attn_prefill_tc gemm ops moe; do
   /usr/local/cuda/bin/nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
     --expt-relaxed-constexpr "$@" -c $C/$f.cu -o $OUT/obj/$f.o &
 done
