@@ -640,10 +640,19 @@ def canary_compare(got, g) -> dict:
     e_fp32 = float(np.linalg.norm(got - fp32) / np.linalg.norm(fp32))
     top5 = np.argsort(-fp32)[:5].tolist()
     bound = 1.25 * intrinsic + 5e-3
-    ok = e_fp32 <= bound and int(got.argmax()) in top5
-    return {"status": "pass" if ok else "FAIL", "rel_l2_err_vs_fp32_oracle": round(e_fp32, 5),
-            "bound": round(bound, 5), "intrinsic_bf16_storage_err": round(intrinsic, 5),
-            "rel_l2_err_vs_bf16_storage_oracle": round(e_emu, 5), "argmax": int(got.argmax()), "oracle_top5": top5}
+    # routed-expert models are chaotic end to end: at 36 layers a router near-tie decided
+    # differently by any two precisions changes a token's experts, and the fp32 oracle and its
+    # own bf16-storage run already differ by ~60%. There the bound alone is checked (a garbage
+    # model sits at ~sqrt(2)); the per-layer teacher-forced check is the binding one.
+    chaotic = intrinsic > 0.25
+    ok = e_fp32 <= bound and (chaotic or int(got.argmax()) in top5)
+    res = {"status": "pass" if ok else "FAIL", "rel_l2_err_vs_fp32_oracle": round(e_fp32, 5),
+           "bound": round(bound, 5), "intrinsic_bf16_storage_err": round(intrinsic, 5),
+           "rel_l2_err_vs_bf16_storage_oracle": round(e_emu, 5), "argmax": int(got.argmax()), "oracle_top5": top5}
+    if chaotic:
+        res["note"] = ("routed experts: end-to-end logits are chaotic across precisions (intrinsic error above); "
+                       "tests/test_gpu_canary.py checks every layer teacher-forced at 2e-2")
+    return res
 
 
 def pct_ms(xs, window: str) -> dict:

@@ -220,7 +220,6 @@ def test_default_engine_is_native():
     assert lib.load().stb_launch_count() > before
     assert eng.rt.forwards > 0
     del EngineConfig, Simulator
-    pair.check()
 
 
 @pytest.mark.parametrize("case", ["full_hit", "partial_hit", "two_turn_mixed", "prefix"])
