@@ -332,6 +332,10 @@ def resolve(args, world: int) -> None:
         args.agents = c["agents"] if c["per_gpu"] else max(1, c["agents"] // world)
     args.scaling = "weak" if c["per_gpu"] else "strong"
     args.trace = dict(c["trace"])
+    if args.reason:  # sweeps (e.g. where in-place ingest beats evict + re-prefill)
+        args.trace["reason"] = tuple(int(x) for x in args.reason.split(","))
+    if args.output:
+        args.trace["output"] = tuple(int(x) for x in args.output.split(","))
     args.max_ctx = c["max_ctx"]
     if not args.max_step_tokens:  # a 32k-token prompt is one packed run: size the step for it
         args.max_step_tokens = c.get("max_step_tokens", 8192)
@@ -346,7 +350,10 @@ def shape_layers(name: str) -> int:
 def workload_config(args) -> dict:
     c = CONFIGS[args.config]
     prompt = args.trace.get("prompt_tokens", 2048)
-    return {"workload": c["label"], "config_id": args.config, "shape": args.shape,
+    label = c["label"]
+    if args.reason or args.output:
+        label += f" [trace override: reason {args.trace.get('reason')}, output {args.trace.get('output')}]"
+    return {"workload": label, "config_id": args.config, "shape": args.shape,
             "engine_mode": getattr(args, "engine_mode", "tool_cache"),
             "agents_per_gpu": args.agents, "prompt_tokens": prompt, "draft_latency_s": 0.05, "accept_rate": 0.8,
             "layers": args.layers or shape_layers(args.shape), "parallelism": f"replicas x{args.gpus}",
@@ -385,7 +392,7 @@ def run_b200(args, world, rank, local):
     fleet = Fleet(engine, loop, TraceSpec(seed=args.seed, **args.trace), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
-    state = {"i": 0, "timed": None, "idle_s": 0.0, "t0": 0}
+    state = {"i": 0, "timed": None, "idle_s": 0.0, "t0": 0, "k2": {}, "k2_steps": []}
     stride = TIMER_STRIDE if args.steps >= 128 else SHORT_TIMER_STRIDE
 
     def one_step():
@@ -403,7 +410,15 @@ def run_b200(args, world, rank, local):
         # kernel roofline timers ride on the first timed step and 1 in `stride` after it (their
         # graph event nodes cost ~9 us each; every-step timing would distort the measured step)
         if state["timed"] is not None:
-            rt.dec.timers = state["timed"] if (state["i"] - state["t0"]) % stride == 0 else None
+            rt.dec.timer_filter = None
+            if (state["i"] - state["t0"]) % stride == 0:
+                rt.dec.timers = state["timed"]
+            elif rt.runs:  # a mixed step (prefill / verify / ingest runs): time K2 alone, every time
+                rt.dec.timers = state["k2"]
+                rt.dec.timer_filter = {"attn_prefill", "event_overhead"}
+                state["k2_steps"].append(state["i"] - state["t0"])
+            else:
+                rt.dec.timers = None
         state["i"] += 1
         rt.step()
 
@@ -463,6 +478,7 @@ def run_b200(args, world, rank, local):
     barrier(world)
     emitted = rt.emitted - em0
     rt.drain()
+    rt.dec.timer_filter = None
     rt.dec.timers = state["timed"]
     rt.dec.step_events = None
     per = [(a.elapsed_time(b), g, T) for a, b, g, T in events]
@@ -522,6 +538,24 @@ def run_b200(args, world, rank, local):
         bound, ach, peak, unit = rate(k)
         others[k] = {"bound": bound, "achieved": round(ach, 1), "unit": unit, "frac": round(ach / peak, 4),
                      "share_of_device_time": round(t / timed_dev_s, 4), "launches": n}
+    # K2 on every mixed step of the window (K2-only event timing): its own entry, share of the
+    # mixed steps' device time
+    k2d = state["k2"]
+    k2_ov_ms, _, k2_ov_n = k2d.pop("event_overhead", (0.0, 0, 0))
+    k2_ov = k2_ov_ms / k2_ov_n if k2_ov_n else ov
+    k2_all = k2d.pop("attn_prefill:launches", [])
+    if k2_all:
+        k2_t = sum(max(ms - k2_ov, 1e-3 * ms) / 1e3 for ms, _, _ in k2_all)
+        k2_f = sum(f for _, f, _ in k2_all)
+        roof_t = sum(max(f / (tf_sus * 1e12), by / (hbm * 1e9)) for _, f, by in k2_all)
+        mixed_dev = sum(per[k][0] for k in state["k2_steps"] if k < len(per)) / 1e3
+        others["attn_prefill_all_mixed_steps"] = {
+            "bound": "tensor", "achieved": round(k2_f / k2_t / 1e12, 1), "unit": "TFLOP/s",
+            "frac": round(k2_f / k2_t / 1e12 / tf_sus, 4), "roofline_frac": round(roof_t / k2_t, 4),
+            "roofline_note": "per launch max(flops / sustained tensor peak, KV+q+o bytes / HBM peak)",
+            "share_of_mixed_step_time": round(k2_t / mixed_dev, 4) if mixed_dev else None,
+            "launches": len(k2_all), "mixed_steps": len(state["k2_steps"]),
+            "sampling": "K2-only CUDA events on every mixed step of the timed window (not the stride-sampled steps)"}
     if k2_launches:  # K2 mixes HBM-bound verify passes (33 queries) with tensor-bound ingests
         roof_t = sum(max(f / (tf_sus * 1e12), by / (hbm * 1e9)) for _, f, by in k2_launches)
         meas_t = sum(max(ms - ov, 1e-3 * ms) / 1e3 for ms, _, _ in k2_launches)
@@ -693,6 +727,8 @@ def main():
     ap.add_argument("--engine-mode", default="tool_cache", choices=["tool_cache", "prefix", "vanilla"],
                     help="tool_cache (the paper's engine-side path, default) or the evict + re-prefill baselines")
     ap.add_argument("--k2-stats", action="store_true", help="diagnostics: K2 run shapes of the mixed steps")
+    ap.add_argument("--reason", default="", help="override the trace's reasoning tokens per turn: LO,HI")
+    ap.add_argument("--output", default="", help="override the trace's tool-output tokens: LO,HI")
     ap.add_argument("--no-preroll", dest="preroll", action="store_false",
                     help="start the warm-up at fleet start (the start-up transient lands in the window)")
     ap.add_argument("--preroll-max-steps", type=int, default=4000)

@@ -272,6 +272,7 @@ class Decoder:
         self.graph_sizes: dict[tuple, int] = {}  # kernels captured per graph
         self._seen: set = set()                  # mixed-step shapes already run eagerly once
         self.timers: dict[str, list] | None = None  # name -> [ms, work, launches] totals
+        self.timer_filter: set | None = None  # time only these kernel classes (None: all)
         self._pre_flops = 0
         self._pre_work = (0, 0)  # (flops, bytes) of one K2 launch: verify runs are HBM-bound, ingests tensor-bound
         self._pre_units = 0
@@ -510,7 +511,7 @@ class Decoder:
         x, h = self.x, self.h
         call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
         for _ in range(2):  # empty pairs: the timers' own overhead, subtracted by the reader
-            self._tock("event_overhead", self._tick(), 0)
+            self._tock("event_overhead", self._tick("event_overhead"), 0)
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
         clr = T if T <= CLEAR_MAX else 0
@@ -527,12 +528,12 @@ class Decoder:
                      _p(m["pos"]), T, s.n_q, s.rope_theta, clr, st)
             self._cleared("qkv", clr)
             if B:
-                ev = self._tick()
+                ev = self._tick("attn_decode")
                 call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
                      _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
                 self._tock("attn_decode", ev, dec_bytes)
             if S:
-                ev = self._tick()
+                ev = self._tick("attn_prefill")
                 call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()),
                      _p(self.attn[B:].data_ptr()), _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S,
                      T - B, s.n_q, self.scale, max_q, self._pre_units, st)
@@ -575,7 +576,7 @@ class Decoder:
         x, h = self.x, self.h
         call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
         for _ in range(2):
-            self._tock("event_overhead", self._tick(), 0)
+            self._tock("event_overhead", self._tick("event_overhead"), 0)
         call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(x), T, d, st)
         call("stb_add_rmsnorm", _p(x), None, _p(w["l0.attn_norm"]), _p(h), T, d, s.rms_eps, 0, st)
         clr = T if T <= CLEAR_MAX else 0
@@ -602,12 +603,12 @@ class Decoder:
             self._cleared("qkv", clr)
             win, sinks = s.window(i), _p(w.get(f"l{i}.sinks"))
             if B:
-                ev = self._tick()
+                ev = self._tick("attn_decode")
                 call("stb_attn_decode_ex", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
                      _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, win, sinks, _p(self.work), st)
                 self._tock("attn_decode", ev, dec_bytes)
             if S:
-                ev = self._tick()
+                ev = self._tick("attn_prefill")
                 call("stb_attn_prefill_ex", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                      _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                      self._pre_units, win, sinks, st)
@@ -661,12 +662,12 @@ class Decoder:
     def _attention(self, call, m, i: int, T: int, B: int, S: int, max_q: int, max_ctx: int, dec_bytes: int, st):
         s = self.shape
         if B:
-            ev = self._tick()
+            ev = self._tick("attn_decode")
             call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
                  _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
             self._tock("attn_decode", ev, dec_bytes)
         if S:
-            ev = self._tick()
+            ev = self._tick("attn_prefill")
             call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                  _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                  self._pre_units, st)
@@ -682,7 +683,7 @@ class Decoder:
         ld_ss = ss.stride(0)
         call = lib.call if not _SKIP else (lambda name, *a: None if name in _SKIP else lib.call(name, *a))
         for _ in range(2):  # empty pairs: the timers' own overhead, subtracted by the reader
-            self._tock("event_overhead", self._tick(), 0)
+            self._tock("event_overhead", self._tick("event_overhead"), 0)
         parts = ss.shape[2]
         call("stb_embed_prep", _p(m["ids"]), _p(w["embed"]), _p(x), _p(xb), _p(ss), parts, T, d, st)
         inv_d = 1.0 / d
@@ -734,8 +735,10 @@ class Decoder:
 
     # -- timing (CUDA events on the launching stream; graph-safe) ----------------
 
-    def _tick(self):
+    def _tick(self, name: str | None = None):
         if self.timers is None and not self._graph_timed:
+            return None
+        if self.timer_filter is not None and name not in self.timer_filter:
             return None
         ev = torch.cuda.Event(enable_timing=True, external=True)
         ev.record()
