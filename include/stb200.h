@@ -226,6 +226,50 @@ int stb_gemm_is_stream(int M, int N, int K);
 int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
                   int split_k, int flags, void* stream);
 
+/* ---- K5 decode block: a chain of decode-shaped GEMMs and the row ops between them in
+ * ONE persistent launch (one CTA per SM, grid-wide barriers between phases). Each
+ * GEMM is stream-K over every SM with fp32 red.add into c; its weight tiles stream
+ * into the shared-memory ring while the previous phase's reductions and row ops are
+ * still finishing, so HBM stays busy across the chain. A decode step then runs
+ * [O, norm, gate-up, SiLU, down, norm, QKV(next layer), RoPE+commit] as one launch per
+ * layer between the attention launches (replaces the per-token decode charges
+ * `engine.py:270,276,302,317` — the same math as the stb_gemm_bf16 /
+ * stb_add_rmsnorm / stb_silu_mul / stb_qkv_norm_rope_commit sequence).
+ *   STB_OP_GEMM  c[M][n] += x[M][k] (bf16, row stride ldx) * w^T; w in the
+ *                stb_weight_tile layout; c fp32 (row stride ldc), zero on entry
+ *   STB_OP_NORM  x_res[M][n] += c (when c != NULL; c cleared to 0);
+ *                y = bf16(x_res * rsqrt(mean(x_res^2) + eps) * w) when y != NULL
+ *                (stb_add_rmsnorm with clear_rows = M)
+ *   STB_OP_SILU  y[M][n] = silu(c[t][2i]) * c[t][2i+1] (c cleared; stb_silu_mul)
+ *   STB_OP_ROPE  stb_qkv_norm_rope_commit on c = qkv[M][(n_q + 2 n_kv) d_head]
+ *                (cleared), q -> y, k / v into layer `layer` of `pool`
+ * M <= 64; at most 4 GEMMs and 5 row ops; a row op that opens the chain reads the
+ * output of the previous launch on the stream. */
+#define STB_OP_GEMM 1
+#define STB_OP_NORM 2
+#define STB_OP_SILU 3
+#define STB_OP_ROPE 4
+typedef struct stb_block_op {
+  int kind;
+  const void* x;       /* GEMM: activations */
+  int64_t ldx;
+  const void* w;       /* GEMM: tiled weights; NORM: norm weight (bf16 [n]) */
+  float* c;            /* GEMM: accumulator; NORM: delta; SILU: gate/up; ROPE: qkv */
+  int64_t ldc;
+  int n, k;            /* GEMM: N, K; NORM: d; SILU: d_ff */
+  float* x_res;        /* NORM: fp32 residual stream [M][n] */
+  void* y;             /* NORM / SILU / ROPE: bf16 output */
+  float eps;           /* NORM; ROPE (qk-norm) */
+  stb_kv_pool* pool;   /* ROPE */
+  int layer, n_q;
+  const int32_t* slot_of;
+  const int32_t* pos_of;
+  float rope_theta;
+  const void* q_norm;  /* ROPE: Qwen3 qk-norm weights (both or neither) */
+  const void* k_norm;
+} stb_block_op;
+int stb_gemm_block(const stb_block_op* ops, int n_ops, int M, void* stream);
+
 /* ---- small fused ops (HBM-bound elementwise / row ops) ------------------ */
 /* x fp32 [n][d] <- table bf16 [ids[i]][d] */
 int stb_embed(const int32_t* ids, const void* table, float* x, int n, int d, void* stream);

@@ -353,7 +353,13 @@ inline void* stream_scratch(int kind, cudaStream_t st, size_t bytes) {
   slots.emplace(key, p);
   return p;
 }
-enum ScratchKind { kScratchSample = 1, kScratchK2Split = 2, kScratchGridBar = 3, kScratchTileTickets = 4 };
+enum ScratchKind {
+  kScratchSample = 1,
+  kScratchK2Split = 2,
+  kScratchGridBar = 3,
+  kScratchTileTickets = 4,
+  kScratchBlockBar = 5
+};
 
 // SM count of the current device (cached per device, not for the first device only).
 inline int device_sms() {

@@ -48,6 +48,7 @@
 #include "../../include/stb200.h"
 #include "common.cuh"
 #include "pool.cuh"
+#include "rope.cuh"
 
 using namespace stb;
 
@@ -136,12 +137,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 struct SegIter {
   Sched s;
   int cta, G;
-  int64_t u, u_end;  // stream mode cursor
-  int t;             // tile mode cursor
+  int u, u_end;  // stream mode cursor (32-bit: the launcher checks units * grid < 2^31)
+  int t;         // tile mode cursor
   __device__ SegIter(const Sched& sc) : s(sc), cta(blockIdx.x), G(gridDim.x) {
     if (s.stream) {
-      u = s.units * cta / G;
-      u_end = s.units * (cta + 1) / G;
+      const int U = (int)s.units;
+      u = U * cta / G;
+      u_end = U * (cta + 1) / G;
     } else {
       t = cta;
     }
@@ -149,11 +151,11 @@ struct SegIter {
   __device__ __forceinline__ bool next(int& tile, int& k0, int& k1) {
     if (s.stream) {
       if (u >= u_end) return false;
-      tile = (int)(u / s.kb);
-      k0 = (int)(u - (int64_t)tile * s.kb);
-      int64_t tile_end = (int64_t)(tile + 1) * s.kb;
-      int64_t e = tile_end < u_end ? tile_end : u_end;
-      k1 = (int)(e - (int64_t)tile * s.kb);
+      tile = u / s.kb;
+      const int base = tile * s.kb;
+      k0 = u - base;
+      const int e = min(base + s.kb, u_end);
+      k1 = e - base;
       u = e;
       return true;
     }
@@ -427,7 +429,9 @@ __device__ __forceinline__ void fused_epilogue(const Epi& ep, const Sched& sched
   }
 }
 
-template <int BN>
+// FUSED selects the fused-epilogue instantiation (stb_gemm_bf16_fused): the plain kernel carries
+// none of that code, so its instruction footprint (fetched cold at every launch) stays small.
+template <int BN, bool FUSED>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_persistent(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                          float* __restrict__ C, int64_t ldc, int M, int N, Sched sched, int bn,
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
   EpiSmem& esm = *reinterpret_cast<EpiSmem*>(smem + STAGES * CF::STAGE + 256);
-  __shared__ unsigned long long tt[5];
+  __shared__ unsigned long long tt[6];
   const bool tracing = g_trace != nullptr;
   if (tracing && threadIdx.x == 0) tt[0] = gtime();
 
@@ -488,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       const int prefetched = i;
+      if (tracing) tt[5] = gtime();
       pdl_wait();
       if (tracing) tt[1] = gtime();
       pdl_launch();
@@ -557,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue warps 2..5 -> TMEM lane quarters 2,3,0,1
     pdl_wait();
     const int quarter = warp & 3;
-    if (ep.kind != 0) {
+    if constexpr (FUSED) {
       fused_epilogue<BN>(ep, sched, C, ldc, M, N, bn, tmem, acc_full, acc_empty, s_last, esm, quarter, lane);
     } else {
     const bool atomic = sched.stream != 0;
@@ -708,7 +713,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned long long* r = g_trace + (size_t)slot * 8;
       r[0] = (unsigned long long)sched.tag;
       r[1] = tt[4];
-      r[2] = sm;
+      r[2] = tt[5];  // producer: ring pre-filled, about to wait on the previous grid
+      (void)sm;
       r[3] = tt[0];
       r[4] = tt[1];
       r[5] = tt[2];
@@ -860,6 +866,445 @@ Plan plan(int M, int N, int sms) {
   return p;
 }
 
+
+// ============================================================================================
+// K5 decode block (stb_gemm_block): a chain of decode-shaped GEMMs and the row ops between
+// them in ONE persistent launch. A decode layer used to be nine dependent launches (QKV,
+// RoPE+commit, attention, O, add+norm, gate-up, SiLU, down, add+norm): every boundary costs
+// a CTA turnover, a prologue and an HBM first-byte latency, and the row ops sit on the
+// critical path between weight streams. Here the chain between two attention launches —
+// [O, norm, gate-up, SiLU, down, norm, QKV(next layer), RoPE+commit] — is one grid of one
+// CTA per SM:
+//   warp 0     producer: walks every GEMM's stream-K (tile, K-block) stages in order and
+//              issues each stage's weight tile as soon as its ring slot is free — weights
+//              never depend on the previous phase — and its activation tile once the phase
+//              that produces those activations has completed grid-wide (a generation
+//              counter it polls), so the ring is full of the next GEMM's weights while the
+//              previous phase's reductions and row op finish
+//   warp 1     MMA issuer (one thread), as gemm_bf16_persistent, across all GEMM phases
+//   warps 2-5  epilogue: per GEMM phase, TMEM -> fp32 red.add into that phase's zeroed
+//              accumulator; per row-op phase, the op on this CTA's slice of rows /
+//              elements (the same arithmetic as stb_add_rmsnorm / stb_silu_mul /
+//              rope_commit_elem); a grid barrier (arrive + generation) after every phase
+// Co-residency: grid = SM count at one CTA per SM (the stream-K GEMMs already rely on it).
+// ============================================================================================
+constexpr int kBlkMaxGemm = 4;
+constexpr int kBlkMaxGlue = 5;
+constexpr int kBlkMaxOps = kBlkMaxGemm + kBlkMaxGlue;
+
+struct alignas(64) BlkGemm {
+  CUtensorMap tx;           // activations [M][K] bf16, box [bn][64], 128B swizzle
+  const __nv_bfloat16* w;   // stb_weight_tile layout
+  float* c;                 // fp32 accumulator, zero on entry
+  int64_t ldc;
+  int N;
+  Sched s;                  // stream-K over the grid, one token tile
+};
+
+struct BlkGlue {
+  int kind;                 // STB_OP_NORM / SILU / ROPE
+  float* c;                 // NORM delta, SILU gate/up, ROPE qkv (all cleared)
+  float* x;                 // NORM residual stream
+  const __nv_bfloat16* w;   // NORM weight
+  __nv_bfloat16* y;         // bf16 output (NORM: may be null -> residual add only)
+  int n;                    // NORM d, SILU d_ff
+  float eps;
+  __nv_bfloat16* kpages;    // ROPE
+  __nv_bfloat16* vpages;
+  const int32_t* table;
+  int max_bps, n_q, n_kv, d_head;
+  const int32_t* slot_of;
+  const int32_t* pos_of;
+  const float* inv_freq;
+  const __nv_bfloat16* q_norm;
+  const __nv_bfloat16* k_norm;
+};
+
+struct BlkArgs {
+  BlkGemm g[kBlkMaxGemm];
+  BlkGlue u[kBlkMaxGlue];
+  int n_ops, n_gemm, M, bn;
+  int8_t kind[kBlkMaxOps];  // 0: GEMM, else the row op's STB_OP_* kind
+  int8_t idx[kBlkMaxOps];   // index into g / u
+  int8_t gneed[kBlkMaxGemm];  // GEMM j: barrier completions before its activations exist
+  unsigned* bar;            // {arrivals, generation}: self-resetting grid barrier
+  int tag;                  // launch sequence number (debug trace only)
+};
+
+// Debug timeline of decode-block launches (stb_debug_block_trace): per CTA 32 x u64 =
+// {tag, cta, t_entry, t_dep_wait, then per op k: t_start (wait passed), t_done, t_arrived, ..., t_exit}
+__device__ unsigned long long* g_btrace = nullptr;
+__device__ unsigned int g_btrace_n = 0;
+__device__ unsigned int g_btrace_cap = 0;
+
+// grid barrier layout: the arrival counter and the generation word sit 4 KiB apart (different
+// L2 lines and slices), so the pollers of the generation never queue behind the arrivals
+constexpr int kGenOff = 1024;
+
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
+// wait until k barrier completions past g0 have been published (one poller per CTA)
+__device__ __forceinline__ void blk_wait_gen(const unsigned* bar, unsigned g0, int k) {
+  if ((int)(ld_relaxed_gpu(bar + kGenOff) - g0) < k) {
+    do {
+      __nanosleep(100);
+    } while ((int)(ld_relaxed_gpu(bar + kGenOff) - g0) < k);
+  }
+  fence_acq_rel_gpu();
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// every stream-K stage (GEMM j, tile, K block) of the chain, in issue order
+struct BlkCursor {
+  const BlkArgs* a;
+  int j;
+  SegIter it;
+  int tile, k, k1;
+  __device__ explicit BlkCursor(const BlkArgs& args) : a(&args), j(0), it(args.g[0].s), tile(0), k(0), k1(0) { seek(); }
+  __device__ __forceinline__ void seek() {
+    while (j < a->n_gemm) {
+      if (it.next(tile, k, k1)) return;
+      if (++j < a->n_gemm) it = SegIter(a->g[j].s);
+    }
+  }
+  __device__ __forceinline__ bool done() const { return j >= a->n_gemm; }
+  __device__ __forceinline__ void advance() {
+    if (++k >= k1) seek();
+  }
+};
+
+// NORM: row r of M on CTA r mod G; the 128 epilogue threads hold the row (float4 each per
+// 512 columns, d <= 8192): x += delta (delta cleared), y = bf16(x * rsqrt(mean x^2 + eps) * w)
+__device__ __forceinline__ void blk_norm(const BlkGlue& u, int M, float* red) {
+  const int et = threadIdx.x - 64, we = et >> 5, lane = threadIdx.x & 31;
+  const int d4 = u.n >> 2;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    float4* __restrict__ xr = reinterpret_cast<float4*>(u.x + (int64_t)r * u.n);
+    float4* __restrict__ cr = u.c ? reinterpret_cast<float4*>(u.c + (int64_t)r * u.n) : nullptr;
+    float4 v[16], e[16];
+    // every load of the row first (one L2 latency, not one per float4), then the stores
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c4 = et + i * 128;
+      v[i] = c4 < d4 ? __ldcg(xr + c4) : z;
+      e[i] = (cr && c4 < d4) ? __ldcg(cr + c4) : z;
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c4 = et + i * 128;
+      if (c4 >= d4) continue;
+      if (cr) {
+        v[i].x += e[i].x, v[i].y += e[i].y, v[i].z += e[i].z, v[i].w += e[i].w;
+        __stcg(cr + c4, z);
+        __stcg(xr + c4, v[i]);
+      }
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) red[we] = ss;
+    epi_bar();
+    const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+    epi_bar();  // red is reused by the next row
+    if (u.y == nullptr) continue;
+    const float inv = rsqrtf(tot / u.n + u.eps);
+    __nv_bfloat16* yr = u.y + (int64_t)r * u.n;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c4 = et + i * 128;
+      if (c4 >= d4) continue;
+      const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(u.w + 4 * c4));
+      const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(u.w + 4 * c4 + 2));
+      *reinterpret_cast<uint2*>(yr + 4 * c4) = make_uint2(pack_bf16(v[i].x * inv * w01.x, v[i].y * inv * w01.y),
+                                                          pack_bf16(v[i].z * inv * w23.x, v[i].w * inv * w23.y));
+    }
+  }
+}
+
+// SILU: y[t][i] = silu(gu[t][2i]) * gu[t][2i+1] over every CTA's epilogue threads; gu cleared.
+// Each thread's items are loaded in batches of 8 before any store (one L2 latency per batch).
+__device__ __forceinline__ void blk_silu(const BlkGlue& u, int M) {
+  const int et = threadIdx.x - 64;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t total4 = (int64_t)M * u.n / 4, step = (int64_t)gridDim.x * 128;
+  constexpr int kBatch = 8;
+  for (int64_t b0 = (int64_t)blockIdx.x * 128 + et; b0 < total4; b0 += kBatch * step) {
+    float4 a[kBatch], b[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int64_t i4 = b0 + j * step;
+      a[j] = b[j] = z;
+      if (i4 < total4) {
+        const int64_t i = i4 * 4, t = i / u.n, c = i - t * u.n;
+        const float4* p = reinterpret_cast<const float4*>(u.c + t * 2 * u.n + 2 * c);
+        a[j] = __ldcg(p);      // g0 u0 g1 u1
+        b[j] = __ldcg(p + 1);  // g2 u2 g3 u3
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int64_t i4 = b0 + j * step;
+      if (i4 >= total4) break;
+      const int64_t i = i4 * 4, t = i / u.n, c = i - t * u.n;
+      float4* p = reinterpret_cast<float4*>(u.c + t * 2 * u.n + 2 * c);
+      __stcg(p, z);
+      __stcg(p + 1, z);
+      *reinterpret_cast<uint2*>(u.y + i) =
+          make_uint2(pack_bf16(silu_gate(a[j].x, a[j].y), silu_gate(a[j].z, a[j].w)),
+                     pack_bf16(silu_gate(b[j].x, b[j].y), silu_gate(b[j].z, b[j].w)));
+    }
+  }
+}
+
+// ROPE: rope_commit_elem over (token, head, rotation group) elements, a warp-aligned range
+// per epilogue warp (the qk-norm shuffles need whole warps)
+__device__ __forceinline__ void blk_rope(const BlkGlue& u, int M) {
+  const int we = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)M * (u.n_q + 2 * u.n_kv) * (u.d_head / 16);
+  for (int64_t base = ((int64_t)blockIdx.x * 4 + we) * 32; base < total; base += (int64_t)gridDim.x * 128)
+    rope_commit_elem(base + lane, u.c, u.y, u.slot_of, u.pos_of, M, u.n_q, u.n_kv, u.d_head, u.inv_freq, u.table,
+                     u.max_bps, u.kpages, u.vpages, M, u.q_norm, u.k_norm, u.eps, nullptr, 1.f);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_block_kernel(const __grid_constant__ BlkArgs a) {
+  using CF = Cfg<BN>;
+  constexpr int STAGES = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  __shared__ unsigned s_g0;
+  __shared__ volatile int s_g0_set;
+  __shared__ volatile int s_done;  // barrier completions the epilogue's poller has observed
+  __shared__ float s_red[4];
+  __shared__ unsigned long long bt[32];
+  const bool btracing = g_btrace != nullptr;
+  if (btracing && threadIdx.x == 0) bt[2] = gtime();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bn = a.bn, M = a.M;
+  if (warp == 0 && lane == 0) {
+    for (int j = 0; j < a.n_gemm; ++j) tma_prefetch(&a.g[j].tx);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    fence_mbar_init();
+    s_g0_set = 0;
+    s_done = 0;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, CF::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t kStageTx = (uint32_t)CF::W_BYTES;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t tx_bytes = kStageTx + (uint32_t)bn * BK * 2;
+      BlkCursor cw(a), cx(a);
+      int nw = 0, nx = 0;
+      auto issue_w = [&]() {
+        const int s = nw % STAGES;
+        mbar_wait(&empty[s], ((nw / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], tx_bytes);
+        const BlkGemm& g = a.g[cw.j];
+        bulk_load(smem_u32(smem + s * CF::STAGE), g.w + ((int64_t)cw.tile * g.s.kb + cw.k) * (BM * BK), CF::W_BYTES,
+                  &full[s]);
+        cw.advance();
+        ++nw;
+      };
+      // weights of the first ring slots before the dependency wait
+      while (!cw.done() && nw < STAGES) issue_w();
+      pdl_wait();
+      const unsigned g0 = ld_acquire_gpu(a.bar + kGenOff);  // stable: the previous launch has completed
+      if (btracing) bt[3] = gtime();
+      s_g0 = g0;
+      __threadfence_block();
+      s_g0_set = 1;
+      pdl_launch();
+      int ready_j = -1;  // highest GEMM whose activations are known to exist
+      while (!cx.done()) {
+        if (nx < nw) {
+          if (cx.j > ready_j) {
+            // completions observed by this CTA's epilogue poller (no second global poller)
+            const int need = a.gneed[cx.j];
+            if (need == 0 || s_done >= need) {
+              fence_acq_rel_gpu();
+              fence_proxy_async_global();  // row-op outputs (generic stores) -> TMA reads
+              ready_j = cx.j;
+            }
+          }
+          if (cx.j <= ready_j) {
+            const int s = nx % STAGES;
+            tma_load_2d(smem + s * CF::STAGE + CF::W_BYTES, &a.g[cx.j].tx, &full[s], cx.k * BK, 0);
+            cx.advance();
+            ++nx;
+            continue;
+          }
+        }
+        if (!cw.done() && nw - nx < STAGES) {
+          issue_w();
+          continue;
+        }
+        __nanosleep(32);  // the next phase's activations are still being produced
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t idesc = umma_idesc_bf16(BM, bn, false, false);
+      int i = 0, jj = 0;
+      for (int j = 0; j < a.n_gemm; ++j) {
+        SegIter it(a.g[j].s);
+        int tile, k0, k1;
+        while (it.next(tile, k0, k1)) {
+          const int buf = jj & 1;
+          mbar_wait(&acc_empty[buf], ((jj >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * BN;
+          for (int k = k0; k < k1; ++k, ++i) {
+            const int s = i % STAGES;
+            mbar_wait(&full[s], (i / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t wa = smem_u32(smem + s * CF::STAGE);
+            const uint32_t xa = wa + CF::W_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_f16_ss(d, umma_desc_kmajor_sw128(wa + kk * 32, 1024), umma_desc_kmajor_sw128(xa + kk * 32, 1024),
+                          idesc, (k > k0 || kk > 0) ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
+          umma_commit(&acc_full[buf]);
+          ++jj;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    if (threadIdx.x == 64)
+      while (!s_g0_set) __nanosleep(32);
+    epi_bar();
+    const unsigned g0 = s_g0;
+    const int quarter = warp & 3, G = gridDim.x;
+    int jj = 0;
+    for (int op = 0; op < a.n_ops; ++op) {
+      const int kind = a.kind[op];
+      // every phase before this one has completed grid-wide (op barriers so far). Waited for
+      // by every CTA — also before a GEMM phase in which it owns no stream-K segment — so no
+      // CTA arrives at barrier op+1 while barrier op is still counting arrivals
+      if (threadIdx.x == 64 && op > 0) {
+        blk_wait_gen(a.bar, g0, op);
+        s_done = op;
+      }
+      if (btracing && threadIdx.x == 64) bt[4 + 3 * op] = gtime();
+      if (kind == 0) {
+        const BlkGemm& g = a.g[a.idx[op]];
+        SegIter it(g.s);
+        int tile, k0, k1;
+        while (it.next(tile, k0, k1)) {
+          const int buf = jj & 1;
+          mbar_wait(&acc_full[buf], (jj >> 1) & 1);
+          tc_fence_after();
+          const int feat = tile * BM + quarter * 32 + lane;
+          const bool fok = feat < g.N;
+          float* crow = g.c + feat;
+          const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
+          int c = 0;
+#pragma unroll 1
+          for (; c + 32 <= bn; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(base + c, r);
+            tmem_ld_wait();
+            if (fok) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (c + q < M) atomicAdd(crow + (int64_t)(c + q) * g.ldc, __uint_as_float(r[q]));
+            }
+          }
+          if (c < bn) {
+            uint32_t r[16];
+            tmem_ld16(base + c, r);
+            tmem_ld_wait();
+            if (fok) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (c + q < M) atomicAdd(crow + (int64_t)(c + q) * g.ldc, __uint_as_float(r[q]));
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[buf]);
+          ++jj;
+        }
+      } else {
+        epi_bar();
+        const BlkGlue& u = a.u[a.idx[op]];
+        if (kind == STB_OP_NORM) blk_norm(u, M, s_red);
+        else if (kind == STB_OP_SILU) blk_silu(u, M);
+        else blk_rope(u, M);
+      }
+      if (btracing && threadIdx.x == 64) bt[5 + 3 * op] = gtime();
+      if (op + 1 < a.n_ops) {  // grid barrier: this phase's results are visible everywhere
+        __threadfence();
+        if (kind != 0) fence_proxy_async_global();
+        epi_bar();
+        if (threadIdx.x == 64) {
+          __threadfence();
+          if (atomicAdd(a.bar, 1u) == (unsigned)G - 1) {
+            *(volatile unsigned*)a.bar = 0u;
+            __threadfence();
+            atomicAdd(a.bar + kGenOff, 1u);
+          }
+          if (btracing) bt[6 + 3 * op] = gtime();
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, CF::TMEM_COLS);
+  if (btracing && threadIdx.x == 64) {
+    const unsigned slot = atomicAdd(&g_btrace_n, 1u);
+    if (slot < g_btrace_cap) {
+      bt[0] = ((unsigned long long)a.tag << 8) | (unsigned long long)a.n_ops;
+      bt[1] = blockIdx.x;
+      bt[31] = gtime();
+      for (int i = 0; i < 32; ++i) g_btrace[(size_t)slot * 32 + i] = bt[i];
+    }
+  }
+}
+
+template <int BN>
+int launch_block(const BlkArgs& a, int grid, cudaStream_t st) {
+  auto kern = gemm_block_kernel<BN>;
+  smem_attr_once(kern, Cfg<BN>::SMEM);
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(kThreads), Cfg<BN>::SMEM, st, a);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "gemm_block launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
 
 // ============================================================================================
 // K5 pair kernel: prefill-shaped GEMMs (whole tiles) on CTA pairs, tcgen05.mma.cta_group::2.
@@ -1207,6 +1652,8 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   int grid = s.stream ? sms : (s.tiles < sms ? s.tiles : sms);
   if (mode >= 2 && mode < grid) grid = mode;
   if (s.stream && s.units < grid) grid = (int)s.units;
+  if (s.stream && s.units * (int64_t)(grid + 1) >= (int64_t)1 << 31)
+    return fail(STB_EINVAL, "gemm_bf16: %lld stream-K units exceed the 32-bit schedule", (long long)s.units);
   s.c_zeroed = (flags & STB_GEMM_C_ZEROED) ? 1 : 0;
   s.silu = (flags & STB_GEMM_SILU_MUL) ? 1 : 0;
   if (s.silu && (s.stream || N % 2))
@@ -1217,7 +1664,7 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
   s.load_debug = load_debug;
   s.bar = grid_barrier(st);
   if (!s.bar) return fail(STB_ENOMEM, "gemm_bf16: barrier state");
-  auto kern = gemm_bf16_persistent<BN>;
+  auto kern = ep.kind != 0 ? gemm_bf16_persistent<BN, true> : gemm_bf16_persistent<BN, false>;
   smem_attr_once(kern, CF::SMEM);
   if (ep.kind != 0 && s.stream && (C == nullptr || ep.cnt == nullptr))
     return fail(STB_EINVAL, "gemm_bf16_fused: the stream-K schedule needs the zeroed fp32 workspace");
@@ -1319,6 +1766,111 @@ extern "C" int stb_gemm_bf16(const void* A, int64_t lda, const void* W, int64_t 
   Epi none;
   memset(&none, 0, sizeof(none));
   return dispatch(A, lda, W, ldw, C, ldc, M, N, K, split_k, flags, st, none);
+}
+
+extern "C" int stb_debug_block_trace(void* buf, int cap) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, g_btrace_n, sizeof(n));
+  unsigned long long* p = (unsigned long long*)buf;
+  unsigned int c = (unsigned int)cap, z = 0;
+  cudaMemcpyToSymbol(g_btrace, &p, sizeof(p));
+  cudaMemcpyToSymbol(g_btrace_cap, &c, sizeof(c));
+  cudaMemcpyToSymbol(g_btrace_n, &z, sizeof(z));
+  return (int)n;
+}
+
+extern "C" int stb_gemm_block(const stb_block_op* ops, int n_ops, int M, void* stream) {
+  if (!ops || n_ops < 1 || n_ops > kBlkMaxOps) return fail(STB_EINVAL, "gemm_block: 1..%d ops", kBlkMaxOps);
+  if (M < 1 || M > 64) return fail(STB_EINVAL, "gemm_block: M = %d outside 1..64 (decode batches)", M);
+  cudaStream_t st = (cudaStream_t)stream;
+  BlkArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n_ops = n_ops;
+  a.M = M;
+  a.bn = (M + 15) / 16 * 16;
+  const int grid = sm_count();
+  int ng = 0, nu = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    const stb_block_op& o = ops[i];
+    if (o.kind == STB_OP_GEMM) {
+      if (ng >= kBlkMaxGemm) return fail(STB_EINVAL, "gemm_block: at most %d GEMMs", kBlkMaxGemm);
+      if (!o.x || !o.w || !o.c || o.n <= 0 || o.k <= 0 || o.k % 8 || o.ldx % 8 || o.ldx < o.k || o.ldc < o.n)
+        return fail(STB_EINVAL, "gemm_block: GEMM %d: bad operands", i);
+      if ((reinterpret_cast<uintptr_t>(o.x) | reinterpret_cast<uintptr_t>(o.w)) & 15)
+        return fail(STB_EINVAL, "gemm_block: GEMM %d: operands must be 16-byte aligned", i);
+      BlkGemm& g = a.g[ng];
+      if (int rc = cached_map(&g.tx, o.x, M, o.k, o.ldx, a.bn)) return rc;
+      g.w = (const __nv_bfloat16*)o.w;
+      g.c = o.c;
+      g.ldc = o.ldc;
+      g.N = o.n;
+      Sched& s = g.s;
+      s.stream = 1;
+      s.tiles_n = (o.n + BM - 1) / BM;
+      s.tiles_m = 1;
+      s.tiles = s.tiles_n;
+      s.kb = (o.k + BK - 1) / BK;
+      s.units = (int64_t)s.tiles * s.kb;
+      s.c_zeroed = 1;
+      if (s.units * (int64_t)(grid + 1) >= (int64_t)1 << 31)
+        return fail(STB_EINVAL, "gemm_block: GEMM %d has too many stream-K units", i);
+      a.kind[i] = 0;
+      a.idx[i] = (int8_t)ng;
+      a.gneed[ng] = (int8_t)i;  // a barrier follows every op: op i starts after i completions
+      ++ng;
+      continue;
+    }
+    if (nu >= kBlkMaxGlue) return fail(STB_EINVAL, "gemm_block: at most %d row ops", kBlkMaxGlue);
+    BlkGlue& u = a.u[nu];
+    u.kind = o.kind;
+    u.c = o.c;
+    u.y = (__nv_bfloat16*)o.y;
+    u.n = o.n;
+    u.eps = o.eps;
+    if (o.kind == STB_OP_NORM) {
+      if (!o.x_res || o.n <= 0 || o.n % 4 || o.n > 8192 || (o.y && !o.w))
+        return fail(STB_EINVAL, "gemm_block: NORM %d: needs x_res, d a multiple of 4 up to 8192, w with y", i);
+      u.x = o.x_res;
+      u.w = (const __nv_bfloat16*)o.w;
+    } else if (o.kind == STB_OP_SILU) {
+      if (!o.c || !o.y || o.n <= 0 || o.n % 4) return fail(STB_EINVAL, "gemm_block: SILU %d: bad operands", i);
+    } else if (o.kind == STB_OP_ROPE) {
+      stb_kv_pool* p = o.pool;
+      if (!p || o.layer < 0 || o.layer >= p->layers || !o.c || !o.y || !o.slot_of || !o.pos_of || o.n_q <= 0 ||
+          o.n_q % p->n_kv || p->d_head % 16 || (o.q_norm == nullptr) != (o.k_norm == nullptr))
+        return fail(STB_EINVAL, "gemm_block: ROPE %d: bad operands", i);
+      void *kp, *vp;
+      stb_kv_layer_ptrs(p, o.layer, &kp, &vp);
+      u.kpages = (__nv_bfloat16*)kp;
+      u.vpages = (__nv_bfloat16*)vp;
+      u.table = p->dev_table;
+      u.max_bps = p->max_bps;
+      u.n_q = o.n_q;
+      u.n_kv = p->n_kv;
+      u.d_head = p->d_head;
+      u.slot_of = o.slot_of;
+      u.pos_of = o.pos_of;
+      u.inv_freq = stb_rope_inv_freq(o.rope_theta, p->d_head);
+      if (!u.inv_freq) return fail(STB_ENOMEM, "gemm_block: inv_freq");
+      u.q_norm = (const __nv_bfloat16*)o.q_norm;
+      u.k_norm = (const __nv_bfloat16*)o.k_norm;
+    } else {
+      return fail(STB_EINVAL, "gemm_block: op %d has unknown kind %d", i, o.kind);
+    }
+    a.kind[i] = (int8_t)o.kind;
+    a.idx[i] = (int8_t)nu;
+    ++nu;
+  }
+  if (ng == 0) return fail(STB_EINVAL, "gemm_block: no GEMM in the chain");
+  a.n_gemm = ng;
+  a.bar = (unsigned*)stream_scratch(kScratchBlockBar, st, (kGenOff + 32) * sizeof(unsigned));
+  if (!a.bar) return fail(STB_ENOMEM, "gemm_block: barrier state");
+  static int launch_seq = 0;
+  a.tag = launch_seq++;
+  const int BNt = bn_template(M);
+  if (BNt == 16) return launch_block<16>(a, grid, st);
+  if (BNt == 32) return launch_block<32>(a, grid, st);
+  return launch_block<64>(a, grid, st);
 }
 
 extern "C" int stb_gemm_bf16_fused(const void* A, int64_t lda, const void* W, int64_t ldw, float* work,

@@ -105,6 +105,26 @@ class GemmEpi(C.Structure):
 EPI_SILU, EPI_QKV, EPI_RESID = 1, 2, 3   # include/stb200.h STB_EPI_*
 
 
+class BlockOp(C.Structure):
+    """include/stb200.h stb_block_op: one phase of a decode-block chain (stb_gemm_block)."""
+
+    _fields_ = [("kind", C.c_int), ("x", C.c_void_p), ("ldx", C.c_int64), ("w", C.c_void_p), ("c", C.c_void_p),
+                ("ldc", C.c_int64), ("n", C.c_int), ("k", C.c_int), ("x_res", C.c_void_p), ("y", C.c_void_p),
+                ("eps", C.c_float), ("pool", C.c_void_p), ("layer", C.c_int), ("n_q", C.c_int),
+                ("slot_of", C.c_void_p), ("pos_of", C.c_void_p), ("rope_theta", C.c_float),
+                ("q_norm", C.c_void_p), ("k_norm", C.c_void_p)]
+
+
+OP_GEMM, OP_NORM, OP_SILU, OP_ROPE = 1, 2, 3, 4   # include/stb200.h STB_OP_*
+# Decode block (stb_gemm_block, opt-in STB200_GEMM_BLOCK=1): decode-only steps of dense models
+# as [attention, block] per layer, the O / gate-up / down / next QKV projections and the row ops
+# between them in one launch with grid barriers. Parity-green but measured slower than the
+# PDL-chained per-op launches (C2 decode step at ctx 2k 4.93 -> 5.5-6.2 ms): a grid barrier plus a
+# row-op phase costs 6-7 us where a programmatic-dependent kernel boundary plus the row kernel
+# costs 3-4, and merging two GEMMs into one launch saves nothing (DESIGN.md §4).
+BLOCK_MAX_T = 64 if os.environ.get("STB200_GEMM_BLOCK", "0") == "1" else 0
+
+
 def fusable(shape: ModelShape) -> bool:
     """The fused QKV epilogue needs 128-aligned q / kv widths and d_head <= 128."""
     return shape.d_head in (32, 64, 128) and shape.q_dim % 128 == 0 and shape.kv_dim % 128 == 0
@@ -295,6 +315,7 @@ class Decoder:
         # leading rows of each GEMM output that may be non-zero (rows at and past it are zero)
         self._dirty = {"qkv": 0, "proj": 0, "gu": 0, "logits": 0}
         self._stream_cache: dict = {}
+        self._blk_cache: dict = {}   # (T, buffers, metadata pointers) -> decode-block op arrays
         self.taps: list | None = None  # debug (canary): residual stream after the embedding and each layer
         # MoE routing statistics for the grouped GEMM's algorithmic bytes: each timed step copies the
         # per-layer expert offsets to pinned memory (4 buffers: eager / graph x 2 flight parities)
@@ -339,6 +360,7 @@ class Decoder:
             self._cap_t = cap
             self._dirty.update(qkv=0, proj=0, gu=0)
             self.graphs.clear()  # captured graphs point at the old buffers
+            self._blk_cache.clear()
         if R > self._cap_r:
             cap = max(R, 2 * self._cap_r, 64)
             self.rows = torch.empty(cap, s.d_model, dtype=torch.bfloat16, device=dev)
@@ -505,6 +527,12 @@ class Decoder:
             return self._launch_moe(m, T, R, B, S, max_q, max_ctx, dec_bytes)
         if self.fused:
             return self._launch_fused(m, T, R, B, S, max_q, max_ctx, dec_bytes)
+        if S == 0 and T == B and T <= BLOCK_MAX_T and not _SKIP:
+            for name in ("qkv", "proj", "gu"):  # the block's stream-K phases accumulate into zeroed rows
+                if self._dirty[name]:
+                    getattr(self, name)[:self._dirty[name]].zero_()
+                    self._dirty[name] = 0
+            return self._launch_blocks(m, T, R, B, max_ctx, dec_bytes)
         s, w = self.shape, self.w
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         d = s.d_model
@@ -558,6 +586,97 @@ class Decoder:
         self.gemm(rows, w["lm_head"], "logits", st, "lm_head")
         # the sampler re-zeroes the logits only when the LM head accumulated them (stream-K);
         # whole-tile LM heads (any decode batch) overwrite them with plain stores
+        clear = 0 if self.keep_logits or not self._stream_cache[(R, s.vocab, d)] else 1
+        call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
+             _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)
+        if clear:
+            self._cleared("logits", R)
+
+    def _block_ops(self, m: dict[str, int], T: int) -> list:
+        """The decode-block chains of one decode step (stb_gemm_block op arrays), built once per
+        (T, buffer set, step-record pointers): [norm, QKV_0, RoPE_0] before the first attention,
+        then per layer i [O_i, norm, gate-up_i, SiLU, down_i, norm, QKV_{i+1}, RoPE_{i+1}] (the
+        last layer ends with the residual add). Returns [(ops array, n_ops, algorithmic bytes)]."""
+        key = (T, m["slot_of"], m["pos"], self.x.data_ptr(), self.qkv.data_ptr(), self.h.data_ptr())
+        hit = self._blk_cache.get(key)
+        if hit is not None:
+            return hit
+        s, w = self.shape, self.w
+        d = s.d_model
+        x, h = self.x, self.h
+
+        def gemm(a, wt, out):
+            return BlockOp(kind=OP_GEMM, x=a.data_ptr(), ldx=a.stride(0), w=wt.data_ptr(), c=out.data_ptr(),
+                           ldc=out.stride(0), n=wt.N, k=wt.K), wt.N * wt.K * 2 + T * wt.K * 2 + T * wt.N * 4
+
+        def norm(delta, weight, y):
+            return BlockOp(kind=OP_NORM, c=delta.data_ptr() if delta is not None else None,
+                           w=weight.data_ptr() if weight is not None else None, n=d, x_res=x.data_ptr(),
+                           y=y.data_ptr() if y is not None else None, eps=s.rms_eps), 0
+
+        def rope(i):
+            qn = w[f"l{i}.q_norm"].data_ptr() if s.qk_norm else None
+            kn = w[f"l{i}.k_norm"].data_ptr() if s.qk_norm else None
+            return BlockOp(kind=OP_ROPE, c=self.qkv.data_ptr(), y=self.q.data_ptr(), pool=self.pool.h, layer=i,
+                           n_q=s.n_q, slot_of=m["slot_of"], pos_of=m["pos"], rope_theta=s.rope_theta, q_norm=qn,
+                           k_norm=kn, eps=s.rms_eps), 0
+
+        def qkv(i):
+            return [norm(None if i == 0 else self.proj, w[f"l{i}.attn_norm"], h),
+                    gemm(h[:T], w[f"l{i}.wqkv"], self.qkv), rope(i)]
+
+        chains = [qkv(0)]
+        for i in range(s.layers):
+            ops = [gemm(self.attn[:T], w[f"l{i}.wo"], self.proj), norm(self.proj, w[f"l{i}.mlp_norm"], h),
+                   gemm(h[:T], w[f"l{i}.w_gate_up"], self.gu),
+                   (BlockOp(kind=OP_SILU, c=self.gu.data_ptr(), y=self.act.data_ptr(), n=s.d_ff), 0),
+                   gemm(self.act[:T], w[f"l{i}.w_down"], self.proj)]
+            if i + 1 < s.layers:
+                ops += qkv(i + 1)
+            else:
+                ops.append(norm(self.proj, None, None))  # residual add only (the final norm: sampled rows)
+            chains.append(ops)
+        out = []
+        for ops in chains:
+            arr = (BlockOp * len(ops))(*[o for o, _ in ops])
+            out.append((arr, len(ops), sum(b for _, b in ops)))
+        if len(self._blk_cache) > 64:
+            self._blk_cache.clear()
+        self._blk_cache[key] = out
+        return out
+
+    def _launch_blocks(self, m: dict[str, int], T: int, R: int, B: int, max_ctx: int, dec_bytes: int) -> None:
+        """A decode-only step as 2 launches per layer: attention (K3) and one decode block."""
+        s, w = self.shape, self.w
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        d = s.d_model
+        call = lib.call
+        for _ in range(2):  # empty pairs: the timers' own overhead, subtracted by the reader
+            self._tock("event_overhead", self._tick("event_overhead"), 0)
+        call("stb_embed", _p(m["ids"]), _p(w["embed"]), _p(self.x), T, d, st)
+        chains = self._block_ops(m, T)
+        if self.taps is not None:
+            self.taps.append(self.x[:T].clone())
+
+        def block(k):
+            arr, n, nbytes = chains[k]
+            ev = self._tick()
+            call("stb_gemm_block", C.cast(arr, C.c_void_p), n, T, st)
+            self._tock("gemm_decode", ev, nbytes)
+
+        block(0)
+        for i in range(s.layers):
+            ev = self._tick("attn_decode")
+            call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]), _p(m["dec_ctx"]),
+                 B, s.n_q, self.scale, max_ctx, _p(self.work), st)
+            self._tock("attn_decode", ev, dec_bytes)
+            block(i + 1)
+            if self.taps is not None:
+                self.taps.append(self.x[:T].clone())
+        rows = self.rows[:R]
+        call("stb_gather_rmsnorm", _p(self.x), _p(m["sample_rows"]), _p(w["final_norm"]), _p(rows), R, d, s.rms_eps,
+             st)
+        self.gemm(rows, w["lm_head"], "logits", st, "lm_head")
         clear = 0 if self.keep_logits or not self._stream_cache[(R, s.vocab, d)] else 1
         call("stb_sample_forced", _p(self.logits), s.vocab, _p(m["targets"]), R, s.vocab, FORCE_BIAS,
              _p(self.sampled), _p(self.raw_arg), _p(self.raw_max), clear, st)

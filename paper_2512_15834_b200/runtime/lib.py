@@ -49,6 +49,7 @@ SIGNATURES: dict[str, tuple] = {
     "stb_gemm_bf16": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, I32, I32, P]),
     "stb_gemm_is_stream": (I32, [I32, I32, I32]),
     "stb_gemm_bf16_fused": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, I32, P, P]),
+    "stb_gemm_block": (I32, [P, I32, I32, P]),
     "stb_embed_prep": (I32, [P, P, P, P, P, I32, I32, I32, P]),
     "stb_weight_tiled_elems": (I64, [I32, I32]),
     "stb_weight_tile": (I32, [P, I64, I32, I32, P, P]),
