@@ -392,7 +392,8 @@ def run_b200(args, world, rank, local):
     fleet = Fleet(engine, loop, TraceSpec(seed=args.seed, **args.trace), args.agents, agent_offset=rank * args.agents)
     fleet.start()
 
-    state = {"i": 0, "timed": None, "idle_s": 0.0, "t0": 0, "k2": {}, "k2_steps": []}
+    state = {"i": 0, "timed": None, "idle_s": 0.0, "t0": 0, "k2": {}, "k2_steps": [], "sampled": 0,
+             "sampled_steps": []}
     stride = TIMER_STRIDE if args.steps >= 128 else SHORT_TIMER_STRIDE
 
     def one_step():
@@ -411,7 +412,14 @@ def run_b200(args, world, rank, local):
         # graph event nodes cost ~9 us each; every-step timing would distort the measured step)
         if state["timed"] is not None:
             rt.dec.timer_filter = None
-            if (state["i"] - state["t0"]) % stride == 0:
+            k = state["i"] - state["t0"]
+            # short runs: every kernel timed on the first decode-only step of the window (one
+            # instrumented step: its ~290 event pairs cost ~1.7 ms of device time); long runs: on
+            # the first timed step and 1 in `stride` after it
+            full = (not rt.runs and not state["sampled"]) if args.steps < 128 else k % stride == 0
+            if full:
+                state["sampled"] += 1
+                state["sampled_steps"].append(k)
                 rt.dec.timers = state["timed"]
             elif rt.runs:  # a mixed step (prefill / verify / ingest runs): time K2 alone, every time
                 rt.dec.timers = state["k2"]
@@ -482,7 +490,7 @@ def run_b200(args, world, rank, local):
     rt.dec.timers = state["timed"]
     rt.dec.step_events = None
     per = [(a.elapsed_time(b), g, T) for a, b, g, T in events]
-    timed_idx = [k for k in range(len(per)) if k % stride == 0]
+    timed_idx = state["sampled_steps"]
     n_timed_steps = len(timed_idx)
     timed_dev_s = max(1e-9, sum(per[k][0] for k in timed_idx) / 1e3)
     # device idle between consecutive steps (end of step k -> start of step k+1)
@@ -528,8 +536,10 @@ def run_b200(args, world, rank, local):
                 "frac": round(ach / peak, 4), "traffic": tr, "traffic_over_algorithmic": tr_ratio,
                 "traffic_source": tr_src, "peak_source": src, "launches": n,
                 "avg_us": round(t / n * 1e6, 2), "share_of_device_time": round(t / timed_dev_s, 4),
-                "sampling": f"CUDA events on timed-region steps 0, {stride}, {2 * stride}, ... "
-                            f"({n_timed_steps} of {args.steps}); share = kernel time / those steps' device time; "
+                "sampling": f"CUDA events around every kernel of timed-region step(s) {timed_idx[:8]} "
+                            f"({n_timed_steps} of {args.steps}: " + ("the first decode-only step" if args.steps < 128
+                                                                     else f"1 in {stride}") +
+                            f"); share = kernel time / those steps' device time; "
                             f"event-pair overhead {ov * 1e3:.2f} us subtracted per launch"}
     others = {}
     for k, (t, w, n) in kern.items():
@@ -544,7 +554,7 @@ def run_b200(args, world, rank, local):
     k2_ov_ms, _, k2_ov_n = k2d.pop("event_overhead", (0.0, 0, 0))
     k2_ov = k2_ov_ms / k2_ov_n if k2_ov_n else ov
     k2_all = k2d.pop("attn_prefill:launches", [])
-    if k2_all:
+    if k2_all:  # noqa: SIM102
         k2_t = sum(max(ms - k2_ov, 1e-3 * ms) / 1e3 for ms, _, _ in k2_all)
         k2_f = sum(f for _, f, _ in k2_all)
         roof_t = sum(max(f / (tf_sus * 1e12), by / (hbm * 1e9)) for _, f, by in k2_all)
@@ -618,12 +628,12 @@ def run_b200(args, world, rank, local):
         qd = SHAPES[args.shape].q_dim
         by_flops = {int(4 * qd * float(sum(n * (c - n) + n * (n + 1) / 2 for n, c in runs))): runs for runs in steps}
         per_launch = collections.defaultdict(list)
-        for ms, f, _ in k2_launches:
+        for ms, f, _ in list(k2_launches) + list(k2_all):
             per_launch[f].append(max(ms - ov, 1e-3 * ms))
         slow = sorted(range(len(per)), key=lambda k: -per[k][0])[:10]
         print("slowest steps (index, ms, decode-only, tokens, event-timed):", file=sys.stderr)
         for k in slow:
-            print(f"   {k:4d} {per[k][0]:8.2f} {per[k][1]!s:5s} {per[k][2]:5d} {k % stride == 0}",
+            print(f"   {k:4d} {per[k][0]:8.2f} {per[k][1]!s:5s} {per[k][2]:5d} {k in timed_idx}",
                   file=sys.stderr)
         print("K2 timed launches (us avg, TFLOP/s, runs (n, ctx)):", file=sys.stderr)
         for f, ts in sorted(per_launch.items(), key=lambda kv: -sum(kv[1])):
