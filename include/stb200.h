@@ -111,6 +111,15 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
 int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                        const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, int window,
                        const float* sinks, void* work, void* stream);
+/* Same with multi-query entries (the verify pass of engine.py:296 riding in the decode launch):
+ * entry b holds n_qs[b] (1 .. 16 / group) consecutive query rows of q / out starting at packed row
+ * q_rows[b]; they are the last n_qs[b] positions of the entry's ctx_lens[b] keys and attend
+ * causally (query i of the entry sees keys < ctx_lens[b] - (n_qs[b] - 1 - i)). A short run of n
+ * queries is ceil(n * group / 16) entries with the same slot; a decode row is an entry with
+ * n_qs = 1. Plain attention only (no window, no sinks).                                     */
+int stb_attn_decode_mq(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                       const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
+                       float scale, int max_ctx, void* work, void* stream);
 
 /* ---- K2: append-prefill attention (n new queries against resident pages)
  * Replaces prefill engine.py:251, verify engine.py:296 and ingest

@@ -297,13 +297,21 @@ __device__ __forceinline__ int warp_of(int64_t u, int64_t U, int W) {
   return (int)(((u + 1) * W + U - 1) / U) - 1;  // largest w with floor(U*w/W) <= u
 }
 
-template <int D, int G, int STAGES>
+// QE > 1 (multi-query entries, stb_attn_decode_mq): entry b holds n_qs[b] <= QE consecutive
+// query rows starting at packed row q_rows[b] — the last n_qs[b] positions of its context, each
+// attending causally (query i of the entry sees keys < ctx - (n - 1 - i)). The 16-row MMA tile of
+// a (entry, kv head) pair is then QE queries x G heads instead of one query's G heads (rows G..15
+// of a decode tile are dead), so a short verify run rides in the decode launch: the entries of
+// one run re-read the same pages from L2, and no separate prefill launch or merge is needed.
+template <int D, int G, int QE, int STAGES>
 __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
     float* __restrict__ o_part, float* __restrict__ lse_part, int* __restrict__ tickets, int window,
-    const float* __restrict__ sinks) {
+    const float* __restrict__ sinks, const int32_t* __restrict__ q_rows, const int32_t* __restrict__ n_qs) {
+  constexpr int R = G * QE;  // live rows of an entry's 16-row tile (query-major: r = i * G + g)
+  static_assert(R <= 16, "an entry's rows must fit one 16-row MMA tile");
   constexpr int PAGE = 16 * D * 2;
   constexpr int NP = kChunkPages;
   // sliding window (gpt-oss, window > 0): a sequence's keys are [kst, ctx), kst = max(0, ctx -
@@ -315,6 +323,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int prefix[kMaxB + 1];  // chunk units before sequence b (< 2^31: B * n_kv * ctx/32)
   __shared__ int s_ctx[kMaxB], s_slot[kMaxB];
+  __shared__ int s_qrow[QE > 1 ? kMaxB : 1], s_nq[QE > 1 ? kMaxB : 1];
   __shared__ int s_wbase[kMaxB + 1];  // pair-aligned partition: warps before sequence b
   __shared__ int s_wsum[kDecWarps], s_target;
   __shared__ __align__(8) uint64_t full_bars[kDecWarps * STAGES];
@@ -336,6 +345,10 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
         const int c = ctx_lens[b];
         s_ctx[b] = c;
         s_slot[b] = slots[b];
+        if constexpr (QE > 1) {
+          s_qrow[b] = q_rows[b];
+          s_nq[b] = n_qs[b];
+        }
         local += n_kv * nchunks(c);
       }
     }
@@ -506,7 +519,11 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
 #pragma unroll
     for (int s2 = 0; s2 < STAGES - 1; ++s2) {
       if (s2 < n) {
+#ifndef STB_MQ_NODEFER
+        if (QE > 1 || ld.c == ld.chunks - 1) {  // multi-query entries: a run's new rows span pages
+#else
         if (ld.c == ld.chunks - 1) {
+#endif
           deferred |= 1 << s2;
           dcur[s2] = ld;
 #pragma unroll
@@ -526,6 +543,13 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       if (deferred & (1 << s2)) issue(dcur[s2], s2, dpid[s2]);
   }
   Cur cu = locate(u0);
+  // row r of pair (b, kh): query r / G of the entry (always 0 for decode entries), head r % G
+  auto live = [&](int b, int r) { return QE > 1 ? (r < R && r / G < s_nq[b]) : r < G; };
+  auto row_off = [&](int b, int kh, int r) -> int64_t {
+    const int qrow = QE > 1 ? s_qrow[b] + r / G : b;
+    return ((int64_t)qrow * n_q + kh * G + r % G) * D;
+  };
+  static_assert(QE == 1 || kChunkPages == 1, "multi-query entries need one page per chunk (warp-uniform limits)");
   uint32_t qf[D / 16][4];
   RowState<D> st;
   bool open = false;
@@ -538,15 +562,21 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       seg_ctx = cu.ctx;
       seg_start = u0 + i;
       const int r0 = lane >> 2, r1 = r0 + 8;
-      const __nv_bfloat16* qb = q + ((int64_t)cu.b * n_q + cu.kh * G) * D;
-      load_q<D>(qf, r0 < G ? qb + r0 * D : nullptr, r1 < G ? qb + r1 * D : nullptr, qscale, lane);
+      load_q<D>(qf, live(cu.b, r0) ? q + row_off(cu.b, cu.kh, r0) : nullptr,
+                live(cu.b, r1) ? q + row_off(cu.b, cu.kh, r1) : nullptr, qscale, lane);
       st.init();
     }
     mbar_wait(full + (i % STAGES), (uint32_t)(i / STAGES) & 1u);
     const int kbase = (cu.c0 + cu.c) * 16 * NP;
     const int lim = seg_ctx - kbase;
     const int lo = window > 0 ? max(0, seg_ctx - window) - kbase : 0;
-    chunk_step<D, NP>(qf, wbase + (i % STAGES) * STAGE, lim, lim, st, lane, lo);
+    int lim0 = lim, lim1 = lim;
+    if constexpr (QE > 1) {  // query i of an n-query entry sees keys < ctx - (n - 1 - i)
+      const int nq = s_nq[cu.b], r0 = lane >> 2, r1 = r0 + 8;
+      if (r0 < R && r0 / G < nq) lim0 = lim - (nq - 1 - r0 / G);
+      if (r1 < R && r1 / G < nq) lim1 = lim - (nq - 1 - r1 / G);
+    }
+    chunk_step<D, NP>(qf, wbase + (i % STAGES) * STAGE, lim0, lim1, st, lane, lo);
     __syncwarp();  // every lane's ldmatrix reads of the slot refilled below are done
     if (lane == 0 && i + STAGES - 1 < n) {
       fence_proxy_async_smem();
@@ -565,36 +595,39 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       const int r0 = lane >> 2, r1 = r0 + 8;
       const int sb = cu.b, skh = cu.kh;
       const bool whole = seg_first == 0 && pair_end;
+#ifdef STB_MQ_DEBUG
+      if (QE > 1 && lane == 0 && cu.kh == 0)
+        printf("close b=%d kh=%d w=%d whole=%d seg_first=%d chunks=%d c=%d i=%d n=%d T_al=%d W=%d\n", cu.b, cu.kh, w,
+               (int)whole, seg_first, cu.chunks, cu.c, i, n, T_al, W);
+#endif
       if (whole && sinks != nullptr) {  // the sink's exp(logit) joins the denominator (log2 domain)
-        if (r0 < G) l0 += fast_exp2(sinks[skh * G + r0] * kLog2e - st.m[0]);
-        if (r1 < G) l1 += fast_exp2(sinks[skh * G + r1] * kLog2e - st.m[1]);
+        if (live(sb, r0)) l0 += fast_exp2(sinks[skh * G + r0 % G] * kLog2e - st.m[0]);
+        if (live(sb, r1)) l1 += fast_exp2(sinks[skh * G + r1 % G] * kLog2e - st.m[1]);
       }
       const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
       if (whole) {
 #pragma unroll
         for (int nd = 0; nd < D / 8; ++nd) {
           const int c = nd * 8 + (lane & 3) * 2;
-          if (r0 < G)
-            *reinterpret_cast<uint32_t*>(out + ((int64_t)sb * n_q + skh * G + r0) * D + c) =
-                pack_bf16(st.o[nd][0] * inv0, st.o[nd][1] * inv0);
-          if (r1 < G)
-            *reinterpret_cast<uint32_t*>(out + ((int64_t)sb * n_q + skh * G + r1) * D + c) =
-                pack_bf16(st.o[nd][2] * inv1, st.o[nd][3] * inv1);
+          if (live(sb, r0))
+            *reinterpret_cast<uint32_t*>(out + row_off(sb, skh, r0) + c) = pack_bf16(st.o[nd][0] * inv0, st.o[nd][1] * inv0);
+          if (live(sb, r1))
+            *reinterpret_cast<uint32_t*>(out + row_off(sb, skh, r1) + c) = pack_bf16(st.o[nd][2] * inv1, st.o[nd][3] * inv1);
         }
       } else {
         const int slot = w * 2 + (seg_start == u0 ? 0 : 1);
-        float* op = o_part + (int64_t)slot * G * D;
+        float* op = o_part + (int64_t)slot * R * D;
 #pragma unroll
         for (int nd = 0; nd < D / 8; ++nd) {
           const int c = nd * 8 + (lane & 3) * 2;
-          if (r0 < G)
+          if (r0 < R)
             __stcg(reinterpret_cast<float2*>(op + r0 * D + c), make_float2(st.o[nd][0] * inv0, st.o[nd][1] * inv0));
-          if (r1 < G)
+          if (r1 < R)
             __stcg(reinterpret_cast<float2*>(op + r1 * D + c), make_float2(st.o[nd][2] * inv1, st.o[nd][3] * inv1));
         }
         if ((lane & 3) == 0) {
-          if (r0 < G) __stcg(lse_part + slot * G + r0, l0 > 0.f ? st.m[0] + log2f(l0) : -INFINITY);
-          if (r1 < G) __stcg(lse_part + slot * G + r1, l1 > 0.f ? st.m[1] + log2f(l1) : -INFINITY);
+          if (r0 < R) __stcg(lse_part + slot * R + r0, l0 > 0.f ? st.m[0] + log2f(l0) : -INFINITY);
+          if (r1 < R) __stcg(lse_part + slot * R + r1, l1 > 0.f ? st.m[1] + log2f(l1) : -INFINITY);
         }
         __threadfence();
         __syncwarp();
@@ -611,6 +644,11 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
         int last = 0;
         if (lane == 0) last = atomicAdd(&tickets[sb * n_kv + skh], 1) == wl - wf;
         last = __shfl_sync(0xffffffffu, last, 0);
+#ifdef STB_MQ_DEBUG
+        if (QE > 1 && lane == 0 && skh == 0)
+          printf("seg b=%d kh=%d w=%d wf=%d wl=%d ticket_last=%d qrow=%d nq=%d live0=%d off0=%lld\n", sb, skh, w, wf, wl,
+                 last, s_qrow[sb], s_nq[sb], (int)live(sb, 0), (long long)row_off(sb, skh, 0));
+#endif
         if (last) {
           __threadfence();
           // merge the nc partials of this pair: lanes own contributors for the LSE
@@ -620,57 +658,67 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
           auto part = [&](int c) {
             return c * 2 + ((!T_al && c == wf && (U * c / W) < pstart) ? 1 : 0);
           };
-          float M[G], L[G], wt_l[G];
+          // rows in groups of RG (a multi-query entry's 16 rows would not fit the registers at
+          // once); groups whose first row is a dead query are skipped
+          constexpr int RG = QE > 1 ? 4 : R;
+#pragma unroll 1
+          for (int rg = 0; rg < R; rg += RG) {
+            if (QE > 1 && !live(sb, rg)) continue;
+            float M[RG], L[RG], wt_l[RG];
 #pragma unroll
-          for (int r = 0; r < G; ++r) M[r] = -INFINITY, L[r] = 0.f, wt_l[r] = 0.f;
-          for (int j = lane; j < nc; j += 32) {
-            const int sl = part(wf + j);
+            for (int r = 0; r < RG; ++r) M[r] = -INFINITY, L[r] = 0.f, wt_l[r] = 0.f;
+            for (int j = lane; j < nc; j += 32) {
+              const int sl = part(wf + j);
 #pragma unroll
-            for (int r = 0; r < G; ++r) M[r] = fmaxf(M[r], __ldcg(lse_part + sl * G + r));
-          }
-#pragma unroll
-          for (int r = 0; r < G; ++r)
-#pragma unroll
-            for (int o = 16; o; o >>= 1) M[r] = fmaxf(M[r], __shfl_xor_sync(0xffffffffu, M[r], o));
-          for (int j = lane; j < nc; j += 32) {
-            const int sl = part(wf + j);
-#pragma unroll
-            for (int r = 0; r < G; ++r) {
-              const float wt = M[r] == -INFINITY ? 0.f : exp2f(__ldcg(lse_part + sl * G + r) - M[r]);
-              L[r] += wt;
-              if (j < 32) wt_l[r] = wt;
+              for (int r = 0; r < RG; ++r) M[r] = fmaxf(M[r], __ldcg(lse_part + sl * R + rg + r));
             }
-          }
 #pragma unroll
-          for (int r = 0; r < G; ++r)
+            for (int r = 0; r < RG; ++r)
 #pragma unroll
-            for (int o = 16; o; o >>= 1) L[r] += __shfl_xor_sync(0xffffffffu, L[r], o);
-          if (sinks != nullptr) {
+              for (int o = 16; o; o >>= 1) M[r] = fmaxf(M[r], __shfl_xor_sync(0xffffffffu, M[r], o));
+            for (int j = lane; j < nc; j += 32) {
+              const int sl = part(wf + j);
 #pragma unroll
-            for (int r = 0; r < G; ++r) L[r] += exp2f(sinks[skh * G + r] * kLog2e - M[r]);
-          }
-          float acc[G][D / 32];
+              for (int r = 0; r < RG; ++r) {
+                const float wt = M[r] == -INFINITY ? 0.f : exp2f(__ldcg(lse_part + sl * R + rg + r) - M[r]);
+                L[r] += wt;
+                if (j < 32) wt_l[r] = wt;
+              }
+            }
 #pragma unroll
-          for (int r = 0; r < G; ++r)
+            for (int r = 0; r < RG; ++r)
 #pragma unroll
-            for (int j = 0; j < D / 32; ++j) acc[r][j] = 0.f;
+              for (int o = 16; o; o >>= 1) L[r] += __shfl_xor_sync(0xffffffffu, L[r], o);
+            if (sinks != nullptr) {
+#pragma unroll
+              for (int r = 0; r < RG; ++r) L[r] += exp2f(sinks[skh * G + (rg + r) % G] * kLog2e - M[r]);
+            }
+            float acc[RG][D / 32];
+#pragma unroll
+            for (int r = 0; r < RG; ++r)
+#pragma unroll
+              for (int j = 0; j < D / 32; ++j) acc[r][j] = 0.f;
 #pragma unroll 4
-          for (int c = 0; c < nc; ++c) {
-            const int sl = part(wf + c);
+            for (int c = 0; c < nc; ++c) {
+              const int sl = part(wf + c);
 #pragma unroll
-            for (int r = 0; r < G; ++r) {
-              float wt = __shfl_sync(0xffffffffu, wt_l[r], c & 31);
-              if (c >= 32) wt = M[r] == -INFINITY ? 0.f : exp2f(__ldcg(lse_part + sl * G + r) - M[r]);
+              for (int r = 0; r < RG; ++r) {
+                float wt = __shfl_sync(0xffffffffu, wt_l[r], c & 31);
+                if (c >= 32) wt = M[r] == -INFINITY ? 0.f : exp2f(__ldcg(lse_part + sl * R + rg + r) - M[r]);
 #pragma unroll
-              for (int j = 0; j < D / 32; ++j) acc[r][j] += wt * __ldcg(o_part + ((int64_t)sl * G + r) * D + j * 32 + lane);
+                for (int j = 0; j < D / 32; ++j)
+                  acc[r][j] += wt * __ldcg(o_part + ((int64_t)sl * R + rg + r) * D + j * 32 + lane);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+              if (!live(sb, rg + r)) continue;
+#pragma unroll
+              for (int j = 0; j < D / 32; ++j)
+                out[row_off(sb, skh, rg + r) + j * 32 + lane] =
+                    __float2bfloat16_rn(L[r] > 0.f ? acc[r][j] / L[r] : 0.f);
             }
           }
-#pragma unroll
-          for (int r = 0; r < G; ++r)
-#pragma unroll
-            for (int j = 0; j < D / 32; ++j)
-              out[((int64_t)sb * n_q + skh * G + r) * D + j * 32 + lane] =
-                  __float2bfloat16_rn(L[r] > 0.f ? acc[r][j] / L[r] : 0.f);
           if (lane == 0) tickets[sb * n_kv + skh] = 0;
         }
       }
@@ -794,21 +842,25 @@ inline int decode_sms(int) { return device_sms(); }
 // (B * n_kv, zeroed by the caller once; the merging warp resets its ticket, so the region
 // is zero again after every launch). Nothing is allocated here: a CUDA graph captured for
 // any B keeps pointing at the caller's buffer, whose growth the caller owns.
-inline size_t decode_part_floats(int sms, int G, int D) {
-  return (size_t)kDecMaxPerSm * sms * kDecWarps * 2 * G * (D + 1);
+// Rows per partial slot are sized for the widest entry (16: a multi-query entry's full tile), so
+// decode-only and multi-query launches share one workspace and one ticket offset.
+constexpr int kPartRows = 16;
+inline size_t decode_part_floats(int sms, int D) {
+  return (size_t)kDecMaxPerSm * sms * kDecWarps * 2 * kPartRows * (D + 1);
 }
 
-template <int D, int G>
+template <int D, int G, int QE>
 int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
-                  float qscale, int window, const float* sinks, void* work, cudaStream_t st) {
+                  float qscale, int window, const float* sinks, const int32_t* q_rows, const int32_t* n_qs, void* work,
+                  cudaStream_t st) {
   if (B > kMaxB) return fail(STB_EINVAL, "attn_decode: at most %d sequences per step", kMaxB);
   if (!work) return fail(STB_EINVAL, "attn_decode: NULL workspace");
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = decode_sms(dev);
   constexpr size_t smem = (size_t)kDecWarps * kDecodeStages * kChunkPages * 2 * 16 * D * 2;
-  auto kern = attn_decode_kernel<D, G, kDecodeStages>;
+  auto kern = attn_decode_kernel<D, G, QE, kDecodeStages>;
   static int per_sm_of[kMaxDevices] = {};
   int& per_sm = per_sm_of[dev < kMaxDevices ? dev : 0];
   if (!per_sm) {
@@ -817,13 +869,15 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32 * kDecWarps, smem) != cudaSuccess || n < 1) n = 1;
     per_sm = std::min(n, kDecMaxPerSm);
   }
+  smem_attr_once(kern, (int)smem);
   const int grid = per_sm * sms;
   const int W = grid * kDecWarps;
+  constexpr int R = G * QE;
   float* o_part = (float*)work;
-  float* lse_part = o_part + (size_t)W * 2 * G * D;
-  int* tickets = (int*)(o_part + decode_part_floats(sms, G, D));
+  float* lse_part = o_part + (size_t)W * 2 * R * D;
+  int* tickets = (int*)(o_part + decode_part_floats(sms, D));
   cudaError_t e = launch_k(kern, dim3(grid), dim3(32 * kDecWarps), smem, st, q, out, kp, vp, table, max_bps, slots, ctx,
-                           B, n_kv, qscale, o_part, lse_part, tickets, window, sinks);
+                           B, n_kv, qscale, o_part, lse_part, tickets, window, sinks, q_rows, n_qs);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_decode launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
@@ -850,7 +904,7 @@ int64_t stb_attn_decode_workspace(int B, int n_q, int n_kv, int d_head) {
   if (B < 0 || n_q <= 0 || n_kv <= 0 || n_q % n_kv || d_head <= 0) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t floats = decode_part_floats(decode_sms(dev), n_q / n_kv, d_head);
+  const size_t floats = decode_part_floats(decode_sms(dev), d_head);
   return (int64_t)(floats * 4 + (size_t)B * n_kv * 4 + 256);
 }
 
@@ -859,9 +913,28 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
   return stb_attn_decode_ex(pool, layer, q, out, slots, ctx_lens, B, n_q, scale, max_ctx, 0, nullptr, work, stream);
 }
 
+static int attn_decode_impl(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                            const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
+                            float scale, int max_ctx, int window, const float* sinks, void* work, void* stream);
+
 int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                        const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, int window,
                        const float* sinks, void* work, void* stream) {
+  return attn_decode_impl(pool, layer, q, out, slots, ctx_lens, nullptr, nullptr, B, n_q, scale, max_ctx, window, sinks,
+                          work, stream);
+}
+
+int stb_attn_decode_mq(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                       const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
+                       float scale, int max_ctx, void* work, void* stream) {
+  if (!q_rows || !n_qs) return fail(STB_EINVAL, "attn_decode_mq: q_rows and n_qs are required");
+  return attn_decode_impl(pool, layer, q, out, slots, ctx_lens, q_rows, n_qs, B, n_q, scale, max_ctx, 0, nullptr, work,
+                          stream);
+}
+
+static int attn_decode_impl(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                            const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
+                            float scale, int max_ctx, int window, const float* sinks, void* work, void* stream) {
   if (window < 0) return fail(STB_EINVAL, "attn_decode: window %d < 0", window);
   void *kp, *vp;
   if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
@@ -881,13 +954,26 @@ int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, c
   auto* kk = (const __nv_bfloat16*)kp;
   auto* vv = (const __nv_bfloat16*)vp;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, window, sinks, work, st
-  if (d_head == 128 && g == 4) return launch_decode<128, 4>(ARGS);
-  if (d_head == 128 && g == 8) return launch_decode<128, 8>(ARGS);
-  if (d_head == 128 && g == 1) return launch_decode<128, 1>(ARGS);
-  if (d_head == 64 && g == 2) return launch_decode<64, 2>(ARGS);
-  if (d_head == 64 && g == 8) return launch_decode<64, 8>(ARGS);
-  if (d_head == 64 && g == 4) return launch_decode<64, 4>(ARGS);
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, window, sinks, q_rows, n_qs, work, st
+#ifdef STB_MQ_FORCE_QE1
+  if (false) {
+#else
+  if (q_rows != nullptr) {  // multi-query entries: QE = 16 / G queries per 16-row tile
+#endif
+    if (d_head == 128 && g == 4) return launch_decode<128, 4, 4>(ARGS);
+    if (d_head == 128 && g == 8) return launch_decode<128, 8, 2>(ARGS);
+    if (d_head == 128 && g == 1) return launch_decode<128, 1, 16>(ARGS);
+    if (d_head == 64 && g == 2) return launch_decode<64, 2, 8>(ARGS);
+    if (d_head == 64 && g == 8) return launch_decode<64, 8, 2>(ARGS);
+    if (d_head == 64 && g == 4) return launch_decode<64, 4, 4>(ARGS);
+  } else {
+    if (d_head == 128 && g == 4) return launch_decode<128, 4, 1>(ARGS);
+    if (d_head == 128 && g == 8) return launch_decode<128, 8, 1>(ARGS);
+    if (d_head == 128 && g == 1) return launch_decode<128, 1, 1>(ARGS);
+    if (d_head == 64 && g == 2) return launch_decode<64, 2, 1>(ARGS);
+    if (d_head == 64 && g == 8) return launch_decode<64, 8, 1>(ARGS);
+    if (d_head == 64 && g == 4) return launch_decode<64, 4, 1>(ARGS);
+  }
 #undef ARGS
   return fail(STB_EINVAL, "attn_decode: unsupported (d_head=%d, group=%d)", d_head, g);
 }

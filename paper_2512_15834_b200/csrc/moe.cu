@@ -85,7 +85,10 @@ constexpr int a_stages() { return std::min(8, (512 - a_col0<BN>()) / (32 * NTP))
 template <int BN>
 struct MCfg {
   static constexpr int X_BYTES = BN * BK * 2;  // fp16 token rows of one K block, SW128 K-major
-  static constexpr int XS = 8;                 // token-tile ring (L2-resident rows, freed by the MMA)
+#ifndef STB_MOE_XS
+#define STB_MOE_XS 8
+#endif
+  static constexpr int XS = STB_MOE_XS;        // token-tile ring (L2-resident rows, freed by the MMA)
 #ifndef STB_MOE_RING_KB
 #define STB_MOE_RING_KB 196
 #endif

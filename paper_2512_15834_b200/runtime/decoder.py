@@ -30,6 +30,7 @@ static buffers), so the graph is valid for every step of that size.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import math
 import os
 from dataclasses import dataclass
@@ -221,6 +222,10 @@ class StepBatch:
     pre_ctx: np.ndarray      # [S]
     sample_rows: np.ndarray  # [R] rows of the packed step whose logits are sampled
     targets: np.ndarray      # [R] forced ids (-1: unforced)
+    # multi-query K3 entries (filled by Decoder._forward, not by the caller): packed first row and
+    # query count of every K3 entry — decode rows first, then the short runs folded into K3
+    dec_qrow: np.ndarray | None = None
+    dec_nq: np.ndarray | None = None
 
     @property
     def T(self) -> int:
@@ -240,7 +245,17 @@ class StepBatch:
 
 
 FIELDS = ("ids", "pos", "slot_of", "dec_slots", "dec_ctx", "pre_slots", "pre_qstart", "pre_ctx", "sample_rows",
-          "targets")
+          "targets", "dec_qrow", "dec_nq")
+# Short runs (verify passes: the last sampled token + the draft) ride in the decode attention
+# launch as multi-query K3 entries (stb_attn_decode_mq: 16 / group queries per 16-row tile)
+# instead of a separate K2 launch + split merge — when every run of the step has at most this
+# many queries and the model has plain attention (no sliding window, no sinks).
+# STB200_MQ_MAX=0 keeps them on K2.
+MQ_MAX_N = int(os.environ.get("STB200_MQ_MAX", "40"))
+MQ_MIN_DECODE = 16  # decode rows the step must carry for its short runs to ride in K3
+
+
+_EMPTY_I32 = np.zeros(0, dtype=np.int32)
 
 
 def _p(t) -> C.c_void_p:
@@ -316,6 +331,7 @@ class Decoder:
         self._dirty = {"qkv": 0, "proj": 0, "gu": 0, "logits": 0}
         self._stream_cache: dict = {}
         self._blk_cache: dict = {}   # (T, buffers, metadata pointers) -> decode-block op arrays
+        self._mq_B = 0               # K3 entries of the current step when its short runs ride in K3
         self.taps: list | None = None  # debug (canary): residual stream after the embedding and each layer
         # MoE routing statistics for the grouped GEMM's algorithmic bytes: each timed step copies the
         # per-layer expert offsets to pinned memory (4 buffers: eager / graph x 2 flight parities)
@@ -389,6 +405,8 @@ class Decoder:
         off, spans = 0, {}
         for name in FIELDS:
             a = getattr(b, name)
+            if a is None:
+                a = _EMPTY_I32
             n = int(a.shape[0])
             hv[off:off + n] = a
             spans[name] = off
@@ -415,13 +433,49 @@ class Decoder:
             if _NVTX:
                 torch.cuda.nvtx.range_pop()
 
+    def _mq_entries(self, b: StepBatch) -> StepBatch | None:
+        """Fold the step's short runs into K3 as multi-query entries (MQ_MAX_N): entry j of a run of
+        n queries holds queries [QE j, min(QE (j+1), n)) at packed rows B + q_start + QE j, QE = 16 /
+        group; decode rows are single-query entries. None when the step keeps K2."""
+        s = self.shape
+        if not (b.S and MQ_MAX_N and GRAPH_MAX_T == 0 and not s.moe and not s.sinks and not s.sliding_window):
+            return None
+        n = np.diff(b.pre_qstart)
+        # the folded entries re-read their run's pages from L2 ceil(n / QE) times: worth it when the
+        # launch is dominated by decode rows (measured: B=31 + a 33-query run 62 us vs 76 us for K3 +
+        # K2; a lone run 55 us vs 21 us on K2)
+        if int(n.max()) > MQ_MAX_N or b.B_dec < MQ_MIN_DECODE:
+            return None
+        qe = 16 // (s.n_q // s.n_kv)
+        B = b.B_dec
+        slots, ctxs, rows, nqs = [b.dec_slots], [b.dec_ctx], [np.arange(B, dtype=np.int32)], [np.ones(B, np.int32)]
+        for i in range(b.S):
+            ni, c = int(n[i]), int(b.pre_ctx[i])
+            j = np.arange(0, ni, qe, dtype=np.int32)
+            nq = np.minimum(qe, ni - j).astype(np.int32)
+            slots.append(np.full(len(j), b.pre_slots[i], np.int32))
+            ctxs.append((c - ni + j + nq).astype(np.int32))
+            rows.append((B + int(b.pre_qstart[i]) + j).astype(np.int32))
+            nqs.append(nq)
+        return dataclasses.replace(b, dec_slots=np.concatenate(slots), dec_ctx=np.concatenate(ctxs),
+                                   dec_qrow=np.concatenate(rows), dec_nq=np.concatenate(nqs))
+
     def _forward(self, b: StepBatch) -> torch.Tensor:
         T, R, B, S = b.T, b.R, b.B_dec, b.S
-        self._ensure(T, R, B)
+        dec_bytes = (int(b.dec_ctx.sum()) * 2 * self.shape.kv_dim * 2 + 2 * B * self.shape.q_dim * 2) if B else 0
+        mq = self._mq_entries(b)
+        self._mq_B = 0
+        if mq is not None:
+            # K3's algorithmic bytes gain each folded run's K/V once (its entries re-read them from
+            # L2) plus its q and o rows
+            n = np.diff(b.pre_qstart)
+            dec_bytes += int(np.sum(b.pre_ctx)) * 2 * self.shape.kv_dim * 2 + int(np.sum(n)) * 2 * self.shape.q_dim * 2
+            self._mq_B = int(mq.dec_slots.shape[0])
+            b = mq
+        self._ensure(T, R, max(B, self._mq_B))
         stream = torch.cuda.current_stream().cuda_stream
         self.pool.sync(stream)
         m = self._upload(b)
-        dec_bytes = (int(b.dec_ctx.sum()) * 2 * self.shape.kv_dim * 2 + 2 * B * self.shape.q_dim * 2) if B else 0
         max_q = int(np.max(np.diff(b.pre_qstart))) if S else 0
         if S:  # K2 algorithmic flops per layer: 4 H_q d (n ctx_prev + n(n+1)/2) per run
             n = np.diff(b.pre_qstart).astype(np.float64)
@@ -451,7 +505,7 @@ class Decoder:
         if not graphable:
             if e0 is not None:
                 e0.record()
-            self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if B else 0, dec_bytes)
+            self._launch(m, T, R, B, S, max_q, int(b.dec_ctx.max()) if len(b.dec_ctx) else 0, dec_bytes)
         else:
             # decode graphs assume (and leave) zeroed every GEMM output they accumulate into
             # (stream-K); a whole-tile LM head overwrites the logits, so those stay as they are
@@ -555,17 +609,7 @@ class Decoder:
                 call("stb_qkv_rope_commit", self.pool.h, i, _p(self.qkv), _p(self.q), _p(m["slot_of"]),
                      _p(m["pos"]), T, s.n_q, s.rope_theta, clr, st)
             self._cleared("qkv", clr)
-            if B:
-                ev = self._tick("attn_decode")
-                call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
-                     _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
-                self._tock("attn_decode", ev, dec_bytes)
-            if S:
-                ev = self._tick("attn_prefill")
-                call("stb_attn_prefill_split", self.pool.h, i, _p(self.q[B:].data_ptr()),
-                     _p(self.attn[B:].data_ptr()), _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S,
-                     T - B, s.n_q, self.scale, max_q, self._pre_units, st)
-                self._tock("attn_prefill", ev, self._pre_work)
+            self._attention(call, m, i, T, B, S, max_q, max_ctx, dec_bytes, st)
             self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_rmsnorm", _p(x), _p(self.proj), _p(w[f"l{i}.mlp_norm"]), _p(h), T, d, s.rms_eps, clr, st)
             self._cleared("proj", clr)
@@ -780,6 +824,13 @@ class Decoder:
 
     def _attention(self, call, m, i: int, T: int, B: int, S: int, max_q: int, max_ctx: int, dec_bytes: int, st):
         s = self.shape
+        if self._mq_B:  # decode rows + the step's short runs in one multi-query K3 launch
+            ev = self._tick("attn_decode")
+            call("stb_attn_decode_mq", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
+                 _p(m["dec_ctx"]), _p(m["dec_qrow"]), _p(m["dec_nq"]), self._mq_B, s.n_q, self.scale, max_ctx,
+                 _p(self.work), st)
+            self._tock("attn_decode", ev, dec_bytes)
+            return
         if B:
             ev = self._tick("attn_decode")
             call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),

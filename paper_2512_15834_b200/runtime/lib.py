@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "stb_qkv_norm_rope_commit": (I32, [P, I32, P, P, P, P, I32, I32, F32, P, P, F32, I32, P]),
     "stb_attn_decode_workspace": (I64, [I32, I32, I32, I32]),
     "stb_attn_decode": (I32, [P, I32, P, P, P, P, I32, I32, F32, I32, P, P]),
+    "stb_attn_decode_mq": (I32, [P, I32, P, P, P, P, P, P, I32, I32, F32, I32, P, P]),
     "stb_attn_prefill": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, P]),
     "stb_attn_prefill_split": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, I32, P]),
     "stb_spec_validate": (I32, [P, P, P, P, P, P, P, P, I32, P, P, P, P]),

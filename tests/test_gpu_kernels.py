@@ -413,6 +413,62 @@ def test_attn_decode(lib, shape, ctxs):
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
+@pytest.mark.parametrize("case", [
+    ([700] * 3, [(33, 2984)]),                 # C2 verify pass riding with decode rows
+    ([5, 16, 17], [(1, 1), (4, 10), (21, 33)]),  # ragged runs, a 1-query run, a run that is its whole context
+    ([], [(40, 4096), (33, 100)]),             # runs only (no decode rows)
+    ([8000] * 2, [(17, 8017), (2, 20)]),       # long context, split pairs merged by the ticket warp
+])
+def test_attn_decode_multi_query(lib, shape, case):
+    """stb_attn_decode_mq: decode rows (1-query entries) and short runs folded into K3 as multi-query
+    entries (16 / group queries per 16-row tile, causal inside the run) vs torch fp32."""
+    dec_ctxs, runs = case
+    G = shape.n_q // shape.n_kv
+    qe = 16 // G
+    ctxs = dec_ctxs + [c for _, c in runs]
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) + 8, slots=len(ctxs), bps=600)
+    dense = _fill_pool(lib, pool, shape, ctxs, seed=11)
+    B = len(dec_ctxs)
+    T = B + sum(n for n, _ in runs)
+    q = torch.randn(T, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+    out = torch.full_like(q, float("nan"))
+    e_slot, e_ctx, e_row, e_nq = list(range(B)), list(dec_ctxs), list(range(B)), [1] * B
+    row = B
+    for r, (n, c) in enumerate(runs):
+        for j in range(0, n, qe):
+            nq = min(qe, n - j)
+            e_slot.append(B + r)
+            e_ctx.append(c - n + j + nq)
+            e_row.append(row + j)
+            e_nq.append(nq)
+        row += n
+    t = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
+    E = len(e_slot)
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(E, shape.n_q, shape.n_kv, shape.d_head) // 4),
+                     device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+    meta = [t(a) for a in (e_slot, e_ctx, e_row, e_nq)]  # kept alive until the launches complete
+    lib.call("stb_attn_decode_mq", pool.h, 0, P(q), P(out), *[P(a) for a in meta], E, shape.n_q, scale, max(ctxs),
+             P(ws), stream())
+    for b in range(B):
+        k, v = dense[b]
+        ref = _ref_attn(q[b:b + 1], k, v, torch.tensor([dec_ctxs[b] - 1], device="cuda"), scale)
+        assert rel(out[b:b + 1], ref) < 1e-2, ("decode", b)
+    row = B
+    for r, (n, c) in enumerate(runs):
+        k, v = dense[B + r]
+        ref = _ref_attn(q[row:row + n], k, v, torch.arange(c - n, c, device="cuda"), scale)
+        assert rel(out[row:row + n], ref) < 1e-2, ("run", r)
+        row += n
+    assert torch.isfinite(out.float()).all()  # every row written
+    # the ticket region is left zeroed (graph-safe): a second launch gives the same result
+    out2 = torch.full_like(q, float("nan"))
+    lib.call("stb_attn_decode_mq", pool.h, 0, P(q), P(out2), *[P(a) for a in meta], E, shape.n_q, scale, max(ctxs),
+             P(ws), stream())
+    assert rel(out2, out) < 1e-3
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
 @pytest.mark.parametrize("runs", [[(1, 1)], [(4, 10), (21, 33)], [(300, 300), (33, 1200), (7, 8)],
                                   [(996, 3044), (33, 2174)]])  # C2 trace: ragged ingest + verify
 @pytest.mark.parametrize("amp", [1.0, 40.0], ids=["unit", "spiky"])
