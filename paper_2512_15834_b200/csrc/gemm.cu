@@ -482,11 +482,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(dst, &tm_w, bar, k * BK, f0);
       };
       // weights first: the ring's first slots fill before the dependency wait
+#ifndef STB_GEMM_PREFETCH_STAGES
+#define STB_GEMM_PREFETCH_STAGES 64  // (capped at the ring depth) A/B knob: weight stages issued before the wait
+#endif
+      constexpr int PRE = STB_GEMM_PREFETCH_STAGES < STAGES ? STB_GEMM_PREFETCH_STAGES : STAGES;
       SegIter pre(sched);
       int tile, k0, k1, i = 0;
-      while (i < STAGES && pre.next(tile, k0, k1)) {
+      while (i < PRE && pre.next(tile, k0, k1)) {
         const int f0 = (tile / sched.tiles_m) * BM;
-        for (int k = k0; k < k1 && i < STAGES; ++k, ++i) {
+        for (int k = k0; k < k1 && i < PRE; ++k, ++i) {
           mbar_expect_tx(&full[i], CF::W_BYTES + bn * BK * 2);
           load_w(smem + i * CF::STAGE, k, f0, &full[i]);
         }
