@@ -1619,6 +1619,15 @@ bool pair_enabled() {
   }
   return on == 1;
 }
+// STB200_GEMM_PAIR=2 (A/B only): every whole-tile product with N % 256 == 0 on the pair kernel
+bool pair_forced() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STB200_GEMM_PAIR");
+    on = (e && e[0] == '2') ? 1 : 0;
+  }
+  return on == 1;
+}
 
 template <int BN>
 int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int64_t ldc, int M, int N, int K,
@@ -1641,7 +1650,7 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
     // path across boxes vs a steady 0.77-0.80 on the 1-CTA kernel: they stay there)
     const PairPlan pp = pair_plan(M, N, sms);
     const long pair_tiles = (long)(N / PAIR_BM) * pp.tiles_m;
-    if ((pair_tiles >= 2L * (sms / 2) && N > 8192) || K >= 8192)
+    if ((pair_tiles >= 2L * (sms / 2) && N > 8192) || K >= 8192 || pair_forced())
       return launch_pair<256>(X, lda, W, ldw, C, ldc, M, N, K, pp.bn, pp.tiles_m, flags, st);
   }
   const int bn = pl.bn;

@@ -148,3 +148,31 @@ def test_batch_runtime_parity(name):
     assert len(rt.flights) >= 100 and rows_checked >= 500
     assert mixed >= 10 and verify >= 5 and multi_run >= 3, (mixed, verify, multi_run)
     assert {"full_hit", "partial_hit"} <= set(fates) and engine.evictions > 0, (set(fates), engine.evictions)
+
+
+@pytest.mark.parametrize("name", ["tiny", "qwen3-mini", "llama3-8b[L=2,V=32k]"])
+def test_batch_runtime_parity_verify_in_k3(name, monkeypatch):
+    """The same wall-clock fleet with every step's short runs (verify passes, small ingests)
+    folded into the decode attention launch as multi-query K3 entries (stb_attn_decode_mq) — the
+    benchmarked path for steps with >= 16 decode rows, forced here for this fleet's smaller
+    batches: sampled-row logits within 2e-2 of the oracle replay, raw argmax a near-max, block
+    tables equal to the LIFO replay."""
+    from paper_2512_15834_b200.modelcfg import QWEN3_MINI, SHAPES, TINY
+    from paper_2512_15834_b200.runtime import decoder as D
+
+    monkeypatch.setattr(D, "MQ_MIN_DECODE", 1)
+    calls = {"mq": 0}
+    orig = D.Decoder._mq_entries
+
+    def counted(self, b):
+        r = orig(self, b)
+        calls["mq"] += r is not None
+        return r
+
+    monkeypatch.setattr(D.Decoder, "_mq_entries", counted)
+    shape = {"tiny": TINY, "qwen3-mini": QWEN3_MINI}.get(name) or dataclasses.replace(
+        SHAPES["llama3-8b"], name=name, layers=2, vocab=32768)
+    big = name.startswith("llama")
+    rt, engine = _run_fleet(shape, agents=10 if big else 12, steps=140 if big else 260)
+    assert calls["mq"] >= 5, calls  # steps whose runs rode in K3
+    assert _replay(rt, shape) <= LOGIT_RTOL
