@@ -6,7 +6,8 @@ fp32 inverse frequencies from a float64 pow, fp32 angle pos*inv_freq), GQA
 causal attention, SwiGLU MLP, untied LM head; Qwen3 qk-norm (per-head RMSNorm of q
 and k before RoPE) for qk_norm shapes. Each sequence keeps a
 contiguous fp32 K/V cache; `forward` appends rows at `start` and returns the
-logits of the requested rows.
+logits of the requested rows. Pinned to HuggingFace transformers' Llama / Qwen3 / GptOss
+models on the same weights (tests/test_oracle_vs_hf.py: ~1e-6 relative).
 
 gpt-oss family (config C4, HF GptOss restated): QKV / O biases, per-head attention sinks (an extra
 softmax logit with no value row), sliding-window attention on even layers (key j visible from
