@@ -125,10 +125,20 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// two e2m1 codes (low byte of x) -> fp16x2 (low nibble -> low half)
+// two e2m1 codes (byte B of x) -> fp16x2 (low nibble -> low half). The byte is named as a .b8
+// piece of x, so ptxas folds the selection into the conversion (F2FP.F16.E2M1.UNPACK_B R, x.B1):
+// no shift per byte, a quarter of the converters' instructions
+template <int B>
 __device__ __forceinline__ uint32_t e2m1x2_to_f16x2(uint32_t x) {
   uint32_t d;
-  asm("{\n.reg .b8 b;\nmov.b32 {b, _, _, _}, %1;\ncvt.rn.f16x2.e2m1x2 %0, b;\n}" : "=r"(d) : "r"(x));
+  if constexpr (B == 0)
+    asm("{\n.reg .b8 b0, b1, b2, b3;\nmov.b32 {b0, b1, b2, b3}, %1;\ncvt.rn.f16x2.e2m1x2 %0, b0;\n}" : "=r"(d) : "r"(x));
+  else if constexpr (B == 1)
+    asm("{\n.reg .b8 b0, b1, b2, b3;\nmov.b32 {b0, b1, b2, b3}, %1;\ncvt.rn.f16x2.e2m1x2 %0, b1;\n}" : "=r"(d) : "r"(x));
+  else if constexpr (B == 2)
+    asm("{\n.reg .b8 b0, b1, b2, b3;\nmov.b32 {b0, b1, b2, b3}, %1;\ncvt.rn.f16x2.e2m1x2 %0, b2;\n}" : "=r"(d) : "r"(x));
+  else
+    asm("{\n.reg .b8 b0, b1, b2, b3;\nmov.b32 {b0, b1, b2, b3}, %1;\ncvt.rn.f16x2.e2m1x2 %0, b3;\n}" : "=r"(d) : "r"(x));
   return d;
 }
 __device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
@@ -333,6 +343,27 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+#ifdef STB_MOE_PROF
+// timing experiments only: cycles each role spends in its waits, summed over the grid
+__device__ unsigned long long g_moe_prof[16];
+#define MPROF_DECL unsigned long long mp_[4] = {0, 0, 0, 0}, mp_t0 = clock64();
+#define MPROF_WAIT(slot, call)            \
+  {                                       \
+    const unsigned long long t_ = clock64(); \
+    call;                                 \
+    mp_[slot] += clock64() - t_;          \
+  }
+#define MPROF_FLUSH(base, cond)                                                       \
+  if (cond) {                                                                         \
+    for (int q_ = 0; q_ < 3; ++q_) atomicAdd(&g_moe_prof[base + q_], mp_[q_]);        \
+    atomicAdd(&g_moe_prof[base + 3], clock64() - mp_t0);                             \
+  }
+#else
+#define MPROF_DECL
+#define MPROF_WAIT(slot, call) call;
+#define MPROF_FLUSH(base, cond)
+#endif
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __grid_constant__ CUtensorMap tm_x,
                                                                      const MoeArgs a) {
@@ -418,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
   if (warp == 0) {
     // weight producer: the item's NTP tiles of one K block per stage (one bulk copy each)
     if (elect_one()) {
+      MPROF_DECL
       int i = 0;
       for (int it = blockIdx.x; it < total; it += gridDim.x) {
         int e, nt0, m;
@@ -426,12 +458,13 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
         const uint8_t* wt = a.w + ((int64_t)e * NT + nt0) * KB * RAW;
         for (int kb = 0; kb < KB; ++kb, ++i) {
           const int s = i % WS;
-          mbar_wait(&w_empty[s], ((i / WS) & 1) ^ 1);
+          MPROF_WAIT(0, mbar_wait(&w_empty[s], ((i / WS) & 1) ^ 1));
           mbar_expect_tx(&w_full[s], nt_n * RAW);
           for (int t = 0; t < nt_n; ++t)
             bulk_load(smem_u32(sw + s * WSTAGE + t * RAW), wt + ((int64_t)t * KB + kb) * RAW, RAW, &w_full[s]);
         }
       }
+      MPROF_FLUSH(0, true)
     }
     __syncwarp();
   } else if (warp == 3) {
@@ -457,18 +490,19 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
 #ifndef STB_MOE_MMA_PER_STAGE
 #define STB_MOE_MMA_PER_STAGE (BK / 16)  // < 4: timing experiments only (results are wrong)
 #endif
+      MPROF_DECL
       int i = 0, j = 0;
       for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
         int e, nt0, m;
         decode(it, e, nt0, m);
         const int nt_n = min(NTP, NT - nt0);
         const int buf = j & 1;
-        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        MPROF_WAIT(0, mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1));
         tc_fence_after();
         for (int kb = 0; kb < KB; ++kb, ++i) {
           const int xs = i % XS, as = i % A_STAGES;
-          mbar_wait(&x_full[xs], (i / XS) & 1);        // token rows landed (TMA)
-          mbar_wait(&a_full[as], (i / A_STAGES) & 1);  // weights dequantised into TMEM
+          MPROF_WAIT(1, mbar_wait(&x_full[xs], (i / XS) & 1));        // token rows landed (TMA)
+          MPROF_WAIT(2, mbar_wait(&a_full[as], (i / A_STAGES) & 1));  // weights dequantised into TMEM
           tc_fence_after();
           const uint64_t bdesc = umma_desc_kmajor_sw128(smem_u32(sx + xs * CF::X_BYTES), 1024);
           for (int t = 0; t < nt_n; ++t) {
@@ -483,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
         }
         umma_commit(&acc_full[buf]);
       }
+      MPROF_FLUSH(4, true)
     }
     __syncwarp();
   } else if (warp >= 4 && warp < 4 + kConvWarps) {
@@ -491,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
     const int q = warp & 3, t = ((warp - 4) >> 2) % NTP, par = (warp - 4) / (4 * NTP), r = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t sw_u32 = smem_u32(sw);
+    MPROF_DECL
     int i = 0;
     for (int it = blockIdx.x; it < total; it += gridDim.x) {
       int e, nt0, m;
@@ -499,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
       for (int kb = 0; kb < KB; ++kb, ++i) {
         if (i % CPAR != par) continue;
         const int s = i % WS, as = i % A_STAGES;
-        mbar_wait(&w_full[s], (i / WS) & 1);
+        MPROF_WAIT(0, mbar_wait(&w_full[s], (i / WS) & 1));
         uint32_t out[32];
 #ifdef STB_MOE_SKIP_CONVERT  // timing experiments only: stream the weights, convert nothing
         __syncwarp();
@@ -522,20 +558,23 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
 #pragma unroll
           for (int w = 0; w < 8; ++w) {
             const uint32_t scl = w < 4 ? s0 : s1;  // bytes 0-15: values 0-31 (scale 0), 16-31: scale 1
-#pragma unroll
-            for (int b = 0; b < 4; ++b) out[w * 4 + b] = hmul2(e2m1x2_to_f16x2(wv[w] >> (8 * b)), scl);
+            out[w * 4 + 0] = hmul2(e2m1x2_to_f16x2<0>(wv[w]), scl);
+            out[w * 4 + 1] = hmul2(e2m1x2_to_f16x2<1>(wv[w]), scl);
+            out[w * 4 + 2] = hmul2(e2m1x2_to_f16x2<2>(wv[w]), scl);
+            out[w * 4 + 3] = hmul2(e2m1x2_to_f16x2<3>(wv[w]), scl);
           }
         } else {
           __syncwarp();
           if (lane == 0) mbar_arrive(&w_empty[s]);
         }
-        mbar_wait(&a_empty[as], ((i / A_STAGES) & 1) ^ 1);
+        MPROF_WAIT(1, mbar_wait(&a_empty[as], ((i / A_STAGES) & 1) ^ 1));
         tc_fence_after();
         if (live) tmem_st32_wait_fence(tmem + lane_addr + A_COL0 + (as * NTP + t) * 32, out);
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[as]);
       }
     }
+    MPROF_FLUSH(8, lane == 0)
   } else if (warp >= 4 + kConvWarps) {
     // epilogue: thread = weight row (feature) of each of the item's tiles; columns = tokens
     const int q = warp & 3;
@@ -710,3 +749,12 @@ int stb_moe_combine(float* x, const float* y, int T, int d, int k, const int32_t
 }
 
 }  // extern "C"
+
+#ifdef STB_MOE_PROF
+extern "C" int stb_debug_moe_prof(unsigned long long* host16) {
+  cudaMemcpyFromSymbol(host16, g_moe_prof, 16 * sizeof(unsigned long long));
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_moe_prof, z, sizeof(z));
+  return 0;
+}
+#endif

@@ -80,6 +80,18 @@ def main():
             us = e0.elapsed_time(e1) / a.iters * 1e3
             byts = touched * (-(-N // 128)) * (K // 64) * W.TILE_BYTES + rows * K * 2 + rows * ob
             res["gate_up" if kind == 1 else "down"] = (round(us, 1), round(byts / us / 1e3, 1), round(byts / us / 1e3 / peak, 3))
+            prof = getattr(L.load(), "stb_debug_moe_prof", None)  # -DSTB_MOE_PROF variants only
+            if prof is not None:
+                buf = (C.c_ulonglong * 16)()
+                prof(buf)
+                run(kind)
+                torch.cuda.synchronize()
+                prof(buf)
+                v = list(buf)
+                pct = lambda w, t: f"{100 * w / max(t, 1):4.1f}%"  # noqa: E731
+                print(f"   T={T} {'gate_up' if kind == 1 else 'down'} waits: producer w_empty {pct(v[0], v[3])} | "
+                      f"MMA acc_empty {pct(v[4], v[7])} x_full {pct(v[5], v[7])} a_full {pct(v[6], v[7])} | "
+                      f"converters w_full {pct(v[8], v[11])} a_empty {pct(v[9], v[11])}", flush=True)
         print(f"T={T:5d} experts touched {touched:3d}: " + "  ".join(f"{n} {u} us {g} GB/s ({f})" for n, (u, g, f) in res.items()),
               flush=True)
 
