@@ -303,6 +303,20 @@ __device__ __forceinline__ int warp_of(int64_t u, int64_t U, int W) {
 // a (entry, kv head) pair is then QE queries x G heads instead of one query's G heads (rows G..15
 // of a decode tile are dead), so a short verify run rides in the decode launch: the entries of
 // one run re-read the same pages from L2, and no separate prefill launch or merge is needed.
+#ifdef STB_K3_TRACE
+// timing experiments only: per warp {entry, partition done, first page landed, last chunk done,
+// exit} in %globaltimer ns (stb_debug_k3_trace)
+__device__ unsigned long long* g_k3t = nullptr;
+__device__ unsigned int g_k3t_n = 0, g_k3t_cap = 0;
+__device__ __forceinline__ unsigned long long k3_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K3T(i) k3t[i] = k3_now()
+#else
+#define K3T(i)
+#endif
 template <int D, int G, int QE, int STAGES>
 __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ kpages,
@@ -329,6 +343,18 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   __shared__ __align__(8) uint64_t full_bars[kDecWarps * STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = n_kv * G;
+#ifdef STB_K3_TRACE
+  unsigned long long k3t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  K3T(0);
+  auto k3_flush = [&]() {
+    if (g_k3t != nullptr && lane == 0) {
+      K3T(5);
+      const unsigned slot = atomicAdd(&g_k3t_n, 1u);
+      if (slot < g_k3t_cap)
+        for (int j = 0; j < 8; ++j) g_k3t[(size_t)slot * 8 + j] = j == 7 ? (unsigned long long)(blockIdx.x * 64 + warp) : k3t[j];
+    }
+  };
+#endif
   if (threadIdx.x == 0) {
     for (int s2 = 0; s2 < kDecWarps * STAGES; ++s2) mbar_init(&full_bars[s2], 1);
     fence_mbar_init();
@@ -372,6 +398,9 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     if (threadIdx.x == 32 * kDecWarps - 1) prefix[B] = run;
   }
   __syncthreads();
+#ifdef STB_K3_TRACE
+  K3T(6);
+#endif
   pdl_launch();
   const int64_t U = prefix[B];
   // Work partition. Pair-aligned when it fits: every (sequence, kv head) pair is cut into
@@ -420,7 +449,12 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   const int T_al = s_target;  // > 0: pair-aligned partition with chunk target T_al
   const int W = T_al ? s_wbase[B] : (int)max((int64_t)1, min((int64_t)Wmax, U / kMinChunks));
   const int w = blockIdx.x * kDecWarps + warp;
+#ifdef STB_K3_TRACE
+  K3T(1);
+  if (w >= W) { k3_flush(); return; }
+#else
   if (w >= W) return;
+#endif
   int64_t u0, u1;
   if (T_al) {
     int lo = 0, hi = B - 1;  // sequence of warp w
@@ -439,7 +473,11 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     u1 = U * (w + 1) / W;
   }
   const int n = (int)(u1 - u0);
+#ifdef STB_K3_TRACE
+  if (n <= 0) { k3_flush(); return; }
+#else
   if (n <= 0) return;
+#endif
 
   // cursor over (b, kh, chunk) — located once by binary search, then incremented;
   // the pair's block-table row and length are cached when the cursor enters it
@@ -567,6 +605,9 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       st.init();
     }
     mbar_wait(full + (i % STAGES), (uint32_t)(i / STAGES) & 1u);
+#ifdef STB_K3_TRACE
+    if (i == 0) K3T(2);
+#endif
     const int kbase = (cu.c0 + cu.c) * 16 * NP;
     const int lim = seg_ctx - kbase;
     const int lo = window > 0 ? max(0, seg_ctx - window) - kbase : 0;
@@ -724,8 +765,14 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       }
       open = false;
     }
+#ifdef STB_K3_TRACE
+    if (i == n - 1) K3T(3);  // (after the last segment's close: its merge, if this warp merged)
+#endif
     advance(cu);
   }
+#ifdef STB_K3_TRACE
+  k3_flush();
+#endif
 }
 
 // ---------------------------------------------------------- short-run prefill
@@ -1034,3 +1081,16 @@ int stb_attn_prefill_ex(stb_kv_pool* pool, int layer, const void* q, void* out, 
 }
 
 }  // extern "C"
+
+#ifdef STB_K3_TRACE
+extern "C" int stb_debug_k3_trace(void* buf, int cap) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, g_k3t_n, sizeof(n));
+  unsigned long long* p = (unsigned long long*)buf;
+  unsigned int c = (unsigned int)cap, z = 0;
+  cudaMemcpyToSymbol(g_k3t, &p, sizeof(p));
+  cudaMemcpyToSymbol(g_k3t_cap, &c, sizeof(c));
+  cudaMemcpyToSymbol(g_k3t_n, &z, sizeof(z));
+  return (int)n;
+}
+#endif
