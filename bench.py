@@ -449,8 +449,12 @@ def run_b200(args, world, rank, local):
     steady_resume0 = len(engine.resume_latencies)
     steady_fates0 = fate_counts(engine)
 
+    body = None
     for _ in range(args.warmup):
-        one_step()
+        if body is None and not rt.runs and not rt.dec.shape.moe:
+            body = gemm_body_fraction(rt, rt.dec.shape, one_step)
+        else:
+            one_step()
     torch.cuda.synchronize()
     barrier(world)
     state["timed"] = {}
@@ -594,7 +598,7 @@ def run_b200(args, world, rank, local):
                                                  f"steps after the pre-roll"),
         "tool_resume_ms_timed_window": pct_ms(rs, f"the {args.steps} timed steps only"),
         "fates_steady_state": steady_fates, "preroll": preroll, "canary": canary,
-        "roofline": roof, "kernels": others, "gpu_launches": int(launches), "clocks": clocks.summary(),
+        "roofline": roof, "gemm_decode_in_step_body": body, "kernels": others, "gpu_launches": int(launches), "clocks": clocks.summary(),
         "cpu_baseline": cpu, "emitted_tokens": int(tot_emit), "tasks_completed": fleet.completed,
         "graph_replays": rt.dec.graph_replays,
         "step_mix": {"decode_steps": len(graphed), "decode_ms_avg": round(sum(graphed) / max(1, len(graphed)), 3),
@@ -717,6 +721,55 @@ def fate_counts(engine) -> dict:
 
 
 IDLE_LIMIT_S = 120.0
+
+
+def gemm_body_fraction(rt, shape, one_step):
+    """Secondary view of the decode GEMMs (one decode-only warm-up step, outside the timed window):
+    each launch's dependent execution (first CTA past griddepcontrol.wait -> last CTA exit,
+    %globaltimer, stb_debug_gemm_trace) inside the real PDL-chained step, against its algorithmic
+    bytes. The roofline entry itself is
+    the CUDA-event timing of the timed window, where every bracketed launch starts cold."""
+    import ctypes as C
+
+    import numpy as np
+
+    import torch
+
+    from paper_2512_15834_b200.runtime import lib
+
+    fn = lib.load().stb_debug_gemm_trace
+    fn.argtypes, fn.restype = [C.c_void_p, C.c_int], C.c_int
+    rt.drain()
+    torch.cuda.synchronize()
+    cap = 1 << 16
+    buf = torch.zeros(cap * 8, dtype=torch.int64, device="cuda")
+    fn(C.c_void_p(buf.data_ptr()), cap)
+    one_step()
+    rt.drain()
+    torch.cuda.synchronize()
+    n = fn(None, 0)
+    fn(None, 0)
+    if n <= 0 or n >= cap:
+        return None
+    rec = buf[:n * 8].view(n, 8).cpu().numpy().astype(np.int64)
+    # from the first CTA's return from griddepcontrol.wait (the launch is programmatically early:
+    # its CTAs enter, set up and prefetch weights while the previous kernel still runs) to the
+    # last CTA's exit
+    bodies = [(rec[rec[:, 0] == t, 7].max() - rec[rec[:, 0] == t, 4].min()) / 1e9 for t in np.unique(rec[:, 0])]
+    M = rt.dec.last_step_tokens
+    s = shape
+    per_layer = [(s.q_dim + 2 * s.kv_dim, s.d_model), (s.d_model, s.q_dim), (2 * s.d_ff, s.d_model), (s.d_model, s.d_ff)]
+    if len(bodies) != 4 * s.layers + 1:  # not a plain decode step (e.g. the fused / block paths)
+        return None
+    byts = s.layers * sum(N * K * 2 + M * K * 2 + M * N * 4 for N, K in per_layer)
+    byts += s.vocab * s.d_model * 2 + M * s.d_model * 2 + M * s.vocab * 4
+    t = float(sum(bodies))
+    hbm = peaks()[0]
+    return {"launches": len(bodies), "avg_body_us": round(t / len(bodies) * 1e6, 2),
+            "achieved": round(byts / t / 1e9, 1), "frac": round(byts / t / 1e9 / hbm, 4),
+            "what": "decode GEMMs of one decode-only warm-up step (graph-replayed, PDL-chained): from the first "
+                    "CTA past its dependency wait to the last CTA's exit (%globaltimer) per launch vs algorithmic "
+                    "bytes"}
 
 
 def main():

@@ -332,6 +332,7 @@ class Decoder:
         self._stream_cache: dict = {}
         self._blk_cache: dict = {}   # (T, buffers, metadata pointers) -> decode-block op arrays
         self._mq_B = 0               # K3 entries of the current step when its short runs ride in K3
+        self.last_step_tokens = 0
         self.taps: list | None = None  # debug (canary): residual stream after the embedding and each layer
         # MoE routing statistics for the grouped GEMM's algorithmic bytes: each timed step copies the
         # per-layer expert offsets to pinned memory (4 buffers: eager / graph x 2 flight parities)
@@ -462,6 +463,7 @@ class Decoder:
 
     def _forward(self, b: StepBatch) -> torch.Tensor:
         T, R, B, S = b.T, b.R, b.B_dec, b.S
+        self.last_step_tokens = T
         dec_bytes = (int(b.dec_ctx.sum()) * 2 * self.shape.kv_dim * 2 + 2 * B * self.shape.q_dim * 2) if B else 0
         mq = self._mq_entries(b)
         self._mq_B = 0
