@@ -1619,7 +1619,16 @@ bool pair_enabled() {
   }
   return on == 1;
 }
-// STB200_GEMM_PAIR=2 (A/B only): every whole-tile product with N % 256 == 0 on the pair kernel
+// STB200_GEMM_PAIR=3 (A/B only): the round-1 rule (pairs only for >= 2 waves of pair tiles or long K)
+bool pair_legacy() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STB200_GEMM_PAIR");
+    on = (e && e[0] == '3') ? 1 : 0;
+  }
+  return on == 1;
+}
+// STB200_GEMM_PAIR=2: every whole-tile product with N % 256 == 0 on the pair kernel (the default now)
 bool pair_forced() {
   static int on = -1;
   if (on < 0) {
@@ -1648,9 +1657,15 @@ int launch(const void* X, int64_t lda, const void* W, int64_t ldw, float* C, int
     // LM head at M = 608..2080 gain 7-17%; QKV / O at M = 608 — one partial wave — lose 5-13%)
     // (QKV / O-shaped products, N <= 8192 with K = 4096, measured from 0.56 to 0.79 on the pair
     // path across boxes vs a steady 0.77-0.80 on the 1-CTA kernel: they stay there)
+    // Every whole-tile product with N a multiple of 256 runs on CTA pairs: measured in the decode
+    // step with one prefill run packed in (tools/profile_step.py --mix, B = 32, ctx 2k, same box,
+    // alternating runs) 8.41 -> 7.47 ms at 150 new tokens, 9.54 -> 9.41 at 300, 12.19 -> 12.18
+    // at 576, 18.06 -> 17.80 at 1000 — the earlier rule (pairs only with >= 2 waves of pair
+    // tiles or K >= 8192, from microbenchmarks of single products) kept QKV / O and the
+    // one-wave gate-up of small runs on the 1-CTA kernel. STB200_GEMM_PAIR=3 restores that rule.
     const PairPlan pp = pair_plan(M, N, sms);
     const long pair_tiles = (long)(N / PAIR_BM) * pp.tiles_m;
-    if ((pair_tiles >= 2L * (sms / 2) && N > 8192) || K >= 8192 || pair_forced())
+    if (!pair_legacy() || (pair_tiles >= 2L * (sms / 2) && N > 8192) || K >= 8192 || pair_forced())
       return launch_pair<256>(X, lda, W, ldw, C, ldc, M, N, K, pp.bn, pp.tiles_m, flags, st);
   }
   const int bn = pl.bn;
