@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kh = (lin % nyz) % gridDim.y, zz = (lin % nyz) / gridDim.y;
   const int s = zz / max_splits, sp = zz % max_splits;  // run, KV split
   constexpr int QPT = ROWS / G;  // queries per tile
-  pdl_wait();
-  pdl_launch();
+  // the run metadata and the block table are host-uploaded (not written by the preceding kernel),
+  // so everything up to the first Q / K / V copy overlaps the preceding kernel's tail
   const int t0 = q_start[s], n = q_start[s + 1] - t0;
   const int qi0 = bx * 2 * QPT;
   if (qi0 >= n) return;
@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // q and this step's new K / V rows come from the preceding kernels
+  pdl_launch();
   const uint32_t tmem = *tmem_slot;
   // column map: S/P of tile t at t*KT, O of tile t at 2*KT + t*D
   auto tS = [&](int t) { return tmem + t * KT; };
@@ -226,23 +228,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int h = 0; h < CF::HALVES; ++h)
           tma_load_4d(sQ + t * CF::Q_BYTES + h * ROWS * 128, &tm_q, q_full, h * 64, 0, kh, t0 + qi0 + t * QPT);
+      // page ids one KV tile ahead: the block-table loads of tile jj + 1 are in flight while the
+      // producer waits for tile jj's ring slot (they used to sit between the wait and the copies)
+      // (pages past the context are still fetched: finite pool rows, masked to -inf)
+      int pid[KT / 16];
+      auto load_pids = [&](int j, int* dst) {
+#pragma unroll
+        for (int p = 0; p < KT / 16; ++p) dst[p] = __ldg(row + min(j * (KT / 16) + p, max_bps - 1));
+      };
+      load_pids(j0, pid);
       for (int jj = 0; jj < nt; ++jj) {
-        const int j = j0 + jj;
         const int st = jj % KV_STAGES;
+        int nxt[KT / 16];
+        if (jj + 1 < nt) load_pids(j0 + jj + 1, nxt);
         mbar_wait(&kv_empty[st], ((jj / KV_STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], CF::STAGE);
         uint8_t* sk = sKV + st * CF::STAGE;
         uint8_t* sv = sk + CF::KV_BYTES;
 #pragma unroll
         for (int p = 0; p < KT / 16; ++p) {
-          // pages past the context are still fetched (finite pool rows; masked to -inf)
-          const int page = min(j * (KT / 16) + p, max_bps - 1);
-          const int prow = (row[page] * n_kv + kh) * 16;
+          const int prow = (pid[p] * n_kv + kh) * 16;
 #pragma unroll
           for (int h = 0; h < CF::HALVES; ++h) {
             tma_load_2d(sk + h * KT * 128 + p * 16 * 128, &tm_k, &kv_full[st], h * 64, prow);
             tma_load_2d(sv + h * KT * 128 + p * 16 * 128, &tm_v, &kv_full[st], h * 64, prow);
           }
+        }
+        if (jj + 1 < nt) {
+#pragma unroll
+          for (int p = 0; p < KT / 16; ++p) pid[p] = nxt[p];
         }
       }
     }
