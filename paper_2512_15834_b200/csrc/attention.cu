@@ -280,7 +280,10 @@ constexpr int kMaxB = STB_K3_MAXB;  // sequences per decode launch (static smem:
 #endif
 constexpr int kChunkPages = STB_K3_PAGES;  // pages (16 keys each) per online-softmax update
 constexpr int kDecWarps = STB_K3_WARPS;    // warps per CTA (one CTA per SM: smem-bound)
-constexpr int kMinChunks = 8 / STB_K3_PAGES;  // fewest chunks (128 keys) a warp is given: bounds merge fan-in
+#ifndef STB_K3_MINCH
+#define STB_K3_MINCH (8 / STB_K3_PAGES)
+#endif
+constexpr int kMinChunks = STB_K3_MINCH;  // fewest chunks (128 keys) a warp is given: bounds merge fan-in
 
 __device__ __forceinline__ int warp_sum_i(int v) {
 #pragma unroll
