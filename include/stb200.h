@@ -158,6 +158,13 @@ int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t*
                       const int32_t* base_extra, int S, int32_t* accepted, int32_t* consume, int32_t* new_len,
                       void* stream);
 
+/* K4b: canonical tool-call key digests (the `_span_end` key lookup, engine.py:339-355, and the
+ * store's key index, engine.py:63-65): probe / keys hold 128-bit digests as two uint64 each (the
+ * host hashes the canonical key bytes, domain.py:123-158); out[i] = the lowest j with
+ * key_rid[j] == probe_rid[i] and keys[j] == probe[i] (bit-exact), else -1. */
+int stb_key_match(const void* probe, const int32_t* probe_rid, int n, const void* keys, const int32_t* key_rid, int m,
+                  int32_t* out, void* stream);
+
 /* ---- K5: bf16 tensor-core GEMM (tcgen05 + TMA + TMEM) --------------------
  * C[M][N] (fp32, row stride ldc) = A[M][K] (bf16, lda) * W[N][K]^T (bf16, ldw).
  * Persistent, one CTA per SM. split_k: 0 = automatic schedule; 1 = whole

@@ -395,6 +395,48 @@ int stb_sample_forced(float* logits, int64_t ld, const int32_t* target, int R, i
   return STB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// K4b: canonical-key digests, bit-exact. One warp per probe: lanes stride over the key table and
+// the lowest matching index wins (ballot + ffs per 32-entry block, first block with a match).
+__global__ void key_match_kernel(const unsigned long long* __restrict__ probe, const int32_t* __restrict__ probe_rid,
+                                 int n, const unsigned long long* __restrict__ keys,
+                                 const int32_t* __restrict__ key_rid, int m, int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const unsigned long long p0 = probe[2 * i], p1 = probe[2 * i + 1];
+  const int rid = probe_rid[i];
+  int found = -1;
+  for (int base = 0; base < m; base += 32) {
+    const int j = base + lane;
+    const bool hit = j < m && key_rid[j] == rid && keys[2 * j] == p0 && keys[2 * j + 1] == p1;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (bal) {
+      found = base + __ffs(bal) - 1;
+      break;
+    }
+  }
+  if (lane == 0) out[i] = found;
+}
+}  // namespace
+
+extern "C" {
+
+int stb_key_match(const void* probe, const int32_t* probe_rid, int n, const void* keys, const int32_t* key_rid, int m,
+                  int32_t* out, void* stream) {
+  if (n <= 0) return STB_OK;
+  if (m < 0 || !probe || !probe_rid || !out || (m > 0 && (!keys || !key_rid)))
+    return fail(STB_EINVAL, "key_match: bad operands");
+  const int threads = 128, blocks = (n * 32 + threads - 1) / threads;
+  launch_k(key_match_kernel, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream,
+           (const unsigned long long*)probe, probe_rid, n, (const unsigned long long*)keys, key_rid, m, out);
+  STB_CHECK_LAUNCH("key_match");
+  return STB_OK;
+}
+
 int stb_spec_validate(const int32_t* draft, const int32_t* d_off, const int32_t* model, const int32_t* m_off,
                       const int32_t* model_first, const int32_t* span_len, const int32_t* kv_len,
                       const int32_t* base_extra, int S, int32_t* accepted, int32_t* consume, int32_t* new_len,

@@ -47,6 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "stb_attn_prefill": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, P]),
     "stb_attn_prefill_split": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, I32, P]),
     "stb_spec_validate": (I32, [P, P, P, P, P, P, P, P, I32, P, P, P, P]),
+    "stb_key_match": (I32, [P, P, I32, P, P, I32, P, P]),
     "stb_gemm_bf16": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, I32, I32, P]),
     "stb_gemm_is_stream": (I32, [I32, I32, I32]),
     "stb_gemm_bf16_fused": (I32, [P, I64, P, I64, P, I64, I32, I32, I32, I32, P, P]),
