@@ -439,7 +439,7 @@ class Decoder:
         n queries holds queries [QE j, min(QE (j+1), n)) at packed rows B + q_start + QE j, QE = 16 /
         group; decode rows are single-query entries. None when the step keeps K2."""
         s = self.shape
-        if not (b.S and MQ_MAX_N and GRAPH_MAX_T == 0 and not s.moe and not s.sinks and not s.sliding_window):
+        if not (b.S and MQ_MAX_N and not s.moe and not s.sinks and not s.sliding_window):
             return None
         n = np.diff(b.pre_qstart)
         # the folded entries re-read their run's pages from L2 ceil(n / QE) times: worth it when the
@@ -497,7 +497,7 @@ class Decoder:
         graphable = (self.use_graphs and B > 0 and not self.keep_logits
                      and (S == 0 or (T <= GRAPH_MAX_T and S <= GRAPH_MAX_RUNS)))
         e0 = torch.cuda.Event(enable_timing=True) if self.step_events is not None else None
-        shape_key = (B, T, R, S, max_q)
+        shape_key = (B, T, R, S, max_q, self._mq_B)
         if graphable and S > 0 and shape_key not in self._seen:
             # first occurrence of a mixed-step shape runs eagerly (it also initialises every
             # launch's one-time state); the graph is captured, without a warm-up run, only
@@ -522,7 +522,7 @@ class Decoder:
             if timed:
                 par = self._timed_parity
                 self._timed_parity ^= 1
-            key = (B, T, R, S, max_q, timed, par)
+            key = (B, T, R, S, max_q, timed, par, self._mq_B)
             if key not in self.graphs:
                 if len(self.graphs) >= GRAPH_CACHE:  # drop the oldest mixed-step graph
                     old = next((k for k in self.graphs if k[3] > 0), None)
