@@ -120,6 +120,13 @@ int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, c
 int stb_attn_decode_mq(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                        const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
                        float scale, int max_ctx, void* work, void* stream);
+/* Same (q_rows / n_qs may both be NULL: one query per entry), with the work partition shared
+ * across a step's layers: plan_mode 0 computes it in the launch, 1 also stores it in the
+ * workspace, 2 loads the one stored by an earlier launch on the same stream with the same
+ * (B, slots, ctx_lens, q_rows, n_qs) — every layer of a decode step after the first.      */
+int stb_attn_decode_planned(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                            const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
+                            float scale, int max_ctx, int plan_mode, void* work, void* stream);
 
 /* ---- K2: append-prefill attention (n new queries against resident pages)
  * Replaces prefill engine.py:251, verify engine.py:296 and ingest

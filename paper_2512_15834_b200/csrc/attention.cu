@@ -326,7 +326,12 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ vpages, const int32_t* __restrict__ table, int max_bps,
     const int32_t* __restrict__ slots, const int32_t* __restrict__ ctx_lens, int B, int n_kv, float qscale,
     float* __restrict__ o_part, float* __restrict__ lse_part, int* __restrict__ tickets, int window,
-    const float* __restrict__ sinks, const int32_t* __restrict__ q_rows, const int32_t* __restrict__ n_qs) {
+    const float* __restrict__ sinks, const int32_t* __restrict__ q_rows, const int32_t* __restrict__ n_qs,
+    int32_t* __restrict__ plan, int plan_mode) {
+  // plan_mode (the step's later layers reuse layer 0's work partition — same contexts, same grid):
+  // 0 compute the partition here; 1 compute it and CTA 0 stores it in `plan`; 2 load it from
+  // `plan` (stored by an earlier launch of the step: completed before this launch's prologue, by
+  // the programmatic-dependency chain of the layers in between)
   constexpr int R = G * QE;  // live rows of an entry's 16-row tile (query-major: r = i * G + g)
   static_assert(R <= 16, "an entry's rows must fit one 16-row MMA tile");
   constexpr int PAGE = 16 * D * 2;
@@ -362,7 +367,22 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
     for (int s2 = 0; s2 < kDecWarps * STAGES; ++s2) mbar_init(&full_bars[s2], 1);
     fence_mbar_init();
   }
-  {
+  if (plan_mode == 2) {
+    // plan layout: [T_al, W, prefix[0..B], wbase[0..B]]
+    for (int b = threadIdx.x; b <= B; b += blockDim.x) {
+      if (b < B) {
+        s_ctx[b] = ctx_lens[b];
+        s_slot[b] = slots[b];
+        if constexpr (QE > 1) {
+          s_qrow[b] = q_rows[b];
+          s_nq[b] = n_qs[b];
+        }
+      }
+      prefix[b] = __ldcg(plan + 2 + b);
+      s_wbase[b] = __ldcg(plan + 3 + B + b);
+    }
+    if (threadIdx.x == 0) s_target = __ldcg(plan);
+  } else {
     // step metadata (host-uploaded, not produced by the preceding kernel): all threads load
     // ctx / slot in parallel (a serial loop would chain B global-load latencies in front of
     // the first page copy), then a block scan gives the unit prefix
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   // enough pages are in flight. Otherwise (more pairs than warps): equal contiguous ranges
   // of the unit space, segments crossing pair boundaries.
   const int Wmax = gridDim.x * kDecWarps;
-  if (warp == 0) {  // one warp, shuffles only (no block barriers inside the search)
+  if (warp == 0 && plan_mode != 2) {  // one warp, shuffles only (no block barriers inside the search)
     auto chunks = [&](int b) { return nchunks(s_ctx[b]); };
     auto count = [&](int T) {  // warps the pair-aligned cut with target T needs
       int c = 0;
@@ -451,6 +471,16 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
   __syncthreads();
   const int T_al = s_target;  // > 0: pair-aligned partition with chunk target T_al
   const int W = T_al ? s_wbase[B] : (int)max((int64_t)1, min((int64_t)Wmax, U / kMinChunks));
+  if (plan_mode == 1 && blockIdx.x == 0) {  // store the partition for the step's later layers
+    for (int b = threadIdx.x; b <= B; b += blockDim.x) {
+      plan[2 + b] = prefix[b];
+      plan[3 + B + b] = T_al ? s_wbase[b] : 0;
+    }
+    if (threadIdx.x == 0) {
+      plan[0] = T_al;
+      plan[1] = W;
+    }
+  }
   const int w = blockIdx.x * kDecWarps + warp;
 #ifdef STB_K3_TRACE
   K3T(1);
@@ -889,12 +919,15 @@ inline int decode_sms(int) { return device_sms(); }
 
 // Caller workspace layout (stb_attn_decode_workspace): partial (o, lse) rows for every warp
 // of the largest grid K3 can launch on this device, then the split-pair merge tickets
-// (B * n_kv, zeroed by the caller once; the merging warp resets its ticket, so the region
+// (B * n_kv, after the stored partition; zeroed by the caller once; the merging warp resets its ticket, so the region
 // is zero again after every launch). Nothing is allocated here: a CUDA graph captured for
 // any B keeps pointing at the caller's buffer, whose growth the caller owns.
 // Rows per partial slot are sized for the widest entry (16: a multi-query entry's full tile), so
 // decode-only and multi-query launches share one workspace and one ticket offset.
 constexpr int kPartRows = 16;
+// the step's stored K3 partition (plan_mode 1 / 2) sits between the partials and the tickets, at
+// an offset independent of B (the tickets region must stay zero for any later, larger B)
+constexpr int kPlanInts = 2 * kMaxB + 8;
 inline size_t decode_part_floats(int sms, int D) {
   return (size_t)kDecMaxPerSm * sms * kDecWarps * 2 * kPartRows * (D + 1);
 }
@@ -902,8 +935,8 @@ inline size_t decode_part_floats(int sms, int D) {
 template <int D, int G, int QE>
 int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
                   const int32_t* table, int max_bps, const int32_t* slots, const int32_t* ctx, int B, int n_kv,
-                  float qscale, int window, const float* sinks, const int32_t* q_rows, const int32_t* n_qs, void* work,
-                  cudaStream_t st) {
+                  float qscale, int window, const float* sinks, const int32_t* q_rows, const int32_t* n_qs,
+                  int plan_mode, void* work, cudaStream_t st) {
   if (B > kMaxB) return fail(STB_EINVAL, "attn_decode: at most %d sequences per step", kMaxB);
   if (!work) return fail(STB_EINVAL, "attn_decode: NULL workspace");
   int dev = 0;
@@ -925,9 +958,10 @@ int launch_decode(const __nv_bfloat16* q, __nv_bfloat16* out, const __nv_bfloat1
   constexpr int R = G * QE;
   float* o_part = (float*)work;
   float* lse_part = o_part + (size_t)W * 2 * R * D;
-  int* tickets = (int*)(o_part + decode_part_floats(sms, D));
+  int32_t* plan = (int32_t*)(o_part + decode_part_floats(sms, D));  // [T_al, W, prefix[B+1], wbase[B+1]]
+  int* tickets = plan + kPlanInts;
   cudaError_t e = launch_k(kern, dim3(grid), dim3(32 * kDecWarps), smem, st, q, out, kp, vp, table, max_bps, slots, ctx,
-                           B, n_kv, qscale, o_part, lse_part, tickets, window, sinks, q_rows, n_qs);
+                           B, n_kv, qscale, o_part, lse_part, tickets, window, sinks, q_rows, n_qs, plan, plan_mode);
   if (e != cudaSuccess) return fail(STB_ECUDA, "attn_decode launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
@@ -955,7 +989,7 @@ int64_t stb_attn_decode_workspace(int B, int n_q, int n_kv, int d_head) {
   int dev = 0;
   cudaGetDevice(&dev);
   const size_t floats = decode_part_floats(decode_sms(dev), d_head);
-  return (int64_t)(floats * 4 + (size_t)B * n_kv * 4 + 256);
+  return (int64_t)(floats * 4 + (size_t)kPlanInts * 4 + (size_t)B * n_kv * 4 + 256);
 }
 
 int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
@@ -965,26 +999,38 @@ int stb_attn_decode(stb_kv_pool* pool, int layer, const void* q, void* out, cons
 
 static int attn_decode_impl(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                             const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
-                            float scale, int max_ctx, int window, const float* sinks, void* work, void* stream);
+                            float scale, int max_ctx, int window, const float* sinks, int plan_mode, void* work,
+                            void* stream);
 
 int stb_attn_decode_ex(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                        const int32_t* ctx_lens, int B, int n_q, float scale, int max_ctx, int window,
                        const float* sinks, void* work, void* stream) {
   return attn_decode_impl(pool, layer, q, out, slots, ctx_lens, nullptr, nullptr, B, n_q, scale, max_ctx, window, sinks,
-                          work, stream);
+                          0, work, stream);
 }
 
 int stb_attn_decode_mq(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                        const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
                        float scale, int max_ctx, void* work, void* stream) {
   if (!q_rows || !n_qs) return fail(STB_EINVAL, "attn_decode_mq: q_rows and n_qs are required");
-  return attn_decode_impl(pool, layer, q, out, slots, ctx_lens, q_rows, n_qs, B, n_q, scale, max_ctx, 0, nullptr, work,
-                          stream);
+  return attn_decode_impl(pool, layer, q, out, slots, ctx_lens, q_rows, n_qs, B, n_q, scale, max_ctx, 0, nullptr, 0,
+                          work, stream);
+}
+
+int stb_attn_decode_planned(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
+                            const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
+                            float scale, int max_ctx, int plan_mode, void* work, void* stream) {
+  if (plan_mode < 0 || plan_mode > 2) return fail(STB_EINVAL, "attn_decode_planned: plan_mode %d", plan_mode);
+  if ((q_rows == nullptr) != (n_qs == nullptr))
+    return fail(STB_EINVAL, "attn_decode_planned: q_rows and n_qs go together");
+  return attn_decode_impl(pool, layer, q, out, slots, ctx_lens, q_rows, n_qs, B, n_q, scale, max_ctx, 0, nullptr,
+                          plan_mode, work, stream);
 }
 
 static int attn_decode_impl(stb_kv_pool* pool, int layer, const void* q, void* out, const int32_t* slots,
                             const int32_t* ctx_lens, const int32_t* q_rows, const int32_t* n_qs, int B, int n_q,
-                            float scale, int max_ctx, int window, const float* sinks, void* work, void* stream) {
+                            float scale, int max_ctx, int window, const float* sinks, int plan_mode, void* work,
+                            void* stream) {
   if (window < 0) return fail(STB_EINVAL, "attn_decode: window %d < 0", window);
   void *kp, *vp;
   if (int rc = stb_kv_layer_ptrs(pool, layer, &kp, &vp)) return rc;
@@ -1004,7 +1050,7 @@ static int attn_decode_impl(stb_kv_pool* pool, int layer, const void* q, void* o
   auto* kk = (const __nv_bfloat16*)kp;
   auto* vv = (const __nv_bfloat16*)vp;
   cudaStream_t st = (cudaStream_t)stream;
-#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, window, sinks, q_rows, n_qs, work, st
+#define ARGS qq, oo, kk, vv, table, max_bps, slots, ctx_lens, B, n_kv, qs, window, sinks, q_rows, n_qs, plan_mode, work, st
 #ifdef STB_MQ_FORCE_QE1
   if (false) {
 #else

@@ -253,6 +253,9 @@ FIELDS = ("ids", "pos", "slot_of", "dec_slots", "dec_ctx", "pre_slots", "pre_qst
 # STB200_MQ_MAX=0 keeps them on K2.
 MQ_MAX_N = int(os.environ.get("STB200_MQ_MAX", "40"))
 MQ_MIN_DECODE = 16  # decode rows the step must carry for its short runs to ride in K3
+# K3 partition computed once per step (layer 0) and reused by the later layers; STB200_K3_PLAN=0
+# has every launch compute its own
+K3_PLAN = os.environ.get("STB200_K3_PLAN", "1") != "0"
 
 
 _EMPTY_I32 = np.zeros(0, dtype=np.int32)
@@ -826,17 +829,20 @@ class Decoder:
 
     def _attention(self, call, m, i: int, T: int, B: int, S: int, max_q: int, max_ctx: int, dec_bytes: int, st):
         s = self.shape
+        # K3's work partition depends only on the step's entries: layer 0 computes and stores it,
+        # the later layers load it (plan_mode 1 / 2, stb_attn_decode_planned)
+        plan = (1 if i == 0 else 2) if K3_PLAN else 0
         if self._mq_B:  # decode rows + the step's short runs in one multi-query K3 launch
             ev = self._tick("attn_decode")
-            call("stb_attn_decode_mq", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
+            call("stb_attn_decode_planned", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
                  _p(m["dec_ctx"]), _p(m["dec_qrow"]), _p(m["dec_nq"]), self._mq_B, s.n_q, self.scale, max_ctx,
-                 _p(self.work), st)
+                 plan, _p(self.work), st)
             self._tock("attn_decode", ev, dec_bytes)
             return
         if B:
             ev = self._tick("attn_decode")
-            call("stb_attn_decode", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
-                 _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, _p(self.work), st)
+            call("stb_attn_decode_planned", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
+                 _p(m["dec_ctx"]), None, None, B, s.n_q, self.scale, max_ctx, plan, _p(self.work), st)
             self._tock("attn_decode", ev, dec_bytes)
         if S:
             ev = self._tick("attn_prefill")

@@ -44,6 +44,7 @@ SIGNATURES: dict[str, tuple] = {
     "stb_attn_decode_workspace": (I64, [I32, I32, I32, I32]),
     "stb_attn_decode": (I32, [P, I32, P, P, P, P, I32, I32, F32, I32, P, P]),
     "stb_attn_decode_mq": (I32, [P, I32, P, P, P, P, P, P, I32, I32, F32, I32, P, P]),
+    "stb_attn_decode_planned": (I32, [P, I32, P, P, P, P, P, P, I32, I32, F32, I32, I32, P, P]),
     "stb_attn_prefill": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, P]),
     "stb_attn_prefill_split": (I32, [P, I32, P, P, P, P, P, I32, I32, I32, F32, I32, I32, P]),
     "stb_spec_validate": (I32, [P, P, P, P, P, P, P, P, I32, P, P, P, P]),

@@ -23,7 +23,7 @@ def lib():
 
 
 def P(t):
-    return C.c_void_p(t.data_ptr())
+    return C.c_void_p(0 if t is None else t.data_ptr())
 
 
 def stream():
@@ -466,6 +466,49 @@ def test_attn_decode_multi_query(lib, shape, case):
     lib.call("stb_attn_decode_mq", pool.h, 0, P(q), P(out2), *[P(a) for a in meta], E, shape.n_q, scale, max(ctxs),
              P(ws), stream())
     assert rel(out2, out) < 1e-3
+
+
+@pytest.mark.parametrize("shape", SHAPES[:2], ids=lambda s: s.name)
+@pytest.mark.parametrize("mq", [False, True], ids=["decode", "multi_query"])
+@pytest.mark.parametrize("ctxs", [[5, 16, 17, 33], [700] * 32, [4096] * 4 + [100, 2500], [8000, 2]])
+def test_attn_decode_planned(lib, shape, mq, ctxs):
+    """stb_attn_decode_planned: the partition layer 0 stores (plan_mode 1) and the later layers load
+    (plan_mode 2) is the one each launch computes itself (plan_mode 0): bit-identical outputs, for
+    several "layers" (fresh q each) of one step, then a step with other contexts re-planned."""
+    G = shape.n_q // shape.n_kv
+    B = len(ctxs)
+    pool = _pool(lib, shape, nb=sum(-(-c // 16) for c in ctxs) * 2 + 8, slots=B, bps=600)
+    _fill_pool(lib, pool, shape, ctxs, seed=5)
+    t = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
+    ws = torch.zeros(-(-lib.load().stb_attn_decode_workspace(2 * B, shape.n_q, shape.n_kv, shape.d_head) // 4),
+                     device="cuda")
+    scale = 1 / math.sqrt(shape.d_head)
+
+    def step(cl, layers=3):
+        if mq:  # every entry a 1..16/G-query run ending at its context
+            nq = [1 + (b % (16 // G)) for b in range(B)]
+            rows = [sum(nq[:b]) for b in range(B)]
+            meta = [t(list(range(B))), t(cl), t(rows), t(nq)]
+            T = sum(nq)
+        else:
+            meta = [t(list(range(B))), t(cl), None, None]
+            T = B
+        for layer in range(layers):
+            q = torch.randn(T, shape.n_q, shape.d_head, device="cuda").to(torch.bfloat16)
+            outs = []
+            for mode in (0, 1 if layer == 0 else 2):
+                out = torch.full_like(q, float("nan"))
+                lib.call("stb_attn_decode_planned", pool.h, 0, P(q), P(out), *[P(a) for a in meta], B, shape.n_q,
+                         scale, max(cl), mode, P(ws), stream())
+                outs.append(out)
+            torch.cuda.synchronize()
+            assert torch.isfinite(outs[0].float()).all()
+            assert torch.equal(outs[0], outs[1]), layer
+
+    step(ctxs)
+    step([max(1, c // 2) for c in ctxs])  # a new step: layer 0 re-plans
+    tickets = ws.view(torch.int32)[-(2 * B * shape.n_kv + 64):]
+    assert int(tickets.abs().sum()) == 0
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
