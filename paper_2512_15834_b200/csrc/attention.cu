@@ -481,7 +481,10 @@ __global__ void __launch_bounds__(32 * kDecWarps, 1) attn_decode_kernel(
       plan[1] = W;
     }
   }
-  const int w = blockIdx.x * kDecWarps + warp;
+  // logical warp ids run across CTAs first: a partition that leaves warps idle (pair-aligned
+  // cuts use e.g. 1024 of 1184) spreads its busy warps over every SM instead of idling whole
+  // SMs (measured: decode step 4.81 -> 4.78 ms at B=32 ctx 2k)
+  const int w = warp * gridDim.x + blockIdx.x;
 #ifdef STB_K3_TRACE
   K3T(1);
   if (w >= W) { k3_flush(); return; }
