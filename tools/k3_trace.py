@@ -34,4 +34,6 @@ for B, c in ((32, 128), (32, 2048), (32, 4096)):
         v = r[:, col]
         v = (v[v > 0] - e0) / 1e3
         return f"{name} p10 {np.percentile(v, 10):5.1f} p50 {np.median(v):5.1f} p90 {np.percentile(v, 90):5.1f} max {v.max():5.1f}"
+    if len(sys.argv) > 1:
+        np.save(f"{sys.argv[1]}_B{B}_c{c}.npy", r)
     print(f"B={B} ctx={c}: {n} warps | " + " | ".join(st(i, nm) for i, nm in ((0, "entry"), (6, "metadata"), (1, "partition"), (2, "first page"), (3, "last chunk"), (5, "exit"))))
