@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=2048)
     ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--headroom", type=int, default=4096, help="KV tokens per sequence beyond --ctx in the pool")
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--timers", action="store_true", help="per-kernel CUDA-event times inside the step")
@@ -50,7 +51,7 @@ def main():
     shape = SHAPES[args.shape]
     if args.layers:
         shape = shape.with_layers(args.layers)
-    nb = args.batch * (args.ctx + 4096) // 16 + 64 + 4096
+    nb = args.batch * (args.ctx + args.headroom) // 16 + 64 + args.headroom
     rt = BatchRuntime(shape, init_device="cuda", num_blocks=nb, max_slots=max(64, args.batch) + 1024,
                       max_ctx=args.ctx + 8192, max_step_tokens=16384)
     loop = RealtimeLoop()
