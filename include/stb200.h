@@ -345,6 +345,22 @@ int stb_moe_gemm_mxfp4(const void* xperm, int rows_cap, const void* wtiles, cons
 int stb_moe_combine(float* x, const float* y, int T, int d, int k, const int32_t* perm, const float* weight,
                     const void* norm_w, void* h_out, float eps, int32_t* counts, int E, void* stream);
 
+/* Block-scaled path (the default for the MoE GEMMs): the same product on tcgen05.mma
+ * kind::mxf8f6f4.block_scale, with the tensor core applying the weights' own ue8m0 scales, so no
+ * thread dequantises the MXFP4 codes. The token rows are split first (stb_moe_quant) into two e4m3
+ * halves with one ue8m0 scale per 32 along K (x = hi 2^s_hi + lo 2^s_lo, exact power-of-two
+ * scaling; the pair keeps ~2^-8 of each 32-block's maximum, the precision of the bf16 activation):
+ *   xq  [2][rows_cap][K] bytes (hi rows, then lo rows)   stb_moe_quant_bytes(rows_cap, K)
+ *   xsf [ceil(K/128)][2][pitch = rows_cap rounded up to 4] words of four scale bytes (+ 72 words of overhang)   stb_moe_quant_scale_words(rows_cap, K)
+ * stb_moe_gemm_mx takes them in place of the fp16 xperm; everything else as stb_moe_gemm_mxfp4.
+ * Replaces the same charges (engine.py:251,270,296,358).                                  */
+int64_t stb_moe_quant_bytes(int rows_cap, int K);
+int64_t stb_moe_quant_scale_words(int rows_cap, int K);
+int stb_moe_quant(const void* x, int64_t ldx, int rows, int K, int rows_cap, void* xq, uint32_t* xsf, void* stream);
+int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
+                    const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   uint16_t v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -631,6 +636,431 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
   if (warp == 2) tmem_free(tmem, 512);
 }
 
+// ---------------------------------------------------------------- block-scaled MXFP4 grouped GEMM
+// tcgen05.mma kind::mxf8f6f4.block_scale: A = the e2m1 expert weights with their own ue8m0
+// scales (one per 32 along K, straight from the checkpoint), B = the token rows split exactly
+// into two e4m3 halves with one ue8m0 scale per 32 (x = hi * 2^s_hi + lo * 2^s_lo, stb_moe_quant):
+// B carries 2 BN rows (BN hi rows, then BN lo rows) and the epilogue adds the two accumulator
+// column halves. The tensor core applies every scale, so no thread dequantises: unpack warps only
+// re-space the packed codes into the operand layout the MMA reads (16 codes in the low 8 bytes of
+// each 16-byte chunk) and post the scale words into tensor memory. Formats settled by
+// tools/probe_mxf8f6f4.cu on a B200: SFA of weight row r at TMEM lane r, column r / 32, byte = the
+// MMA's 32-wide K slice (the scale id also goes into the instruction descriptor); SFB of B row n
+// at lane n % 32 of every lane quarter, column n / 32; N = 2 BN >= 32.
+__host__ __device__ constexpr int sf_pitch(int rows_cap) { return (rows_cap + 3) & ~3; }
+constexpr int MX_BK = 128;   // K per pipeline stage: two RAW tiles (one 128-byte swizzled row of codes)
+#ifndef STB_MX_UPAR
+#define STB_MX_UPAR 2
+#endif
+constexpr int MX_UPAR = STB_MX_UPAR;  // unpack warps per lane quarter (alternating stages)
+constexpr int kMxThreads = 32 * (4 + 4 * MX_UPAR + 4);
+
+template <int BN>
+struct MxCfg {
+  static constexpr int XB = 2 * BN * MX_BK;  // e4m3 hi + lo rows of one stage
+#ifndef STB_MX_XS
+#define STB_MX_XS 4
+#endif
+#ifndef STB_MX_AS
+#define STB_MX_AS 4
+#endif
+  static constexpr int XS = STB_MX_XS;       // token stages (L2-resident rows, TMA)
+  static constexpr int AB = BM * MX_BK;      // unpacked codes of one 128-row tile (16 KB)
+  static constexpr int AS = STB_MX_AS;       // unpacked A stages (+ their scale words in TMEM)
+  static constexpr int WB = 2 * RAW;         // packed codes + scales of one stage (two RAW tiles)
+#ifndef STB_MOE_MX_RING_KB
+#define STB_MOE_MX_RING_KB 220
+#endif
+  static constexpr int WS = std::min(24, (STB_MOE_MX_RING_KB * 1024 - XS * (XB + 512) - AS * AB) / WB);
+  static constexpr int XF = ((8 * (BN + 4) + 127) / 128) * 128;  // scale words of one stage: [2][BN + 4]
+  static constexpr int SMEM = 1024 + XS * XB + AS * AB + WS * WB + XS * XF + 1024;
+  static constexpr int SFB_COLS = (2 * BN + 31) / 32;
+  static constexpr int SF0 = 2 * 2 * BN;     // after the double-buffered accumulators
+  static constexpr int SFS = 8;              // TMEM columns of one A stage's scale words: 4 SFA + 4 SFB
+  static_assert(SFB_COLS <= 4 && SF0 + AS * SFS <= 512, "TMEM budget");
+};
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]));
+}
+__device__ __forceinline__ void umma_mx(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// A = e2m1 (format 5), B = e4m3 (0), K-major, ue8m0 scales (bit 23), M = 128, N; scale ids per slice
+__host__ __device__ constexpr uint32_t idesc_mx(int M, int N) {
+  return (5u << 7) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_x,
+                                                                    const uint32_t* __restrict__ xsf, int rows_cap,
+                                                                    const MoeArgs a) {
+  using CF = MxCfg<BN>;
+  constexpr int XS = CF::XS, AS = CF::AS, WS = CF::WS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sx = smem;                   // [XS][2 BN rows][128 B], SW128
+  uint8_t* sa = sx + XS * CF::XB;       // [AS][128 rows][128 B], SW128 (unpacked codes)
+  uint8_t* sw = sa + AS * CF::AB;       // [WS][2][RAW] packed tiles as stored
+  uint8_t* sf = sw + WS * CF::WB;       // [XS][2][BN + 4] token scale words (bulk copies, with the rows)
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(sf + XS * CF::XF);
+  uint64_t* w_empty = w_full + WS;      // unpackers -> weight producer
+  uint64_t* x_full = w_empty + WS;
+  uint64_t* x_empty = x_full + XS;      // MMA -> token producer
+  uint64_t* a_full = x_empty + XS;      // unpackers -> MMA
+  uint64_t* a_empty = a_full + AS;      // MMA -> unpackers
+  uint64_t* acc_full = a_empty + AS;    // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  __shared__ int s_off[kMaxE + 1];
+  __shared__ int s_item[kMaxE + 1];
+  __shared__ int s_cnt[kMaxE];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = a.E, NT = ceil_div(a.N, BM), KB = a.K / BK, KS = ceil_div(KB, 2);
+  const int pitch = sf_pitch(rows_cap);
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_x);
+    for (int s = 0; s < WS; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 4);
+    }
+    for (int s = 0; s < XS; ++s) {
+      mbar_init(&x_full[s], 1);
+      mbar_init(&x_empty[s], 1);
+    }
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&a_full[s], 4);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  pdl_wait();
+  block_prefix(a.counts, E, s_off);
+  if (threadIdx.x < kMaxE) s_cnt[threadIdx.x] = threadIdx.x < E ? s_off[threadIdx.x + 1] - s_off[threadIdx.x] : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int e = 0; e < E; ++e) {
+      s_item[e] = run;
+      run += ceil_div(s_cnt[e], BN) * NT;
+    }
+    s_item[E] = run;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_launch();
+  const uint32_t tmem = *tmem_slot;
+  const int total = s_item[E];
+#ifdef STB_MX_CONTIG  // experiment: each CTA a contiguous range of items
+  const int it0 = (int)((int64_t)total * blockIdx.x / gridDim.x), it1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x), istep = 1;
+#else
+  const int it0 = blockIdx.x, it1 = total, istep = gridDim.x;
+#endif
+  // item -> (expert, weight tile, token tile); token tiles of one weight tile on neighbouring CTAs
+  auto decode = [&](int it, int& e, int& nt, int& m) {
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_item[mid] <= it) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    const int mt = ceil_div(s_cnt[e], BN);
+    const int local = it - s_item[e];
+    nt = local / mt;
+    m = local - nt * mt;
+  };
+
+  if (warp == 0) {
+    // weight producer: two RAW tiles (128 K) of the item's weight tile per stage, one bulk copy
+    if (elect_one()) {
+      int i = 0;
+      for (int it = it0; it < it1; it += istep) {
+        int e, nt, m;
+        decode(it, e, nt, m);
+        const uint8_t* wt = a.w + ((int64_t)e * NT + nt) * KB * RAW;
+        for (int ks = 0; ks < KS; ++ks, ++i) {
+          const int s = i % WS;
+          const int nraw = min(2, KB - 2 * ks);
+          mbar_wait(&w_empty[s], ((i / WS) & 1) ^ 1);
+          mbar_expect_tx(&w_full[s], nraw * RAW);
+          bulk_load(smem_u32(sw + s * CF::WB), wt + (int64_t)(2 * ks) * RAW, nraw * RAW, &w_full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // token producer: BN hi rows and BN lo rows of the expert's token tile per stage (TMA, L2)
+    if (elect_one()) {
+      int i = 0;
+      for (int it = it0; it < it1; it += istep) {
+        int e, nt, m;
+        decode(it, e, nt, m);
+        const int xrow = s_off[e] + m * BN;
+        for (int ks = 0; ks < KS; ++ks, ++i) {
+          const int s = i % XS;
+          mbar_wait(&x_empty[s], ((i / XS) & 1) ^ 1);
+          // scale words of the tile's hi and lo rows: 16-byte aligned supersets (the pitch is a
+          // multiple of 4 words, so both start xrow & 3 words early)
+          const uint32_t sfw = (uint32_t)(((xrow & 3) + BN + 3) & ~3);
+          mbar_expect_tx(&x_full[s], CF::XB + 8 * sfw);
+          tma_load_2d(sx + s * CF::XB, &tm_x, &x_full[s], ks * MX_BK, xrow);
+          tma_load_2d(sx + s * CF::XB + BN * MX_BK, &tm_x, &x_full[s], ks * MX_BK, rows_cap + xrow);
+          for (int h = 0; h < 2; ++h)
+            bulk_load(smem_u32(sf + s * CF::XF + h * (BN + 4) * 4),
+                      xsf + ((int64_t)(2 * ks + h) * pitch + (xrow & ~3)), 4 * sfw, &x_full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_mx(BM, 2 * BN);
+      int i = 0, j = 0;
+      for (int it = it0; it < it1; it += istep, ++j) {
+        const int buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * 2 * BN;
+        for (int ks = 0; ks < KS; ++ks, ++i) {
+          const int xs = i % XS, as = i % AS;
+          mbar_wait(&x_full[xs], (i / XS) & 1);
+          mbar_wait(&a_full[as], (i / AS) & 1);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_kmajor_sw128(smem_u32(sa + as * CF::AB), 1024);
+          const uint64_t bdesc = umma_desc_kmajor_sw128(smem_u32(sx + xs * CF::XB), 1024);
+          const uint32_t sfa = tmem + CF::SF0 + as * CF::SFS, sfb = sfa + 4;
+          const int kk_n = (KB - 2 * ks) >= 2 ? 4 : 2;  // a lone last RAW tile is 64 of K
+#ifdef STB_MX_SKIP_MMA  // timing experiments only (results are wrong)
+          if (ks == 0)
+#endif
+          for (int kk = 0; kk < kk_n; ++kk)  // 32 of K per MMA: +32 B in both descriptors
+            umma_mx(d, adesc + 2 * kk, bdesc + 2 * kk, idesc | ((uint32_t)kk << 29) | ((uint32_t)kk << 4),
+                    sfa | ((uint32_t)kk << 30), sfb | ((uint32_t)kk << 30), (ks > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&x_empty[xs]);
+          umma_commit(&a_empty[as]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 4 + 4 * MX_UPAR) {
+    // unpackers: warp = (parity, lane quarter q); thread = weight row r = 32 q + lane
+    const int q = warp & 3, par = (warp - 4) >> 2, r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t sw_u32 = smem_u32(sw), sa_u32 = smem_u32(sa), sf_u32 = smem_u32(sf);
+    int i = 0;
+    for (int it = it0; it < it1; it += istep) {
+      int e, nt, m;
+      decode(it, e, nt, m);
+      const int xrow = s_off[e] + m * BN;
+      for (int ks = 0; ks < KS; ++ks, ++i) {
+        if (i % MX_UPAR != par) continue;
+        const int s = i % WS, as = i % AS;
+        const bool two = (KB - 2 * ks) >= 2;
+        mbar_wait(&w_full[s], (i / WS) & 1);
+        const uint32_t raw = sw_u32 + s * CF::WB;
+        const uint4 c0 = lds128(raw + r * 32), c1 = lds128(raw + r * 32 + 16);
+        uint4 c2 = make_uint4(0u, 0u, 0u, 0u), c3 = c2;
+        const uint32_t sc0 = lds16(raw + 4096 + r * 2);
+        uint32_t sc1 = 0x7f7fu;
+        if (two) {
+          c2 = lds128(raw + RAW + r * 32);
+          c3 = lds128(raw + RAW + r * 32 + 16);
+          sc1 = lds16(raw + RAW + 4096 + r * 2);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&w_empty[s]);
+        mbar_wait(&a_empty[as], ((i / AS) & 1) ^ 1);
+        tc_fence_after();
+        // row r: 8 chunks of 16 codes (8 bytes each, padded to 16), 128-byte swizzle
+        const uint32_t row = sa_u32 + as * CF::AB + r * 128;
+#ifdef STB_MX_SKIP_UNPACK  // timing experiments only (results are wrong)
+        if (ks == 0) {
+#else
+        {
+#endif
+        const uint32_t sx7 = r & 7;
+        sts128(row + ((0 ^ sx7) << 4), c0.x, c0.y, 0u, 0u);
+        sts128(row + ((1 ^ sx7) << 4), c0.z, c0.w, 0u, 0u);
+        sts128(row + ((2 ^ sx7) << 4), c1.x, c1.y, 0u, 0u);
+        sts128(row + ((3 ^ sx7) << 4), c1.z, c1.w, 0u, 0u);
+        if (two) {
+          sts128(row + ((4 ^ sx7) << 4), c2.x, c2.y, 0u, 0u);
+          sts128(row + ((5 ^ sx7) << 4), c2.z, c2.w, 0u, 0u);
+          sts128(row + ((6 ^ sx7) << 4), c3.x, c3.y, 0u, 0u);
+          sts128(row + ((7 ^ sx7) << 4), c3.z, c3.w, 0u, 0u);
+        }
+        }
+        // SFA: row r's four 32-wide K slices at lane r, column r / 32 (= q)
+        uint32_t sfa[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sfa[c] = c == q ? (sc0 | (sc1 << 16)) : 0x7f7f7f7fu;
+        // SFB: B row n = 32 c + lane (BN hi rows, then BN lo rows) at lane n % 32 of every quarter
+        const int xs = i % XS;
+        mbar_wait(&x_full[xs], (i / XS) & 1);
+        uint32_t sfb[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int n = 32 * c + lane;
+          const int h = n >= BN, tok = n - h * BN;
+          sfb[c] = n < 2 * BN ? lds32(sf_u32 + xs * CF::XF + (h * (BN + 4) + (xrow & 3) + tok) * 4) : 0x7f7f7f7fu;
+        }
+        const uint32_t sfcol = tmem + lane_addr + CF::SF0 + as * CF::SFS;
+        tmem_st4(sfcol, sfa);
+        tmem_st4(sfcol + 4, sfb);
+        tmem_st_wait();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[as]);
+      }
+    }
+  } else if (warp >= 4 + 4 * MX_UPAR) {
+    // epilogue: thread = weight row (feature); columns = tokens (hi half + lo half)
+    const int q = warp & 3;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int j = 0;
+    for (int it = it0; it < it1; it += istep, ++j) {
+      int e, nt, m;
+      decode(it, e, nt, m);
+      const int buf = j & 1;
+      const int row0 = s_off[e] + m * BN;
+      const int nv = min(BN, s_cnt[e] - m * BN);
+      mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const int f = nt * BM + q * 32 + lane;
+      const float b = f < a.N ? __ldg(a.bias + (int64_t)e * a.N + f) : 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t rr[16], rl[16];
+        tmem_ld16(tmem + lane_addr + buf * 2 * BN + c, rr);
+        tmem_ld16(tmem + lane_addr + buf * 2 * BN + BN + c, rl);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) rr[u] = __float_as_uint(__uint_as_float(rr[u]) + __uint_as_float(rl[u]));
+        if (a.kind == 2) {
+          float* y = reinterpret_cast<float*>(a.out);
+          if (f < a.N) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              if (c + u < nv) y[(int64_t)(row0 + c + u) * a.ldo + f] = __uint_as_float(rr[u]) + b;
+          }
+        } else {
+          __half* act = reinterpret_cast<__half*>(a.out);
+          const bool odd = lane & 1;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float mine = __uint_as_float(odd ? rr[8 + u] : rr[u]) + b;
+            const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? rr[u] : rr[8 + u]) + b, 1);
+            const int tok = c + (odd ? 8 : 0) + u;
+            const float g = odd ? other : mine, up = odd ? mine : other;
+            if (f < a.N && tok < nv)
+              act[(int64_t)(row0 + tok) * a.ldo + (f >> 1)] = __float2half_rn(gpt_oss_glu(g, up, a.limit));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_free(tmem, 512);
+}
+
+// fp16 token rows -> two e4m3 halves with one ue8m0 scale per 32 (the B operand of the block-scaled
+// GEMM): per 32-wide block, s_hi = floor(log2 amax) - 7 (so |x| / 2^s_hi < 256 <= 448, exact
+// power-of-two scaling), hi = e4m3(x / 2^s_hi), r = x / 2^s_hi - hi (exact in fp32), lo the same
+// split of r. x = hi 2^s_hi + lo 2^(s_hi + s_lo) to the rounding of lo (about 2^-8 of the block
+// maximum). Warp per (row, 128-wide stage); lane = 4 values; xq [2][rows_cap][K] (hi rows, then lo
+// rows), xsf [stages][2][pitch] words of four scale bytes (blocks past K: 127, i.e. 1.0), pitch =
+// rows_cap rounded up to 4 words (the GEMM reads them with a 2-D TMA box).
+__device__ __forceinline__ int blk_exp(float amax) {
+  int e;
+  frexpf(amax, &e);  // amax = m 2^e, m in [0.5, 1)
+  return amax > 0.f ? e - 8 : 0;
+}
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
+  uint16_t lo, hi;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(lo) : "f"(a), "f"(b));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(hi) : "f"(c), "f"(d));
+  return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ float2 e4m3x2_to_f2(uint16_t v) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
+  return __half22float2(*reinterpret_cast<__half2*>(&h));
+}
+__global__ void __launch_bounds__(256) moe_quant_kernel(const __half* __restrict__ x, int64_t ldx, int rows, int K,
+                                                        int rows_cap, uint8_t* __restrict__ xq,
+                                                        uint32_t* __restrict__ xsf) {
+  pdl_wait();
+  pdl_launch();
+  const int KS = (K + MX_BK - 1) / MX_BK;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < (int64_t)rows * KS; w += nw) {
+    const int row = (int)(w / KS), ks = (int)(w - (int64_t)row * KS);
+    const int k = ks * MX_BK + lane * 4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (k < K) {
+      const uint2 u = *reinterpret_cast<const uint2*>(x + row * ldx + k);
+      const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+      const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+      v[0] = a0.x, v[1] = a0.y, v[2] = a1.x, v[3] = a1.y;
+    }
+    float am = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+    const int eh = blk_exp(am);
+    float s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = ldexpf(v[u], -eh);
+    const uint32_t hq = e4m3x4(s[0], s[1], s[2], s[3]);
+    const float2 h01 = e4m3x2_to_f2((uint16_t)(hq & 0xFFFF)), h23 = e4m3x2_to_f2((uint16_t)(hq >> 16));
+    float r[4] = {s[0] - h01.x, s[1] - h01.y, s[2] - h23.x, s[3] - h23.y};
+    float ar = fmaxf(fmaxf(fabsf(r[0]), fabsf(r[1])), fmaxf(fabsf(r[2]), fabsf(r[3])));
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) ar = fmaxf(ar, __shfl_xor_sync(0xffffffffu, ar, o));
+    const int el = blk_exp(ar);
+    const uint32_t lq = e4m3x4(ldexpf(r[0], -el), ldexpf(r[1], -el), ldexpf(r[2], -el), ldexpf(r[3], -el));
+    if (k < K) {
+      *reinterpret_cast<uint32_t*>(xq + (int64_t)row * K + k) = hq;
+      *reinterpret_cast<uint32_t*>(xq + ((int64_t)rows_cap + row) * K + k) = lq;
+    }
+    // block b = lane / 8: scale bytes of the four blocks gathered into lane 0
+    const bool live = ks * MX_BK + (lane & ~7) * 4 < K;
+    const uint32_t bh = live ? (uint32_t)(eh + 127) : 127u, bl = live ? (uint32_t)(eh + el + 127) : 127u;
+    uint32_t wh = 0, wl = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      wh |= __shfl_sync(0xffffffffu, bh, 8 * b) << (8 * b);
+      wl |= __shfl_sync(0xffffffffu, bl, 8 * b) << (8 * b);
+    }
+    if (lane == 0) {
+      const int64_t pitch = sf_pitch(rows_cap);
+      xsf[((int64_t)ks * 2) * pitch + row] = wh;
+      xsf[((int64_t)ks * 2 + 1) * pitch + row] = wl;
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -644,13 +1074,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// fp16 [rows][K] token rows, box [BN rows][64], 128B swizzle; cached per (base, rows, K, BN, device)
-int x_map(CUtensorMap* out, const void* base, int64_t rows, int K, int bn) {
+// token rows [rows][K], box [BN rows][128 B], 128B swizzle: fp16 (esize 2, the dequantising kernel)
+// or e4m3 bytes (esize 1, the block-scaled kernel); cached per (base, rows, K, BN, esize, device)
+int x_map(CUtensorMap* out, const void* base, int64_t rows, int K, int bn, int esize = 2) {
   static std::mutex mu;
-  static std::map<std::tuple<const void*, int64_t, int, int, int>, CUtensorMap> cache;
+  static std::map<std::tuple<const void*, int64_t, int, int, int, int>, CUtensorMap> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  const auto key = std::make_tuple(base, rows, K, bn, dev);
+  const auto key = std::make_tuple(base, rows, K, bn, esize, dev);
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -660,10 +1091,10 @@ int x_map(CUtensorMap* out, const void* base, int64_t rows, int K, int bn) {
   auto fn = encode_fn();
   if (!fn) return fail(STB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)bn};
+  cuuint64_t strides[1] = {(cuuint64_t)K * esize};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esize), (cuuint32_t)bn};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(out, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(STB_ECUDA, "moe: tensor map encode failed (%d)", (int)r);
@@ -683,9 +1114,56 @@ int launch_moe_gemm(const void* xperm, int rows_cap, const MoeArgs& a, cudaStrea
   return STB_OK;
 }
 
+template <int BN>
+int launch_moe_mx(const void* xq, const uint32_t* xsf, int rows_cap, const MoeArgs& a, cudaStream_t st) {
+  CUtensorMap tm;
+  if (int rc = x_map(&tm, xq, 2 * (int64_t)rows_cap, a.K, BN, 1)) return rc;
+  auto kern = moe_gemm_mx_kernel<BN>;
+  smem_attr_once(kern, MxCfg<BN>::SMEM);
+  cudaError_t e = launch_k(kern, dim3(device_sms()), dim3(kMxThreads), MxCfg<BN>::SMEM, st, tm, xsf, rows_cap, a);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_gemm_mx launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int64_t stb_moe_quant_bytes(int rows_cap, int K) {
+  if (rows_cap <= 0 || K <= 0) return 0;
+  return 2 * (int64_t)rows_cap * K;
+}
+int64_t stb_moe_quant_scale_words(int rows_cap, int K) {
+  if (rows_cap <= 0 || K <= 0) return 0;
+  return (int64_t)((K + MX_BK - 1) / MX_BK) * 2 * sf_pitch(rows_cap) + 72;  // + the last tile's overhang
+}
+
+int stb_moe_quant(const void* x, int64_t ldx, int rows, int K, int rows_cap, void* xq, uint32_t* xsf, void* stream) {
+  if (rows <= 0) return STB_OK;
+  if (K % 4 || ldx % 4 || rows > rows_cap) return fail(STB_EINVAL, "moe_quant: rows=%d cap=%d K=%d", rows, rows_cap, K);
+  const int64_t warps = (int64_t)rows * ((K + MX_BK - 1) / MX_BK);
+  const int blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (warps + 7) / 8), 8 * device_sms());
+  cudaError_t e = launch_k(moe_quant_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, (const __half*)x, ldx,
+                           rows, K, rows_cap, (uint8_t*)xq, xsf);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_quant launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
+                    const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
+                    void* stream) {
+  if (rows <= 0) return STB_OK;
+  if (E <= 0 || E > kMaxE || K % BK || K % 16 || N <= 0 || (kind != STB_MOE_GATE_UP && kind != STB_MOE_DOWN) ||
+      (kind == STB_MOE_GATE_UP && N % 2))
+    return fail(STB_EINVAL, "moe_gemm_mx: E=%d N=%d K=%d kind=%d", E, N, K, kind);
+  MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit};
+  const double avg = (double)rows / E;
+  const double busy = avg + 2.0 * std::sqrt(avg);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (busy <= 16.0) return launch_moe_mx<16>(xq, xsf, rows_cap, a, st);
+  if (busy <= 32.0) return launch_moe_mx<32>(xq, xsf, rows_cap, a, st);
+  return launch_moe_mx<64>(xq, xsf, rows_cap, a, st);
+}
 
 int stb_moe_route(const float* logits, int64_t ld, const float* bias, int T, int E, int k, int32_t* counts,
                   int32_t* expert, int32_t* rank, float* weight, void* stream) {

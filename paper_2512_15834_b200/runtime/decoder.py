@@ -71,6 +71,9 @@ GRAPH_CACHE = 48    # captured graphs kept
 PROJECTIONS = ("wqkv", "wo", "w_gate_up", "w_down")
 MOE_PROJECTIONS = ("wqkv", "wo", "router")   # gpt-oss: the experts are MXFP4 tiles (weights.MoELayer)
 MOE_GATE_UP, MOE_DOWN = 1, 2                 # include/stb200.h STB_MOE_*
+# MoE GEMMs on the block-scaled tensor-core path (stb_moe_quant + stb_moe_gemm_mx);
+# STB200_MOE_MX=0 keeps the dequantising kernel (stb_moe_gemm_mxfp4) for A/B
+MOE_MX = os.environ.get("STB200_MOE_MX", "1") != "0"
 MOE_TILE_BYTES = 4352                        # one 128 x 64 MXFP4 tile (weights.TILE_BYTES)
 
 
@@ -376,6 +379,11 @@ class Decoder:
                 self.m_x = torch.zeros(rows, s.d_model, dtype=torch.float16, device=dev)
                 self.m_act = torch.zeros(rows, s.d_ff, dtype=torch.float16, device=dev)
                 self.m_y = torch.empty(rows, s.d_model, dtype=f32, device=dev)
+                if MOE_MX:  # e4m3 hi / lo halves + scale words of either GEMM's token rows
+                    kq = max(s.d_model, s.d_ff)
+                    L = lib.load()
+                    self.m_xq = torch.zeros(L.stb_moe_quant_bytes(rows, kq), dtype=torch.uint8, device=dev)
+                    self.m_xsf = torch.zeros(L.stb_moe_quant_scale_words(rows, kq), dtype=torch.int32, device=dev)
                 self._moe_rows = rows
             self._cap_t = cap
             self._dirty.update(qkv=0, proj=0, gu=0)
@@ -801,14 +809,32 @@ class Decoder:
             call("stb_moe_gather", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
                  _p(self.m_rank), _p(offs), _p(self.m_perm), _p(self.m_x), st)
             ex = w[f"l{i}.experts"]
-            ev = self._tick()
-            call("stb_moe_gemm_mxfp4", _p(self.m_x), self._moe_rows, _p(ex.gate_up), _p(ex.b_gate_up),
-                 _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),
-                 self.m_act.stride(0), rows, st)
+            cap_r = self._moe_rows
+            if MOE_MX:  # block-scaled tensor-core path: split the rows into e4m3 halves first
+                call("stb_moe_quant", _p(self.m_x), self.m_x.stride(0), rows, d, cap_r, _p(self.m_xq),
+                     _p(self.m_xsf), st)
+                ev = self._tick()
+                call("stb_moe_gemm_mx", _p(self.m_xq), _p(self.m_xsf), cap_r, _p(ex.gate_up), _p(ex.b_gate_up),
+                     _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),
+                     self.m_act.stride(0), rows, st)
+            else:
+                ev = self._tick()
+                call("stb_moe_gemm_mxfp4", _p(self.m_x), cap_r, _p(ex.gate_up), _p(ex.b_gate_up),
+                     _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),
+                     self.m_act.stride(0), rows, st)
             self._tock("moe_gemm", ev, _MoeWork(offs_host, i, 2 * s.d_ff, d, rows, 2, 2) if timed else 0)
-            ev = self._tick()
-            call("stb_moe_gemm_mxfp4", _p(self.m_act), self._moe_rows, _p(ex.down), _p(ex.b_down),
-                 _p(self.m_counts), E, d, s.d_ff, MOE_DOWN, C.c_float(0.0), _p(self.m_y), self.m_y.stride(0), rows, st)
+            if MOE_MX:
+                call("stb_moe_quant", _p(self.m_act), self.m_act.stride(0), rows, s.d_ff, cap_r, _p(self.m_xq),
+                     _p(self.m_xsf), st)
+                ev = self._tick()
+                call("stb_moe_gemm_mx", _p(self.m_xq), _p(self.m_xsf), cap_r, _p(ex.down), _p(ex.b_down),
+                     _p(self.m_counts), E, d, s.d_ff, MOE_DOWN, C.c_float(0.0), _p(self.m_y), self.m_y.stride(0),
+                     rows, st)
+            else:
+                ev = self._tick()
+                call("stb_moe_gemm_mxfp4", _p(self.m_act), cap_r, _p(ex.down), _p(ex.b_down),
+                     _p(self.m_counts), E, d, s.d_ff, MOE_DOWN, C.c_float(0.0), _p(self.m_y), self.m_y.stride(0),
+                     rows, st)
             self._tock("moe_gemm", ev, _MoeWork(offs_host, i, d, s.d_ff, rows, 2, 4) if timed else 0)
             last = i + 1 == s.layers
             call("stb_moe_combine", _p(x), _p(self.m_y), T, d, k, _p(self.m_perm), _p(self.m_wt),

@@ -133,6 +133,80 @@ def test_moe_gemm_mxfp4(lib, T, E, k, d, ff):
     assert not torch.isnan(act[:rows]).any() and not torch.isnan(y[:rows]).any()
 
 
+def _quant(lib, x, rows, cap):
+    K = x.shape[1]
+    xq = torch.zeros(lib.load().stb_moe_quant_bytes(cap, K), dtype=torch.uint8, device="cuda")
+    xsf = torch.zeros(lib.load().stb_moe_quant_scale_words(cap, K), dtype=torch.int32, device="cuda")
+    lib.call("stb_moe_quant", P(x), x.stride(0), rows, K, cap, P(xq), P(xsf), stream())
+    return xq, xsf
+
+
+def _dequant(xq, xsf, rows, cap, K):
+    """fp32 value of the two e4m3 halves with their per-32 ue8m0 scales (test-side restatement)."""
+    q = xq.view(torch.float8_e4m3fn).float().view(2, cap, K)[:, :rows]
+    ks = -(-K // 128)
+    pitch = (cap + 3) // 4 * 4
+    words = xsf[:ks * 2 * pitch].view(ks, 2, pitch)[:, :, :rows].cpu().numpy().astype(np.uint32)
+    b = np.stack([(words >> (8 * j)) & 255 for j in range(4)], -1)  # [ks][2][rows][4]
+    e = torch.from_numpy(b.transpose(1, 2, 0, 3).reshape(2, rows, ks * 4).astype(np.float32)).cuda() - 127
+    sc = torch.exp2(e).repeat_interleave(32, -1)[..., :K]
+    return (q * sc).sum(0)
+
+
+@pytest.mark.parametrize("rows,K", [(1, 64), (37, 2880), (256, 512), (130, 384)])
+def test_moe_quant(lib, rows, K):
+    """Token rows -> two e4m3 halves with one ue8m0 scale per 32: the pair reconstructs the fp16
+    row to ~2^-8 of each block's maximum (blocks spanning 2^-12..2^4 in magnitude)."""
+    cap = rows + 16
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn(rows, K, device="cuda", generator=g) * torch.exp2(torch.randint(-12, 5, (rows, K), device="cuda",
+                                                                                   generator=g).float())
+    x = x.to(torch.float16)
+    xq, xsf = _quant(lib, x, rows, cap)
+    torch.cuda.synchronize()
+    back = _dequant(xq, xsf, rows, cap, K)
+    blk = x.float().abs().view(rows, -1, 32) if K % 32 == 0 else None
+    err = (back - x.float()).abs()
+    bound = blk.amax(-1, keepdim=True).expand(-1, -1, 32).reshape(rows, K) * 2.0 ** -8
+    assert torch.all(err <= bound + 1e-30), float((err - bound).max())
+    assert rel(back, x.float()) < 2e-3
+
+
+@pytest.mark.parametrize("T,E,k,d,ff", [(1, 16, 4, 512, 256), (32, 128, 4, 2880, 2880), (300, 16, 4, 512, 256),
+                                        (700, 32, 4, 1024, 512), (64, 8, 2, 256, 384), (16, 8, 2, 64, 128)])
+def test_moe_gemm_mx(lib, T, E, k, d, ff):
+    """Block-scaled grouped GEMM (tcgen05 kind::mxf8f6f4: e2m1 weights x e4m3 hi/lo token halves, the
+    tensor core applying both ue8m0 scales), both kinds, vs fp32 math on the dequantised weights and
+    the fp16 token rows; token tiles 16 / 32 / 64, K with a lone 64-wide last stage (2880, 64)."""
+    gu_t, gu_w, gu_b = _experts(E, 2 * ff, d, 1)
+    dn_t, dn_w, dn_b = _experts(E, d, ff, 2)
+    logits = torch.randn(T, E, device="cuda")
+    counts, ex, rk, wt = _route(lib, logits, torch.zeros(E, device="cuda"), k)
+    h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    offs, perm, xp = _gather(lib, h, counts, ex, rk, E, k)
+    rows = T * k
+    cap = xp.shape[0]
+    act = torch.full((cap, ff), float("nan"), device="cuda").to(torch.float16)
+    y = torch.full((cap, d), float("nan"), device="cuda")
+    xq, xsf = _quant(lib, xp, rows, cap)
+    lib.call("stb_moe_gemm_mx", P(xq), P(xsf), cap, P(gu_t), P(gu_b), P(counts), E, 2 * ff, d, 1, C.c_float(7.0),
+             P(act), ff, rows, stream())
+    aq, asf = _quant(lib, act, rows, cap)
+    lib.call("stb_moe_gemm_mx", P(aq), P(asf), cap, P(dn_t), P(dn_b), P(counts), E, d, ff, 2, C.c_float(0.0), P(y),
+             d, rows, stream())
+    torch.cuda.synchronize()
+    o = offs.cpu().tolist()
+    for e in range(E):
+        a, b = o[e], o[e + 1]
+        if a == b:
+            continue
+        ref_act = glu_ref(xp[a:b].float() @ gu_w[e].T + gu_b[e])
+        assert rel(act[a:b], ref_act) < 5e-3, ("gate_up", e, rel(act[a:b], ref_act))
+        ref_y = act[a:b].float() @ dn_w[e].T + dn_b[e]
+        assert rel(y[a:b], ref_y) < 5e-3, ("down", e, rel(y[a:b], ref_y))
+    assert not torch.isnan(act[:rows]).any() and not torch.isnan(y[:rows]).any()
+
+
 def test_moe_combine(lib):
     T, E, k, d = 9, 16, 4, 2880
     counts, ex, rk, wt = _route(lib, torch.randn(T, E, device="cuda"), torch.zeros(E, device="cuda"), k)

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--ff", type=int, default=2880)
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--impl", default="mx,mxfp4", help="mx = block-scaled tcgen05 path (stb_moe_gemm_mx, the "
+                    "default), mxfp4 = the dequantising kernel (stb_moe_gemm_mxfp4)")
     a = ap.parse_args()
     L.load()
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -58,41 +60,57 @@ def main():
         L.call("stb_moe_gather", P(h), d, T, d, k, E, P(counts), P(ex), P(rk), P(offs), P(perm), P(xp), st)
         touched = int((counts > 0).sum())
         rows = T * k
+        kq = max(d, ff)
+        xq = [torch.zeros(L.load().stb_moe_quant_bytes(cap, kq), dtype=torch.uint8, device="cuda") for _ in range(2)]
+        xsf = [torch.zeros(L.load().stb_moe_quant_scale_words(cap, kq), dtype=torch.int32, device="cuda")
+               for _ in range(2)]
+        L.call("stb_moe_quant", P(xp), d, rows, d, cap, P(xq[0]), P(xsf[0]), st)
+        L.call("stb_moe_quant", P(act), ff, rows, ff, cap, P(xq[1]), P(xsf[1]), st)
+        impl = "mxfp4"
 
         def run(kind):
-            if kind == 1:
+            if impl == "quant":
+                L.call("stb_moe_quant", P(xp), d, rows, d, cap, P(xq[0]), P(xsf[0]), st)
+            elif impl == "mx" and kind == 1:
+                L.call("stb_moe_gemm_mx", P(xq[0]), P(xsf[0]), cap, P(gu), P(bgu), P(counts), E, 2 * ff, d, 1, 7.0,
+                       P(act), ff, rows, st)
+            elif impl == "mx":
+                L.call("stb_moe_gemm_mx", P(xq[1]), P(xsf[1]), cap, P(dn), P(bdn), P(counts), E, d, ff, 2, 0.0, P(y),
+                       d, rows, st)
+            elif kind == 1:
                 L.call("stb_moe_gemm_mxfp4", P(xp), cap, P(gu), P(bgu), P(counts), E, 2 * ff, d, 1, 7.0, P(act), ff,
                        rows, st)
             else:
                 L.call("stb_moe_gemm_mxfp4", P(act), cap, P(dn), P(bdn), P(counts), E, d, ff, 2, 0.0, P(y), d, rows, st)
 
-        res = {}
-        for kind, N, K, ob in ((1, 2 * ff, d, ff * 2), (2, d, ff, d * 4)):
-            for _ in range(3):
-                run(kind)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(a.iters):
-                run(kind)
-            e1.record()
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) / a.iters * 1e3
-            byts = touched * (-(-N // 128)) * (K // 64) * W.TILE_BYTES + rows * K * 2 + rows * ob
-            res["gate_up" if kind == 1 else "down"] = (round(us, 1), round(byts / us / 1e3, 1), round(byts / us / 1e3 / peak, 3))
-            prof = getattr(L.load(), "stb_debug_moe_prof", None)  # -DSTB_MOE_PROF variants only
-            if prof is not None:
-                buf = (C.c_ulonglong * 16)()
-                prof(buf)
-                run(kind)
-                torch.cuda.synchronize()
-                prof(buf)
-                v = list(buf)
-                pct = lambda w, t: f"{100 * w / max(t, 1):4.1f}%"  # noqa: E731
-                print(f"   T={T} {'gate_up' if kind == 1 else 'down'} waits: producer w_empty {pct(v[0], v[3])} | "
-                      f"MMA acc_empty {pct(v[4], v[7])} x_full {pct(v[5], v[7])} a_full {pct(v[6], v[7])} | "
-                      f"converters w_full {pct(v[8], v[11])} a_empty {pct(v[9], v[11])}", flush=True)
-        print(f"T={T:5d} experts touched {touched:3d}: " + "  ".join(f"{n} {u} us {g} GB/s ({f})" for n, (u, g, f) in res.items()),
+        for impl in a.impl.split(",") + (["quant"] if "mx" in a.impl.split(",") else []):
+          res = {}
+          for kind, N, K, ob in ((1, 2 * ff, d, ff * 2), (2, d, ff, d * 4)) if impl != "quant" else ((1, 0, d, 0),):
+              for _ in range(3):
+                  run(kind)
+              torch.cuda.synchronize()
+              e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+              e0.record()
+              for _ in range(a.iters):
+                  run(kind)
+              e1.record()
+              torch.cuda.synchronize()
+              us = e0.elapsed_time(e1) / a.iters * 1e3
+              byts = touched * (-(-N // 128)) * (K // 64) * W.TILE_BYTES + rows * K * 2 + rows * ob
+              res["gate_up" if kind == 1 else "down"] = (round(us, 1), round(byts / us / 1e3, 1), round(byts / us / 1e3 / peak, 3))
+              prof = getattr(L.load(), "stb_debug_moe_prof", None)  # -DSTB_MOE_PROF variants only
+              if prof is not None:
+                  buf = (C.c_ulonglong * 16)()
+                  prof(buf)
+                  run(kind)
+                  torch.cuda.synchronize()
+                  prof(buf)
+                  v = list(buf)
+                  pct = lambda w, t: f"{100 * w / max(t, 1):4.1f}%"  # noqa: E731
+                  print(f"   T={T} {'gate_up' if kind == 1 else 'down'} waits: producer w_empty {pct(v[0], v[3])} | "
+                        f"MMA acc_empty {pct(v[4], v[7])} x_full {pct(v[5], v[7])} a_full {pct(v[6], v[7])} | "
+                        f"converters w_full {pct(v[8], v[11])} a_empty {pct(v[9], v[11])}", flush=True)
+          print(f"[{impl:5s}] T={T:5d} experts touched {touched:3d}: " + "  ".join(f"{n} {u} us {g} GB/s ({f})" for n, (u, g, f) in res.items()),
               flush=True)
 
 
