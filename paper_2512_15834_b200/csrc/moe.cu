@@ -117,10 +117,8 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   uint16_t v;
@@ -637,53 +635,59 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_mxfp4_kernel(const __gri
 }
 
 // ---------------------------------------------------------------- block-scaled MXFP4 grouped GEMM
-// tcgen05.mma kind::mxf8f6f4.block_scale: A = the e2m1 expert weights with their own ue8m0
-// scales (one per 32 along K, straight from the checkpoint), B = the token rows split exactly
-// into two e4m3 halves with one ue8m0 scale per 32 (x = hi * 2^s_hi + lo * 2^s_lo, stb_moe_quant):
-// B carries 2 BN rows (BN hi rows, then BN lo rows) and the epilogue adds the two accumulator
-// column halves. The tensor core applies every scale, so no thread dequantises: unpack warps only
-// re-space the packed codes into the operand layout the MMA reads (16 codes in the low 8 bytes of
-// each 16-byte chunk) and post the scale words into tensor memory. Formats settled by
-// tools/probe_mxf8f6f4.cu on a B200: SFA of weight row r at TMEM lane r, column r / 32, byte = the
-// MMA's 32-wide K slice (the scale id also goes into the instruction descriptor); SFB of B row n
-// at lane n % 32 of every lane quarter, column n / 32; N = 2 BN >= 32.
+// tcgen05.mma kind::mxf8f6f4.block_scale: A = the e2m1 expert weights with their own ue8m0 scales
+// (one per 32 along K, the checkpoint's), B = the token rows split exactly into two e4m3 halves with
+// one ue8m0 scale per 32 (x = hi 2^s_hi + lo 2^s_lo, stb_moe_quant): B carries 2 BN rows (BN hi
+// rows, then BN lo rows) and the epilogue adds the two accumulator column halves. No thread touches
+// a weight byte: the tensor-memory-accelerator unpacks the packed codes into the operand layout
+// (CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B: 16 codes in the low 8 bytes of each 16-byte chunk, 128-byte
+// swizzle; the transaction counts the 8 KB read, not the 16 KB written), and the MMA thread moves
+// both operands' scale words into tensor memory itself (tcgen05.cp.32x128b.warpx4), in issue order
+// with its MMAs. Weight format (runtime/weights.py pack_mx_stages): per (expert, 128-row tile,
+// 128-wide K stage) 8704 B = [128 rows][64 B] codes + [32 lanes][4] scale words (word (l, j) = the
+// four K-slice scales of row 32 j + l: the tcgen05.cp source layout). Formats settled on a B200 by
+// tools/probe_mxf8f6f4.cu and tools/probe_mx_tma.cu.
+//   warp 0      weight producer: one 3-D TMA (codes) + one bulk copy (scale words) per stage
+//   warp 1      MMA issuer: per stage 2 tcgen05.cp + 4 MMAs (32 of K each), commits free the rings
+//   warp 2      TMEM allocator, then token-scale stager: an item's B scale words for every stage,
+//               gathered from the [stage][hi|lo][row] words into the tcgen05.cp layout (double-buffered
+//               per item, so the L2 round trips overlap the previous item's stream)
+//   warp 3      token producer: BN hi rows + BN lo rows per stage (TMA, L2-resident)
+//   warps 4-7   epilogue: TMEM accumulator (double-buffered) -> SwiGLU / bias -> global
 __host__ __device__ constexpr int sf_pitch(int rows_cap) { return (rows_cap + 3) & ~3; }
-constexpr int MX_BK = 128;   // K per pipeline stage: two RAW tiles (one 128-byte swizzled row of codes)
-#ifndef STB_MX_UPAR
-#define STB_MX_UPAR 2
-#endif
-constexpr int MX_UPAR = STB_MX_UPAR;  // unpack warps per lane quarter (alternating stages)
-constexpr int kMxThreads = 32 * (4 + 4 * MX_UPAR + 4);
+constexpr int MX_BK = 128;          // K per pipeline stage
+constexpr int MX_STAGE = 8704;      // bytes of one weight stage in HBM (codes + scale words)
+constexpr int MX_KS_MAX = 24;       // K <= 3072: an item's token scale words fit one staging buffer
+constexpr int kMxThreads = 32 * 8;
 
 template <int BN>
 struct MxCfg {
   static constexpr int XB = 2 * BN * MX_BK;  // e4m3 hi + lo rows of one stage
-#ifndef STB_MX_XS
-#define STB_MX_XS 4
-#endif
-#ifndef STB_MX_AS
-#define STB_MX_AS 4
-#endif
-  static constexpr int XS = STB_MX_XS;       // token stages (L2-resident rows, TMA)
-  static constexpr int AB = BM * MX_BK;      // unpacked codes of one 128-row tile (16 KB)
-  static constexpr int AS = STB_MX_AS;       // unpacked A stages (+ their scale words in TMEM)
-  static constexpr int WB = 2 * RAW;         // packed codes + scales of one stage (two RAW tiles)
-#ifndef STB_MOE_MX_RING_KB
-#define STB_MOE_MX_RING_KB 220
-#endif
-  static constexpr int WS = std::min(24, (STB_MOE_MX_RING_KB * 1024 - XS * (XB + 512) - AS * AB) / WB);
-  static constexpr int XF = ((8 * (BN + 4) + 127) / 128) * 128;  // scale words of one stage: [2][BN + 4]
-  static constexpr int SMEM = 1024 + XS * XB + AS * AB + WS * WB + XS * XF + 1024;
+  static constexpr int AB = BM * MX_BK;      // unpacked codes of one 128-row stage (16 KB)
   static constexpr int SFB_COLS = (2 * BN + 31) / 32;
-  static constexpr int SF0 = 2 * 2 * BN;     // after the double-buffered accumulators
-  static constexpr int SFS = 8;              // TMEM columns of one A stage's scale words: 4 SFA + 4 SFB
-  static_assert(SFB_COLS <= 4 && SF0 + AS * SFS <= 512, "TMEM budget");
+  static constexpr int SFB_ITEM = MX_KS_MAX * 512;  // an item's token scale words, every stage
+#ifndef STB_MOE_MX_RING_KB
+#define STB_MOE_MX_RING_KB 222
+#endif
+  // one ring: a stage holds the weight codes, their scale words and the token halves, filled by two
+  // producers onto one barrier and freed by one commit (the MMA thread paces the kernel: every
+  // barrier operation it saves is issue time)
+  static constexpr int WS = std::min(16, (STB_MOE_MX_RING_KB * 1024 - 2 * SFB_ITEM) / (AB + 512 + XB));
+  static constexpr int XS = WS;
+  static constexpr int SMEM = 1024 + WS * AB + XS * XB + WS * 512 + 2 * SFB_ITEM + 1024;
+#ifndef STB_MX_ACC2
+#define STB_MX_ACC2 0
+#endif
+  // independent accumulators per buffer (K slices alternate between them, summed by the epilogue):
+  // consecutive MMAs of a stage do not wait on each other's accumulator
+  static constexpr int NACC = (STB_MX_ACC2 && BN <= 32) ? 2 : 1;
+  static constexpr int ACC_COLS = NACC * 2 * BN;  // one buffer
+  static constexpr int SF0 = 2 * ACC_COLS;   // TMEM: after the double-buffered accumulators
+  static constexpr int SFS = 8;              // 4 SFA + 4 SFB columns per scale slot
+  static constexpr int SLOTS = 4;
+  static_assert(SFB_COLS <= 4 && SF0 + SLOTS * SFS <= 512 && WS >= 4, "MX GEMM budget");
 };
 
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
-               "r"(r[2]), "r"(r[3]));
-}
 __device__ __forceinline__ void umma_mx(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb,
                                         uint32_t acc) {
   asm volatile(
@@ -691,33 +695,34 @@ __device__ __forceinline__ void umma_mx(uint32_t d, uint64_t a, uint64_t b, uint
       "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
 }
-__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+// 32 rows x 16 B of shared memory -> TMEM lanes 0-31 x 4 columns, replicated into every lane quarter
+__device__ __forceinline__ void tc_cp_sf(uint32_t taddr, uint32_t saddr) {
+  const uint64_t desc = (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;\n" ::"r"(taddr), "l"(desc));
 }
-// A = e2m1 (format 5), B = e4m3 (0), K-major, ue8m0 scales (bit 23), M = 128, N; scale ids per slice
+// A = e2m1 (format 5), B = e4m3 (0), K-major, ue8m0 scales (bit 23), M, N; scale ids per slice
 __host__ __device__ constexpr uint32_t idesc_mx(int M, int N) {
   return (5u << 7) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_x,
+__global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w,
+                                                                    const __grid_constant__ CUtensorMap tm_x,
                                                                     const uint32_t* __restrict__ xsf, int rows_cap,
                                                                     const MoeArgs a) {
   using CF = MxCfg<BN>;
-  constexpr int XS = CF::XS, AS = CF::AS, WS = CF::WS;
+  constexpr int WS = CF::WS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sx = smem;                   // [XS][2 BN rows][128 B], SW128
-  uint8_t* sa = sx + XS * CF::XB;       // [AS][128 rows][128 B], SW128 (unpacked codes)
-  uint8_t* sw = sa + AS * CF::AB;       // [WS][2][RAW] packed tiles as stored
-  uint8_t* sf = sw + WS * CF::WB;       // [XS][2][BN + 4] token scale words (bulk copies, with the rows)
-  uint64_t* w_full = reinterpret_cast<uint64_t*>(sf + XS * CF::XF);
-  uint64_t* w_empty = w_full + WS;      // unpackers -> weight producer
-  uint64_t* x_full = w_empty + WS;
-  uint64_t* x_empty = x_full + XS;      // MMA -> token producer
-  uint64_t* a_full = x_empty + XS;      // unpackers -> MMA
-  uint64_t* a_empty = a_full + AS;      // MMA -> unpackers
-  uint64_t* acc_full = a_empty + AS;    // [2]
+  uint8_t* sa = smem;                   // [WS][128 rows][128 B] unpacked codes, SW128 (TMA)
+  uint8_t* sx = sa + WS * CF::AB;       // [WS][2 BN rows][128 B] token halves, SW128 (TMA)
+  uint8_t* ssa = sx + WS * CF::XB;      // [WS][512 B] weight scale words
+  uint8_t* ssb = ssa + WS * 512;        // [2 items][KSB stages][512 B] token scale words
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(ssb + 2 * CF::SFB_ITEM);  // both producers (TMA bytes)
+  uint64_t* w_empty = w_full + WS;      // MMA -> both producers
+  uint64_t* b_full = w_empty + WS;      // [2] stager -> MMA (an item's token scale words)
+  uint64_t* b_empty = b_full + 2;       // [2] MMA -> stager
+  uint64_t* acc_full = b_empty + 2;     // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   __shared__ int s_off[kMaxE + 1];
@@ -725,23 +730,18 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
   __shared__ int s_cnt[kMaxE];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int E = a.E, NT = ceil_div(a.N, BM), KB = a.K / BK, KS = ceil_div(KB, 2);
+  const int E = a.E, NT = ceil_div(a.N, BM), KS = ceil_div(a.K, MX_BK);
   const int pitch = sf_pitch(rows_cap);
   if (threadIdx.x == 0) {
+    tma_prefetch(&tm_w);
     tma_prefetch(&tm_x);
     for (int s = 0; s < WS; ++s) {
-      mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], 4);
-    }
-    for (int s = 0; s < XS; ++s) {
-      mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1);
-    }
-    for (int s = 0; s < AS; ++s) {
-      mbar_init(&a_full[s], 4);
-      mbar_init(&a_empty[s], 1);
+      mbar_init(&w_full[s], 2);
+      mbar_init(&w_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&b_full[b], 1);
+      mbar_init(&b_empty[b], 1);
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 4);
     }
@@ -766,11 +766,6 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
   pdl_launch();
   const uint32_t tmem = *tmem_slot;
   const int total = s_item[E];
-#ifdef STB_MX_CONTIG  // experiment: each CTA a contiguous range of items
-  const int it0 = (int)((int64_t)total * blockIdx.x / gridDim.x), it1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x), istep = 1;
-#else
-  const int it0 = blockIdx.x, it1 = total, istep = gridDim.x;
-#endif
   // item -> (expert, weight tile, token tile); token tiles of one weight tile on neighbouring CTAs
   auto decode = [&](int it, int& e, int& nt, int& m) {
     int lo = 0, hi = E - 1;
@@ -786,156 +781,110 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
   };
 
   if (warp == 0) {
-    // weight producer: two RAW tiles (128 K) of the item's weight tile per stage, one bulk copy
     if (elect_one()) {
-      int i = 0;
-      for (int it = it0; it < it1; it += istep) {
+      int s = 0, ph = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x) {
         int e, nt, m;
         decode(it, e, nt, m);
-        const uint8_t* wt = a.w + ((int64_t)e * NT + nt) * KB * RAW;
-        for (int ks = 0; ks < KS; ++ks, ++i) {
-          const int s = i % WS;
-          const int nraw = min(2, KB - 2 * ks);
-          mbar_wait(&w_empty[s], ((i / WS) & 1) ^ 1);
-          mbar_expect_tx(&w_full[s], nraw * RAW);
-          bulk_load(smem_u32(sw + s * CF::WB), wt + (int64_t)(2 * ks) * RAW, nraw * RAW, &w_full[s]);
+        const int st0 = (e * NT + nt) * KS;
+        for (int ks = 0; ks < KS; ++ks, s = s + 1 == WS ? 0 : s + 1, ph ^= s == 0) {
+          mbar_wait(&w_empty[s], ph ^ 1);
+          mbar_expect_tx(&w_full[s], 8192 + 512);
+          tma_load_3d(sa + s * CF::AB, &tm_w, &w_full[s], 0, 0, st0 + ks);
+          bulk_load(smem_u32(ssa + s * 512), a.w + (int64_t)(st0 + ks) * MX_STAGE + 8192, 512, &w_full[s]);
         }
       }
     }
     __syncwarp();
   } else if (warp == 3) {
-    // token producer: BN hi rows and BN lo rows of the expert's token tile per stage (TMA, L2)
     if (elect_one()) {
-      int i = 0;
-      for (int it = it0; it < it1; it += istep) {
+      int s = 0, ph = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x) {
         int e, nt, m;
         decode(it, e, nt, m);
         const int xrow = s_off[e] + m * BN;
-        for (int ks = 0; ks < KS; ++ks, ++i) {
-          const int s = i % XS;
-          mbar_wait(&x_empty[s], ((i / XS) & 1) ^ 1);
-          // scale words of the tile's hi and lo rows: 16-byte aligned supersets (the pitch is a
-          // multiple of 4 words, so both start xrow & 3 words early)
-          const uint32_t sfw = (uint32_t)(((xrow & 3) + BN + 3) & ~3);
-          mbar_expect_tx(&x_full[s], CF::XB + 8 * sfw);
-          tma_load_2d(sx + s * CF::XB, &tm_x, &x_full[s], ks * MX_BK, xrow);
-          tma_load_2d(sx + s * CF::XB + BN * MX_BK, &tm_x, &x_full[s], ks * MX_BK, rows_cap + xrow);
-          for (int h = 0; h < 2; ++h)
-            bulk_load(smem_u32(sf + s * CF::XF + h * (BN + 4) * 4),
-                      xsf + ((int64_t)(2 * ks + h) * pitch + (xrow & ~3)), 4 * sfw, &x_full[s]);
+        for (int ks = 0; ks < KS; ++ks, s = s + 1 == WS ? 0 : s + 1, ph ^= s == 0) {
+          mbar_wait(&w_empty[s], ph ^ 1);
+          mbar_expect_tx(&w_full[s], CF::XB);
+          tma_load_2d(sx + s * CF::XB, &tm_x, &w_full[s], ks * MX_BK, xrow);
+          tma_load_2d(sx + s * CF::XB + BN * MX_BK, &tm_x, &w_full[s], ks * MX_BK, rows_cap + xrow);
         }
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    if (elect_one()) {
-      constexpr uint32_t idesc = idesc_mx(BM, 2 * BN);
-      int i = 0, j = 0;
-      for (int it = it0; it < it1; it += istep, ++j) {
-        const int buf = j & 1;
-        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + buf * 2 * BN;
-        for (int ks = 0; ks < KS; ++ks, ++i) {
-          const int xs = i % XS, as = i % AS;
-          mbar_wait(&x_full[xs], (i / XS) & 1);
-          mbar_wait(&a_full[as], (i / AS) & 1);
-          tc_fence_after();
-          const uint64_t adesc = umma_desc_kmajor_sw128(smem_u32(sa + as * CF::AB), 1024);
-          const uint64_t bdesc = umma_desc_kmajor_sw128(smem_u32(sx + xs * CF::XB), 1024);
-          const uint32_t sfa = tmem + CF::SF0 + as * CF::SFS, sfb = sfa + 4;
-          const int kk_n = (KB - 2 * ks) >= 2 ? 4 : 2;  // a lone last RAW tile is 64 of K
-#ifdef STB_MX_SKIP_MMA  // timing experiments only (results are wrong)
-          if (ks == 0)
-#endif
-          for (int kk = 0; kk < kk_n; ++kk)  // 32 of K per MMA: +32 B in both descriptors
-            umma_mx(d, adesc + 2 * kk, bdesc + 2 * kk, idesc | ((uint32_t)kk << 29) | ((uint32_t)kk << 4),
-                    sfa | ((uint32_t)kk << 30), sfb | ((uint32_t)kk << 30), (ks > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&x_empty[xs]);
-          umma_commit(&a_empty[as]);
-        }
-        umma_commit(&acc_full[buf]);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4 && warp < 4 + 4 * MX_UPAR) {
-    // unpackers: warp = (parity, lane quarter q); thread = weight row r = 32 q + lane
-    const int q = warp & 3, par = (warp - 4) >> 2, r = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t sw_u32 = smem_u32(sw), sa_u32 = smem_u32(sa), sf_u32 = smem_u32(sf);
-    int i = 0;
-    for (int it = it0; it < it1; it += istep) {
+  } else if (warp == 2) {
+    // token-scale stager: word (l, c) of stage ks = the scale word of B row n = 32 c + l
+    int j = 0;
+    for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
       int e, nt, m;
       decode(it, e, nt, m);
       const int xrow = s_off[e] + m * BN;
-      for (int ks = 0; ks < KS; ++ks, ++i) {
-        if (i % MX_UPAR != par) continue;
-        const int s = i % WS, as = i % AS;
-        const bool two = (KB - 2 * ks) >= 2;
-        mbar_wait(&w_full[s], (i / WS) & 1);
-        const uint32_t raw = sw_u32 + s * CF::WB;
-        const uint4 c0 = lds128(raw + r * 32), c1 = lds128(raw + r * 32 + 16);
-        uint4 c2 = make_uint4(0u, 0u, 0u, 0u), c3 = c2;
-        const uint32_t sc0 = lds16(raw + 4096 + r * 2);
-        uint32_t sc1 = 0x7f7fu;
-        if (two) {
-          c2 = lds128(raw + RAW + r * 32);
-          c3 = lds128(raw + RAW + r * 32 + 16);
-          sc1 = lds16(raw + RAW + 4096 + r * 2);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&w_empty[s]);
-        mbar_wait(&a_empty[as], ((i / AS) & 1) ^ 1);
+      const int ib = j & 1;
+      mbar_wait(&b_empty[ib], ((j >> 1) & 1) ^ 1);
+      const uint32_t base = smem_u32(ssb + ib * CF::SFB_ITEM);
+      for (int ks0 = 0; ks0 < KS; ks0 += 8) {
+        uint32_t v[8][4];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int n = 32 * c + lane, h = n >= BN, tok = n - h * BN, row = xrow + tok;
+            v[u][c] = (c < CF::SFB_COLS && ks0 + u < KS && n < 2 * BN && row < rows_cap)
+                          ? __ldg(xsf + (int64_t)(2 * (ks0 + u) + h) * pitch + row) : 0x7f7f7f7fu;
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (ks0 + u < KS) sts128(base + (ks0 + u) * 512 + lane * 16, v[u][0], v[u][1], v[u][2], v[u][3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&b_full[ib]);
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_mx(BM, 2 * BN);
+      const uint32_t sa0 = smem_u32(sa), sx0 = smem_u32(sx), ssa0 = smem_u32(ssa);
+      int s = 0, ph = 0, slot = 0, j = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
+        const int buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&b_full[buf], (j >> 1) & 1);
         tc_fence_after();
-        // row r: 8 chunks of 16 codes (8 bytes each, padded to 16), 128-byte swizzle
-        const uint32_t row = sa_u32 + as * CF::AB + r * 128;
-#ifdef STB_MX_SKIP_UNPACK  // timing experiments only (results are wrong)
-        if (ks == 0) {
-#else
-        {
+        const uint32_t d = tmem + buf * CF::ACC_COLS;
+        uint32_t sbi = smem_u32(ssb + buf * CF::SFB_ITEM);
+        for (int ks = 0; ks < KS; ++ks, s = s + 1 == WS ? 0 : s + 1, ph ^= s == 0, sbi += 512) {
+          mbar_wait(&w_full[s], ph);
+          tc_fence_after();
+          const uint32_t sfa = tmem + CF::SF0 + slot * CF::SFS, sfb = sfa + 4;
+          slot = (slot + 1) & (CF::SLOTS - 1);
+          tc_cp_sf(sfa, ssa0 + s * 512);
+          tc_cp_sf(sfb, sbi);
+          const uint64_t adesc = umma_desc_kmajor_sw128(sa0 + s * CF::AB, 1024);
+          const uint64_t bdesc = umma_desc_kmajor_sw128(sx0 + s * CF::XB, 1024);
+          // always 4 slices of 32: a last stage of 64 of K reads zero codes and zero token bytes
+#ifdef STB_MX_SKIP_MMA  // timing experiments only (results are wrong)
+          if (ks == 0)
 #endif
-        const uint32_t sx7 = r & 7;
-        sts128(row + ((0 ^ sx7) << 4), c0.x, c0.y, 0u, 0u);
-        sts128(row + ((1 ^ sx7) << 4), c0.z, c0.w, 0u, 0u);
-        sts128(row + ((2 ^ sx7) << 4), c1.x, c1.y, 0u, 0u);
-        sts128(row + ((3 ^ sx7) << 4), c1.z, c1.w, 0u, 0u);
-        if (two) {
-          sts128(row + ((4 ^ sx7) << 4), c2.x, c2.y, 0u, 0u);
-          sts128(row + ((5 ^ sx7) << 4), c2.z, c2.w, 0u, 0u);
-          sts128(row + ((6 ^ sx7) << 4), c3.x, c3.y, 0u, 0u);
-          sts128(row + ((7 ^ sx7) << 4), c3.z, c3.w, 0u, 0u);
-        }
-        }
-        // SFA: row r's four 32-wide K slices at lane r, column r / 32 (= q)
-        uint32_t sfa[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) sfa[c] = c == q ? (sc0 | (sc1 << 16)) : 0x7f7f7f7fu;
-        // SFB: B row n = 32 c + lane (BN hi rows, then BN lo rows) at lane n % 32 of every quarter
-        const int xs = i % XS;
-        mbar_wait(&x_full[xs], (i / XS) & 1);
-        uint32_t sfb[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int n = 32 * c + lane;
-          const int h = n >= BN, tok = n - h * BN;
-          sfb[c] = n < 2 * BN ? lds32(sf_u32 + xs * CF::XF + (h * (BN + 4) + (xrow & 3) + tok) * 4) : 0x7f7f7f7fu;
+          for (int kk = 0; kk < 4; ++kk) {  // +32 B along K in both descriptors
+            const int acc = CF::NACC == 2 ? (kk & 1) : 0;
+            umma_mx(d + acc * 2 * BN, adesc + 2 * kk, bdesc + 2 * kk,
+                    idesc | ((uint32_t)kk << 29) | ((uint32_t)kk << 4), sfa | ((uint32_t)kk << 30),
+                    sfb | ((uint32_t)kk << 30), (ks > 0 || kk > acc) ? 1u : 0u);
+          }
+          umma_commit(&w_empty[s]);
         }
-        const uint32_t sfcol = tmem + lane_addr + CF::SF0 + as * CF::SFS;
-        tmem_st4(sfcol, sfa);
-        tmem_st4(sfcol + 4, sfb);
-        tmem_st_wait();
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[as]);
+        umma_commit(&acc_full[buf]);
+        umma_commit(&b_empty[buf]);
       }
     }
-  } else if (warp >= 4 + 4 * MX_UPAR) {
+    __syncwarp();
+  } else {
     // epilogue: thread = weight row (feature); columns = tokens (hi half + lo half)
     const int q = warp & 3;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int j = 0;
-    for (int it = it0; it < it1; it += istep, ++j) {
+    for (int it = blockIdx.x; it < total; it += gridDim.x, ++j) {
       int e, nt, m;
       decode(it, e, nt, m);
       const int buf = j & 1;
@@ -948,11 +897,22 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         uint32_t rr[16], rl[16];
-        tmem_ld16(tmem + lane_addr + buf * 2 * BN + c, rr);
-        tmem_ld16(tmem + lane_addr + buf * 2 * BN + BN + c, rl);
+        const uint32_t cb = tmem + lane_addr + buf * CF::ACC_COLS + c;
+        tmem_ld16(cb, rr);
+        tmem_ld16(cb + BN, rl);
         tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < 16; ++u) rr[u] = __float_as_uint(__uint_as_float(rr[u]) + __uint_as_float(rl[u]));
+        if constexpr (CF::NACC == 2) {
+          tmem_ld16(cb + 2 * BN, rl);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) rr[u] = __float_as_uint(__uint_as_float(rr[u]) + __uint_as_float(rl[u]));
+          tmem_ld16(cb + 3 * BN, rl);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) rr[u] = __float_as_uint(__uint_as_float(rr[u]) + __uint_as_float(rl[u]));
+        }
         if (a.kind == 2) {
           float* y = reinterpret_cast<float*>(a.out);
           if (f < a.N) {
@@ -1114,13 +1074,44 @@ int launch_moe_gemm(const void* xperm, int rows_cap, const MoeArgs& a, cudaStrea
   return STB_OK;
 }
 
+// MX weight stages of every expert of one projection as a 3-D map: [stages][128 rows][128 codes],
+// rows 64 B apart, stages 8704 B apart; box = one stage, unpacked to 16-byte chunks (16U4_ALIGN16B)
+int w_map(CUtensorMap* out, const void* base, int64_t stages) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int>, CUtensorMap> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(base, stages, dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return STB_OK;
+  }
+  auto fn = encode_fn();
+  if (!fn) return fail(STB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)MX_BK, (cuuint64_t)BM, (cuuint64_t)stages};
+  cuuint64_t strides[2] = {(cuuint64_t)(MX_BK / 2), (cuuint64_t)MX_STAGE};
+  cuuint32_t box[3] = {(cuuint32_t)MX_BK, (cuuint32_t)BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(STB_ECUDA, "moe: weight tensor map encode failed (%d)", (int)r);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *out);
+  return STB_OK;
+}
+
 template <int BN>
 int launch_moe_mx(const void* xq, const uint32_t* xsf, int rows_cap, const MoeArgs& a, cudaStream_t st) {
-  CUtensorMap tm;
-  if (int rc = x_map(&tm, xq, 2 * (int64_t)rows_cap, a.K, BN, 1)) return rc;
+  CUtensorMap tw, tx;
+  const int64_t stages = (int64_t)a.E * ((a.N + BM - 1) / BM) * ((a.K + MX_BK - 1) / MX_BK);
+  if (int rc = w_map(&tw, a.w, stages)) return rc;
+  if (int rc = x_map(&tx, xq, 2 * (int64_t)rows_cap, a.K, BN, 1)) return rc;
   auto kern = moe_gemm_mx_kernel<BN>;
   smem_attr_once(kern, MxCfg<BN>::SMEM);
-  cudaError_t e = launch_k(kern, dim3(device_sms()), dim3(kMxThreads), MxCfg<BN>::SMEM, st, tm, xsf, rows_cap, a);
+  cudaError_t e = launch_k(kern, dim3(device_sms()), dim3(kMxThreads), MxCfg<BN>::SMEM, st, tw, tx, xsf, rows_cap, a);
   if (e != cudaSuccess) return fail(STB_ECUDA, "moe_gemm_mx launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
@@ -1153,8 +1144,9 @@ int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const voi
                     const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
                     void* stream) {
   if (rows <= 0) return STB_OK;
-  if (E <= 0 || E > kMaxE || K % BK || K % 16 || N <= 0 || (kind != STB_MOE_GATE_UP && kind != STB_MOE_DOWN) ||
-      (kind == STB_MOE_GATE_UP && N % 2))
+  if (E <= 0 || E > kMaxE || K % BK || K > MX_KS_MAX * MX_BK || N <= 0 ||
+      (kind != STB_MOE_GATE_UP && kind != STB_MOE_DOWN) || (kind == STB_MOE_GATE_UP && N % 2) ||
+      (reinterpret_cast<uintptr_t>(wtiles) & 15))
     return fail(STB_EINVAL, "moe_gemm_mx: E=%d N=%d K=%d kind=%d", E, N, K, kind);
   MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit};
   const double avg = (double)rows / E;

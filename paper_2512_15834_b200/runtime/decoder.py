@@ -73,7 +73,7 @@ MOE_PROJECTIONS = ("wqkv", "wo", "router")   # gpt-oss: the experts are MXFP4 ti
 MOE_GATE_UP, MOE_DOWN = 1, 2                 # include/stb200.h STB_MOE_*
 # MoE GEMMs on the block-scaled tensor-core path (stb_moe_quant + stb_moe_gemm_mx);
 # STB200_MOE_MX=0 keeps the dequantising kernel (stb_moe_gemm_mxfp4) for A/B
-MOE_MX = os.environ.get("STB200_MOE_MX", "1") != "0"
+from .weights import MOE_MX  # noqa: E402  (the experts' packing follows the same switch)
 MOE_TILE_BYTES = 4352                        # one 128 x 64 MXFP4 tile (weights.TILE_BYTES)
 
 

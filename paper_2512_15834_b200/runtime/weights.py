@@ -24,7 +24,10 @@ from __future__ import annotations
 
 import zlib
 
+import os
+
 import numpy as np
+
 import torch
 
 from ..modelcfg import ModelShape
@@ -130,9 +133,41 @@ def pack_mxfp4_tiles(codes: torch.Tensor, exps: torch.Tensor) -> torch.Tensor:
     return torch.cat([byte, sc], dim=2).contiguous()
 
 
+MX_STAGE_K = 128
+MX_STAGE_BYTES = TILE_ROWS * MX_STAGE_K // 2 + 512  # 8192 B of codes + 32 x 4 scale words
+# experts in the block-scaled GEMM's stage format (csrc/moe.cu stb_moe_gemm_mx); STB200_MOE_MX=0 keeps
+# the dequantising kernel's tiles (stb_moe_gemm_mxfp4) for A/B
+MOE_MX = os.environ.get("STB200_MOE_MX", "1") != "0"
+
+
+def pack_mx_stages(codes: torch.Tensor, exps: torch.Tensor) -> torch.Tensor:
+    """(codes [N][K], exps [N][K/32]) -> uint8 [ceil(N/128)][ceil(K/128)][8704]: stage (n, s) = 128
+    rows x 128 values of K as [128 rows][64 bytes] (byte j of a row: value 2j in the low nibble, 2j+1
+    in the high; the tensor-memory accelerator unpacks them to 16-byte chunks) followed by 32 x 4
+    scale words, word (l, j) = the four ue8m0 bytes (exponent + 127) of row 32 j + l, K slice t in
+    byte t (the tcgen05.cp source layout). Rows past N and K past K are zero codes with scale 127."""
+    N, K = codes.shape
+    if K % TILE_K:
+        raise ValueError("MX stages need K % 64 == 0")
+    NT, KS = -(-N // TILE_ROWS), -(-K // MX_STAGE_K)
+    c = torch.zeros(NT * TILE_ROWS, KS * MX_STAGE_K, dtype=torch.uint8, device=codes.device)
+    c[:N, :K] = codes
+    s = torch.full((NT * TILE_ROWS, KS * 4), 127, dtype=torch.uint8, device=codes.device)
+    s[:N, :K // 32] = (exps.to(torch.int16) + 127).to(torch.uint8)
+    byte = c[:, 0::2] | (c[:, 1::2] << 4)                                         # [NT*128][KS*64]
+    byte = byte.reshape(NT, TILE_ROWS, KS, 64).permute(0, 2, 1, 3).reshape(NT, KS, TILE_ROWS * 64)
+    sc = s.reshape(NT, 4, 32, KS, 4).permute(0, 3, 2, 1, 4).reshape(NT, KS, 512)  # [n][s][l][j][t]
+    return torch.cat([byte, sc], dim=2).contiguous()
+
+
+def pack_experts(codes: torch.Tensor, exps: torch.Tensor) -> torch.Tensor:
+    """The product's expert packing: MX stages (block-scaled GEMM) or MXFP4 tiles (STB200_MOE_MX=0)."""
+    return pack_mx_stages(codes, exps) if MOE_MX else pack_mxfp4_tiles(codes, exps)
+
+
 class MoELayer:
-    """One layer's experts on the device: packed MXFP4 gate-up / down tiles for all experts
-    (uint8 [E][NT][KB][4352] each) and fp32 biases [E][2ff] / [E][d]."""
+    """One layer's experts on the device: packed MXFP4 gate-up / down experts (uint8 [E][NT][KS][8704]
+    MX stages, or [E][NT][KB][4352] tiles with STB200_MOE_MX=0) and fp32 biases [E][2ff] / [E][d]."""
 
     __slots__ = ("gate_up", "b_gate_up", "down", "b_down")
 
@@ -147,8 +182,8 @@ def build_experts(shape: ModelShape, layer: int, seed: int, init_device: str, de
     gu, bgu, dn, bdn = [], [], [], []
     for e in range(shape.n_experts):
         (n_gu, s_gu), (n_bgu, s_bgu), (n_dn, s_dn), (n_bdn, s_bdn) = expert_specs(shape, layer, e)
-        gu.append(pack_mxfp4_tiles(*quantize_mxfp4(draw(s_gu, seed, n_gu, init_device))).to(device))
-        dn.append(pack_mxfp4_tiles(*quantize_mxfp4(draw(s_dn, seed, n_dn, init_device))).to(device))
+        gu.append(pack_experts(*quantize_mxfp4(draw(s_gu, seed, n_gu, init_device))).to(device))
+        dn.append(pack_experts(*quantize_mxfp4(draw(s_dn, seed, n_dn, init_device))).to(device))
         bgu.append(draw(s_bgu, seed, n_bgu, init_device).float().to(device))
         bdn.append(draw(s_bdn, seed, n_bdn, init_device).float().to(device))
     return MoELayer(torch.stack(gu), torch.stack(bgu), torch.stack(dn), torch.stack(bdn))

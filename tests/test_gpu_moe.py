@@ -84,13 +84,13 @@ def test_moe_gather(lib):
         assert torch.equal(xp[pm[p]], h[p // k].to(torch.float16))
 
 
-def _experts(E, N, K, seed):
+def _experts(E, N, K, seed, pack=W.pack_mxfp4_tiles):
     g = torch.Generator(device="cuda").manual_seed(seed)
     tiles, deq = [], []
     for _ in range(E):
         w = (0.02 * torch.randn(N, K, device="cuda", generator=g)).to(torch.bfloat16)
         c, e = W.quantize_mxfp4(w)
-        tiles.append(W.pack_mxfp4_tiles(c, e))
+        tiles.append(pack(c, e))
         deq.append(W.dequantize_mxfp4(c, e))
     bias = 0.02 * torch.randn(E, N, device="cuda", generator=g)
     return torch.stack(tiles).contiguous(), torch.stack(deq), bias
@@ -175,11 +175,12 @@ def test_moe_quant(lib, rows, K):
 @pytest.mark.parametrize("T,E,k,d,ff", [(1, 16, 4, 512, 256), (32, 128, 4, 2880, 2880), (300, 16, 4, 512, 256),
                                         (700, 32, 4, 1024, 512), (64, 8, 2, 256, 384), (16, 8, 2, 64, 128)])
 def test_moe_gemm_mx(lib, T, E, k, d, ff):
-    """Block-scaled grouped GEMM (tcgen05 kind::mxf8f6f4: e2m1 weights x e4m3 hi/lo token halves, the
-    tensor core applying both ue8m0 scales), both kinds, vs fp32 math on the dequantised weights and
-    the fp16 token rows; token tiles 16 / 32 / 64, K with a lone 64-wide last stage (2880, 64)."""
-    gu_t, gu_w, gu_b = _experts(E, 2 * ff, d, 1)
-    dn_t, dn_w, dn_b = _experts(E, d, ff, 2)
+    """Block-scaled grouped GEMM (tcgen05 kind::mxf8f6f4: e2m1 weights unpacked by the TMA x e4m3 hi/lo
+    token halves, the tensor core applying both ue8m0 scales moved in by tcgen05.cp), both kinds, vs
+    fp32 math on the dequantised weights and the fp16 token rows; token tiles 16 / 32 / 64, K with a
+    64-wide last stage (2880, 64), N not a multiple of 128 (384 -> 768 gate-up rows are; d = 64 not)."""
+    gu_t, gu_w, gu_b = _experts(E, 2 * ff, d, 1, W.pack_mx_stages)
+    dn_t, dn_w, dn_b = _experts(E, d, ff, 2, W.pack_mx_stages)
     logits = torch.randn(T, E, device="cuda")
     counts, ex, rk, wt = _route(lib, logits, torch.zeros(E, device="cuda"), k)
     h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
@@ -205,6 +206,27 @@ def test_moe_gemm_mx(lib, T, E, k, d, ff):
         ref_y = act[a:b].float() @ dn_w[e].T + dn_b[e]
         assert rel(y[a:b], ref_y) < 5e-3, ("down", e, rel(y[a:b], ref_y))
     assert not torch.isnan(act[:rows]).any() and not torch.isnan(y[:rows]).any()
+
+
+def test_pack_mx_stages():
+    """MX stage layout: codes row-major in 64-byte rows, scale word (l, j) = row 32 j + l."""
+    N, K = 200, 320
+    g = torch.Generator().manual_seed(3)
+    codes = torch.randint(0, 16, (N, K), generator=g).to(torch.uint8)
+    exps = torch.randint(-13, 13, (N, K // 32), generator=g).to(torch.int8)
+    st = W.pack_mx_stages(codes, exps)
+    assert st.shape == (2, 3, W.MX_STAGE_BYTES)
+    for n, r, s_, k in [(0, 0, 0, 0), (1, 71, 2, 63), (0, 127, 1, 100), (1, 50, 0, 5)]:
+        row = n * 128 + r
+        b = int(st[n, s_, r * 64 + k // 2])
+        kk = s_ * 128 + k
+        want = int(codes[row, kk]) if row < N and kk < K else 0
+        assert (b >> (4 * (k & 1))) & 15 == want
+        word = st[n, s_, 8192:].view(torch.int32)[(r % 32) * 4 + r // 32].item() & 0xFFFFFFFF
+        for t in range(4):
+            blk = s_ * 4 + t
+            want_s = int(exps[row, blk]) + 127 if row < N and blk < K // 32 else 127
+            assert (word >> (8 * t)) & 255 == want_s
 
 
 def test_moe_combine(lib):

@@ -41,7 +41,13 @@ def main():
         t = torch.randint(0, 256, (E, -(-N // 128), K // 64, W.TILE_BYTES), dtype=torch.uint8, device="cuda")
         t[..., 4096:] = 120
         return t
-    gu, dn = tiles(2 * ff, d), tiles(d, ff)
+    def stages(N, K):  # MX stage format (stb_moe_gemm_mx)
+        t = torch.randint(0, 256, (E, -(-N // 128), -(-K // 128), W.MX_STAGE_BYTES), dtype=torch.uint8, device="cuda")
+        t[..., 8192:] = 120
+        return t
+    impls = a.impl.split(",")
+    gu, dn = (tiles(2 * ff, d), tiles(d, ff)) if "mxfp4" in impls else (None, None)
+    gum, dnm = (stages(2 * ff, d), stages(d, ff)) if "mx" in impls else (None, None)
     bgu, bdn = torch.zeros(E, 2 * ff, device="cuda"), torch.zeros(E, d, device="cuda")
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     for T in [int(x) for x in a.T.split(",")]:
@@ -72,10 +78,10 @@ def main():
             if impl == "quant":
                 L.call("stb_moe_quant", P(xp), d, rows, d, cap, P(xq[0]), P(xsf[0]), st)
             elif impl == "mx" and kind == 1:
-                L.call("stb_moe_gemm_mx", P(xq[0]), P(xsf[0]), cap, P(gu), P(bgu), P(counts), E, 2 * ff, d, 1, 7.0,
+                L.call("stb_moe_gemm_mx", P(xq[0]), P(xsf[0]), cap, P(gum), P(bgu), P(counts), E, 2 * ff, d, 1, 7.0,
                        P(act), ff, rows, st)
             elif impl == "mx":
-                L.call("stb_moe_gemm_mx", P(xq[1]), P(xsf[1]), cap, P(dn), P(bdn), P(counts), E, d, ff, 2, 0.0, P(y),
+                L.call("stb_moe_gemm_mx", P(xq[1]), P(xsf[1]), cap, P(dnm), P(bdn), P(counts), E, d, ff, 2, 0.0, P(y),
                        d, rows, st)
             elif kind == 1:
                 L.call("stb_moe_gemm_mxfp4", P(xp), cap, P(gu), P(bgu), P(counts), E, 2 * ff, d, 1, 7.0, P(act), ff,
