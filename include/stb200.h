@@ -357,6 +357,11 @@ int stb_moe_combine(float* x, const float* y, int T, int d, int k, const int32_t
 int64_t stb_moe_quant_bytes(int rows_cap, int K);
 int64_t stb_moe_quant_scale_words(int rows_cap, int K);
 int stb_moe_quant(const void* x, int64_t ldx, int rows, int K, int rows_cap, void* xq, uint32_t* xsf, void* stream);
+/* gather + quant in one pass for the gate-up input: offsets / perm exactly as stb_moe_gather, the
+ * routed bf16 rows of h split into xq / xsf as stb_moe_quant would (no fp16 xperm). */
+int stb_moe_gather_mx(const void* h, int64_t ldh, int T, int d, int k, int E, const int32_t* counts,
+                      const int32_t* expert, const int32_t* rank, int32_t* offsets, int32_t* perm, int rows_cap,
+                      void* xq, uint32_t* xsf, void* stream);
 int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
                     const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
                     void* stream);

@@ -967,6 +967,46 @@ __device__ __forceinline__ float2 e4m3x2_to_f2(uint16_t v) {
   asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
   return __half22float2(*reinterpret_cast<__half2*>(&h));
 }
+// one 128-wide stage of one token row, lane = 4 values (v): hi / lo codes and the scale words
+__device__ __forceinline__ void quant_stage(const float* v, int lane, int ks, int K, int row, int rows_cap,
+                                            uint8_t* __restrict__ xq, uint32_t* __restrict__ xsf) {
+  const int k = ks * MX_BK + lane * 4;
+  float am = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  const int eh = blk_exp(am);
+  float s[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) s[u] = ldexpf(v[u], -eh);
+  const uint32_t hq = e4m3x4(s[0], s[1], s[2], s[3]);
+  const float2 h01 = e4m3x2_to_f2((uint16_t)(hq & 0xFFFF)), h23 = e4m3x2_to_f2((uint16_t)(hq >> 16));
+  float r[4] = {s[0] - h01.x, s[1] - h01.y, s[2] - h23.x, s[3] - h23.y};
+  float ar = fmaxf(fmaxf(fabsf(r[0]), fabsf(r[1])), fmaxf(fabsf(r[2]), fabsf(r[3])));
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) ar = fmaxf(ar, __shfl_xor_sync(0xffffffffu, ar, o));
+  const int el = blk_exp(ar);
+  const uint32_t lq = e4m3x4(ldexpf(r[0], -el), ldexpf(r[1], -el), ldexpf(r[2], -el), ldexpf(r[3], -el));
+  if (k < K) {
+    *reinterpret_cast<uint32_t*>(xq + (int64_t)row * K + k) = hq;
+    *reinterpret_cast<uint32_t*>(xq + ((int64_t)rows_cap + row) * K + k) = lq;
+  }
+  // block b = lane / 8: scale bytes of the four blocks gathered into lane 0
+  const bool live = ks * MX_BK + (lane & ~7) * 4 < K;
+  const uint32_t bh = live ? (uint32_t)(eh + 127) : 127u, bl = live ? (uint32_t)(eh + el + 127) : 127u;
+  uint32_t wh = 0, wl = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    wh |= __shfl_sync(0xffffffffu, bh, 8 * b) << (8 * b);
+    wl |= __shfl_sync(0xffffffffu, bl, 8 * b) << (8 * b);
+  }
+  if (lane == 0) {
+    const int64_t pitch = sf_pitch(rows_cap);
+    xsf[((int64_t)ks * 2) * pitch + row] = wh;
+    xsf[((int64_t)ks * 2 + 1) * pitch + row] = wl;
+  }
+
+}
+
 __global__ void __launch_bounds__(256) moe_quant_kernel(const __half* __restrict__ x, int64_t ldx, int rows, int K,
                                                         int rows_cap, uint8_t* __restrict__ xq,
                                                         uint32_t* __restrict__ xsf) {
@@ -985,39 +1025,41 @@ __global__ void __launch_bounds__(256) moe_quant_kernel(const __half* __restrict
       const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
       v[0] = a0.x, v[1] = a0.y, v[2] = a1.x, v[3] = a1.y;
     }
-    float am = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
-    const int eh = blk_exp(am);
-    float s[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) s[u] = ldexpf(v[u], -eh);
-    const uint32_t hq = e4m3x4(s[0], s[1], s[2], s[3]);
-    const float2 h01 = e4m3x2_to_f2((uint16_t)(hq & 0xFFFF)), h23 = e4m3x2_to_f2((uint16_t)(hq >> 16));
-    float r[4] = {s[0] - h01.x, s[1] - h01.y, s[2] - h23.x, s[3] - h23.y};
-    float ar = fmaxf(fmaxf(fabsf(r[0]), fabsf(r[1])), fmaxf(fabsf(r[2]), fabsf(r[3])));
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) ar = fmaxf(ar, __shfl_xor_sync(0xffffffffu, ar, o));
-    const int el = blk_exp(ar);
-    const uint32_t lq = e4m3x4(ldexpf(r[0], -el), ldexpf(r[1], -el), ldexpf(r[2], -el), ldexpf(r[3], -el));
-    if (k < K) {
-      *reinterpret_cast<uint32_t*>(xq + (int64_t)row * K + k) = hq;
-      *reinterpret_cast<uint32_t*>(xq + ((int64_t)rows_cap + row) * K + k) = lq;
+    quant_stage(v, lane, ks, K, row, rows_cap, xq, xsf);
+  }
+}
+
+// stb_moe_gather + stb_moe_quant in one pass for the gate-up input: offsets / perm as the gather,
+// and the routed bf16 token rows split straight into the e4m3 halves (no fp16 copy)
+__global__ void __launch_bounds__(256) moe_gather_mx_kernel(const __nv_bfloat16* __restrict__ h, int64_t ldh, int T,
+                                                            int d, int k, int E, const int* __restrict__ counts,
+                                                            const int* __restrict__ expert,
+                                                            const int* __restrict__ rank, int* __restrict__ offsets,
+                                                            int* __restrict__ perm, int rows_cap,
+                                                            uint8_t* __restrict__ xq, uint32_t* __restrict__ xsf) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ int off[kMaxE + 1];
+  block_prefix(counts, E, off);
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) offsets[e] = off[e];
+  const int KS = (d + MX_BK - 1) / MX_BK;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < (int64_t)T * k * KS; w += nw) {
+    const int p = (int)(w / KS), ks = (int)(w - (int64_t)p * KS);
+    const int t = p / k;
+    const int row = off[expert[p]] + rank[p];
+    if (ks == 0 && lane == 0) perm[p] = row;
+    const int c = ks * MX_BK + lane * 4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c < d) {
+      const uint2 u = *reinterpret_cast<const uint2*>(h + (int64_t)t * ldh + c);
+      const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      v[0] = a0.x, v[1] = a0.y, v[2] = a1.x, v[3] = a1.y;
     }
-    // block b = lane / 8: scale bytes of the four blocks gathered into lane 0
-    const bool live = ks * MX_BK + (lane & ~7) * 4 < K;
-    const uint32_t bh = live ? (uint32_t)(eh + 127) : 127u, bl = live ? (uint32_t)(eh + el + 127) : 127u;
-    uint32_t wh = 0, wl = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      wh |= __shfl_sync(0xffffffffu, bh, 8 * b) << (8 * b);
-      wl |= __shfl_sync(0xffffffffu, bl, 8 * b) << (8 * b);
-    }
-    if (lane == 0) {
-      const int64_t pitch = sf_pitch(rows_cap);
-      xsf[((int64_t)ks * 2) * pitch + row] = wh;
-      xsf[((int64_t)ks * 2 + 1) * pitch + row] = wl;
-    }
+    quant_stage(v, lane, ks, d, row, rows_cap, xq, xsf);
   }
 }
 
@@ -1137,6 +1179,21 @@ int stb_moe_quant(const void* x, int64_t ldx, int rows, int K, int rows_cap, voi
   cudaError_t e = launch_k(moe_quant_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, (const __half*)x, ldx,
                            rows, K, rows_cap, (uint8_t*)xq, xsf);
   if (e != cudaSuccess) return fail(STB_ECUDA, "moe_quant launch: %s", cudaGetErrorString(e));
+  return STB_OK;
+}
+
+int stb_moe_gather_mx(const void* h, int64_t ldh, int T, int d, int k, int E, const int32_t* counts,
+                      const int32_t* expert, const int32_t* rank, int32_t* offsets, int32_t* perm, int rows_cap,
+                      void* xq, uint32_t* xsf, void* stream) {
+  if (T <= 0) return STB_OK;
+  if (E <= 0 || E > kMaxE || d % 4 || ldh % 4 || T * k > rows_cap)
+    return fail(STB_EINVAL, "moe_gather_mx: E=%d d=%d rows=%d cap=%d", E, d, T * k, rows_cap);
+  const int64_t warps = (int64_t)T * k * ((d + MX_BK - 1) / MX_BK);
+  const int blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (warps + 7) / 8), 4 * device_sms());
+  cudaError_t e = launch_k(moe_gather_mx_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream,
+                           (const __nv_bfloat16*)h, ldh, T, d, k, E, counts, expert, rank, offsets, perm, rows_cap,
+                           (uint8_t*)xq, xsf);
+  if (e != cudaSuccess) return fail(STB_ECUDA, "moe_gather_mx launch: %s", cudaGetErrorString(e));
   return STB_OK;
 }
 

@@ -806,18 +806,18 @@ class Decoder:
             if self.route_log is not None:
                 self.route_log.append(self.m_expert[:rows].clone())
             offs = self.m_offs[i]
-            call("stb_moe_gather", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
-                 _p(self.m_rank), _p(offs), _p(self.m_perm), _p(self.m_x), st)
             ex = w[f"l{i}.experts"]
             cap_r = self._moe_rows
-            if MOE_MX:  # block-scaled tensor-core path: split the rows into e4m3 halves first
-                call("stb_moe_quant", _p(self.m_x), self.m_x.stride(0), rows, d, cap_r, _p(self.m_xq),
-                     _p(self.m_xsf), st)
+            if MOE_MX:  # block-scaled tensor-core path: the gather splits the rows into e4m3 halves
+                call("stb_moe_gather_mx", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
+                     _p(self.m_rank), _p(offs), _p(self.m_perm), cap_r, _p(self.m_xq), _p(self.m_xsf), st)
                 ev = self._tick()
                 call("stb_moe_gemm_mx", _p(self.m_xq), _p(self.m_xsf), cap_r, _p(ex.gate_up), _p(ex.b_gate_up),
                      _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),
                      self.m_act.stride(0), rows, st)
             else:
+                call("stb_moe_gather", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
+                     _p(self.m_rank), _p(offs), _p(self.m_perm), _p(self.m_x), st)
                 ev = self._tick()
                 call("stb_moe_gemm_mxfp4", _p(self.m_x), cap_r, _p(ex.gate_up), _p(ex.b_gate_up),
                      _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),

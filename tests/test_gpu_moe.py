@@ -172,6 +172,31 @@ def test_moe_quant(lib, rows, K):
     assert rel(back, x.float()) < 2e-3
 
 
+@pytest.mark.parametrize("T,E,k,d", [(1, 16, 4, 512), (50, 128, 4, 2880), (300, 16, 4, 64)])
+def test_moe_gather_mx(lib, T, E, k, d):
+    """Fused gather + split: the same offsets / permutation as stb_moe_gather, and hi / lo halves that
+    reconstruct each routed bf16 row to 2^-8 of its 32-block maxima."""
+    logits = torch.randn(T, E, device="cuda")
+    counts, ex, rk, wt = _route(lib, logits, torch.zeros(E, device="cuda"), k)
+    h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    offs, perm, xp = _gather(lib, h, counts, ex, rk, E, k)
+    cap = xp.shape[0]
+    offs2 = torch.zeros_like(offs)
+    perm2 = torch.zeros_like(perm)
+    xq = torch.zeros(lib.load().stb_moe_quant_bytes(cap, d), dtype=torch.uint8, device="cuda")
+    xsf = torch.zeros(lib.load().stb_moe_quant_scale_words(cap, d), dtype=torch.int32, device="cuda")
+    lib.call("stb_moe_gather_mx", P(h), d, T, d, k, E, P(counts), P(ex), P(rk), P(offs2), P(perm2), cap, P(xq),
+             P(xsf), stream())
+    torch.cuda.synchronize()
+    assert torch.equal(offs, offs2) and torch.equal(perm, perm2)
+    rows = T * k
+    back = _dequant(xq, xsf, rows, cap, d)
+    ref = torch.empty(rows, d, device="cuda")
+    ref[perm.long()] = h.float().repeat_interleave(k, 0)
+    bound = ref.abs().view(rows, -1, 32).amax(-1, keepdim=True).expand(-1, -1, 32).reshape(rows, d) * 2.0 ** -8
+    assert torch.all((back - ref).abs() <= bound + 1e-30)
+
+
 @pytest.mark.parametrize("T,E,k,d,ff", [(1, 16, 4, 512, 256), (32, 128, 4, 2880, 2880), (300, 16, 4, 512, 256),
                                         (700, 32, 4, 1024, 512), (64, 8, 2, 256, 384), (16, 8, 2, 64, 128)])
 def test_moe_gemm_mx(lib, T, E, k, d, ff):
