@@ -62,6 +62,10 @@ constexpr int EPI_LD = BM + 4;    // fp32 row stride of the QKV staging tile
 constexpr int EPI_SMEM = 256 * 4 * 7 + EPI_CH * EPI_LD * 4;  // sizeof(EpiSmem)
 constexpr int kMaxSsParts = 64;   // d_model <= 8192 (ss partials per row, a multiple of 4)
 
+#ifndef STB_GEMM_RING_COUNTERS
+#define STB_GEMM_RING_COUNTERS 1
+#endif
+
 template <int BN>
 struct Cfg {
   static constexpr int W_BYTES = BM * BK * 2;
@@ -536,13 +540,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       const uint32_t idesc = umma_idesc_bf16(BM, bn, false, false);
       SegIter it(sched);
-      int tile, k0, k1, i = 0, j = 0;
+      int tile, k0, k1, i = 0, j = 0, rs = 0, rph = 0;
+      const uint64_t wdesc0 = umma_desc_kmajor_sw128(smem_u32(smem), 1024);
+      (void)rs, (void)rph, (void)wdesc0;
       while (it.next(tile, k0, k1)) {
         const int buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + buf * BN;
         for (int k = k0; k < k1; ++k, ++i) {
+#if STB_GEMM_RING_COUNTERS
+          const int s = rs;
+          mbar_wait(&full[s], rph);
+          if (++rs == STAGES) rs = 0, rph ^= 1;
+          if (tracing && i == 0) tt[2] = gtime();
+          const uint64_t adesc = wdesc0 + (uint64_t)((s * CF::STAGE) >> 4);
+          const uint64_t bdesc = adesc + (CF::W_BYTES >> 4);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_f16_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (k > k0 || kk > 0) ? 1u : 0u);
+#else
           const int s = i % STAGES;
           mbar_wait(&full[s], (i / STAGES) & 1);
           if (tracing && i == 0) tt[2] = gtime();
@@ -554,6 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_f16_ss(d, umma_desc_kmajor_sw128(wa + kk * 32, 1024), umma_desc_kmajor_sw128(xa + kk * 32, 1024),
                         idesc, (k > k0 || kk > 0) ? 1u : 0u);
           }
+#endif
           umma_commit(&empty[s]);
         }
         umma_commit(&acc_full[buf]);
@@ -1470,13 +1489,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {  // MMA issuer (leader)
       const uint32_t idesc = umma_idesc_bf16(PAIR_BM, bn, false, false);
-      int i = 0, j = 0;
+      int i = 0, j = 0, rs = 0, rph = 0;
+      const uint64_t wdesc0 = umma_desc_kmajor_sw128(smem_u32(smem), 1024);
+      (void)rs, (void)rph, (void)wdesc0;
       for (int t = pair; t < tiles; t += npairs, ++j) {
         const int buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + buf * BN;
         for (int k = 0; k < kb; ++k, ++i) {
+#if STB_GEMM_RING_COUNTERS
+          // ring slot / phase as counters: a modulo by a stage count that is not a power of two
+          // sits on the issuing thread's critical path every stage (the MoE GEMM measured it)
+          const int st = rs;
+          mbar_wait(&full[st], rph);
+          if (++rs == STAGES) rs = 0, rph ^= 1;
+          const uint64_t adesc = wdesc0 + (uint64_t)((st * CF::STAGE) >> 4);
+          const uint64_t bdesc = adesc + (CF::W_BYTES >> 4);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_f16_ss_pair(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+#else
           const int st = i % STAGES;
           mbar_wait(&full[st], (i / STAGES) & 1);
           tc_fence_after();
@@ -1486,6 +1520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk)
             umma_f16_ss_pair(d, umma_desc_kmajor_sw128(wa + kk * 32, 1024), umma_desc_kmajor_sw128(xa + kk * 32, 1024),
                              idesc, (k > 0 || kk > 0) ? 1u : 0u);
+#endif
           umma_commit_pair(&empty[st]);
         }
         umma_commit_pair(&acc_full[buf]);
