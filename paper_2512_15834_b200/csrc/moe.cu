@@ -4,9 +4,12 @@
 // Replaces, for the MoE model family, the MLP part of every `rate x tokens` charge of the
 // reference engine (`engine.py:251,270,296,358`); the reference itself has no model
 // (SPEC.md:17). Expert weights are MXFP4 — e2m1 values with one ue8m0 scale per 32 along K, the
-// released gpt-oss checkpoint's format — which is what lets a 120B replica (65.6 GB) live on one
-// B200. Activations stay 16-bit: the tensor core runs kind::f16 (fp16 x fp16 -> fp32)
-// on weights dequantised on chip, so the only quantisation is the checkpoint's own.
+// released gpt-oss checkpoint's format — which is what lets a 120B replica (~67 GB) live on one
+// B200. The default GEMM (moe_gemm_mx_kernel, further down) is block-scaled: the tensor
+// core reads the e2m1 codes and applies their scales itself (kind::mxf8f6f4), with the token rows
+// split exactly into two e4m3 halves; the description below is the dequantising kernel it replaced
+// (kept for A/B, STB200_MOE_MX=0), whose activations stay fp16 (kind::f16 on weights dequantised
+// on chip).
 //
 // Per layer (one stream, programmatic dependent launch throughout):
 //   K5 router GEMM (bf16, gemm.cu) -> logits [T][E]

@@ -233,27 +233,6 @@ def test_moe_gemm_mx(lib, T, E, k, d, ff):
     assert not torch.isnan(act[:rows]).any() and not torch.isnan(y[:rows]).any()
 
 
-def test_pack_mx_stages():
-    """MX stage layout: codes row-major in 64-byte rows, scale word (l, j) = row 32 j + l."""
-    N, K = 200, 320
-    g = torch.Generator().manual_seed(3)
-    codes = torch.randint(0, 16, (N, K), generator=g).to(torch.uint8)
-    exps = torch.randint(-13, 13, (N, K // 32), generator=g).to(torch.int8)
-    st = W.pack_mx_stages(codes, exps)
-    assert st.shape == (2, 3, W.MX_STAGE_BYTES)
-    for n, r, s_, k in [(0, 0, 0, 0), (1, 71, 2, 63), (0, 127, 1, 100), (1, 50, 0, 5)]:
-        row = n * 128 + r
-        b = int(st[n, s_, r * 64 + k // 2])
-        kk = s_ * 128 + k
-        want = int(codes[row, kk]) if row < N and kk < K else 0
-        assert (b >> (4 * (k & 1))) & 15 == want
-        word = st[n, s_, 8192:].view(torch.int32)[(r % 32) * 4 + r // 32].item() & 0xFFFFFFFF
-        for t in range(4):
-            blk = s_ * 4 + t
-            want_s = int(exps[row, blk]) + 127 if row < N and blk < K // 32 else 127
-            assert (word >> (8 * t)) & 255 == want_s
-
-
 def test_moe_combine(lib):
     T, E, k, d = 9, 16, 4, 2880
     counts, ex, rk, wt = _route(lib, torch.randn(T, E, device="cuda"), torch.zeros(E, device="cuda"), k)
