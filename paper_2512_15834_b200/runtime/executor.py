@@ -599,6 +599,7 @@ class BatchRuntime(Runtime):
         self.spilled: deque = deque()
         self._in_step: set = set()  # slots of the step being packed (never preempted mid-launch)
         self.spills = 0        # sequences preempted
+        self._prev_in_air = False  # step(): a packed forward is still in flight while this one packs
         self.deferred = 0      # steps that held a prefill / ingest run back for lack of blocks
 
     def _submit_run(self, run: Run) -> None:
@@ -657,6 +658,14 @@ class BatchRuntime(Runtime):
             self._spill(victim)
             free = self.pool.free_blocks()
             need = self._need(decodes, runs)
+        if need > free and self._prev_in_air:
+            # the blocks still missing sit with the sequences of the step in the air (busy, so not
+            # preemptible now): launch nothing, let step() complete that flight, and pack again on
+            # the next call, when they can be preempted
+            for r in reversed(runs):
+                self.runs.appendleft(r)
+            self.deferred += 1
+            return [], []
         if need > free:
             raise KVCapacityError(f"KV pool exhausted: the step needs {need} blocks, {free} free, nothing left to "
                                   "preempt")
@@ -714,6 +723,7 @@ class BatchRuntime(Runtime):
     def step(self) -> int:
         """Launch the next packed forward (if any work), then complete the previous one."""
         prev, self.flight = self.flight, None
+        self._prev_in_air = prev is not None
         decodes, runs = self._pack()
         emitted = 0
         if decodes or runs:
