@@ -825,19 +825,24 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
       const int ib = j & 1;
       mbar_wait(&b_empty[ib], ((j >> 1) & 1) ^ 1);
       const uint32_t base = smem_u32(ssb + ib * CF::SFB_ITEM);
-      for (int ks0 = 0; ks0 < KS; ks0 += 8) {
-        uint32_t v[8][4];
+      // all of a batch's loads in flight at once (one L2 round trip per batch): 24 stages x 1 column
+      // at BN = 16, 12 x 2 at BN = 32, 6 x 4 at BN = 64
+      constexpr int C = CF::SFB_COLS, U = 24 / C;
+      for (int ks0 = 0; ks0 < KS; ks0 += U) {
+        uint32_t v[U][C];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < C; ++c) {
             const int n = 32 * c + lane, h = n >= BN, tok = n - h * BN, row = xrow + tok;
-            v[u][c] = (c < CF::SFB_COLS && ks0 + u < KS && n < 2 * BN && row < rows_cap)
+            v[u][c] = (ks0 + u < KS && n < 2 * BN && row < rows_cap)
                           ? __ldg(xsf + (int64_t)(2 * (ks0 + u) + h) * pitch + row) : 0x7f7f7f7fu;
           }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (ks0 + u < KS) sts128(base + (ks0 + u) * 512 + lane * 16, v[u][0], v[u][1], v[u][2], v[u][3]);
+        for (int u = 0; u < U; ++u)
+          if (ks0 + u < KS)
+            sts128(base + (ks0 + u) * 512 + lane * 16, v[u][0], C > 1 ? v[u][C > 1 ? 1 : 0] : 0x7f7f7f7fu,
+                   C > 2 ? v[u][C > 2 ? 2 : 0] : 0x7f7f7f7fu, C > 3 ? v[u][C > 3 ? 3 : 0] : 0x7f7f7f7fu);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
