@@ -352,7 +352,10 @@ int stb_moe_combine(float* x, const float* y, int T, int d, int k, const int32_t
  * scaling; the pair keeps ~2^-8 of each 32-block's maximum, the precision of the bf16 activation):
  *   xq  [2][rows_cap][K] bytes (hi rows, then lo rows)   stb_moe_quant_bytes(rows_cap, K)
  *   xsf [ceil(K/128)][2][pitch = rows_cap rounded up to 4] words of four scale bytes (+ 72 words of overhang)   stb_moe_quant_scale_words(rows_cap, K)
- * stb_moe_gemm_mx takes them in place of the fp16 xperm; everything else as stb_moe_gemm_mxfp4.
+ * stb_moe_gemm_mx takes them in place of the fp16 xperm, and the experts in the MX stage format
+ * (runtime/weights.py pack_mx_stages: [E][ceil(N/128)][ceil(K/128)][8704] bytes, per 128-row x
+ * 128-wide stage 8192 B of packed codes then 32 x 4 scale words, word (l, j) = the four K-slice
+ * scales of row 32 j + l; 16-byte aligned); everything else as stb_moe_gemm_mxfp4. K <= 3072.
  * Replaces the same charges (engine.py:251,270,296,358).                                  */
 int64_t stb_moe_quant_bytes(int rows_cap, int K);
 int64_t stb_moe_quant_scale_words(int rows_cap, int K);
