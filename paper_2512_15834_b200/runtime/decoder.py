@@ -316,6 +316,8 @@ class Decoder:
         self.timer_filter: set | None = None  # time only these kernel classes (None: all)
         self._pre_flops = 0
         self._pre_work = (0, 0)  # (flops, bytes) of one K2 launch: verify runs are HBM-bound, ingests tensor-bound
+        self._pre_work_win = (0, 0)  # the same on a sliding-window layer
+        self._dec_bytes_win = 0      # K3's algorithmic bytes on a sliding-window layer
         self._pre_units = 0
         self.run_log: list | None = None
         self._pending: list | None = []             # (name, ev0, ev1, work) awaiting a sync
@@ -476,6 +478,10 @@ class Decoder:
         T, R, B, S = b.T, b.R, b.B_dec, b.S
         self.last_step_tokens = T
         dec_bytes = (int(b.dec_ctx.sum()) * 2 * self.shape.kv_dim * 2 + 2 * B * self.shape.q_dim * 2) if B else 0
+        # sliding-window layers (gpt-oss, every other layer) read only the last `window` keys
+        W = self.shape.sliding_window
+        self._dec_bytes_win = ((int(np.minimum(b.dec_ctx, W).sum()) * 2 * self.shape.kv_dim * 2
+                                + 2 * B * self.shape.q_dim * 2) if B else 0) if W else dec_bytes
         mq = self._mq_entries(b)
         self._mq_B = 0
         if mq is not None:
@@ -497,6 +503,14 @@ class Decoder:
             # algorithmic bytes: every run's K/V read once plus its q and o rows
             pre_bytes = int(np.sum(b.pre_ctx)) * 2 * self.shape.kv_dim * 2 + int(np.sum(n)) * 2 * self.shape.q_dim * 2
             self._pre_work = (self._pre_flops, pre_bytes)
+            if W:  # a window layer: query at position p attends min(p + 1, W) keys; keys read once
+                pos = [prev_i + np.arange(n_i) for prev_i, n_i in zip(prev, n)]
+                keys = sum(int(np.minimum(p_ + 1, W).sum()) for p_ in pos)
+                kread = int(np.sum(np.minimum(b.pre_ctx, n + W - 1)))
+                self._pre_work_win = (int(4 * self.shape.q_dim * keys),
+                                      kread * 2 * self.shape.kv_dim * 2 + int(np.sum(n)) * 2 * self.shape.q_dim * 2)
+            else:
+                self._pre_work_win = self._pre_work
             # K2 work units holding queries: (query-tile pair of 2*128/G tokens, kv head, run)
             pair = 2 * 128 // (self.shape.n_q // self.shape.n_kv)
             self._pre_units = int(np.sum(np.ceil(n / pair))) * self.shape.n_kv
@@ -551,9 +565,15 @@ class Decoder:
             self.graph_replays += 1
             self.graph_kernels += self.graph_sizes.get(key, 0)
             if timed:
-                live = {"attn_decode": dec_bytes, "attn_prefill": self._pre_work}
+                live = {"attn_decode": (dec_bytes, self._dec_bytes_win),
+                        "attn_prefill": (self._pre_work, self._pre_work_win)}
+                seen: dict = {}
                 for name, a0, a1, work in events:
-                    self._pending.append((name, a0, a1, live.get(name, work)))
+                    if name in live:  # one launch per layer, in layer order
+                        layer = seen.get(name, 0)
+                        seen[name] = layer + 1
+                        work = live[name][1 if self.shape.window(layer) else 0]
+                    self._pending.append((name, a0, a1, work))
         if self.step_events is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
@@ -782,13 +802,13 @@ class Decoder:
                 ev = self._tick("attn_decode")
                 call("stb_attn_decode_ex", self.pool.h, i, _p(self.q), _p(self.attn), _p(m["dec_slots"]),
                      _p(m["dec_ctx"]), B, s.n_q, self.scale, max_ctx, win, sinks, _p(self.work), st)
-                self._tock("attn_decode", ev, dec_bytes)
+                self._tock("attn_decode", ev, self._dec_bytes_win if win else dec_bytes)
             if S:
                 ev = self._tick("attn_prefill")
                 call("stb_attn_prefill_ex", self.pool.h, i, _p(self.q[B:].data_ptr()), _p(self.attn[B:].data_ptr()),
                      _p(m["pre_slots"]), _p(m["pre_qstart"]), _p(m["pre_ctx"]), S, T - B, s.n_q, self.scale, max_q,
                      self._pre_units, win, sinks, st)
-                self._tock("attn_prefill", ev, self._pre_work)
+                self._tock("attn_prefill", ev, self._pre_work_win if win else self._pre_work)
             self.gemm(self.attn[:T], w[f"l{i}.wo"], "proj", st, "wo")
             call("stb_add_bias_rmsnorm", _p(x), _p(self.proj), _p(w.get(f"l{i}.bo")), _p(w[f"l{i}.mlp_norm"]), _p(h),
                  T, d, s.rms_eps, clr, st)
