@@ -365,6 +365,13 @@ int stb_moe_quant(const void* x, int64_t ldx, int rows, int K, int rows_cap, voi
 int stb_moe_gather_mx(const void* h, int64_t ldh, int T, int d, int k, int E, const int32_t* counts,
                       const int32_t* expert, const int32_t* rank, int32_t* offsets, int32_t* perm, int rows_cap,
                       void* xq, uint32_t* xsf, void* stream);
+/* gate-up on the block-scaled path with the down projection's input split fused into its epilogue:
+ * q_out / q_sf (sized by stb_moe_quant_bytes / _scale_words(q_cap, N/2)) receive what
+ * stb_moe_quant would write from the SwiGLU rows (computed in fp32, not rounded to fp16 first);
+ * `out` (the fp16 act) may then be NULL. Needs N/2 % 64 == 0. */
+int stb_moe_gemm_mx_q(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
+                      const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo,
+                      int rows, void* q_out, uint32_t* q_sf, int q_cap, void* stream);
 int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
                     const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
                     void* stream);

@@ -328,6 +328,9 @@ struct MoeArgs {
   int64_t ldo;
   int E, N, K, kind;
   float limit;          // SwiGLU clamp (kind 1)
+  uint8_t* qout;        // kind 1, block-scaled path: the down input's e4m3 halves [2][qcap][N/2] (or null)
+  uint8_t* qsf;         // ... and its scale words, as bytes ([stages][2][pitch] words)
+  int qcap;
 };
 
 constexpr float kSwigluAlpha = 1.702f;
@@ -708,6 +711,80 @@ __host__ __device__ constexpr uint32_t idesc_mx(int M, int N) {
   return (5u << 7) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
 }
 
+__device__ __forceinline__ int blk_exp(float amax) {
+  int e;
+  frexpf(amax, &e);  // amax = m 2^e, m in [0.5, 1)
+  return amax > 0.f ? e - 8 : 0;
+}
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
+  uint16_t lo, hi;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(lo) : "f"(a), "f"(b));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(hi) : "f"(c), "f"(d));
+  return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ float2 e4m3x2_to_f2(uint16_t v) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
+  return __half22float2(*reinterpret_cast<__half2*>(&h));
+}
+// gate-up epilogue -> the down projection's B operand (no fp16 act round trip, no quant launch): the
+// chunk's 8 SwiGLU values per lane (feature f/2, tokens c..c+7 on even lanes, c+8..c+15 on odd) are
+// split like quant_stage, with each 32-feature block's maxima reduced over the 16 same-parity lanes
+// and the partner warp holding the block's other 16 features (named barrier per warp pair)
+__device__ __forceinline__ void pair_bar(int q) {
+  asm volatile("bar.sync %0, 64;\n" ::"r"(1 + (q >> 1)) : "memory");
+}
+__device__ __forceinline__ void glu_quant_chunk(const float* gv, int q, int lane, int nt, int f, int N, int c, int nv,
+                                                int row0, const MoeArgs& a, float (*s_x)[2][8], float (*s_r)[2][8]) {
+  const int odd = lane & 1;
+  float am[8], sc[8], r[8];
+  int eh[8], el[8];
+  uint32_t hq[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    float x = fabsf(gv[u]);
+#pragma unroll
+    for (int o = 2; o < 32; o <<= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+    am[u] = x;
+  }
+  if (lane < 2)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s_x[q][lane][u] = am[u];
+  pair_bar(q);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    eh[u] = blk_exp(fmaxf(am[u], s_x[q ^ 1][odd][u]));
+    sc[u] = ldexpf(gv[u], -eh[u]);
+    hq[u] = e4m3x4(sc[u], 0.f, 0.f, 0.f) & 0xFFu;
+    r[u] = sc[u] - e4m3x2_to_f2((uint16_t)hq[u]).x;
+    float x = fabsf(r[u]);
+#pragma unroll
+    for (int o = 2; o < 32; o <<= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+    am[u] = x;
+  }
+  if (lane < 2)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s_r[q][lane][u] = am[u];
+  pair_bar(q);
+  const int Kd = a.N >> 1, feat = f >> 1, blk = (nt * BM + (q >> 1) * 64) >> 6;  // 32-feature block
+  const int64_t pitch = sf_pitch(a.qcap);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    el[u] = blk_exp(fmaxf(am[u], s_r[q ^ 1][odd][u]));
+    const uint32_t lq = e4m3x4(ldexpf(r[u], -el[u]), 0.f, 0.f, 0.f) & 0xFFu;
+    const int tok = c + (odd ? 8 : 0) + u;
+    if (f < N && tok < nv) {
+      a.qout[(int64_t)(row0 + tok) * Kd + feat] = (uint8_t)hq[u];
+      a.qout[((int64_t)a.qcap + row0 + tok) * Kd + feat] = (uint8_t)lq;
+    }
+    if (lane < 2 && (q & 1) == 0 && tok < nv) {  // the block's first feature: its two scale bytes
+      const int64_t w = (int64_t)(2 * (blk >> 2)) * pitch + row0 + tok;
+      a.qsf[w * 4 + (blk & 3)] = (uint8_t)(eh[u] + 127);
+      a.qsf[(w + pitch) * 4 + (blk & 3)] = (uint8_t)(eh[u] + el[u] + 127);
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                                     const __grid_constant__ CUtensorMap tm_x,
@@ -731,6 +808,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
   __shared__ int s_off[kMaxE + 1];
   __shared__ int s_item[kMaxE + 1];
   __shared__ int s_cnt[kMaxE];
+  __shared__ float s_qx[4][2][8], s_qr[4][2][8];  // fused down-input split: block maxima of a warp pair
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int E = a.E, NT = ceil_div(a.N, BM), KS = ceil_div(a.K, MX_BK);
@@ -931,15 +1009,18 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
         } else {
           __half* act = reinterpret_cast<__half*>(a.out);
           const bool odd = lane & 1;
+          float gv[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float mine = __uint_as_float(odd ? rr[8 + u] : rr[u]) + b;
             const float other = __shfl_xor_sync(0xffffffffu, __uint_as_float(odd ? rr[u] : rr[8 + u]) + b, 1);
             const int tok = c + (odd ? 8 : 0) + u;
             const float g = odd ? other : mine, up = odd ? mine : other;
-            if (f < a.N && tok < nv)
-              act[(int64_t)(row0 + tok) * a.ldo + (f >> 1)] = __float2half_rn(gpt_oss_glu(g, up, a.limit));
+            const bool ok = f < a.N && tok < nv;
+            gv[u] = ok ? gpt_oss_glu(g, up, a.limit) : 0.f;
+            if (ok && act) act[(int64_t)(row0 + tok) * a.ldo + (f >> 1)] = __float2half_rn(gv[u]);
           }
+          if (a.qout) glu_quant_chunk(gv, q, lane, nt, f, a.N, c, nv, row0, a, s_qx, s_qr);
         }
       }
       tc_fence_before();
@@ -959,22 +1040,6 @@ __global__ void __launch_bounds__(kMxThreads, 1) moe_gemm_mx_kernel(const __grid
 // maximum). Warp per (row, 128-wide stage); lane = 4 values; xq [2][rows_cap][K] (hi rows, then lo
 // rows), xsf [stages][2][pitch] words of four scale bytes (blocks past K: 127, i.e. 1.0), pitch =
 // rows_cap rounded up to 4 words (the GEMM reads them with a 2-D TMA box).
-__device__ __forceinline__ int blk_exp(float amax) {
-  int e;
-  frexpf(amax, &e);  // amax = m 2^e, m in [0.5, 1)
-  return amax > 0.f ? e - 8 : 0;
-}
-__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
-  uint16_t lo, hi;
-  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(lo) : "f"(a), "f"(b));
-  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(hi) : "f"(c), "f"(d));
-  return (uint32_t)lo | ((uint32_t)hi << 16);
-}
-__device__ __forceinline__ float2 e4m3x2_to_f2(uint16_t v) {
-  uint32_t h;
-  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
-  return __half22float2(*reinterpret_cast<__half2*>(&h));
-}
 // one 128-wide stage of one token row, lane = 4 values (v): hi / lo codes and the scale words
 __device__ __forceinline__ void quant_stage(const float* v, int lane, int ks, int K, int row, int rows_cap,
                                             uint8_t* __restrict__ xq, uint32_t* __restrict__ xsf) {
@@ -1205,21 +1270,32 @@ int stb_moe_gather_mx(const void* h, int64_t ldh, int T, int d, int k, int E, co
   return STB_OK;
 }
 
-int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
-                    const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
-                    void* stream) {
+int stb_moe_gemm_mx_q(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
+                      const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo,
+                      int rows, void* q_out, uint32_t* q_sf, int q_cap, void* stream) {
   if (rows <= 0) return STB_OK;
   if (E <= 0 || E > kMaxE || K % BK || K > MX_KS_MAX * MX_BK || N <= 0 ||
       (kind != STB_MOE_GATE_UP && kind != STB_MOE_DOWN) || (kind == STB_MOE_GATE_UP && N % 2) ||
       (reinterpret_cast<uintptr_t>(wtiles) & 15))
     return fail(STB_EINVAL, "moe_gemm_mx: E=%d N=%d K=%d kind=%d", E, N, K, kind);
-  MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit};
+  if (q_out != nullptr && (kind != STB_MOE_GATE_UP || q_sf == nullptr || q_cap < rows || (N / 2) % 64))
+    return fail(STB_EINVAL, "moe_gemm_mx: the fused down-input split needs gate-up, N/2 %% 64 == 0, q_cap >= rows");
+  if (q_out == nullptr && out == nullptr) return fail(STB_EINVAL, "moe_gemm_mx: no output");
+  MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit, (uint8_t*)q_out, (uint8_t*)q_sf,
+            q_cap};
   const double avg = (double)rows / E;
   const double busy = avg + 2.0 * std::sqrt(avg);
   cudaStream_t st = (cudaStream_t)stream;
   if (busy <= 16.0) return launch_moe_mx<16>(xq, xsf, rows_cap, a, st);
   if (busy <= 32.0) return launch_moe_mx<32>(xq, xsf, rows_cap, a, st);
   return launch_moe_mx<64>(xq, xsf, rows_cap, a, st);
+}
+
+int stb_moe_gemm_mx(const void* xq, const uint32_t* xsf, int rows_cap, const void* wtiles, const float* bias,
+                    const int32_t* counts, int E, int N, int K, int kind, float limit, void* out, int64_t ldo, int rows,
+                    void* stream) {
+  return stb_moe_gemm_mx_q(xq, xsf, rows_cap, wtiles, bias, counts, E, N, K, kind, limit, out, ldo, rows, nullptr,
+                           nullptr, 0, stream);
 }
 
 int stb_moe_route(const float* logits, int64_t ld, const float* bias, int T, int E, int k, int32_t* counts,
@@ -1260,7 +1336,7 @@ int stb_moe_gemm_mxfp4(const void* xperm, int rows_cap, const void* wtiles, cons
   if (E <= 0 || E > kMaxE || K % BK || N <= 0 || (kind != STB_MOE_GATE_UP && kind != STB_MOE_DOWN) ||
       (kind == STB_MOE_GATE_UP && N % 2))
     return fail(STB_EINVAL, "moe_gemm: E=%d N=%d K=%d kind=%d", E, N, K, kind);
-  MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit};
+  MoeArgs a{(const uint8_t*)wtiles, bias, counts, out, ldo, E, N, K, kind, limit, nullptr, nullptr, 0};
   // token tile from the mean rows per expert: decode steps put ~T k / E <= a few rows on an
   // expert (BN 16); larger tiles only once experts hold tens of rows
   // (a busy expert holds ~mean + 2 sqrt(mean) rows: one token tile should cover it, or its

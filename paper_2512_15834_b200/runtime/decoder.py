@@ -74,6 +74,12 @@ MOE_GATE_UP, MOE_DOWN = 1, 2                 # include/stb200.h STB_MOE_*
 # MoE GEMMs on the block-scaled tensor-core path (stb_moe_quant + stb_moe_gemm_mx);
 # STB200_MOE_MX=0 keeps the dequantising kernel (stb_moe_gemm_mxfp4) for A/B
 from .weights import MOE_MX  # noqa: E402  (the experts' packing follows the same switch)
+# STB200_MOE_FUSED_SPLIT=1: the gate-up epilogue splits the down projection's input itself
+# (stb_moe_gemm_mx_q) instead of writing fp16 rows for stb_moe_quant — parity-green but slower
+# (in-step A/B, profiles/r2n_c4_fused_split_ab.txt: decode 8.83 -> 9.22 ms, a 400-token ingest step
+# 19.9 -> 23.4 ms: the per-element byte stores and pair barriers lengthen the epilogue past the
+# weight stream), so off by default
+MOE_FUSED_SPLIT = os.environ.get("STB200_MOE_FUSED_SPLIT", "0") == "1"
 MOE_TILE_BYTES = 4352                        # one 128 x 64 MXFP4 tile (weights.TILE_BYTES)
 
 
@@ -381,11 +387,15 @@ class Decoder:
                 self.m_x = torch.zeros(rows, s.d_model, dtype=torch.float16, device=dev)
                 self.m_act = torch.zeros(rows, s.d_ff, dtype=torch.float16, device=dev)
                 self.m_y = torch.empty(rows, s.d_model, dtype=f32, device=dev)
-                if MOE_MX:  # e4m3 hi / lo halves + scale words of either GEMM's token rows
+                if MOE_MX:  # e4m3 hi / lo halves + scale words of the gate-up input, and of the down
+                    # input (written by the gate-up epilogue while the gate-up GEMM still reads the first)
                     kq = max(s.d_model, s.d_ff)
                     L = lib.load()
                     self.m_xq = torch.zeros(L.stb_moe_quant_bytes(rows, kq), dtype=torch.uint8, device=dev)
                     self.m_xsf = torch.zeros(L.stb_moe_quant_scale_words(rows, kq), dtype=torch.int32, device=dev)
+                    self.m_aq = torch.zeros(L.stb_moe_quant_bytes(rows, s.d_ff), dtype=torch.uint8, device=dev)
+                    self.m_asf = torch.zeros(L.stb_moe_quant_scale_words(rows, s.d_ff), dtype=torch.int32,
+                                             device=dev)
                 self._moe_rows = rows
             self._cap_t = cap
             self._dirty.update(qkv=0, proj=0, gu=0)
@@ -832,9 +842,12 @@ class Decoder:
                 call("stb_moe_gather_mx", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
                      _p(self.m_rank), _p(offs), _p(self.m_perm), cap_r, _p(self.m_xq), _p(self.m_xsf), st)
                 ev = self._tick()
-                call("stb_moe_gemm_mx", _p(self.m_xq), _p(self.m_xsf), cap_r, _p(ex.gate_up), _p(ex.b_gate_up),
-                     _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit), _p(self.m_act),
-                     self.m_act.stride(0), rows, st)
+                # the epilogue splits the SwiGLU rows into the down projection's e4m3 halves itself
+                fuse = MOE_FUSED_SPLIT and s.d_ff % 64 == 0
+                call("stb_moe_gemm_mx_q", _p(self.m_xq), _p(self.m_xsf), cap_r, _p(ex.gate_up), _p(ex.b_gate_up),
+                     _p(self.m_counts), E, 2 * s.d_ff, d, MOE_GATE_UP, C.c_float(s.swiglu_limit),
+                     None if fuse else _p(self.m_act), self.m_act.stride(0), rows,
+                     _p(self.m_aq) if fuse else None, _p(self.m_asf) if fuse else None, cap_r, st)
             else:
                 call("stb_moe_gather", _p(h), h.stride(0), T, d, k, E, _p(self.m_counts), _p(self.m_expert),
                      _p(self.m_rank), _p(offs), _p(self.m_perm), _p(self.m_x), st)
@@ -844,10 +857,11 @@ class Decoder:
                      self.m_act.stride(0), rows, st)
             self._tock("moe_gemm", ev, _MoeWork(offs_host, i, 2 * s.d_ff, d, rows, 2, 2) if timed else 0)
             if MOE_MX:
-                call("stb_moe_quant", _p(self.m_act), self.m_act.stride(0), rows, s.d_ff, cap_r, _p(self.m_xq),
-                     _p(self.m_xsf), st)
+                if not fuse:
+                    call("stb_moe_quant", _p(self.m_act), self.m_act.stride(0), rows, s.d_ff, cap_r, _p(self.m_aq),
+                         _p(self.m_asf), st)
                 ev = self._tick()
-                call("stb_moe_gemm_mx", _p(self.m_xq), _p(self.m_xsf), cap_r, _p(ex.down), _p(ex.b_down),
+                call("stb_moe_gemm_mx", _p(self.m_aq), _p(self.m_asf), cap_r, _p(ex.down), _p(ex.b_down),
                      _p(self.m_counts), E, d, s.d_ff, MOE_DOWN, C.c_float(0.0), _p(self.m_y), self.m_y.stride(0),
                      rows, st)
             else:

@@ -73,6 +73,7 @@ SIGNATURES: dict[str, tuple] = {
     "stb_moe_quant_scale_words": (I64, [I32, I32]),
     "stb_moe_quant": (I32, [P, I64, I32, I32, I32, P, P, P]),
     "stb_moe_gather_mx": (I32, [P, I64, I32, I32, I32, I32, P, P, P, P, P, I32, P, P, P]),
+    "stb_moe_gemm_mx_q": (I32, [P, P, I32, P, P, P, I32, I32, I32, I32, F32, P, I64, I32, P, P, I32, P]),
     "stb_moe_gemm_mx": (I32, [P, P, I32, P, P, P, I32, I32, I32, I32, F32, P, I64, I32, P]),
     "stb_moe_combine": (I32, [P, P, I32, I32, I32, P, P, P, P, F32, P, I32, P]),
 }
