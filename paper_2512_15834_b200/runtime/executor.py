@@ -666,6 +666,15 @@ class BatchRuntime(Runtime):
                 self.runs.appendleft(r)
             self.deferred += 1
             return [], []
+        if need > free and decodes and self.runs:
+            # the missing blocks sit with sequences whose prefill / ingest runs were held back above:
+            # preempt the remaining decodes as well, so those runs fit on the next step (the decodes
+            # are recomputed once blocks return, `_restore`)
+            for j in list(decodes):
+                self._spill(j)
+            for r in reversed(runs):
+                self.runs.appendleft(r)
+            return [], []
         if need > free:
             raise KVCapacityError(f"KV pool exhausted: the step needs {need} blocks, {free} free, nothing left to "
                                   "preempt")
