@@ -675,10 +675,33 @@ class BatchRuntime(Runtime):
             for r in reversed(runs):
                 self.runs.appendleft(r)
             return [], []
+        while need > free:
+            # last resort: a held-back (queued) prefill / ingest run whose sequence holds KV gives its
+            # blocks up and becomes a recompute run from row 0 (verify passes are never rewritten)
+            keep = ({r.seq.dev.slot for r in runs} | {j.seq.dev.slot for j in decodes}
+                    | {j.seq.dev.slot for j in self.decodes})
+            cands = [r for r in self.runs if r.verify is None and r.start > 0 and not r.seq.dev.busy
+                     and r.seq.dev.slot not in keep and self.pool.blocks(r.seq.dev.slot)]
+            if not cands:
+                break
+            self._spill_run(max(cands, key=lambda r: r.start))
+            free = self.pool.free_blocks()
         if need > free:
             raise KVCapacityError(f"KV pool exhausted: the step needs {need} blocks, {free} free, nothing left to "
                                   "preempt")
         return decodes, runs
+
+    def _spill_run(self, r: Run) -> None:
+        """Preempt the sequence of a queued run: release its KV and rewrite the run to recompute its
+        rows [0, start) ahead of its own ids (sampled rows shift by `start`)."""
+        d = r.seq.dev
+        prefix = list(d.hist[:r.start])
+        d.kv_len = 0
+        self.pool.release(d.slot)
+        r.rows = [x + r.start for x in r.rows]
+        r.ids = prefix + list(r.ids)
+        r.start = 0
+        self.spills += 1
 
     def _reserve(self, slot: int, n: int) -> None:
         """pool.reserve; under KV pressure drop retained prefixes, then preempt decoding sequences
